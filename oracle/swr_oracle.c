@@ -1,0 +1,686 @@
+/*
+ * oracle/swr_oracle.c — TEST INFRASTRUCTURE ONLY (parity oracle).
+ *
+ * Plain, slow, single-threaded C implementation of the SWR method of
+ * Besse & Xing, arXiv:1503.02564.  Every function follows the paper's
+ * formulas in the paper's order; "P:n" cites PAPER.md line n, "A<k>" cites
+ * a reading listed in DESIGN.md.  Built with
+ * -O2 -ffp-contract=off -fcx-limited-range (plain IEEE products, no FMA).
+ *
+ * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
+ * --impl reference) may load this library.  The CUDA product path never
+ * links, loads or calls it.
+ *
+ * Parity status: every exported function is pinned by a -m "not gpu" test in
+ * tests/test_oracle_*.py against something other than itself (closed forms,
+ * dense brute force, invariants, the paper's printed values).
+ */
+#include "swr_oracle.h"
+#include <math.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define I_ _Complex_I
+
+/* ------------------------------------------------------------------ */
+/* Coefficients alpha, beta, gamma.                        */
+/* alpha = (1, 1, 1/2, 1/2, 3/8, 3/8, 3*5/(2*4*6), ...):               */
+/* alpha_{2k} = alpha_{2k-2} (2k-1)/(2k), alpha_{2k+1} = alpha_{2k};   */
+/* beta_s = (-1)^s alpha_s;  gamma = (1, 2, 2, 2, ...).                */
+/* ------------------------------------------------------------------ */
+void or_coeffs(int32_t n, double *alpha, double *beta, double *gamma) {
+  for (int32_t s = 0; s < n; s++) {
+    double a;
+    if (s == 0) a = 1.0;
+    else if (s % 2 == 1) a = alpha[s - 1];
+    else a = alpha[s - 2] * (double)(s - 1) / (double)s;
+    alpha[s] = a;
+    if (beta) beta[s] = (s % 2 == 0) ? a : -a;
+    if (gamma) gamma[s] = (s == 0) ? 1.0 : 2.0;
+  }
+}
+
+/* Mesh (reading A1): N_x = round((b0-a0)/dx), N_T = round(T/dt),
+ * N | N_x, subdomain j holds global nodes [(j-1)m, jm], m = N_x/N. */
+int32_t or_sizes(const or_problem *P, int32_t *Nx, int32_t *NT, int32_t *Nj) {
+  if (!P || P->N < 1 || !(P->dx > 0) || !(P->dt > 0)) return OR_ERR_ARG;
+  int32_t nx = (int32_t)llround((P->b0 - P->a0) / P->dx);
+  int32_t nt = (int32_t)llround(P->T / P->dt);
+  if (nx < 1 || nt < 1 || nx % P->N != 0) return OR_ERR_ARG;
+  if (nx / P->N < 1) return OR_ERR_ARG;
+  if (Nx) *Nx = nx;
+  if (NT) *NT = nt;
+  if (Nj) *Nj = nx / P->N + 1;
+  return OR_OK;
+}
+
+/* P1 finite elements on a uniform mesh by element assembly.
+ * Element (k,k+1) of length h contributes
+ *   M:   h/3, h/3 on the diagonal, h/6 off-diagonal;
+ *   S:   1/h, 1/h on the diagonal, -1/h off-diagonal  (S = int v' phi');
+ *   M_W: h(3W_k+W_{k+1})/12, h(W_k+3W_{k+1})/12 diagonal,
+ *        h(W_k+W_{k+1})/12 off-diagonal  (exact integral of the linear
+ *        interpolant of W times hat products, reading A2). */
+void or_fem(int32_t nn, double h, const double *W, double *Mdiag, double *Moff,
+            double *Sdiag, double *Soff, double *MWdiag, double *MWoff) {
+  for (int32_t k = 0; k < nn; k++) {
+    if (Mdiag) Mdiag[k] = 0.0;
+    if (Sdiag) Sdiag[k] = 0.0;
+    if (MWdiag) MWdiag[k] = 0.0;
+  }
+  for (int32_t k = 0; k + 1 < nn; k++) {
+    if (Mdiag) { Mdiag[k] += h / 3.0; Mdiag[k + 1] += h / 3.0; }
+    if (Moff) Moff[k] = h / 6.0;
+    if (Sdiag) { Sdiag[k] += 1.0 / h; Sdiag[k + 1] += 1.0 / h; }
+    if (Soff) Soff[k] = -1.0 / h;
+    double w0 = W ? W[k] : 0.0, w1 = W ? W[k + 1] : 0.0;
+    if (MWdiag) {
+      MWdiag[k] += h * (3.0 * w0 + w1) / 12.0;
+      MWdiag[k + 1] += h * (w0 + 3.0 * w1) / 12.0;
+    }
+    if (MWoff) MWoff[k] = h * (w0 + w1) / 12.0;
+  }
+}
+
+/* Thomas algorithm (Gaussian elimination without pivoting on a tridiagonal
+ * system), the "LU direct method" of P:1079. */
+int32_t or_thomas(int32_t n, const ocplx *lo, const ocplx *di, const ocplx *up,
+                  const ocplx *rhs, ocplx *x) {
+  ocplx *cp = (ocplx *)malloc(sizeof(ocplx) * (size_t)n);
+  ocplx *dp = (ocplx *)malloc(sizeof(ocplx) * (size_t)n);
+  if (!cp || !dp) { free(cp); free(dp); return OR_OOM; }
+  int32_t st = OR_OK;
+  for (int32_t k = 0; k < n; k++) {
+    ocplx den = (k == 0) ? di[0] : di[k] - lo[k] * cp[k - 1];
+    if (cabs(den) < 1e-300) { st = OR_ZERO_PIVOT; break; }
+    cp[k] = (k + 1 < n) ? up[k] / den : 0.0;
+    dp[k] = (k == 0) ? rhs[0] / den : (rhs[k] - lo[k] * dp[k - 1]) / den;
+  }
+  if (st == OR_OK) {
+    x[n - 1] = dp[n - 1];
+    for (int32_t k = n - 2; k >= 0; k--) x[k] = dp[k] - cp[k] * x[k + 1];
+  }
+  free(cp); free(dp);
+  return st;
+}
+
+/* ------------------------------------------------------------------ */
+/* Transmission operator constants.                                    */
+/* S0^2: Sv_n = c2 sum_{s=0}^{n} beta_{n-s} v_s, c2 = e^{-i pi/4}
+ * sqrt(2/dt) = (1-i)/sqrt(dt); leading coefficient c0 = c2 beta_0.
+ * Robin: Sv_n = -i p v_n, c0 = -ip, no history.               */
+/* ------------------------------------------------------------------ */
+static ocplx or_c2(const or_problem *P) {
+  /* e^{-i pi/4} sqrt(2/dt) = ((1-i)/sqrt 2) sqrt 2 / sqrt(dt), exactly. */
+  return (1.0 - I_) / sqrt(P->dt);
+}
+
+static ocplx or_c0(const or_problem *P) {
+  if (P->transmission == OR_TC_ROBIN) return -I_ * P->robin_p;
+  return or_c2(P) * 1.0; /* beta_0 = 1 */
+}
+
+/* Nodal W_n on subdomain j: W_n = (V_n + V_{n-1})/2. */
+static void or_local_W(const or_problem *P, int32_t j, int32_t n, int32_t fz,
+                       int32_t Nx, int32_t NT, int32_t Nj, double *W) {
+  int32_t m = Nx / P->N, g0 = (j - 1) * m;
+  for (int32_t k = 0; k < Nj; k++) W[k] = 0.0;
+  if (fz) return;
+  if (P->potential == OR_POT_VX) {
+    for (int32_t k = 0; k < Nj; k++) W[k] = P->V_x[g0 + k];
+  } else if (P->potential == OR_POT_VTX) {
+    for (int32_t t = 0; t < P->n_terms; t++) {
+      const double *tau = P->tau + (size_t)t * (NT + 1);
+      const double *xi = P->xi + (size_t)t * (Nx + 1);
+      double tb = 0.5 * (tau[n] + tau[n - 1]);
+      for (int32_t k = 0; k < Nj; k++) W[k] += tb * xi[g0 + k];
+    }
+  }
+}
+
+/* (A_{j,n} - B_{j,n}) of eq. (9):
+ * A = (2i/dt) M - S + M_{W_n}; B subtracts the leading coefficient c0 of
+ * the transmission operator on each interface row (derived from the weak
+ * form: the boundary term dn v = l - S v moves c0 v to the left side).
+ * The nonlinear matrix of eq. (12) is the same with W = 0. */
+int32_t or_subdomain_matrix(const or_problem *P, int32_t j, int32_t n, int32_t fz,
+                            ocplx *lo, ocplx *di, ocplx *up) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  double *W = (double *)malloc(sizeof(double) * Nj * 7);
+  if (!W) return OR_OOM;
+  double *Md = W + Nj, *Mo = Md + Nj, *Sd = Mo + Nj, *So = Sd + Nj, *Wd = So + Nj, *Wo = Wd + Nj;
+  or_local_W(P, j, n, fz, Nx, NT, Nj, W);
+  or_fem(Nj, P->dx, W, Md, Mo, Sd, So, Wd, Wo);
+  ocplx s = 2.0 * I_ / P->dt;
+  for (int32_t k = 0; k < Nj; k++) di[k] = s * Md[k] - Sd[k] + Wd[k];
+  for (int32_t k = 0; k + 1 < Nj; k++) {
+    ocplx off = s * Mo[k] - So[k] + Wo[k];
+    up[k] = off;
+    lo[k + 1] = off;
+  }
+  lo[0] = 0.0;
+  up[Nj - 1] = 0.0;
+  ocplx c0 = or_c0(P);
+  if (j >= 2) di[0] -= c0;
+  if (j <= P->N - 1) di[Nj - 1] -= c0;
+  free(W);
+  return OR_OK;
+}
+
+/* ------------------------------------------------------------------ */
+/* One whole-window march of subdomain j over n = 1..N_T.              */
+/* v-form of Crank-Nicolson: v_n = (u_n + u_{n-1})/2,      */
+/* v_0 = u_0, u_n = 2 v_n - u_{n-1}.  Local system eq. (9):    */
+/*   (A - B) v_n = (2i/dt) M u_{n-1} + b_n - Q^T (l_n, r_n)^T          */
+/* with the history vector b_n = H e_0 (+ H e_end), H = c2 sum_{s<n}   */
+/* beta_{n-s} v_s.  Outputs by eq. (8):         */
+/*   r_{j-1,n} = -l_{j,n} + 2 S v_{j,n}(a_j),                          */
+/*   l_{j+1,n} = -r_{j,n} + 2 S v_{j,n}(b_j).                          */
+/* Nonlinear f(u) = lambda|u|^2: per step the fixed point  */
+/*   (A_NL - B) z^{s+1} = (2i/dt) M u_{n-1} - M_{f(z^s)} z^s + b - Q^T(l,r)
+ * from z^0 = v_{n-1}, stopped by the relative max-norm test (A3, A4). */
+/* ------------------------------------------------------------------ */
+int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *rin,
+                 int32_t use_u0, int32_t fz, ocplx *out_left, ocplx *out_right,
+                 ocplx *uT, int32_t *fp_max) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  if (j < 1 || j > P->N) return OR_ERR_ARG;
+  int32_t N = P->N, m = Nx / N, g0 = (j - 1) * m;
+  int32_t has_left = (j >= 2), has_right = (j <= N - 1);
+  int32_t pot = fz ? OR_POT_ZERO : P->potential;
+  int32_t s02 = (P->transmission == OR_TC_S02);
+  size_t nb = (size_t)Nj;
+  ocplx *u = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *v = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *vprev = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *rhs = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *rhs2 = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *lo = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *di = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *up = (ocplx *)calloc(nb, sizeof(ocplx));
+  ocplx *va = (ocplx *)calloc((size_t)NT + 1, sizeof(ocplx));
+  ocplx *vb = (ocplx *)calloc((size_t)NT + 1, sizeof(ocplx));
+  double *beta = (double *)calloc((size_t)NT + 1, sizeof(double));
+  double *alpha = (double *)calloc((size_t)NT + 1, sizeof(double));
+  double *Md = (double *)calloc(nb, sizeof(double));
+  double *Mo = (double *)calloc(nb, sizeof(double));
+  double *Wz = (double *)calloc(nb, sizeof(double));
+  double *Wd = (double *)calloc(nb, sizeof(double));
+  double *Wo = (double *)calloc(nb, sizeof(double));
+  int32_t st = OR_OK;
+  if (!u || !v || !vprev || !rhs || !rhs2 || !lo || !di || !up || !va || !vb ||
+      !beta || !alpha || !Md || !Mo || !Wz || !Wd || !Wo) { st = OR_OOM; goto done; }
+
+  or_coeffs(NT + 1, alpha, beta, NULL);
+  or_fem(Nj, P->dx, NULL, Md, Mo, NULL, NULL, NULL, NULL);
+  ocplx c2 = or_c2(P), c0 = or_c0(P);
+  ocplx s2 = 2.0 * I_ / P->dt;
+  if (use_u0)
+    for (int32_t k = 0; k < Nj; k++) u[k] = P->u0[g0 + k];
+  for (int32_t k = 0; k < Nj; k++) vprev[k] = u[k];   /* v_0 = u_0 */
+  va[0] = u[0];
+  vb[0] = u[Nj - 1];
+  int32_t time_dep = (pot == OR_POT_VTX);
+  if (!time_dep) {
+    st = or_subdomain_matrix(P, j, 1, fz, lo, di, up);
+    if (st) goto done;
+  }
+  int32_t fpm = 0, fp_fail = 0;
+  for (int32_t n = 1; n <= NT; n++) {
+    if (time_dep) { st = or_subdomain_matrix(P, j, n, fz, lo, di, up); if (st) goto done; }
+    /* (2i/dt) M u_{n-1} */
+    for (int32_t k = 0; k < Nj; k++) {
+      ocplx mu = Md[k] * u[k];
+      if (k > 0) mu += Mo[k - 1] * u[k - 1];
+      if (k + 1 < Nj) mu += Mo[k] * u[k + 1];
+      rhs[k] = s2 * mu;
+    }
+    ocplx Ha = 0.0, Hb = 0.0;
+    if (s02) {
+      for (int32_t s = 0; s < n; s++) {
+        Ha += beta[n - s] * va[s];
+        Hb += beta[n - s] * vb[s];
+      }
+      Ha = c2 * Ha;
+      Hb = c2 * Hb;
+    }
+    if (has_left) rhs[0] += Ha - (lin ? lin[n - 1] : 0.0);
+    if (has_right) rhs[Nj - 1] += Hb - (rin ? rin[n - 1] : 0.0);
+    if (pot == OR_POT_CUBIC) {
+      /* zeta^0 = v_{n-1}; v holds the iterate. */
+      for (int32_t k = 0; k < Nj; k++) v[k] = vprev[k];
+      int32_t it, conv = 0;
+      for (it = 1; it <= P->maxit_fp; it++) {
+        for (int32_t k = 0; k < Nj; k++)
+          Wz[k] = P->lambda * (creal(v[k]) * creal(v[k]) + cimag(v[k]) * cimag(v[k]));
+        or_fem(Nj, P->dx, Wz, NULL, NULL, NULL, NULL, Wd, Wo);
+        for (int32_t k = 0; k < Nj; k++) {
+          ocplx bf = Wd[k] * v[k];
+          if (k > 0) bf += Wo[k - 1] * v[k - 1];
+          if (k + 1 < Nj) bf += Wo[k] * v[k + 1];
+          rhs2[k] = rhs[k] - bf;
+        }
+        st = or_thomas(Nj, lo, di, up, rhs2, rhs2);
+        if (st) goto done;
+        double dmax = 0.0, nmax = 0.0;
+        for (int32_t k = 0; k < Nj; k++) {
+          double dd = cabs(rhs2[k] - v[k]), nn = cabs(rhs2[k]);
+          if (dd > dmax) dmax = dd;
+          if (nn > nmax) nmax = nn;
+          v[k] = rhs2[k];
+        }
+        if (dmax <= P->tol_fp * nmax) { conv = 1; break; }
+      }
+      if (!conv) { it = P->maxit_fp; fp_fail = 1; }
+      if (it > fpm) fpm = it;
+    } else {
+      st = or_thomas(Nj, lo, di, up, rhs, v);
+      if (st) goto done;
+    }
+    for (int32_t k = 0; k < Nj; k++) {
+      u[k] = 2.0 * v[k] - u[k];
+      vprev[k] = v[k];
+    }
+    va[n] = v[0];
+    vb[n] = v[Nj - 1];
+    if (has_left && out_left) out_left[n - 1] = -(lin ? lin[n - 1] : 0.0) + 2.0 * (c0 * v[0] + Ha);
+    if (has_right && out_right) out_right[n - 1] = -(rin ? rin[n - 1] : 0.0) + 2.0 * (c0 * v[Nj - 1] + Hb);
+  }
+  if (uT) for (int32_t k = 0; k < Nj; k++) uT[k] = u[k];
+  if (fp_max && fpm > *fp_max) *fp_max = fpm;
+  if (fp_fail) st = OR_INNER_NOT_CONVERGED;
+done:
+  free(u); free(v); free(vprev); free(rhs); free(rhs2); free(lo); free(di); free(up);
+  free(va); free(vb); free(beta); free(alpha); free(Md); free(Mo); free(Wz); free(Wd); free(Wo);
+  return st;
+}
+
+/* Slot of l_j (j = 2..N) and r_j (j = 1..N-1) in g. */
+static int32_t slot_l(int32_t j) { return 2 * j - 3; }
+static int32_t slot_r(int32_t j) { return 2 * j - 2; }
+
+/* g -> R(g): every subdomain marches with its incoming fluxes from g and
+ * its outputs land in the neighbours' slots (eq. 13). */
+int32_t or_apply_R(const or_problem *P, const ocplx *g, int32_t use_u0, int32_t fz,
+                   ocplx *Rg, int32_t *fp_max) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  int32_t N = P->N;
+  size_t ng = (size_t)(2 * N - 2) * NT;
+  for (size_t i = 0; i < ng; i++) Rg[i] = 0.0;
+  int32_t st = OR_OK;
+  for (int32_t j = 1; j <= N; j++) {
+    const ocplx *lin = (j >= 2 && g) ? g + (size_t)slot_l(j) * NT : NULL;
+    const ocplx *rin = (j <= N - 1 && g) ? g + (size_t)slot_r(j) * NT : NULL;
+    ocplx *ol = (j >= 2) ? Rg + (size_t)slot_r(j - 1) * NT : NULL;
+    ocplx *orr = (j <= N - 1) ? Rg + (size_t)slot_l(j + 1) * NT : NULL;
+    int32_t s = or_march(P, j, lin, rin, use_u0, fz, ol, orr, NULL, fp_max);
+    if (s == OR_INNER_NOT_CONVERGED) st = s;
+    else if (s) return s;
+  }
+  return st;
+}
+
+/* Probing with u0 = 0 (reading A14): a unit impulse at n = 1 on
+ * l_j gives the first columns of X^{j,1} (out_left) and X^{j,3}
+ * (out_right); on r_j it gives X^{j,2} and X^{j,4}. */
+int32_t or_build_L(const or_problem *P, int32_t fz, ocplx *X) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  int32_t N = P->N;
+  memset(X, 0, sizeof(ocplx) * (size_t)N * 4 * NT);
+  ocplx *e = (ocplx *)calloc((size_t)NT, sizeof(ocplx));
+  if (!e) return OR_OOM;
+  e[0] = 1.0;
+  int32_t st = OR_OK;
+  for (int32_t j = 1; j <= N && !st; j++) {
+    ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+    if (j >= 2) st = or_march(P, j, e, NULL, 0, fz, X1, (j <= N - 1) ? X3 : NULL, NULL, NULL);
+    if (!st && j <= N - 1) st = or_march(P, j, NULL, e, 0, fz, (j >= 2) ? X2 : NULL, X4, NULL, NULL);
+  }
+  free(e);
+  return st;
+}
+
+/* Causal convolution (x * y)_n = sum_{s<=n} x_{n-s} y_s: the action of a
+ * lower-triangular Toeplitz block whose first column is x (Props. 3-4,
+ * P:549-707). */
+static void conv_add(int32_t NT, const ocplx *x, const ocplx *y, ocplx *out) {
+  for (int32_t n = 0; n < NT; n++) {
+    ocplx acc = 0.0;
+    for (int32_t s = 0; s <= n; s++) acc += x[n - s] * y[s];
+    out[n] += acc;
+  }
+}
+
+/* Lg with the block pattern of eq. (15)/(16). */
+void or_apply_L(const or_problem *P, const ocplx *X, const ocplx *g, ocplx *Lg) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return;
+  int32_t N = P->N;
+  memset(Lg, 0, sizeof(ocplx) * (size_t)(2 * N - 2) * NT);
+  for (int32_t j = 1; j <= N; j++) {
+    const ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+    if (j >= 2) { /* r_{j-1}^{k+1} = X^{j,1} l_j + X^{j,2} r_j */
+      ocplx *out = Lg + (size_t)slot_r(j - 1) * NT;
+      conv_add(NT, X1, g + (size_t)slot_l(j) * NT, out);
+      if (j <= N - 1) conv_add(NT, X2, g + (size_t)slot_r(j) * NT, out);
+    }
+    if (j <= N - 1) { /* l_{j+1}^{k+1} = X^{j,3} l_j + X^{j,4} r_j */
+      ocplx *out = Lg + (size_t)slot_l(j + 1) * NT;
+      if (j >= 2) conv_add(NT, X3, g + (size_t)slot_l(j) * NT, out);
+      conv_add(NT, X4, g + (size_t)slot_r(j) * NT, out);
+    }
+  }
+}
+
+/* Order-fixed inner product <x, y> = sum conj(x) y: one partial per
+ * subdomain over the slots it owns (l_j, r_j), partials summed in
+ * subdomain order. */
+ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return 0.0;
+  int32_t N = P->N;
+  ocplx total = 0.0;
+  for (int32_t j = 1; j <= N; j++) {
+    ocplx part = 0.0;
+    int32_t s_lo = (j >= 2) ? slot_l(j) : slot_r(j);
+    int32_t s_hi = (j <= N - 1) ? slot_r(j) : slot_l(j);
+    for (size_t i = (size_t)s_lo * NT; i < (size_t)(s_hi + 1) * NT; i++) part += conj(x[i]) * y[i];
+    total += part;
+  }
+  return total;
+}
+
+/* ------------------------------------------------------------------ */
+/* GMRES(m) with two passes of classical Gram-Schmidt (reading A6) and */
+/* complex Givens rotations; stop when the residual estimate           */
+/* |gamma_{k+1}| <= tol ||b||_2 (A5); true residual at each restart.    */
+/* ------------------------------------------------------------------ */
+typedef int32_t (*or_opfn)(void *ctx, const ocplx *x, ocplx *y);
+typedef ocplx (*or_dotfn)(const void *ctx, const ocplx *x, const ocplx *y);
+
+static double vnorm(or_dotfn dot, const void *dctx, const ocplx *x) { return sqrt(creal(dot(dctx, x, x))); }
+
+static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const void *dctx,
+                          const ocplx *b, ocplx *x, double tol, int32_t m, int32_t maxit,
+                          int32_t *iters, double *hist, int32_t *converged) {
+  *iters = 0;
+  *converged = 0;
+  double bnorm = vnorm(dot, dctx, b);
+  if (bnorm == 0.0) {
+    for (size_t i = 0; i < n; i++) x[i] = 0.0;
+    *converged = 1;
+    return OR_OK;
+  }
+  ocplx *V = (ocplx *)calloc((size_t)(m + 1) * n, sizeof(ocplx));
+  ocplx *H = (ocplx *)calloc((size_t)(m + 1) * m, sizeof(ocplx));
+  ocplx *sn = (ocplx *)calloc((size_t)m, sizeof(ocplx));
+  double *cs = (double *)calloc((size_t)m, sizeof(double));
+  ocplx *gam = (ocplx *)calloc((size_t)m + 1, sizeof(ocplx));
+  ocplx *hc = (ocplx *)calloc((size_t)m + 1, sizeof(ocplx));
+  ocplx *y = (ocplx *)calloc((size_t)m, sizeof(ocplx));
+  ocplx *w = (ocplx *)calloc(n, sizeof(ocplx));
+  int32_t st = OR_OK;
+  if (!V || !H || !sn || !cs || !gam || !hc || !y || !w) { st = OR_OOM; goto out; }
+#define Hm(i, k) H[(size_t)(i) * m + (k)]
+  int32_t total = 0, done = 0;
+  while (!done) {
+    st = A(actx, x, w);
+    if (st && st != OR_INNER_NOT_CONVERGED) goto out;
+    for (size_t i = 0; i < n; i++) V[i] = b[i] - w[i];
+    double beta = vnorm(dot, dctx, V);
+    if (beta <= tol * bnorm) { *converged = 1; break; }
+    if (total >= maxit) break;
+    for (size_t i = 0; i < n; i++) V[i] = V[i] / beta;
+    for (int32_t i = 0; i <= m; i++) gam[i] = 0.0;
+    gam[0] = beta;
+    int32_t k, kend = 0;
+    for (k = 0; k < m; k++) {
+      ocplx *vk = V + (size_t)k * n, *vk1 = V + (size_t)(k + 1) * n;
+      int32_t s = A(actx, vk, w);
+      if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+      if (s) st = s;
+      total++;
+      double wn0 = vnorm(dot, dctx, w);
+      for (int32_t i = 0; i <= k; i++) Hm(i, k) = 0.0;
+      for (int pass = 0; pass < 2; pass++) {        /* CGS2 */
+        for (int32_t i = 0; i <= k; i++) hc[i] = dot(dctx, V + (size_t)i * n, w);
+        for (int32_t i = 0; i <= k; i++) {
+          const ocplx *vi = V + (size_t)i * n;
+          for (size_t q = 0; q < n; q++) w[q] -= hc[i] * vi[q];
+          Hm(i, k) += hc[i];
+        }
+      }
+      double hk1 = vnorm(dot, dctx, w);
+      int32_t breakdown = (hk1 <= 1e-14 * wn0);
+      if (!breakdown) for (size_t q = 0; q < n; q++) vk1[q] = w[q] / hk1;
+      for (int32_t i = 0; i < k; i++) {             /* previous rotations */
+        ocplx t = cs[i] * Hm(i, k) + sn[i] * Hm(i + 1, k);
+        Hm(i + 1, k) = -conj(sn[i]) * Hm(i, k) + cs[i] * Hm(i + 1, k);
+        Hm(i, k) = t;
+      }
+      ocplx a = Hm(k, k);
+      double aa = cabs(a);
+      if (aa == 0.0) { cs[k] = 0.0; sn[k] = 1.0; Hm(k, k) = hk1; }
+      else {
+        double den = sqrt(aa * aa + hk1 * hk1);
+        cs[k] = aa / den;
+        sn[k] = (a / aa) * hk1 / den;
+        Hm(k, k) = (a / aa) * den;
+      }
+      gam[k + 1] = -conj(sn[k]) * gam[k];
+      gam[k] = cs[k] * gam[k];
+      double res = cabs(gam[k + 1]);
+      if (hist) hist[total - 1] = res;
+      kend = k + 1;
+      if (res <= tol * bnorm || breakdown) { *converged = 1; done = 1; break; }
+      if (total >= maxit) { done = 1; break; }
+    }
+    /* y = H^{-1} gamma (upper triangular), x += V y */
+    for (int32_t i = kend - 1; i >= 0; i--) {
+      ocplx acc = gam[i];
+      for (int32_t q = i + 1; q < kend; q++) acc -= Hm(i, q) * y[q];
+      y[i] = acc / Hm(i, i);
+    }
+    for (int32_t i = 0; i < kend; i++) {
+      const ocplx *vi = V + (size_t)i * n;
+      for (size_t q = 0; q < n; q++) x[q] += y[i] * vi[q];
+    }
+  }
+#undef Hm
+  *iters = total;
+out:
+  free(V); free(H); free(sn); free(cs); free(gam); free(hc); free(y); free(w);
+  return st;
+}
+
+/* Dense GMRES (test pin of the Krylov driver). */
+typedef struct { int32_t n; const ocplx *A; } dense_ctx;
+static int32_t dense_op(void *c, const ocplx *x, ocplx *y) {
+  dense_ctx *d = (dense_ctx *)c;
+  for (int32_t i = 0; i < d->n; i++) {
+    ocplx acc = 0.0;
+    for (int32_t k = 0; k < d->n; k++) acc += d->A[(size_t)i * d->n + k] * x[k];
+    y[i] = acc;
+  }
+  return OR_OK;
+}
+typedef struct { size_t n; } seq_ctx;
+static ocplx seq_dot(const void *c, const ocplx *x, const ocplx *y) {
+  const seq_ctx *s = (const seq_ctx *)c;
+  ocplx acc = 0.0;
+  for (size_t i = 0; i < s->n; i++) acc += conj(x[i]) * y[i];
+  return acc;
+}
+int32_t or_gmres_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x, double tol,
+                       int32_t restart, int32_t maxit, int32_t *iters, double *hist) {
+  dense_ctx d = {n, A};
+  seq_ctx s = {(size_t)n};
+  int32_t conv = 0;
+  int32_t st = gmres_core((size_t)n, dense_op, &d, seq_dot, &s, b, x, tol, restart, maxit, iters, hist, &conv);
+  if (st) return st;
+  return conv ? OR_OK : OR_NOT_CONVERGED;
+}
+
+/* ------------------------------------------------------------------ */
+/* Algorithm drivers.                                                  */
+/* ------------------------------------------------------------------ */
+typedef struct {
+  const or_problem *P;
+  const ocplx *X;       /* Toeplitz first columns (L or L0) */
+  ocplx *tmp, *tmp2;    /* scratch of n_g */
+  size_t ng;
+  int32_t inner_total;
+  int32_t inner_fail;
+  int32_t fp_max;
+} drv_ctx;
+
+static ocplx drv_dot(const void *c, const ocplx *x, const ocplx *y) { return or_dot(((const drv_ctx *)c)->P, x, y); }
+
+/* y = (I - L) x (Algorithm 3 step 2, eq. 14). */
+static int32_t op_I_minus_L(void *c, const ocplx *x, ocplx *y) {
+  drv_ctx *d = (drv_ctx *)c;
+  or_apply_L(d->P, d->X, x, y);
+  for (size_t i = 0; i < d->ng; i++) y[i] = x[i] - y[i];
+  return OR_OK;
+}
+
+/* x = P^{-1} y: GMRES on (I - L0) x = y from x = 0 (eq. Pxg, P:1054-1059,
+ * reading A8). */
+static int32_t apply_Pinv(drv_ctx *d, const ocplx *y, ocplx *x) {
+  for (size_t i = 0; i < d->ng; i++) x[i] = 0.0;
+  int32_t it = 0, conv = 0;
+  int32_t st = gmres_core(d->ng, op_I_minus_L, d, drv_dot, d, y, x, d->P->tol_inner,
+                          d->P->restart, d->P->maxit_inner, &it, NULL, &conv);
+  d->inner_total += it;
+  if (!conv) d->inner_fail = 1;
+  return st;
+}
+
+/* y = P^{-1} (x - R_0(x)), R_0(x) = R(x; u0 = 0) with the true potential
+ * (eq. chp2_algopd_Lpf, readings A7, A10). */
+static int32_t op_precond(void *c, const ocplx *x, ocplx *y) {
+  drv_ctx *d = (drv_ctx *)c;
+  int32_t st = or_apply_R(d->P, x, 0, 0, d->tmp, &d->fp_max);
+  if (st) return st;
+  for (size_t i = 0; i < d->ng; i++) d->tmp[i] = x[i] - d->tmp[i];
+  return apply_Pinv(d, d->tmp, y);
+}
+
+/* Final sweep + assembly of u(T) on the global mesh; each duplicated
+ * interface node is the average of its two copies (reading A16). */
+static int32_t final_march(const or_problem *P, const ocplx *g, ocplx *uT, int32_t *fp_max) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  int32_t N = P->N, m = Nx / N;
+  ocplx *loc = (ocplx *)calloc((size_t)Nj, sizeof(ocplx));
+  ocplx *sum = (ocplx *)calloc((size_t)Nx + 1, sizeof(ocplx));
+  int *cnt = (int *)calloc((size_t)Nx + 1, sizeof(int));
+  int32_t st = OR_OK;
+  if (!loc || !sum || !cnt) { st = OR_OOM; goto out; }
+  for (int32_t j = 1; j <= N; j++) {
+    const ocplx *lin = (j >= 2 && g) ? g + (size_t)slot_l(j) * NT : NULL;
+    const ocplx *rin = (j <= N - 1 && g) ? g + (size_t)slot_r(j) * NT : NULL;
+    int32_t s = or_march(P, j, lin, rin, 1, 0, NULL, NULL, loc, fp_max);
+    if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+    if (s) st = s;
+    for (int32_t k = 0; k < Nj; k++) { sum[(size_t)(j - 1) * m + k] += loc[k]; cnt[(size_t)(j - 1) * m + k]++; }
+  }
+  for (int32_t i = 0; i <= Nx; i++) uT[i] = sum[i] / (double)cnt[i];
+out:
+  free(loc); free(sum); free(cnt);
+  return st;
+}
+
+int32_t or_monodomain(const or_problem *P, ocplx *uT, int32_t *fp_max) {
+  or_problem Q = *P;
+  Q.N = 1;
+  return or_march(&Q, 1, NULL, NULL, 1, 0, NULL, NULL, uT, fp_max);
+}
+
+int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  if (P->transmission == OR_TC_ROBIN && !(P->robin_p > 0)) return OR_ERR_ARG;
+  int32_t N = P->N;
+  or_report dummy;
+  if (!rep) rep = &dummy;
+  rep->iterations = 0; rep->inner_iterations = 0; rep->fp_max = 0; rep->converged = 1; rep->n_history = 0;
+  if (N == 1) return or_monodomain(P, uT, &rep->fp_max);
+  int32_t linear = (P->potential != OR_POT_CUBIC);
+  if (P->algorithm == OR_ALG_NEW && !(P->potential == OR_POT_ZERO || P->potential == OR_POT_VX))
+    return OR_UNSUPPORTED;
+  size_t ng = (size_t)(2 * N - 2) * NT;
+  drv_ctx d;
+  memset(&d, 0, sizeof d);
+  d.P = P; d.ng = ng;
+  ocplx *X = (ocplx *)calloc((size_t)N * 4 * NT, sizeof(ocplx));
+  ocplx *g = (ocplx *)calloc(ng, sizeof(ocplx));
+  ocplx *rhs = (ocplx *)calloc(ng, sizeof(ocplx));
+  d.tmp = (ocplx *)calloc(ng, sizeof(ocplx));
+  d.tmp2 = (ocplx *)calloc(ng, sizeof(ocplx));
+  int32_t st = OR_OK, conv = 0, it = 0;
+  if (!X || !g || !rhs || !d.tmp || !d.tmp2) { st = OR_OOM; goto out; }
+  d.X = X;
+  if (P->g0) memcpy(g, P->g0, sizeof(ocplx) * ng);
+  if (P->algorithm == OR_ALG_NEW) {
+    /* Algorithm 3: build d = R(0) and L,
+     * solve (I - L) g = d, final sweep. */
+    st = or_apply_R(P, NULL, 1, 0, rhs, &d.fp_max);
+    if (st) goto out;
+    st = or_build_L(P, 0, X);
+    if (st) goto out;
+    st = gmres_core(ng, op_I_minus_L, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit,
+                    &it, rep->history, &conv);
+    if (st) goto out;
+    rep->n_history = it;
+  } else if (linear) {
+    /* Preconditioned GMRES for V(t,x). */
+    st = or_build_L(P, 1, X);                       /* L0: V = 0 probes */
+    if (st) goto out;
+    st = or_apply_R(P, NULL, 1, 0, d.tmp2, &d.fp_max); /* d = R(0; u0) */
+    if (st) goto out;
+    st = apply_Pinv(&d, d.tmp2, rhs);               /* P^{-1} d */
+    if (st && st != OR_INNER_NOT_CONVERGED) goto out;
+    st = gmres_core(ng, op_precond, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit,
+                    &it, rep->history, &conv);
+    if (st && st != OR_INNER_NOT_CONVERGED) goto out;
+    rep->n_history = it;
+  } else {
+    /* Preconditioned fixed point for f(u) (eq. chp2_algopd_NL, reading A9):
+     * g^{k+1} = g^k - P^{-1}(g^k - R_nl(g^k)), stop ||g^{k+1}-g^k||_2 < tol. */
+    st = or_build_L(P, 1, X);
+    if (st) goto out;
+    while (it < P->maxit) {
+      int32_t s = or_apply_R(P, g, 1, 0, d.tmp, &d.fp_max);
+      if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+      for (size_t i = 0; i < ng; i++) d.tmp[i] = g[i] - d.tmp[i];
+      s = apply_Pinv(&d, d.tmp, d.tmp2);
+      if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+      for (size_t i = 0; i < ng; i++) g[i] = g[i] - d.tmp2[i];
+      double diff = sqrt(creal(or_dot(P, d.tmp2, d.tmp2)));
+      if (rep->history) rep->history[it] = diff;
+      it++;
+      if (diff < P->tol) { conv = 1; break; }
+    }
+    rep->n_history = it;
+    st = OR_OK;
+  }
+  rep->iterations = it;
+  rep->inner_iterations = d.inner_total;
+  rep->converged = conv;
+  {
+    int32_t s = final_march(P, g, uT, &d.fp_max);
+    if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+  }
+  rep->fp_max = d.fp_max;
+  if (g_out) memcpy(g_out, g, sizeof(ocplx) * ng);
+  if (!conv) st = OR_NOT_CONVERGED;
+  else if (d.inner_fail) st = OR_INNER_NOT_CONVERGED;
+out:
+  free(X); free(g); free(rhs); free(d.tmp); free(d.tmp2);
+  return st;
+}

@@ -1,0 +1,119 @@
+/*
+ * oracle/swr_oracle.h — TEST INFRASTRUCTURE ONLY (parity oracle).
+ *
+ * Plain, slow, single-threaded CPU implementation of the Schwarz waveform
+ * relaxation (SWR) method of Besse & Xing, arXiv:1503.02564.
+ * Only tests/, __graft_entry__.smoke() and bench.py's cpu_baseline /
+ * --impl reference leg may load it.  It shares no code, header or constant
+ * with the CUDA product path (paper_1503_02564_b200/), and neither imports
+ * the other.
+ *
+ * Conventions: complex arrays are C99 `double complex` (interleaved re,im);
+ * subdomains are 1-based j = 1..N as in the paper; time steps n = 1..N_T are
+ * stored at index n-1; the interface vector g is slot-major
+ * (r_1, l_2, r_2, ..., l_{N-1}, r_{N-1}, l_N), each slot N_T long.
+ */
+#ifndef SWR_ORACLE_H
+#define SWR_ORACLE_H
+#include <complex.h>
+#include <stdint.h>
+
+typedef double complex ocplx;
+
+enum { OR_OK = 0, OR_ERR_ARG = 1, OR_NOT_CONVERGED = 2, OR_ZERO_PIVOT = 3,
+       OR_BREAKDOWN = 4, OR_INNER_NOT_CONVERGED = 5, OR_UNSUPPORTED = 6,
+       OR_OOM = 9 };
+enum { OR_POT_ZERO = 0, OR_POT_VX = 1, OR_POT_VTX = 2, OR_POT_CUBIC = 3 };
+enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1 };
+enum { OR_ALG_NEW = 0, OR_ALG_PRECOND = 1 };
+
+typedef struct {
+  double a0, b0, T, dx, dt;   /* domain (a0,b0), final time, mesh, time step */
+  int32_t N;                  /* number of subdomains */
+  int32_t potential;          /* OR_POT_* */
+  const double *V_x;          /* [N_x+1] nodal V(x_i) for OR_POT_VX */
+  int32_t n_terms;            /* V(t,x) = sum_k tau_k(t) xi_k(x) for OR_POT_VTX */
+  const double *tau;          /* [n_terms][N_T+1], tau_k(t_n) */
+  const double *xi;           /* [n_terms][N_x+1], xi_k(x_i) */
+  double lambda;              /* f(u) = lambda |u|^2 for OR_POT_CUBIC (paper: 1) */
+  int32_t transmission;       /* OR_TC_* */
+  double robin_p;             /* p > 0 for Robin */
+  const ocplx *u0;            /* [N_x+1] initial datum at the nodes */
+  int32_t algorithm;          /* OR_ALG_* */
+  double tol; int32_t restart, maxit;            /* outer: 1e-10, 30, 2000 */
+  double tol_inner; int32_t maxit_inner;         /* P^{-1} inner GMRES: 1e-12, 2000 */
+  double tol_fp; int32_t maxit_fp;               /* NL inner fixed point: 1e-12, 50 */
+  const ocplx *g0;            /* [(2N-2) N_T] initial interface vector, NULL = zero */
+} or_problem;
+
+typedef struct {
+  int32_t iterations;         /* outer Arnoldi steps (GMRES) or Richardson steps */
+  int32_t inner_iterations;   /* total inner GMRES steps (P^{-1}) */
+  int32_t fp_max;             /* max NL fixed-point iterations in any step */
+  int32_t converged;
+  int32_t n_history;
+  double *history;            /* caller-provided, capacity maxit+1 (may be NULL) */
+} or_report;
+
+/* alpha, beta, gamma sequences, n entries each. */
+void or_coeffs(int32_t n, double *alpha, double *beta, double *gamma);
+
+/* Mesh / partition sizes. */
+int32_t or_sizes(const or_problem *P, int32_t *Nx, int32_t *NT, int32_t *Nj);
+
+/* P1 FEM matrices on a uniform mesh of nn nodes, spacing h, nodal weight W
+ * (NULL = 0): M, S, M_W as (diag[nn], off[nn-1]). */
+void or_fem(int32_t nn, double h, const double *W, double *Mdiag, double *Moff,
+            double *Sdiag, double *Soff, double *MWdiag, double *MWoff);
+
+/* Thomas algorithm without pivoting; lo[0] and up[n-1] unused.
+ * Returns OR_ZERO_PIVOT if a pivot has modulus < 1e-300. */
+int32_t or_thomas(int32_t n, const ocplx *lo, const ocplx *di, const ocplx *up,
+                  const ocplx *rhs, ocplx *x);
+
+/* Tridiagonal of (A_{j,n} - B_{j,n}) for subdomain j at step n. */
+int32_t or_subdomain_matrix(const or_problem *P, int32_t j, int32_t n,
+                            int32_t force_zero_potential,
+                            ocplx *lo, ocplx *di, ocplx *up);
+
+/* One whole-window march of subdomain j.
+ * lin/rin: flux series l_{j,n}, r_{j,n} (length N_T, NULL = 0).
+ * use_u0: start from u0 restricted to the subdomain (else 0).
+ * force_zero_potential: march with V == 0 (the L_0 / preconditioner problem).
+ * out_left:  r_{j-1,n}^{new} = -l_{j,n} + 2 S v_{j,n}(a_j)   (j >= 2)
+ * out_right: l_{j+1,n}^{new} = -r_{j,n} + 2 S v_{j,n}(b_j)   (j <= N-1)
+ * uT: [N_j] local u_{N_T} (NULL allowed).  fp_max: max NL FP iterations. */
+int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *rin,
+                 int32_t use_u0, int32_t force_zero_potential,
+                 ocplx *out_left, ocplx *out_right, ocplx *uT, int32_t *fp_max);
+
+/* g -> R(g) (eq. 13): one sweep of every subdomain + exchange. */
+int32_t or_apply_R(const or_problem *P, const ocplx *g, int32_t use_u0,
+                   int32_t force_zero_potential, ocplx *Rg, int32_t *fp_max);
+
+/* First columns of the Toeplitz blocks by unit-impulse probing
+ * with u0 = 0.  X is [N][4][N_T]: X[(j-1)*4 + (p-1)] = first column of X^{j,p}
+ * (only X^{1,4}, X^{j,1..4} (1<j<N), X^{N,1} are meaningful). */
+int32_t or_build_L(const or_problem *P, int32_t force_zero_potential, ocplx *X);
+
+/* Lg with the block pattern of eq. (15) and causal convolutions. */
+void or_apply_L(const or_problem *P, const ocplx *X, const ocplx *g, ocplx *Lg);
+
+/* Order-fixed inner product over the interface vector: partial per
+ * subdomain (its own slots, sequential), partials summed in j order. */
+ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y);
+
+/* GMRES(m) with CGS2 on a dense n x n matrix (row-major); dot is plain
+ * sequential.  Used by tests to pin the Krylov driver. */
+int32_t or_gmres_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x,
+                       double tol, int32_t restart, int32_t maxit,
+                       int32_t *iters, double *hist);
+
+/* Full algorithm (NEW / PRECOND / NL Richardson) -> u(T) on [N_x+1]. */
+int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep,
+                 ocplx *g_out /* [(2N-2)N_T] or NULL */);
+
+/* Single-domain reference solve (N = 1, Neumann both ends). */
+int32_t or_monodomain(const or_problem *P, ocplx *uT, int32_t *fp_max);
+
+#endif

@@ -1,0 +1,335 @@
+"""Pins of the CPU oracle against what the paper and the mathematics fix.
+
+Each test checks an oracle function against something other than itself:
+closed forms, the paper's printed values (tests/golden/), dense brute force
+on tiny grids, exact invariants, or a textbook routine (numpy LAPACK).
+These run with -m "not gpu".
+"""
+import math
+import os
+from fractions import Fraction
+
+import numpy as np
+import pytest
+
+import swr_inputs as si
+
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _tiny(**over):
+    """A tiny problem (brute-force sized): (-3,3), 12 cells, 6 steps."""
+    base = dict(a0=-3.0, b0=3.0, T=0.06, dx=0.5, dt=0.01, N=3, potential=si.POT_VX,
+                transmission=si.TC_S02, algorithm=si.ALG_NEW, vx_kind="-x2", u0_kind="gaussian")
+    base.update(over)
+    return si.Problem(**base)
+
+
+def _tiny_inputs(p):
+    d = si.inputs(p)
+    # a Gaussian centred in this small domain (x0 = 0 instead of -10)
+    x = p.nodes()
+    d["u0"] = np.exp(-(x * x) + 2j * x)
+    return d
+
+
+# ---------------------------------------------------------------- coefficients
+def test_coeffs_match_paper_prefix(oracle_mod):
+    """alpha, beta, gamma against the values printed at P:225-227."""
+    rows = [l.split() for l in open(os.path.join(GOLDEN, "coeffs_P225.txt")) if l[0] != "#"]
+    a, b, g = oracle_mod.coeffs(8)
+    for r in rows:
+        s = int(r[0])
+        num, den = map(int, r[1].split("/"))
+        assert a[s] == num / den
+        assert b[s] == (-1) ** s * num / den
+        if len(r) > 2:
+            assert g[s] == int(r[2])
+
+
+def test_coeffs_closed_form(oracle_mod):
+    """alpha_{2k} = alpha_{2k+1} = C(2k,k)/4^k, the Taylor coefficients of
+    (1-z^2)^{-1/2}; beta(z) = sqrt((1-z)/(1+z)) = (1-z)(1-z^2)^{-1/2}."""
+    n = 600
+    a, b, _ = oracle_mod.coeffs(n)
+    for s in range(n):
+        k = s // 2
+        exact = Fraction(math.comb(2 * k, k), 4 ** k)
+        assert abs(a[s] - float(exact)) <= 2e-16 * float(exact) * (1 + s / 8)
+    # generating function of beta, evaluated by the truncated series at z=0.3
+    z = 0.3
+    series = sum(b[s] * z ** s for s in range(n))
+    assert abs(series - math.sqrt((1 - z) / (1 + z))) < 1e-14
+
+
+# ---------------------------------------------------------------- FEM
+def test_fem_examples_and_invariants(oracle_mod):
+    Md, Mo, Sd, So, Wd, Wo = oracle_mod.fem(2, 1.0)
+    assert np.allclose(Md, [1 / 3, 1 / 3], rtol=0, atol=1e-16) and np.allclose(Mo, [1 / 6])
+    Md, Mo, Sd, So, Wd, Wo = oracle_mod.fem(3, 1.0)
+    assert np.allclose(Md, [1 / 3, 2 / 3, 1 / 3], atol=1e-16) and np.allclose(Sd, [1, 2, 1]) and np.allclose(So, [-1, -1])
+    rng = np.random.default_rng(0)
+    nn, h = 17, 0.37
+    Md, Mo, Sd, So, _, _ = oracle_mod.fem(nn, h)
+    M = np.diag(Md) + np.diag(Mo, 1) + np.diag(Mo, -1)
+    S = np.diag(Sd) + np.diag(So, 1) + np.diag(So, -1)
+    assert abs(M.sum() - (nn - 1) * h) < 1e-13            # partition of unity
+    assert np.abs(S @ np.ones(nn)).max() < 1e-12          # constants in the kernel
+    _, _, _, _, Wd1, Wo1 = oracle_mod.fem(nn, h, np.ones(nn))
+    assert np.allclose(Wd1, Md, rtol=1e-15) and np.allclose(Wo1, Mo, rtol=1e-15)
+    # weighted mass = exact integral of (linear interpolant of W) phi_k phi_l,
+    # checked by 5-point Gauss-Legendre quadrature on every element
+    W = rng.standard_normal(nn)
+    _, _, _, _, Wd, Wo = oracle_mod.fem(nn, h, W)
+    gx, gw = np.polynomial.legendre.leggauss(5)
+    t, wq = (gx + 1) / 2, gw / 2 * h
+    Q = np.zeros((nn, nn))
+    for e in range(nn - 1):
+        phi = np.stack([1 - t, t])
+        w_lin = W[e] * (1 - t) + W[e + 1] * t
+        for p_ in range(2):
+            for q in range(2):
+                Q[e + p_, e + q] += np.sum(wq * w_lin * phi[p_] * phi[q])
+    assert np.allclose(np.diag(Q), Wd, rtol=0, atol=1e-14)
+    assert np.allclose(np.diag(Q, 1), Wo, rtol=0, atol=1e-14)
+
+
+# ---------------------------------------------------------------- Thomas
+def test_thomas_vs_lapack(oracle_mod):
+    st, x = oracle_mod.thomas(np.zeros(2), np.ones(2), np.zeros(2), np.array([1 + 2j, 3]))
+    assert st == 0 and np.array_equal(x, [1 + 2j, 3])
+    st, x = oracle_mod.thomas(np.zeros(3), 2 * np.ones(3), np.zeros(3), np.array([2, 4, 6.0]))
+    assert np.array_equal(x, [1, 2, 3])
+    rng = np.random.default_rng(1)
+    for n in (8, 33, 64):
+        lo, up = (rng.standard_normal(n) + 1j * rng.standard_normal(n) for _ in range(2))
+        di = 4 + rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        lo[0] = up[-1] = 0
+        A = np.diag(di) + np.diag(up[:-1], 1) + np.diag(lo[1:], -1)
+        b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+        st, x = oracle_mod.thomas(lo, di, up, b)
+        assert st == 0
+        assert np.linalg.norm(x - np.linalg.solve(A, b)) <= 1e-13 * np.linalg.norm(x)
+    st, _ = oracle_mod.thomas(np.zeros(2), np.array([0.0, 1.0]), np.zeros(2), np.ones(2))
+    assert st == 3  # zero pivot
+
+
+# ---------------------------------------------------------------- GMRES driver
+def test_gmres_dense(oracle_mod):
+    b = np.array([1, 2, 3], np.complex128)
+    st, x, it, _ = oracle_mod.gmres_dense(np.eye(3), b)
+    assert st == 0 and it == 1 and np.allclose(x, b, rtol=1e-15)
+    st, x, it, _ = oracle_mod.gmres_dense(np.diag([1.0, 2, 3]), b)
+    assert st == 0 and np.allclose(x, 1, rtol=1e-10)
+    rng = np.random.default_rng(2)
+    A = np.eye(40) * 3 + (rng.standard_normal((40, 40)) + 1j * rng.standard_normal((40, 40))) / 8
+    b = rng.standard_normal(40) + 1j * rng.standard_normal(40)
+    st, x, it, hist = oracle_mod.gmres_dense(A, b, tol=1e-12, restart=7)
+    xs = np.linalg.solve(A, b)
+    assert st == 0 and np.linalg.norm(x - xs) < 1e-10 * np.linalg.norm(xs)
+    assert np.linalg.norm(b - A @ x) <= 1.01e-12 * np.linalg.norm(b) * 10
+    assert len(hist) == it and hist[-1] <= 1e-12 * np.linalg.norm(b)
+
+
+# ---------------------------------------------------------------- monodomain
+@pytest.mark.parametrize("pot", [si.POT_ZERO, si.POT_VX, si.POT_VTX])
+def test_monodomain_mass_conservation(oracle_mod, pot):
+    """CN with a real potential conserves u^* M u exactly (A Hermitian part
+    vanishes): drift <= 1e-12 relative over the whole window."""
+    p = si.Problem(a0=-15, b0=5, T=0.05, dx=0.01, dt=1e-3, N=1, potential=pot)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    st, uT, _ = o.monodomain()
+    assert st == 0
+    Md, Mo, *_ = oracle_mod.fem(p.Nx + 1, p.dx)
+    mass = lambda u: np.real(np.vdot(u, Md * u + np.r_[Mo * u[1:], 0] + np.r_[0, Mo * u[:-1]]))
+    u0 = si.make_u0(p)
+    assert abs(mass(uT) - mass(u0)) <= 1e-12 * mass(u0)
+
+
+def test_monodomain_nl_mass_conservation(oracle_mod):
+    """Duran-Sanz-Serna with the symmetric load M_{|z|^2} z (reading A3)
+    conserves the discrete mass up to the fixed-point tolerance."""
+    p = si.Problem(a0=-15, b0=5, T=0.05, dx=0.01, dt=1e-3, N=1, potential=si.POT_CUBIC,
+                   u0_kind="soliton")
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    st, uT, fp = o.monodomain()
+    assert st == 0 and 1 <= fp <= 50
+    Md, Mo, *_ = oracle_mod.fem(p.Nx + 1, p.dx)
+    mass = lambda u: np.real(np.vdot(u, Md * u + np.r_[Mo * u[1:], 0] + np.r_[0, Mo * u[:-1]]))
+    u0 = si.make_u0(p)
+    assert abs(mass(uT) - mass(u0)) <= 1e-11 * mass(u0)
+
+
+def _gauss_exact(x, t, x0=-10.0, k=20.0):
+    """Free Schrodinger (i u_t + u_xx = 0) from exp(-y^2 + i k y), y = x-x0."""
+    y = x - x0
+    z = 1 + 4j * t
+    return z ** -0.5 * np.exp((-(y * y) + 1j * k * y - 1j * k * k * t) / z)
+
+
+def test_gaussian_closed_form_order(oracle_mod):
+    """V = 0: error vs the closed-form Gaussian decreases at order >= 1.9
+    along the refinement ladder (CN in time, P1 in space) before the packet
+    reaches the Neumann ends."""
+    errs = []
+    for f in (1, 2, 4):
+        p = si.Problem(a0=-16, b0=4, T=0.02, dx=4e-3 / f, dt=4e-4 / f, N=1, potential=si.POT_ZERO)
+        o = oracle_mod.Oracle(p, si.inputs(p))
+        st, uT, _ = o.monodomain()
+        ex = _gauss_exact(p.nodes(), p.T)
+        errs.append(np.linalg.norm(uT - ex) / np.linalg.norm(ex))
+    orders = [math.log2(errs[i] / errs[i + 1]) for i in range(2)]
+    assert all(o_ >= 1.9 for o_ in orders), (errs, orders)
+    assert errs[-1] < 2e-2
+
+
+def test_n1_is_monodomain_bitwise(oracle_mod):
+    p = _tiny(N=1)
+    o = oracle_mod.Oracle(p, _tiny_inputs(p))
+    r = o.solve()
+    st, um, _ = o.monodomain()
+    assert r["status"] == 0 and r["iterations"] == 0
+    assert np.array_equal(r["uT"], um)
+
+
+# ---------------------------------------------------------------- interface
+@pytest.mark.parametrize("tc", [si.TC_ROBIN, si.TC_S02])
+def test_R_is_affine_with_toeplitz_L(oracle_mod, tc):
+    """Props 1-4: R(g) = L g + d for V(x), with L built from first columns."""
+    p = _tiny(transmission=tc, N=4, dx=0.25)
+    o = oracle_mod.Oracle(p, _tiny_inputs(p))
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng)
+    d = o.apply_R(None)
+    X = o.build_L()
+    lhs = o.apply_R(g)
+    rhs = o.apply_L(X, g) + d
+    assert np.linalg.norm(lhs - rhs) <= 1e-13 * np.linalg.norm(lhs)
+
+
+def test_dense_interface_matrix_brute_force(oracle_mod):
+    """Probe every column of R_0 = R(.; u0=0): the dense L equals the
+    block-Toeplitz matrix rebuilt from the first columns, it is block lower
+    triangular in time, and a dense solve of (I-L)g = d matches GMRES."""
+    p = _tiny(N=3)
+    o = oracle_mod.Oracle(p, _tiny_inputs(p))
+    n = o.ng
+    Ld = np.zeros((n, n), np.complex128)
+    for c in range(n):
+        e = np.zeros(n, np.complex128)
+        e[c] = 1
+        Ld[:, c] = o.apply_R(e, use_u0=False)
+    X = o.build_L()
+    Lt = np.zeros_like(Ld)
+    for c in range(n):
+        e = np.zeros(n, np.complex128)
+        e[c] = 1
+        Lt[:, c] = o.apply_L(X, e)
+    assert np.abs(Ld - Lt).max() <= 1e-13 * np.abs(Ld).max()
+    NT = p.NT
+    for si_ in range(2 * p.N - 2):
+        for so in range(2 * p.N - 2):
+            blk = Ld[so * NT:(so + 1) * NT, si_ * NT:(si_ + 1) * NT]
+            assert np.abs(np.triu(blk, 1)).max() == 0.0          # causal
+    d = o.apply_R(None)
+    g_dense = np.linalg.solve(np.eye(n) - Ld, d)
+    r = o.solve()
+    assert r["converged"]
+    cond = np.linalg.cond(np.eye(n) - Ld)
+    assert np.linalg.norm(r["g"] - g_dense) <= 10 * p.tol * cond * np.linalg.norm(g_dense)
+
+
+def test_toeplitz_shift_bitwise(oracle_mod):
+    """Prop. 3-4 with u0 = 0: an impulse at n=2 gives the n=1 response
+    shifted by one step, bitwise (reading A14); every interior block of
+    L0 is identical (translation invariance of the V = 0 problem) and
+    mirror-symmetric (X^{j,1} = X^{j,4}, X^{j,2} = X^{j,3})."""
+    p = _tiny(N=5, dx=0.3, T=0.08)
+    o = oracle_mod.Oracle(p, _tiny_inputs(p))
+    for j in (1, 2, 5):
+        e1 = np.zeros(p.NT, np.complex128); e1[0] = 1
+        e2 = np.zeros(p.NT, np.complex128); e2[1] = 1
+        if j < p.N:
+            _, a1, b1, _, _ = o.march(j, None, e1, use_u0=False)
+            _, a2, b2, _, _ = o.march(j, None, e2, use_u0=False)
+        else:
+            _, a1, b1, _, _ = o.march(j, e1, None, use_u0=False)
+            _, a2, b2, _, _ = o.march(j, e2, None, use_u0=False)
+        assert np.array_equal(a2[1:], a1[:-1]) and a2[0] == 0
+        assert np.array_equal(b2[1:], b1[:-1]) and b2[0] == 0
+    X0 = o.build_L(force_zero=True)
+    for j in range(3, p.N):
+        assert np.array_equal(X0[j - 1], X0[1])
+    sc = np.abs(X0[1]).max()
+    assert np.abs(X0[1, 0] - X0[1, 3]).max() <= 1e-13 * sc
+    assert np.abs(X0[1, 1] - X0[1, 2]).max() <= 1e-13 * sc
+    # reading A13: the "-1" of x^{j,1}_{n,s} sits only at lag 0
+    d = p.NT
+    assert X0.shape == (p.N, 4, d)
+
+
+def test_dot_is_order_fixed_inner_product(oracle_mod):
+    p = _tiny(N=4, dx=0.25)
+    o = oracle_mod.Oracle(p, _tiny_inputs(p))
+    rng = np.random.default_rng(4)
+    x, y = (rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng) for _ in range(2))
+    assert abs(o.dot(x, y) - np.vdot(x, y)) <= 1e-14 * np.linalg.norm(x) * np.linalg.norm(y)
+
+
+# ---------------------------------------------------------------- algorithms
+@pytest.mark.parametrize("tc,pot", [(si.TC_ROBIN, si.POT_ZERO), (si.TC_S02, si.POT_ZERO),
+                                    (si.TC_S02, si.POT_VX), (si.TC_ROBIN, si.POT_VX)])
+def test_new_algorithm_equals_monodomain(oracle_mod, tc, pot):
+    """Converged SWR = the single-domain CN/FEM solution (c0 != 0 makes the
+    FEM fluxes cancel): within tol * a modest factor."""
+    p = si.config("C1", transmission=tc, potential=pot, N=4)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    r = o.solve()
+    st, um, _ = o.monodomain()
+    assert r["status"] == 0 and r["converged"]
+    assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+def test_precond_exact_for_zero_potential(oracle_mod):
+    """With V = 0, P = I - L0 = I - L, so P^{-1}(I - L) = I: one outer
+    iteration."""
+    p = si.config("C1", transmission=si.TC_S02, potential=si.POT_ZERO, algorithm=si.ALG_PRECOND, N=4)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    r = o.solve()
+    assert r["status"] == 0 and r["iterations"] == 1
+
+
+@pytest.mark.parametrize("pot,u0", [(si.POT_VTX, "gaussian"), (si.POT_CUBIC, "soliton")])
+def test_precond_equals_monodomain(oracle_mod, pot, u0):
+    p = si.config("C1", transmission=si.TC_S02, potential=pot, algorithm=si.ALG_PRECOND, N=4, u0_kind=u0)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    r = o.solve()
+    st, um, _ = o.monodomain()
+    assert r["status"] == 0 and r["converged"]
+    assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+def test_new_rejects_time_dependent(oracle_mod):
+    p = si.config("C1", potential=si.POT_VTX, algorithm=si.ALG_NEW)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    assert o.solve()["status"] == 6
+
+
+def test_s02_transmission_is_transparent(oracle_mod):
+    """S0^2 is the discrete transparent condition of the free equation
+    (P:146-159): a Gaussian packet leaving subdomain 1 through b_1
+    with zero incoming flux is absorbed (reflection <= 1e-4 of the packet
+    amplitude vs the solution on a larger domain), whereas the memoryless
+    Robin condition reflects O(1).  Pins the beta history sum and its index
+    range (a shifted or mis-signed history term reflects strongly)."""
+    out = {}
+    for tc in (si.TC_S02, si.TC_ROBIN):
+        p = si.Problem(a0=-16, b0=4, T=0.2, dx=2e-3, dt=2e-4, N=2, potential=si.POT_ZERO,
+                       transmission=tc, robin_p=40.0)
+        o = oracle_mod.Oracle(p, si.inputs(p))
+        st, _, _, uT, _ = o.march(1, None, None, use_u0=True)
+        q = si.Problem(a0=-16, b0=24, T=0.2, dx=2e-3, dt=2e-4, N=1, potential=si.POT_ZERO)
+        st2, ub, _ = oracle_mod.Oracle(q, si.inputs(q)).monodomain()
+        out[tc] = np.abs(uT - ub[: p.Nj]).max()
+    assert out[si.TC_S02] <= 1e-4
+    assert out[si.TC_ROBIN] >= 0.1
