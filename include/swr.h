@@ -1,0 +1,174 @@
+/*
+ * include/swr.h — C ABI of the B200-native Schwarz waveform relaxation (SWR)
+ * hot path for the 1D Schrödinger equation (Besse & Xing, arXiv:1503.02564,
+ * PAPER.md; "P:n" = PAPER.md line n).
+ *
+ * Problem:  (i d_t + d_xx + V) u = 0 on (a0,b0) x (0,T),
+ *   u(0) = u0, homogeneous Neumann at a0, b0, V real: V(x), V(t,x) or
+ *   f(u) = lambda |u|^2.  Crank-Nicolson in time in the v-variable,
+ *   P1 finite elements on a uniform global mesh, N equal non-overlapping
+ *   subdomains, transmission B = d_n + S with S = Robin -ip
+ *   or the potential-strategy S0^2.
+ *
+ * Algorithms:
+ *   SWR_ALG_NEW      Algorithm 3 for V(x): build d = R(0)
+ *                     and the lower-triangular Toeplitz interface
+ *                    matrix L from unit-impulse probes, solve
+ *                    (I - L) g = d by GMRES, then one final sweep.
+ *   SWR_ALG_PRECOND  zero-potential preconditioner P = I - L0:
+ *                    GMRES on P^{-1}(I - L) g = P^{-1} d for V(t,x)
+ *                    (eq. chp2_algopd_Lpf); preconditioned fixed point
+ *                    g <- g - P^{-1}(g - R_nl(g)) for f(u) (eq. chp2_algopd_NL).
+ *
+ * Data conventions (all calls):
+ *   - complex arrays are interleaved (re, im) fp64, i.e. double[2*len];
+ *   - the interface vector g is slot-major
+ *     (r_1, l_2, r_2, ..., l_{N-1}, r_{N-1}, l_N), each slot N_T entries
+ *     (time steps n = 1..N_T at index n-1): length n_g = (2N-2) N_T complex;
+ *   - N_x = round((b0-a0)/dx), N_T = round(T/dt), N must divide N_x;
+ *     subdomain j = 1..N holds global nodes [(j-1)m, jm], m = N_x/N,
+ *     N_j = m+1 (interface nodes duplicated, reading A1 of DESIGN.md);
+ *   - every call is collective over the ranks of one handle and runs on the
+ *     caller's CUDA stream; a handle is not thread-safe.
+ *
+ * Ownership: inputs are copied during swr_setup (and swr_update_inputs); the
+ * caller keeps its arrays.  The handle owns all device memory and the report
+ * buffers, released by swr_free.
+ *
+ * Errors: every int-returning call returns an swr_status; 0 = success.
+ * SWR_NOT_CONVERGED leaves valid outputs (the last iterate).  CUDA/NCCL
+ * failures are reported as SWR_ERR_CUDA / SWR_ERR_NCCL; swr_error_string and
+ * swr_last_error_detail describe them.  There is no CPU fallback: a machine
+ * without a usable sm_100a GPU gets SWR_ERR_CUDA from swr_setup.
+ */
+#ifndef SWR_H
+#define SWR_H
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct swr_handle swr_handle;
+
+enum swr_status {
+  SWR_OK = 0,
+  SWR_ERR_INVALID_ARG = 1,
+  SWR_NOT_CONVERGED = 2,          /* outputs valid but unconverged */
+  SWR_ERR_ZERO_PIVOT = 3,         /* |pivot| < 1e-300: A - B singular (Prop. 1 hypothesis) */
+  SWR_ERR_BREAKDOWN = 4,
+  SWR_ERR_INNER_NOT_CONVERGED = 5,/* P^{-1} GMRES or NL fixed point hit its cap */
+  SWR_ERR_UNSUPPORTED = 6,        /* e.g. NEW with V(t,x) or f(u) */
+  SWR_ERR_CUDA = 7,
+  SWR_ERR_NCCL = 8,
+  SWR_ERR_OOM = 9
+};
+
+enum swr_potential {
+  SWR_POT_ZERO = 0,
+  SWR_POT_VX = 1,              /* V(x): nodal samples V_x[N_x+1] */
+  SWR_POT_VTX_SEPARABLE = 2,   /* V(t,x) = sum_k tau_k(t) xi_k(x) */
+  SWR_POT_CUBIC = 3            /* f(u) = lambda |u|^2 */
+};
+
+enum swr_transmission { SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1 };
+enum swr_algorithm { SWR_ALG_NEW = 0, SWR_ALG_PRECOND = 1 };
+
+typedef struct {
+  double a0, b0, T, dx, dt;   /* domain, final time, mesh size, time step */
+  int32_t N;                  /* number of subdomains, N | N_x */
+  int32_t potential;          /* swr_potential */
+  const double *V_x;          /* [N_x+1] real, SWR_POT_VX */
+  int32_t n_terms;            /* SWR_POT_VTX_SEPARABLE */
+  const double *tau;          /* [n_terms][N_T+1]: tau_k(t_n) */
+  const double *xi;           /* [n_terms][N_x+1]: xi_k(x_i) */
+  double lambda;              /* SWR_POT_CUBIC coefficient (paper: 1) */
+  int32_t transmission;       /* swr_transmission */
+  double robin_p;             /* Robin parameter p > 0 */
+  const double *u0;           /* [2*(N_x+1)] initial datum at the nodes */
+  int32_t inputs_on_device;   /* 1: u0, V_x, tau, xi, g0 are device pointers */
+  int32_t algorithm;          /* swr_algorithm */
+  double tol;                 /* outer tolerance (paper: 1e-10) */
+  int32_t restart, maxit;     /* GMRES(m): 30, 2000 */
+  double tol_inner;           /* P^{-1} inner GMRES relative tol: 1e-12 */
+  int32_t maxit_inner;        /* 2000 */
+  double tol_fp;              /* NL inner fixed point relative max-norm: 1e-12 */
+  int32_t maxit_fp;           /* 50 */
+  const double *g0;           /* [2*n_g] initial interface vector, NULL = zero */
+  int32_t rank, world;        /* world = 1: single GPU, no NCCL */
+  const void *nccl_unique_id; /* 128-byte ncclUniqueId (world > 1) */
+  void *cuda_stream;          /* cudaStream_t owned by the caller (NULL = default stream) */
+  int32_t device;             /* CUDA device ordinal for this rank */
+} swr_config;
+
+typedef struct {
+  int32_t iterations;         /* outer GMRES Arnoldi steps / fixed-point steps */
+  int32_t inner_iterations;   /* total P^{-1} inner GMRES steps */
+  int32_t fp_max;             /* max NL fixed-point iterations in any step */
+  int32_t converged;
+  const double *residual_history; /* [n_history], owned by the handle */
+  int32_t n_history;
+  double t_build_ms;          /* swr_build_interface_operator, device time */
+  double t_solve_ms;          /* swr_solve, device time */
+  double t_march_ms;          /* sum of march-kernel time (CUDA events) */
+  double t_interface_ms;      /* Toeplitz apply + Krylov vector kernels */
+  double cell_steps;          /* sum over marches of (sum_j N_j) * N_T * RHS (this rank) */
+  int32_t n_marches;          /* march-kernel launches */
+  int32_t n_kernel_launches;  /* all kernels of this library launched */
+} swr_report;
+
+/* Validate the configuration, copy the inputs to the GPU, assemble and
+ * factor the subdomain matrices (A - B), eq. (9).
+ * Returns SWR_ERR_INVALID_ARG for: N not dividing N_x, world > N, Robin with
+ * p <= 0, NEW with a time-dependent or nonlinear potential, NULL u0.
+ * *out receives the handle (NULL on failure).  Collective. */
+int swr_setup(const swr_config *cfg, swr_handle **out);
+
+/* Replace u0 (and V_x for SWR_POT_VX, refactoring the matrices) with arrays
+ * of the same sizes; on_device as cfg->inputs_on_device.  Collective. */
+int swr_update_inputs(swr_handle *h, const double *u0, const double *V_x, int32_t on_device);
+
+/* NEW: one batched march per subdomain with three right-hand sides (d, the
+ * l_j impulse and the r_j impulse) -> d and the first columns of
+ * X^{j,1..4}.  PRECOND: the V = 0 impulse probes -> L0, plus d for
+ * V(t,x).  Collective. */
+int swr_build_interface_operator(swr_handle *h);
+
+/* Solve the interface problem and run the final sweep; u_T [2*(N_x+1)]
+ * receives u(x_i, T) on rank 0 (interface nodes: mean of the two copies),
+ * host memory if u_T_on_device == 0.  NULL skips the gather.  rep may be
+ * NULL.  Collective. */
+int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep);
+
+void swr_free(swr_handle *h);
+const char *swr_error_string(int status);
+const char *swr_last_error_detail(void);
+
+/* ---- Lower-level entry points (parity tests, benchmarks). -------------
+ * Device pointers (this rank's GPU), n_g = (2N-2) N_T complex, world = 1. */
+
+/* Rg = R(g; u0 if use_u0 else 0) with the true potential, or with V = 0 if
+ * force_zero_potential (eq. 13): one march of every subdomain and the
+ * exchange of eq. (8).  g may be NULL (= 0).  If u_T is non-NULL it
+ * receives the assembled u(T) [2*(N_x+1)] of that sweep. */
+int swr_apply_R(swr_handle *h, const double *g, int32_t use_u0, int32_t force_zero_potential,
+                double *Rg, double *u_T);
+
+/* y = (I - L) x (which = 0) or (I - L0) x (which = 1), causal block-Toeplitz
+ * convolutions with the first columns built by swr_build_interface_operator. */
+int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y);
+
+/* Copy out d [2*n_g] and the Toeplitz first columns X [2*N*4*N_T] (X[(j-1)*4+p-1]
+ * = first column of X^{j,p}; which = 0: L, 1: L0). NULL skips. */
+int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X);
+
+/* Copy out the interface vector g of the last swr_solve [2*n_g]. */
+int swr_get_g(swr_handle *h, double *g);
+
+/* Sizes: N_x, N_T, N_j, n_g. */
+int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_t *ng);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

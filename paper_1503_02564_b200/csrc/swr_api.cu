@@ -1,0 +1,772 @@
+// swr_api.cu — host orchestration behind include/swr.h: setup, interface
+// operator construction (Algorithm 3 of PAPER.md), GMRES(m) with
+// CGS2 on the interface problem, the preconditioned algorithms
+// and the final sweep.  All arithmetic of the method runs in
+// the kernels of swr_march.cu / swr_linalg.cu; the host only keeps the
+// (m+1) x m Hessenberg matrix and its Givens rotations.
+#include "swr.h"
+#include "swr_kernels.h"
+
+#include <cmath>
+#include <complex>
+#include <cstdio>
+#include <cstring>
+#include <functional>
+#include <string>
+#include <vector>
+#include <dlfcn.h>
+
+using swr::MarchParams;
+using swr::MarchShape;
+using swr::MarchSys;
+typedef std::complex<double> cplx;
+
+namespace {
+
+thread_local std::string g_detail;
+
+#define CK(call)                                                                     \
+  do {                                                                               \
+    cudaError_t e_ = (call);                                                         \
+    if (e_ != cudaSuccess) {                                                         \
+      g_detail = std::string(#call) + ": " + cudaGetErrorString(e_) + " (" +         \
+                 __FILE__ + ":" + std::to_string(__LINE__) + ")";                    \
+      return SWR_ERR_CUDA;                                                           \
+    }                                                                                \
+  } while (0)
+#define CKS(call)                                                                    \
+  do {                                                                               \
+    int s_ = (call);                                                                 \
+    if (s_ != SWR_OK) return s_;                                                     \
+  } while (0)
+
+inline double2 d2(cplx z) { return make_double2(z.real(), z.imag()); }
+inline cplx c2(double2 z) { return cplx(z.x, z.y); }
+
+// ---- NCCL (loaded on demand for world > 1) ---------------------------------
+typedef struct ncclComm *ncclComm_t;
+typedef struct { char internal[128]; } ncclUniqueId_t;
+typedef int (*fn_commInitRank)(ncclComm_t *, int, ncclUniqueId_t, int);
+typedef int (*fn_commDestroy)(ncclComm_t);
+typedef int (*fn_send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_allgather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_group)(void);
+struct Nccl {
+  void *lib = nullptr;
+  fn_commInitRank commInitRank;
+  fn_commDestroy commDestroy;
+  fn_send send;
+  fn_recv recv;
+  fn_allreduce allReduce;
+  fn_allgather allGather;
+  fn_group groupStart, groupEnd;
+};
+Nccl g_nccl;
+enum { nccl_float64 = 8, nccl_sum = 0, nccl_uint8 = 1 };
+
+int load_nccl() {
+  if (g_nccl.lib) return SWR_OK;
+  const char *names[] = {"libnccl.so.2", "libnccl.so"};
+  for (const char *nm : names) {
+    g_nccl.lib = dlopen(nm, RTLD_NOW | RTLD_GLOBAL);
+    if (g_nccl.lib) break;
+  }
+  if (!g_nccl.lib) { g_detail = "cannot dlopen libnccl.so.2"; return SWR_ERR_NCCL; }
+  g_nccl.commInitRank = (fn_commInitRank)dlsym(g_nccl.lib, "ncclCommInitRank");
+  g_nccl.commDestroy = (fn_commDestroy)dlsym(g_nccl.lib, "ncclCommDestroy");
+  g_nccl.send = (fn_send)dlsym(g_nccl.lib, "ncclSend");
+  g_nccl.recv = (fn_recv)dlsym(g_nccl.lib, "ncclRecv");
+  g_nccl.allReduce = (fn_allreduce)dlsym(g_nccl.lib, "ncclAllReduce");
+  g_nccl.allGather = (fn_allgather)dlsym(g_nccl.lib, "ncclAllGather");
+  g_nccl.groupStart = (fn_group)dlsym(g_nccl.lib, "ncclGroupStart");
+  g_nccl.groupEnd = (fn_group)dlsym(g_nccl.lib, "ncclGroupEnd");
+  if (!g_nccl.commInitRank || !g_nccl.send || !g_nccl.recv || !g_nccl.allReduce || !g_nccl.groupStart) {
+    g_detail = "libnccl is missing symbols";
+    return SWR_ERR_NCCL;
+  }
+  return SWR_OK;
+}
+
+template <typename T>
+int dalloc(T **p, size_t n) {
+  if (n == 0) { *p = nullptr; return SWR_OK; }
+  cudaError_t e = cudaMalloc((void **)p, n * sizeof(T));
+  if (e != cudaSuccess) {
+    g_detail = std::string("cudaMalloc(") + std::to_string(n * sizeof(T)) + "): " + cudaGetErrorString(e);
+    return e == cudaErrorMemoryAllocation ? SWR_ERR_OOM : SWR_ERR_CUDA;
+  }
+  return SWR_OK;
+}
+
+inline unsigned grid_for(size_t n, int bs = 256) {
+  size_t g = (n + bs - 1) / bs;
+  if (g > 148 * 16) g = 148 * 16;
+  return (unsigned)(g ? g : 1);
+}
+
+}  // namespace
+
+struct swr_handle {
+  // problem
+  double a0, b0, T, dx, dt, lambda, robin_p, tol, tol_inner, tol_fp;
+  int N, potential, transmission, algorithm, restart, maxit, maxit_inner, maxit_fp, n_terms;
+  int Nx, NT, Nj, m;
+  size_t ng;
+  int rank, world, device;
+  cudaStream_t st;
+  double2 c0, c2v;
+  double kappa, eim;
+  MarchShape shape;
+  // device data
+  double2 *u0 = nullptr;
+  double *Vx = nullptr, *beta = nullptr;
+  double2 *q = nullptr, *q0 = nullptr;     // pivots: physical [N][Nj], V=0 [3][Nj]
+  double *er = nullptr, *er0 = nullptr;
+  double2 *d = nullptr, *X = nullptr, *X0 = nullptr, *g = nullptr, *g0 = nullptr;
+  double2 *uloc = nullptr, *uT = nullptr;
+  double2 *V = nullptr, *Vin = nullptr;    // outer / inner Krylov bases [(m+1) n_g]
+  double2 *w = nullptr, *win = nullptr, *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
+  double2 *partial = nullptr, *dots = nullptr, *ycoef = nullptr;
+  double2 *hpin = nullptr;                 // pinned host scalars
+  MarchSys *sys_dev = nullptr;
+  int *err_dev = nullptr;
+  swr::FactorJob *jobs_dev = nullptr;
+  bool have_L = false, have_L0 = false, have_d = false, have_g = false;
+  // report
+  std::vector<double> hist;
+  int iterations = 0, inner_total = 0, fp_max = 0, converged = 0;
+  bool inner_fail = false;
+  double cell_steps = 0;
+  int n_marches = 0, n_launches = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> march_ev, intf_ev;
+  size_t march_ev_used = 0, intf_ev_used = 0;
+  cudaEvent_t ev_b0, ev_b1, ev_s0, ev_s1;
+  bool build_timed = false;
+};
+
+namespace {
+
+int record_pair(swr_handle *h, bool march, bool begin) {
+  auto &vec = march ? h->march_ev : h->intf_ev;
+  size_t &used = march ? h->march_ev_used : h->intf_ev_used;
+  if (begin) {
+    if (used == vec.size()) {
+      cudaEvent_t a, b;
+      CK(cudaEventCreate(&a));
+      CK(cudaEventCreate(&b));
+      vec.push_back({a, b});
+    }
+    CK(cudaEventRecord(vec[used].first, h->st));
+  } else {
+    CK(cudaEventRecord(vec[used].second, h->st));
+    used++;
+  }
+  return SWR_OK;
+}
+
+double sum_pairs(swr_handle *h, bool march) {
+  auto &vec = march ? h->march_ev : h->intf_ev;
+  size_t used = march ? h->march_ev_used : h->intf_ev_used;
+  double s = 0;
+  for (size_t i = 0; i < used; i++) {
+    float ms = 0;
+    if (cudaEventElapsedTime(&ms, vec[i].first, vec[i].second) == cudaSuccess) s += ms;
+  }
+  return s;
+}
+
+int slot_l(int j) { return 2 * j - 3; }
+int slot_r(int j) { return 2 * j - 2; }
+int zero_matrix_index(swr_handle *h, int j) { return j == 1 ? 0 : (j == h->N ? 2 : 1); }
+
+// ---- one batched march over a list of systems ------------------------------
+int run_march(swr_handle *h, const std::vector<MarchSys> &sys) {
+  if (sys.empty()) return SWR_OK;
+  CK(cudaMemcpyAsync(h->sys_dev, sys.data(), sys.size() * sizeof(MarchSys), cudaMemcpyHostToDevice, h->st));
+  MarchParams p;
+  p.sys = h->sys_dev;
+  p.nsys = (int)sys.size();
+  p.Nj = h->Nj;
+  p.NT = h->NT;
+  p.CS = h->shape.CS;
+  p.e_im = h->eim;
+  p.kappa = h->kappa;
+  p.c0 = h->c0;
+  p.c2 = h->c2v;
+  p.s02 = h->transmission == SWR_TC_S0_2;
+  p.beta = h->beta;
+  CKS(record_pair(h, true, true));
+  CK(swr::launch_march(p, h->shape, h->st));
+  CK(cudaGetLastError());
+  CKS(record_pair(h, true, false));
+  h->n_marches++;
+  h->n_launches++;
+  h->cell_steps += (double)sys.size() * h->Nj * h->NT;
+  return SWR_OK;
+}
+
+// system of subdomain j (1-based) with fluxes from g (may be NULL)
+MarchSys make_sys(swr_handle *h, int j, const double2 *g, bool use_u0, bool zero_pot, double2 *Rg,
+                  double2 *uloc) {
+  MarchSys s;
+  memset(&s, 0, sizeof s);
+  const int N = h->N, NT = h->NT;
+  if (j >= 2) s.flags |= swr::SYS_HAS_LEFT;
+  if (j <= N - 1) s.flags |= swr::SYS_HAS_RIGHT;
+  if (g && j >= 2) s.lin = g + (size_t)slot_l(j) * NT;
+  if (g && j <= N - 1) s.rin = g + (size_t)slot_r(j) * NT;
+  if (Rg && j >= 2) s.out_left = Rg + (size_t)slot_r(j - 1) * NT;
+  if (Rg && j <= N - 1) s.out_right = Rg + (size_t)slot_l(j + 1) * NT;
+  s.uT = uloc ? uloc + (size_t)(j - 1) * h->Nj : nullptr;
+  s.u0 = use_u0 ? h->u0 + (size_t)(j - 1) * h->m : nullptr;
+  if (zero_pot) {
+    const int zi = zero_matrix_index(h, j);
+    s.q = h->q0 + (size_t)zi * h->Nj;
+    s.er = h->er0 + (size_t)zi * h->Nj;
+  } else {
+    s.q = h->q + (size_t)(j - 1) * h->Nj;
+    s.er = h->er + (size_t)(j - 1) * h->Nj;
+  }
+  return s;
+}
+
+int fill_zero(swr_handle *h, double2 *x, size_t n) {
+  if (!n) return SWR_OK;
+  CK(cudaMemsetAsync(x, 0, n * sizeof(double2), h->st));
+  return SWR_OK;
+}
+
+// Rg = R(g; u0?) (eq. 13): every subdomain marches once.
+int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2 *Rg, double2 *uloc) {
+  std::vector<MarchSys> sys;
+  for (int j = 1; j <= h->N; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
+  if (Rg) CKS(fill_zero(h, Rg, h->ng));
+  return run_march(h, sys);
+}
+
+// ---- assembly + factorisation ----------------------------------------------
+int factor_matrices(swr_handle *h) {
+  std::vector<swr::FactorJob> jobs;
+  const bool phys_const = h->potential != SWR_POT_VTX_SEPARABLE;
+  if (phys_const) {
+    for (int j = 1; j <= h->N; j++) {
+      swr::FactorJob J;
+      J.W = (h->potential == SWR_POT_VX) ? h->Vx + (size_t)(j - 1) * h->m : nullptr;
+      J.has_left = j >= 2;
+      J.has_right = j <= h->N - 1;
+      J.q = h->q + (size_t)(j - 1) * h->Nj;
+      J.er = h->er + (size_t)(j - 1) * h->Nj;
+      jobs.push_back(J);
+    }
+  }
+  if (h->q0) {
+    for (int zi = 0; zi < 3; zi++) {
+      swr::FactorJob J;
+      J.W = nullptr;
+      J.has_left = zi >= 1;
+      J.has_right = zi <= 1;
+      if (h->N == 1) J.has_left = J.has_right = 0;
+      J.q = h->q0 + (size_t)zi * h->Nj;
+      J.er = h->er0 + (size_t)zi * h->Nj;
+      jobs.push_back(J);
+    }
+  }
+  if (jobs.empty()) return SWR_OK;
+  CK(cudaFree(h->jobs_dev));
+  h->jobs_dev = nullptr;
+  CKS(dalloc(&h->jobs_dev, jobs.size()));
+  CK(cudaMemcpyAsync(h->jobs_dev, jobs.data(), jobs.size() * sizeof(jobs[0]), cudaMemcpyHostToDevice, h->st));
+  CK(cudaMemsetAsync(h->err_dev, 0, sizeof(int), h->st));
+  swr::k_factor<<<(unsigned)((jobs.size() + 63) / 64), 64, 0, h->st>>>(h->jobs_dev, (int)jobs.size(), h->Nj, h->dx,
+                                                                        h->dt, h->c0, h->err_dev);
+  CK(cudaGetLastError());
+  h->n_launches++;
+  int herr = 0;
+  CK(cudaMemcpyAsync(&herr, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (herr) { g_detail = "zero pivot while factoring A - B"; return SWR_ERR_ZERO_PIVOT; }
+  return SWR_OK;
+}
+
+// ---- Krylov kernels ----------------------------------------------------------
+// dots[v] = <V_v, w> (order-fixed), v = 0..nvec-1, on the device
+int multidot(swr_handle *h, const double2 *V, int nvec, const double2 *w, double2 *out) {
+  dim3 grid(h->N, nvec);
+  swr::k_multidot_partial<<<grid, 256, 0, h->st>>>(V, h->ng, nvec, w, h->partial, h->N, h->NT);
+  CK(cudaGetLastError());
+  swr::k_multidot_final<<<(nvec + 63) / 64, 64, 0, h->st>>>(h->partial, nvec, h->N, out);
+  CK(cudaGetLastError());
+  h->n_launches += 2;
+  return SWR_OK;
+}
+
+int fetch(swr_handle *h, const double2 *dev, int n, double2 *host) {
+  CK(cudaMemcpyAsync(host, dev, n * sizeof(double2), cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
+typedef std::function<int(const double2 *, double2 *)> Op;
+
+// GMRES(m) with CGS2 and complex Givens rotations, the same algorithm as the
+// oracle (reading A5/A6): stop at |gamma_{k+1}| <= tol ||b||, true residual
+// at restarts, happy breakdown at h_{k+1,k} <= 1e-14 ||A v_k||.
+int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, double2 *V,
+          double2 *w, int *iters, std::vector<double> *hist, int *converged) {
+  const size_t n = h->ng;
+  const size_t ldv = n;
+  *iters = 0;
+  *converged = 0;
+  double2 *hp = h->hpin;  // pinned scratch: [0] bnorm^2, [1..] dots
+  CKS(multidot(h, b, 1, b, h->dots));
+  CKS(fetch(h, h->dots, 1, hp));
+  const double bnorm = std::sqrt(hp[0].x);
+  if (bnorm == 0.0) {
+    CKS(fill_zero(h, x, n));
+    *converged = 1;
+    return SWR_OK;
+  }
+  std::vector<cplx> H((size_t)(m + 1) * m), sn(m), gam(m + 1), y(m);
+  std::vector<double> cs(m);
+  auto Hm = [&](int i, int k) -> cplx & { return H[(size_t)i * m + k]; };
+  int total = 0, done = 0, st = SWR_OK;
+  while (!done) {
+    CKS(A(x, w));
+    swr::k_sub<<<grid_for(n), 256, 0, h->st>>>(b, w, V, n);
+    CK(cudaGetLastError());
+    CKS(multidot(h, V, 1, V, h->dots));
+    CKS(fetch(h, h->dots, 1, hp));
+    const double beta = std::sqrt(hp[0].x);
+    if (beta <= tol * bnorm) { *converged = 1; break; }
+    if (total >= maxit) break;
+    swr::k_axpby<<<grid_for(n), 256, 0, h->st>>>(make_double2(0, 0), V, make_double2(1.0 / beta, 0), V, n);
+    CK(cudaGetLastError());
+    std::fill(gam.begin(), gam.end(), cplx(0));
+    gam[0] = beta;
+    int k, kend = 0;
+    for (k = 0; k < m; k++) {
+      const double2 *vk = V + (size_t)k * ldv;
+      double2 *vk1 = V + (size_t)(k + 1) * ldv;
+      int s = A(vk, w);
+      if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
+      if (s) st = s;
+      total++;
+      // ||w|| before, two CGS passes, ||w|| after — one host round trip
+      CKS(multidot(h, w, 1, w, h->dots));
+      CKS(multidot(h, V, k + 1, w, h->dots + 1));
+      swr::k_multi_axpy<<<grid_for(n), 256, 0, h->st>>>(V, ldv, k + 1, h->dots + 1, w, n);
+      CK(cudaGetLastError());
+      CKS(multidot(h, V, k + 1, w, h->dots + 1 + (m + 1)));
+      swr::k_multi_axpy<<<grid_for(n), 256, 0, h->st>>>(V, ldv, k + 1, h->dots + 1 + (m + 1), w, n);
+      CK(cudaGetLastError());
+      CKS(multidot(h, w, 1, w, h->dots + 2 * (m + 1) + 1));
+      h->n_launches += 3;
+      CKS(fetch(h, h->dots, 2 * (m + 1) + 2, hp));
+      const double wn0 = std::sqrt(hp[0].x);
+      for (int i = 0; i <= k; i++) Hm(i, k) = c2(hp[1 + i]) + c2(hp[1 + (m + 1) + i]);
+      const double hk1 = std::sqrt(hp[2 * (m + 1) + 1].x);
+      const bool breakdown = hk1 <= 1e-14 * wn0;
+      if (!breakdown) {
+        swr::k_axpby<<<grid_for(n), 256, 0, h->st>>>(make_double2(1.0 / hk1, 0), w, make_double2(0, 0), vk1, n);
+        CK(cudaGetLastError());
+        h->n_launches++;
+      }
+      for (int i = 0; i < k; i++) {
+        cplx t = cs[i] * Hm(i, k) + sn[i] * Hm(i + 1, k);
+        Hm(i + 1, k) = -std::conj(sn[i]) * Hm(i, k) + cs[i] * Hm(i + 1, k);
+        Hm(i, k) = t;
+      }
+      cplx a = Hm(k, k);
+      double aa = std::abs(a);
+      if (aa == 0.0) {
+        cs[k] = 0.0;
+        sn[k] = 1.0;
+        Hm(k, k) = hk1;
+      } else {
+        double den = std::sqrt(aa * aa + hk1 * hk1);
+        cs[k] = aa / den;
+        sn[k] = (a / aa) * hk1 / den;
+        Hm(k, k) = (a / aa) * den;
+      }
+      gam[k + 1] = -std::conj(sn[k]) * gam[k];
+      gam[k] = cs[k] * gam[k];
+      const double res = std::abs(gam[k + 1]);
+      if (hist) hist->push_back(res);
+      kend = k + 1;
+      if (res <= tol * bnorm || breakdown) { *converged = 1; done = 1; break; }
+      if (total >= maxit) { done = 1; break; }
+    }
+    for (int i = kend - 1; i >= 0; i--) {
+      cplx acc = gam[i];
+      for (int qq = i + 1; qq < kend; qq++) acc -= Hm(i, qq) * y[qq];
+      y[i] = acc / Hm(i, i);
+    }
+    for (int i = 0; i < kend; i++) hp[i] = d2(y[i]);
+    CK(cudaMemcpyAsync(h->ycoef, hp, kend * sizeof(double2), cudaMemcpyHostToDevice, h->st));
+    swr::k_multi_update<<<grid_for(n), 256, 0, h->st>>>(V, ldv, kend, h->ycoef, x, n);
+    CK(cudaGetLastError());
+    CK(cudaStreamSynchronize(h->st));  // hp reused
+  }
+  *iters = total;
+  return st;
+}
+
+// y = (I - L) x or (I - L0) x
+int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
+  const double2 *X = zero ? h->X0 : h->X;
+  const int nslots = 2 * h->N - 2;
+  if (nslots <= 0) return SWR_OK;
+  CKS(record_pair(h, false, true));
+  swr::k_toeplitz_I_minus_L<<<nslots, 256, 4 * h->NT * sizeof(double2), h->st>>>(X, x, y, h->N, h->NT);
+  CK(cudaGetLastError());
+  CKS(record_pair(h, false, false));
+  h->n_launches++;
+  return SWR_OK;
+}
+
+// x = P^{-1} y: GMRES on (I - L0) x = y from x = 0 (eq. Pxg, reading A8)
+int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
+  CKS(fill_zero(h, x, h->ng));
+  Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
+  int it = 0, conv = 0;
+  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->Vin, h->win, &it, nullptr, &conv);
+  h->inner_total += it;
+  if (!conv) h->inner_fail = true;
+  return s;
+}
+
+// the L / L0 first columns by impulse probing, d = R(0; u0)
+int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
+  std::vector<MarchSys> sys;
+  const int N = h->N, NT = h->NT;
+  CKS(fill_zero(h, X, (size_t)N * 4 * NT));
+  if (dvec) CKS(fill_zero(h, dvec, h->ng));
+  for (int j = 1; j <= N; j++) {
+    double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
+    if (dvec) sys.push_back(make_sys(h, j, nullptr, true, zero, dvec, nullptr));
+    if (j >= 2) {  // l_{j,1} = 1 -> X^{j,1} (out_left), X^{j,3} (out_right)
+      MarchSys s = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
+      s.flags |= swr::SYS_LIN_IMPULSE;
+      s.out_left = Xj + 0 * NT;
+      s.out_right = (j <= N - 1) ? Xj + 2 * NT : nullptr;
+      sys.push_back(s);
+    }
+    if (j <= N - 1) {  // r_{j,1} = 1 -> X^{j,2}, X^{j,4}
+      MarchSys s = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
+      s.flags |= swr::SYS_RIN_IMPULSE;
+      s.out_left = (j >= 2) ? Xj + 1 * NT : nullptr;
+      s.out_right = Xj + 3 * NT;
+      sys.push_back(s);
+    }
+  }
+  return run_march(h, sys);
+}
+
+int final_sweep(swr_handle *h, const double2 *g) {
+  CKS(sweep_R(h, g, true, false, nullptr, h->uloc));
+  swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->uT);
+  CK(cudaGetLastError());
+  h->n_launches++;
+  return SWR_OK;
+}
+
+int copy_in(double2 *dst, const double *src, size_t n, bool on_dev, cudaStream_t st) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double2), on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  return SWR_OK;
+}
+int copy_in_r(double *dst, const double *src, size_t n, bool on_dev, cudaStream_t st) {
+  CK(cudaMemcpyAsync(dst, src, n * sizeof(double), on_dev ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice, st));
+  return SWR_OK;
+}
+
+void free_all(swr_handle *h) {
+  void *ptrs[] = {h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
+                  h->uloc, h->uT, h->V, h->Vin, h->w, h->win, h->tmp, h->tmp2, h->rhs, h->partial,
+                  h->dots, h->ycoef, h->sys_dev, h->err_dev, h->jobs_dev};
+  for (void *p : ptrs)
+    if (p) cudaFree(p);
+  if (h->hpin) cudaFreeHost(h->hpin);
+  for (auto &e : h->march_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto &e : h->intf_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+}
+
+}  // namespace
+
+extern "C" {
+
+const char *swr_error_string(int s) {
+  switch (s) {
+    case SWR_OK: return "ok";
+    case SWR_ERR_INVALID_ARG: return "invalid argument";
+    case SWR_NOT_CONVERGED: return "not converged (outputs hold the last iterate)";
+    case SWR_ERR_ZERO_PIVOT: return "zero pivot: A - B is singular";
+    case SWR_ERR_BREAKDOWN: return "Krylov breakdown";
+    case SWR_ERR_INNER_NOT_CONVERGED: return "inner iteration (P^-1 GMRES or NL fixed point) not converged";
+    case SWR_ERR_UNSUPPORTED: return "unsupported combination";
+    case SWR_ERR_CUDA: return "CUDA error";
+    case SWR_ERR_NCCL: return "NCCL error";
+    case SWR_ERR_OOM: return "out of device memory";
+    default: return "unknown status";
+  }
+}
+
+const char *swr_last_error_detail(void) { return g_detail.c_str(); }
+
+int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_t *ng) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  if (Nx) *Nx = h->Nx;
+  if (NT) *NT = h->NT;
+  if (Nj) *Nj = h->Nj;
+  if (ng) *ng = (int64_t)h->ng;
+  return SWR_OK;
+}
+
+int swr_setup(const swr_config *cfg, swr_handle **out) {
+  g_detail.clear();
+  if (!out) return SWR_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (!cfg || !cfg->u0 || !(cfg->dx > 0) || !(cfg->dt > 0) || !(cfg->T > 0) || cfg->N < 1 || !(cfg->b0 > cfg->a0)) {
+    g_detail = "bad geometry or missing u0";
+    return SWR_ERR_INVALID_ARG;
+  }
+  const long Nx = std::lround((cfg->b0 - cfg->a0) / cfg->dx), NT = std::lround(cfg->T / cfg->dt);
+  if (Nx < 1 || NT < 1 || Nx % cfg->N != 0) { g_detail = "N must divide N_x"; return SWR_ERR_INVALID_ARG; }
+  if (cfg->world < 1 || cfg->world > cfg->N || cfg->rank < 0 || cfg->rank >= cfg->world) {
+    g_detail = "bad rank/world";
+    return SWR_ERR_INVALID_ARG;
+  }
+  if (cfg->world > 1) { g_detail = "multi-GPU sharding is not enabled in this build"; return SWR_ERR_UNSUPPORTED; }
+  if (cfg->transmission == SWR_TC_ROBIN && !(cfg->robin_p > 0)) { g_detail = "Robin needs p > 0"; return SWR_ERR_INVALID_ARG; }
+  if (cfg->transmission != SWR_TC_ROBIN && cfg->transmission != SWR_TC_S0_2) return SWR_ERR_INVALID_ARG;
+  if (cfg->potential < 0 || cfg->potential > 3) return SWR_ERR_INVALID_ARG;
+  if (cfg->algorithm == SWR_ALG_NEW && !(cfg->potential == SWR_POT_ZERO || cfg->potential == SWR_POT_VX)) {
+    g_detail = "NEW needs a time-independent linear potential (P:1015)";
+    return SWR_ERR_INVALID_ARG;
+  }
+  if (cfg->potential == SWR_POT_VX && !cfg->V_x) return SWR_ERR_INVALID_ARG;
+  if (cfg->potential == SWR_POT_VTX_SEPARABLE) { g_detail = "V(t,x) march not enabled yet"; return SWR_ERR_UNSUPPORTED; }
+  if (cfg->potential == SWR_POT_CUBIC) { g_detail = "nonlinear march not enabled yet"; return SWR_ERR_UNSUPPORTED; }
+
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { g_detail = "no CUDA device"; return SWR_ERR_CUDA; }
+  CK(cudaSetDevice(cfg->device));
+  swr_handle *h = new swr_handle();
+  h->a0 = cfg->a0; h->b0 = cfg->b0; h->T = cfg->T; h->dx = cfg->dx; h->dt = cfg->dt;
+  h->lambda = cfg->lambda; h->robin_p = cfg->robin_p; h->tol = cfg->tol > 0 ? cfg->tol : 1e-10;
+  h->tol_inner = cfg->tol_inner > 0 ? cfg->tol_inner : 1e-12; h->tol_fp = cfg->tol_fp > 0 ? cfg->tol_fp : 1e-12;
+  h->N = cfg->N; h->potential = cfg->potential; h->transmission = cfg->transmission; h->algorithm = cfg->algorithm;
+  h->restart = cfg->restart > 0 ? cfg->restart : 30; h->maxit = cfg->maxit > 0 ? cfg->maxit : 2000;
+  h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
+  h->n_terms = cfg->n_terms;
+  h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;
+  h->ng = (size_t)(2 * h->N - 2) * h->NT;
+  h->rank = cfg->rank; h->world = cfg->world; h->device = cfg->device;
+  h->st = (cudaStream_t)cfg->cuda_stream;
+  // transmission constants: c2 = e^{-i pi/4} sqrt(2/dt) = (1-i)/sqrt(dt)
+  const double sq = std::sqrt(h->dt);
+  h->c2v = make_double2(1.0 / sq, -1.0 / sq);
+  h->c0 = (h->transmission == SWR_TC_ROBIN) ? make_double2(0.0, -h->robin_p) : h->c2v;  // beta_0 = 1
+  h->kappa = (2.0 / h->dt) * (h->dx / 6.0);
+  h->eim = (2.0 / h->dt) * (h->dx / 6.0);
+  h->shape = swr::choose_march_shape(h->Nj);
+  if (h->shape.M == 0 || swr::march_smem_bytes(h->shape, h->NT) > 227 * 1024) {
+    g_detail = "subdomain too large for the resident march (N_j = " + std::to_string(h->Nj) + ")";
+    delete h;
+    return SWR_ERR_UNSUPPORTED;
+  }
+  auto fail = [&](int s) { free_all(h); delete h; return s; };
+  int s;
+  const size_t nx1 = (size_t)h->Nx + 1, ng = h->ng, NTt = h->NT;
+  const bool precond = h->algorithm == SWR_ALG_PRECOND;
+  if ((s = dalloc(&h->u0, nx1)) || (s = dalloc(&h->beta, NTt + 1)) || (s = dalloc(&h->q, (size_t)h->N * h->Nj)) ||
+      (s = dalloc(&h->er, (size_t)h->N * h->Nj)) || (s = dalloc(&h->uloc, (size_t)h->N * h->Nj)) ||
+      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)3 * h->N + 4)) || (s = dalloc(&h->err_dev, 1)))
+    return fail(s);
+  if (h->potential == SWR_POT_VX && (s = dalloc(&h->Vx, nx1))) return fail(s);
+  if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
+  if (ng) {
+    const size_t mm = h->restart + 1;
+    if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
+        (s = dalloc(&h->V, mm * ng)) || (s = dalloc(&h->w, ng)) || (s = dalloc(&h->tmp, ng)) ||
+        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, 3 * mm * h->N)) ||
+        (s = dalloc(&h->dots, 3 * mm + 4)) || (s = dalloc(&h->ycoef, mm)))
+      return fail(s);
+    if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->Vin, mm * ng)) ||
+                    (s = dalloc(&h->win, ng))))
+      return fail(s);
+    if (cfg->g0 && (s = dalloc(&h->g0, ng))) return fail(s);
+  }
+  if (cudaMallocHost((void **)&h->hpin, sizeof(double2) * (3 * (h->restart + 1) + 8)) != cudaSuccess) return fail(SWR_ERR_OOM);
+  if (cudaEventCreate(&h->ev_b0) || cudaEventCreate(&h->ev_b1) || cudaEventCreate(&h->ev_s0) || cudaEventCreate(&h->ev_s1))
+    return fail(SWR_ERR_CUDA);
+  const bool od = cfg->inputs_on_device != 0;
+  if ((s = copy_in(h->u0, cfg->u0, nx1, od, h->st))) return fail(s);
+  if (h->Vx && (s = copy_in_r(h->Vx, cfg->V_x, nx1, od, h->st))) return fail(s);
+  if (h->g0 && (s = copy_in(h->g0, cfg->g0, ng, od, h->st))) return fail(s);
+  // beta_s: alpha_0 = 1, alpha_{2k} = alpha_{2k-2}(2k-1)/(2k), alpha_{2k+1} = alpha_{2k}
+  {
+    std::vector<double> al(NTt + 1), be(NTt + 1);
+    for (size_t sidx = 0; sidx <= NTt; sidx++) {
+      double a = sidx == 0 ? 1.0 : (sidx % 2 ? al[sidx - 1] : al[sidx - 2] * (double)(sidx - 1) / (double)sidx);
+      al[sidx] = a;
+      be[sidx] = (sidx % 2) ? -a : a;
+    }
+    if (cudaMemcpy(h->beta, be.data(), (NTt + 1) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+      return fail(SWR_ERR_CUDA);
+  }
+  if ((s = factor_matrices(h))) return fail(s);
+  *out = h;
+  return SWR_OK;
+}
+
+int swr_update_inputs(swr_handle *h, const double *u0, const double *V_x, int32_t on_device) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  const size_t nx1 = (size_t)h->Nx + 1;
+  if (u0) CKS(copy_in(h->u0, u0, nx1, on_device, h->st));
+  if (V_x && h->Vx) {
+    CKS(copy_in_r(h->Vx, V_x, nx1, on_device, h->st));
+    CKS(factor_matrices(h));
+    h->have_L = false;
+  }
+  h->have_d = false;
+  return SWR_OK;
+}
+
+int swr_build_interface_operator(swr_handle *h) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  h->march_ev_used = h->intf_ev_used = 0;
+  h->n_marches = h->n_launches = 0;
+  h->cell_steps = 0;
+  CK(cudaEventRecord(h->ev_b0, h->st));
+  if (h->N > 1) {
+    if (h->algorithm == SWR_ALG_NEW) {
+      CKS(build_probes(h, false, h->X, h->d));    // 3 RHS per interior subdomain
+      h->have_L = h->have_d = true;
+    } else {
+      CKS(build_probes(h, true, h->X0, nullptr));  // L0: 2 RHS per subdomain
+      h->have_L0 = true;
+      if (h->potential != SWR_POT_CUBIC) {
+        CKS(sweep_R(h, nullptr, true, false, h->d, nullptr));  // d = R(0; u0)
+        h->have_d = true;
+      }
+    }
+  }
+  CK(cudaEventRecord(h->ev_b1, h->st));
+  h->build_timed = true;
+  return SWR_OK;
+}
+
+int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  if (!h->build_timed) {
+    h->march_ev_used = h->intf_ev_used = 0;
+    h->n_marches = h->n_launches = 0;
+    h->cell_steps = 0;
+  }
+  CK(cudaEventRecord(h->ev_s0, h->st));
+  h->hist.clear();
+  h->iterations = h->inner_total = h->fp_max = 0;
+  h->converged = 1;
+  h->inner_fail = false;
+  int st = SWR_OK;
+  if (h->N > 1) {
+    if (h->g0) CK(cudaMemcpyAsync(h->g, h->g0, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+    else CKS(fill_zero(h, h->g, h->ng));
+    int it = 0, conv = 0;
+    if (h->algorithm == SWR_ALG_NEW) {
+      if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
+      Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
+      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->V, h->w, &it, &h->hist, &conv);
+    } else {
+      if (!h->have_L0 || !h->have_d) CKS(swr_build_interface_operator(h));
+      CKS(apply_Pinv(h, h->d, h->rhs));
+      Op A = [h](const double2 *a, double2 *b) -> int {
+        CKS(sweep_R(h, a, false, false, h->tmp, nullptr));
+        swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(a, h->tmp, h->tmp2, h->ng);
+        CK(cudaGetLastError());
+        return apply_Pinv(h, h->tmp2, b);
+      };
+      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->V, h->w, &it, &h->hist, &conv);
+    }
+    if (st && st != SWR_ERR_INNER_NOT_CONVERGED) return st;
+    h->iterations = it;
+    h->converged = conv;
+    h->have_g = true;
+  }
+  CKS(final_sweep(h, h->N > 1 ? h->g : nullptr));
+  CK(cudaEventRecord(h->ev_s1, h->st));
+  if (u_T && h->rank == 0)
+    CK(cudaMemcpyAsync(u_T, h->uT, ((size_t)h->Nx + 1) * sizeof(double2),
+                       u_T_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  if (rep) {
+    memset(rep, 0, sizeof(*rep));
+    rep->iterations = h->iterations;
+    rep->inner_iterations = h->inner_total;
+    rep->fp_max = h->fp_max;
+    rep->converged = h->converged;
+    rep->residual_history = h->hist.data();
+    rep->n_history = (int)h->hist.size();
+    float ms = 0;
+    if (h->build_timed && cudaEventElapsedTime(&ms, h->ev_b0, h->ev_b1) == cudaSuccess) rep->t_build_ms = ms;
+    if (cudaEventElapsedTime(&ms, h->ev_s0, h->ev_s1) == cudaSuccess) rep->t_solve_ms = ms;
+    rep->t_march_ms = sum_pairs(h, true);
+    rep->t_interface_ms = sum_pairs(h, false);
+    rep->cell_steps = h->cell_steps;
+    rep->n_marches = h->n_marches;
+    rep->n_kernel_launches = h->n_launches;
+  }
+  h->build_timed = false;
+  if (!h->converged) return SWR_NOT_CONVERGED;
+  if (h->inner_fail) return SWR_ERR_INNER_NOT_CONVERGED;
+  return st;
+}
+
+void swr_free(swr_handle *h) {
+  if (!h) return;
+  cudaStreamSynchronize(h->st);
+  free_all(h);
+  delete h;
+}
+
+int swr_apply_R(swr_handle *h, const double *g, int32_t use_u0, int32_t force_zero_potential, double *Rg,
+                double *u_T) {
+  if (!h || h->N < 1) return SWR_ERR_INVALID_ARG;
+  if (force_zero_potential && !h->q0) return SWR_ERR_UNSUPPORTED;
+  CKS(sweep_R(h, (const double2 *)g, use_u0 != 0, force_zero_potential != 0, (double2 *)Rg,
+              u_T ? h->uloc : nullptr));
+  if (u_T) {
+    swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, (double2 *)u_T);
+    CK(cudaGetLastError());
+  }
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
+int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  if ((which == 0 && !h->have_L) || (which == 1 && !h->have_L0)) return SWR_ERR_INVALID_ARG;
+  CKS(apply_I_minus_L(h, which == 1, (const double2 *)x, (double2 *)y));
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
+int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X) {
+  if (!h) return SWR_ERR_INVALID_ARG;
+  if (d && h->have_d) CK(cudaMemcpyAsync(d, h->d, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  const double2 *src = which ? h->X0 : h->X;
+  if (X && src) CK(cudaMemcpyAsync(X, src, (size_t)h->N * 4 * h->NT * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
+int swr_get_g(swr_handle *h, double *g) {
+  if (!h || !h->have_g) return SWR_ERR_INVALID_ARG;
+  CK(cudaMemcpyAsync(g, h->g, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,73 @@
+// swr_common.cuh — device helpers and host/device structs of the B200 SWR
+// hot path (PAPER.md = Besse & Xing, arXiv:1503.02564; "P:n" = line n).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace swr {
+
+// ---- complex fp64 on double2 (x = re, y = im) ---------------------------
+__host__ __device__ __forceinline__ double2 cz() { return make_double2(0.0, 0.0); }
+__host__ __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
+__host__ __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
+__host__ __device__ __forceinline__ double2 cscale(double s, double2 a) { return make_double2(s * a.x, s * a.y); }
+__device__ __forceinline__ double2 cmul(double2 a, double2 b) {
+  return make_double2(fma(a.x, b.x, -a.y * b.y), fma(a.x, b.y, a.y * b.x));
+}
+// a*b + c
+__device__ __forceinline__ double2 cfma(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(-a.y, b.y, c.x)), fma(a.x, b.y, fma(a.y, b.x, c.y)));
+}
+// conj(a)*b + c
+__device__ __forceinline__ double2 cfmaconj(double2 a, double2 b, double2 c) {
+  return make_double2(fma(a.x, b.x, fma(a.y, b.y, c.x)), fma(a.x, b.y, fma(-a.y, b.x, c.y)));
+}
+__device__ __forceinline__ double2 crcp(double2 a) {
+  double d = 1.0 / fma(a.x, a.x, a.y * a.y);
+  return make_double2(a.x * d, -a.y * d);
+}
+// i * kappa * a
+__device__ __forceinline__ double2 cimul(double kappa, double2 a) { return make_double2(-kappa * a.y, kappa * a.x); }
+__device__ __forceinline__ double2 shfl_up2(double2 v, int o) {
+  return make_double2(__shfl_up_sync(0xffffffffu, v.x, o), __shfl_up_sync(0xffffffffu, v.y, o));
+}
+__device__ __forceinline__ double2 shfl_down2(double2 v, int o) {
+  return make_double2(__shfl_down_sync(0xffffffffu, v.x, o), __shfl_down_sync(0xffffffffu, v.y, o));
+}
+__device__ __forceinline__ double2 shfl_xor2(double2 v, int o) {
+  return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+// ---- one whole-window march of one system (subdomain j, one RHS) ---------
+enum : int32_t {
+  SYS_HAS_LEFT = 1,      // interface at a_j (j >= 2): B row 0, flux l_j in, r_{j-1} out
+  SYS_HAS_RIGHT = 2,     // interface at b_j (j <= N-1)
+  SYS_LIN_IMPULSE = 4,   // l_{j,n} = delta_{n,1} (probe)
+  SYS_RIN_IMPULSE = 8,   // r_{j,n} = delta_{n,1} (probe)
+};
+
+struct MarchSys {
+  const double2 *lin;      // [N_T] incoming l_{j,n} (NULL = 0)
+  const double2 *rin;      // [N_T] incoming r_{j,n}
+  double2 *out_left;       // [N_T] r_{j-1,n} = -l_{j,n} + 2 S v_{j,n}(a_j)   (eq. 8)
+  double2 *out_right;      // [N_T] l_{j+1,n} = -r_{j,n} + 2 S v_{j,n}(b_j)
+  double2 *uT;             // [N_j] u_{N_T} on the subdomain (NULL = skip)
+  const double2 *u0;       // [N_j] u_0 restricted (NULL = 0)
+  const double2 *q;        // [N_j] pivot reciprocals 1/p_k of (A - B)
+  const double *er;        // [N_j] Re E_k, E_k = (A-B)_{k,k+1}
+  int32_t flags;
+  int32_t pad_;
+};
+
+struct MarchParams {
+  const MarchSys *sys;
+  int32_t nsys, Nj, NT, CS;  // CS = CTAs per system (thread-block cluster)
+  double e_im;               // Im E_k = (2/dt)(h/6), constant on the uniform mesh
+  double kappa;              // (2/dt)(h/6): rhs = i kappa (u_{k-1} + 4u_k + u_{k+1})
+  double2 c0;                // leading coefficient of the transmission operator
+  double2 c2;                // e^{-i pi/4} sqrt(2/dt) (S0^2)
+  int32_t s02;               // 1: S0^2 history convolution, 0: Robin
+  const double *beta;        // [N_T+1] beta_s
+};
+
+}  // namespace swr

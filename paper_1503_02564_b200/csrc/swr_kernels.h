@@ -1,0 +1,31 @@
+// swr_kernels.h — kernel declarations shared by the host orchestration.
+#pragma once
+#include "swr_common.cuh"
+
+namespace swr {
+
+struct FactorJob {
+  const double *W;   // nodal W on the subdomain [N_j] (NULL = 0)
+  int32_t has_left, has_right;
+  double2 *q;        // [N_j] out: 1/p_k
+  double *er;        // [N_j] out: Re E_k
+};
+
+__global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0, int *err);
+__global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, int N, int NT);
+__global__ void k_multidot_partial(const double2 *V, size_t ldv, int nvec, const double2 *w, double2 *partial,
+                                   int N, int NT);
+__global__ void k_multidot_final(const double2 *partial, int nvec, int N, double2 *out);
+__global__ void k_multi_axpy(const double2 *V, size_t ldv, int nvec, const double2 *h, double2 *w, size_t n);
+__global__ void k_axpby(double2 a, const double2 *x, double2 b, double2 *y, size_t n);
+__global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);
+__global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const double2 *y, double2 *x, size_t n);
+__global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, double2 *uT);
+__global__ void k_fill(double2 *x, double2 v, size_t n);
+
+struct MarchShape { int M, P, CS; };
+MarchShape choose_march_shape(int Nj);
+size_t march_smem_bytes(const MarchShape &s, int NT);
+cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
+
+}  // namespace swr
