@@ -1,0 +1,323 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 SWR hot path (driver contract).
+
+One *step* = one pass of the whole hot path on resident inputs:
+swr_build_interface_operator (the batched 3-RHS march building d and the
+Toeplitz interface matrix L) + swr_solve (GMRES on (I-L)g = d and
+the final sweep, Algorithm 3).  Workload (N=1): BASELINE.json
+configs[4] at N = 500 (C5), the north_star's 500-subdomain configuration:
+V = -x^2, Gaussian u0, (a0,b0) = (-21,21), dx = 1e-5, dt = 1e-3, T = 0.5,
+S0^2 transmission, zero g0.
+
+metric: subdomain cell-steps per second over the whole time-to-solution
+(cell-steps = sum over marches of sum_j N_j * N_T * RHS); ms_per_step is the
+time to solution.
+
+  python bench.py [--gpus N --steps K --warmup W] [--impl reference]
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import swr_inputs as si  # noqa: E402
+
+METRIC = "SWR time-to-solution; subdomain cell-steps/s and % of HBM roofline"
+UNIT = "cell-steps/s"
+PAPER_T_NEW_GMRES_N500_S = 6.86      # 500 Sandy Bridge cores
+FLOP_PER_CELL_STEP = 36.0            # algorithmic flops of one CN cell-step
+BYTES_PER_CELL_STEP = 32.0           # u_{n-1} read + u_n write, complex fp64
+FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 DFMA/clk at 1965 MHz
+TOEPLITZ_FLOP = 8.0                  # per complex multiply-add of the causal convolution
+
+
+def load_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return {}
+
+
+class ClockSampler:
+    """nvidia-smi clocks/throttle reasons sampled during the timed region."""
+
+    FIELDS = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+              "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.rows = []
+        self.proc = None
+        self.thread = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.FIELDS}",
+                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+            return
+        self.thread = threading.Thread(target=self._read, daemon=True)
+        self.thread.start()
+
+    def _read(self):
+        for line in self.proc.stdout:
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) == 6:
+                self.rows.append(parts)
+
+    def stop(self):
+        if self.proc:
+            time.sleep(0.25)
+            self.proc.terminate()
+            try:
+                self.proc.wait(2)
+            except Exception:
+                self.proc.kill()
+        if self.thread:
+            self.thread.join(1)
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows for i in range(4) if r[2 + i].lower().startswith("active")})
+        under = [s for s in sm if s > 0.5 * (max(mx) if mx else 1)] or sm
+        return {"sm_mhz": statistics.median(under) if under else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def dist_env():
+    return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
+
+
+def oracle_cpu_sample(p, arrays, seconds: float, max_subdomains: int | None = None):
+    """The oracle as it stands (single-threaded C): marches of whole C5
+    subdomains with the d right-hand side until ~seconds of CPU work."""
+    from oracle import oracle
+    o = oracle.Oracle(p, arrays)
+    t0 = time.perf_counter()
+    cells = 0
+    nsub = 0
+    order = list(range(1, p.N + 1))
+    rng = np.random.default_rng(0)
+    rng.shuffle(order)
+    for j in order:
+        o.march(j, None, None, use_u0=True)
+        cells += p.Nj * p.NT
+        nsub += 1
+        if time.perf_counter() - t0 >= seconds or (max_subdomains and nsub >= max_subdomains):
+            break
+    dt = time.perf_counter() - t0
+    return cells / dt, dt, nsub, cells
+
+
+def run_reference(args, p, arrays):
+    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return
+    per_step = max(1, args.ref_subdomains)
+    from oracle import oracle
+    o = oracle.Oracle(p, arrays)
+    order = list(range(1, p.N + 1))
+    times, cells = [], 0
+
+    def step(k):
+        nonlocal cells
+        c = 0
+        for i in range(per_step):
+            j = order[(k * per_step + i) % p.N]
+            o.march(j, None, None, use_u0=True)
+            c += p.Nj * p.NT
+        return c
+
+    for k in range(args.warmup):
+        step(k)
+    for k in range(args.steps):
+        t0 = time.perf_counter()
+        cells += step(args.warmup + k)
+        times.append(time.perf_counter() - t0)
+    total = sum(times)
+    value = cells / total
+    sample = (f"oracle or_march of {per_step} full C5 subdomains per step (N_j={p.Nj}, N_T={p.NT}, d RHS), "
+              f"single-threaded C, GMRES not sampled")
+    line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": workload_config(p),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def workload_config(p):
+    return {"workload": f"{p.name}: V=-x^2 NEW+GMRES(30) CGS2, N={p.N}, dx={p.dx:g}, dt={p.dt:g}, T={p.T:g}, "
+                        f"S0^2, Gaussian u0, zero g0 (BASELINE configs[4] at N=500)",
+            "N_subdomains": p.N, "N_x": p.Nx, "N_T": p.NT, "N_j": p.Nj,
+            "cell_steps_per_step": (3 * p.N - 2 + p.N) * p.Nj * p.NT,
+            "parallelism": None, "l2": "flushed before every timed step (256 MiB write)"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--config", default="C5")
+    ap.add_argument("--cpu-seconds", type=float, default=12.0)
+    ap.add_argument("--ref-subdomains", type=int, default=4)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    args = ap.parse_args()
+
+    p = si.config(args.config)
+    arrays = si.inputs(p)
+    if args.impl == "reference":
+        run_reference(args, p, arrays)
+        return
+
+    import torch
+    rank, world, local = dist_env()
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_1503_02564_b200 import SWR
+    stream = torch.cuda.Stream(dev)
+    s = SWR(p, arrays, device=local, stream=stream)
+    uT_dev = torch.empty(p.Nx + 1, dtype=torch.complex128, device=dev)
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=dev)
+
+    def one_step(out):
+        s.build()
+        return s.solve(out=out)
+
+    with torch.cuda.stream(stream):
+        for _ in range(args.warmup):
+            one_step(uT_dev)
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            torch.distributed.barrier()
+        sampler = ClockSampler(local)
+        sampler.start()
+        evs = []
+        reps = []
+        wall0 = time.perf_counter()
+        for _ in range(args.steps):
+            flush.fill_(1.0)
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            st, _, rep = one_step(uT_dev)
+            e1.record(stream)
+            evs.append((e0, e1))
+            reps.append(rep)
+        torch.cuda.synchronize(dev)
+        wall = time.perf_counter() - wall0
+        if world > 1:
+            torch.distributed.barrier()
+        clocks = sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = sum(step_ms) / len(step_ms)
+    if world > 1:
+        t = torch.tensor([ms], device=dev, dtype=torch.float64)
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms = float(t.item())
+    cells = statistics.mean(r["cell_steps"] for r in reps) * world
+    value = cells / (ms / 1e3)
+    t_march = statistics.mean(r["t_march_ms"] for r in reps)
+    t_intf = statistics.mean(r["t_interface_ms"] for r in reps)
+    n_march = reps[0]["n_marches"]
+    launches = sum(r["n_kernel_launches"] for r in reps)
+    iters = reps[-1]["iterations"]
+    cells_rank = statistics.mean(r["cell_steps"] for r in reps)
+    peaks = load_peaks()
+    hbm = peaks.get("hbm_gbs", 6538.6)
+
+    # roofline of the dominant kernel class (the march): FP64-ALU bound
+    # (state register-resident for the whole window)
+    march_flops = FLOP_PER_CELL_STEP * cells_rank
+    achieved = march_flops / (t_march / 1e3) / 1e12
+    roof = {"bound": "alu", "kernel": "k_march_resident", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
+            "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
+            "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+            "algorithmic": f"{FLOP_PER_CELL_STEP:g} flop/cell-step x {cells_rank:.4g} cell-steps over {n_march} launches",
+            "avg_launch_ms": t_march / max(n_march, 1)}
+    prof = os.path.join(ROOT, "profiles", "march_traffic.json")
+    if os.path.exists(prof):
+        try:
+            roof["traffic"] = json.load(open(prof)).get("dram_bytes_per_launch")
+        except Exception:
+            pass
+    hbm_equiv = BYTES_PER_CELL_STEP * cells_rank / (t_march / 1e3) / 1e9
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms, "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": value / (cells / PAPER_T_NEW_GMRES_N500_S) if args.config == "C5" else None,
+            "dtype": "f64", "data": "synthetic", "config": workload_config(p),
+            "time_to_solution_ms": ms, "gmres_iterations": iters,
+            "hbm_roofline_frac": hbm_equiv / hbm,
+            "breakdown_ms": {"march": t_march, "toeplitz": t_intf, "krylov_vector_and_host": ms - t_march - t_intf},
+            "roofline": roof, "gpu_launches": launches, "clocks": clocks, "wall_s_timed": wall}
+    line["config"]["parallelism"] = f"replicas x{world} (sharded path not enabled yet)" if world > 1 else "1 GPU"
+    line["roofline_interface"] = {
+        "bound": "alu", "kernel": "k_toeplitz_I_minus_L",
+        "achieved": TOEPLITZ_FLOP * (4 * (p.N - 2) + 2) * p.NT * (p.NT + 1) / 2 * iters / (t_intf / 1e3) / 1e12
+        if t_intf > 0 else None, "peak": FP64_PEAK_TFLOPS, "unit": "TFLOP/s"}
+    if line["roofline_interface"]["achieved"]:
+        line["roofline_interface"]["frac"] = line["roofline_interface"]["achieved"] / FP64_PEAK_TFLOPS
+
+    # e2e: host buffers through the public API, H2D of the inputs and D2H of u(T)
+    if not args.no_e2e:
+        pin_u0 = torch.from_numpy(arrays["u0"]).pin_memory()
+        pin_vx = torch.from_numpy(arrays["V_x"]).pin_memory() if arrays["V_x"] is not None else None
+        out_h = torch.empty(p.Nx + 1, dtype=torch.complex128).pin_memory()
+        with torch.cuda.stream(stream):
+            s.update_inputs(u0=pin_u0, V_x=pin_vx, on_device=False)
+            one_step(out_h.numpy())
+            torch.cuda.synchronize(dev)
+            e_ms = []
+            for _ in range(max(1, min(args.steps, 3))):
+                flush.fill_(1.0)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                e0.record(stream)
+                s.update_inputs(u0=pin_u0, V_x=pin_vx, on_device=False)
+                one_step(out_h.numpy())
+                e1.record(stream)
+                e1.synchronize()
+                e_ms.append(e0.elapsed_time(e1))
+        em = sum(e_ms) / len(e_ms)
+        bi = pin_u0.numel() * 16 + (pin_vx.numel() * 8 if pin_vx is not None else 0)
+        line["e2e"] = {"value": cells / (em / 1e3), "unit": UNIT, "h2d_bytes_per_step": bi,
+                       "d2h_bytes_per_step": out_h.numel() * 16, "ms_per_step": em,
+                       "path": "swr_update_inputs(host u0, V_x) + swr_build_interface_operator + swr_solve(host u_T)"}
+
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        v, dt, nsub, c = oracle_cpu_sample(p, arrays, args.cpu_seconds)
+        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
+                                "sample": f"oracle or_march of {nsub} whole C5 subdomains ({c:.3g} cell-steps, d RHS, "
+                                          f"{dt:.1f} s single-threaded); GMRES not sampled"}
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

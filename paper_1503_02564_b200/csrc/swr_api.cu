@@ -7,9 +7,11 @@
 #include "swr.h"
 #include "swr_kernels.h"
 
+#include <algorithm>
 #include <cmath>
 #include <complex>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <functional>
 #include <string>
@@ -106,6 +108,16 @@ inline unsigned grid_for(size_t n, int bs = 256) {
   return (unsigned)(g ? g : 1);
 }
 
+// Krylov workspace of one GMRES instance (outer and inner P^{-1} solves
+// have their own, so the outer speculation never races the inner solve).
+struct Krylov {
+  double2 *V, *w;
+  double2 *dots;        // device [2][3(m+2)+8]: per-iteration scalars, double-buffered
+  double2 *hp;          // pinned mirror, same layout
+  double2 *ycoef;       // device [m]
+  cudaEvent_t ev[2];
+};
+
 }  // namespace
 
 struct swr_handle {
@@ -126,12 +138,16 @@ struct swr_handle {
   double *er = nullptr, *er0 = nullptr;
   double2 *d = nullptr, *X = nullptr, *X0 = nullptr, *g = nullptr, *g0 = nullptr;
   double2 *uloc = nullptr, *uT = nullptr;
-  double2 *V = nullptr, *Vin = nullptr;    // outer / inner Krylov bases [(m+1) n_g]
-  double2 *w = nullptr, *win = nullptr, *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
-  double2 *partial = nullptr, *dots = nullptr, *ycoef = nullptr;
-  double2 *hpin = nullptr;                 // pinned host scalars
+  double2 *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
+  // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0, transformed inputs
+  int log4 = 0;
+  double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr, *Fx = nullptr;
+  double2 *partial = nullptr;
+  Krylov kout = {}, kin = {};             // outer / inner (P^{-1}) GMRES workspaces
+  double2 *hpin = nullptr;                 // pinned scalars for restarts and norms
   MarchSys *sys_dev = nullptr;
   int *err_dev = nullptr;
+  unsigned *counter = nullptr;
   swr::FactorJob *jobs_dev = nullptr;
   bool have_L = false, have_L0 = false, have_d = false, have_g = false;
   // report
@@ -312,17 +328,31 @@ typedef std::function<int(const double2 *, double2 *)> Op;
 
 // GMRES(m) with CGS2 and complex Givens rotations, the same algorithm as the
 // oracle (reading A5/A6): stop at |gamma_{k+1}| <= tol ||b||, true residual
-// at restarts, happy breakdown at h_{k+1,k} <= 1e-14 ||A v_k||.
-int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, double2 *V,
-          double2 *w, int *iters, std::vector<double> *hist, int *converged) {
+// at restarts, happy breakdown at h_{k+1,k} <= 1e-14 ||A v_k||.  Device work
+// per Arnoldi step: the operator, three fused CGS kernels (dots; axpy+dots;
+// axpy+norm) and the normalisation; one host round trip for the Givens
+// update.
+int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w, int mode, double2 *out) {
+  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st));
+  h->n_launches++;
+  return SWR_OK;
+}
+
+int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, Krylov &K,
+          int *iters, std::vector<double> *hist, int *converged) {
   const size_t n = h->ng;
   const size_t ldv = n;
+  double2 *V = K.V, *w = K.w;
   *iters = 0;
   *converged = 0;
-  double2 *hp = h->hpin;  // pinned scratch: [0] bnorm^2, [1..] dots
-  CKS(multidot(h, b, 1, b, h->dots));
-  CKS(fetch(h, h->dots, 1, hp));
-  const double bnorm = std::sqrt(hp[0].x);
+  const int stride = 3 * (m + 2) + 8;
+  auto O1 = [&](int par) { return K.dots + (size_t)par * stride; };
+  auto O2 = [&](int par) { return K.dots + (size_t)par * stride + (m + 2); };
+  auto O3 = [&](int par) { return K.dots + (size_t)par * stride + 2 * (m + 2); };
+  auto HP = [&](int par) { return K.hp + (size_t)par * stride; };
+  CKS(cgs(h, nullptr, 0, nullptr, const_cast<double2 *>(b), swr::CGS_NORM, O3(0)));
+  CKS(fetch(h, O3(0), 1, HP(0) + 2 * (m + 2)));
+  const double bnorm = std::sqrt(HP(0)[2 * (m + 2)].x);
   if (bnorm == 0.0) {
     CKS(fill_zero(h, x, n));
     *converged = 1;
@@ -332,47 +362,50 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
   std::vector<double> cs(m);
   auto Hm = [&](int i, int k) -> cplx & { return H[(size_t)i * m + k]; };
   int total = 0, done = 0, st = SWR_OK;
+  // device work of Arnoldi step k: w = A v_k, CGS2, v_{k+1} = w/||w||,
+  // scalars -> pinned buffer (k & 1), event.  No host dependency, so step
+  // k+1 is issued before the host reads step k's scalars.
+  auto issue = [&](int k) -> int {
+    const int par = k & 1;
+    int s = A(V + (size_t)k * ldv, w);
+    if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
+    if (s) st = s;
+    CKS(cgs(h, V, k + 1, nullptr, w, swr::CGS_DOTS | swr::CGS_NORM, O1(par)));                 // h1, ||w||^2
+    CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_DOTS, O2(par)));                // w -= V h1; h2
+    CKS(cgs(h, V, k + 1, O2(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par)));  // w -= V h2
+    swr::k_scale_dev<<<grid_for(n), 256, 0, h->st>>>(w, O3(par) + 1, V + (size_t)(k + 1) * ldv, n);
+    CK(cudaGetLastError());
+    h->n_launches++;
+    CK(cudaMemcpyAsync(HP(par), O1(par), stride * sizeof(double2), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaEventRecord(K.ev[par], h->st));
+    return SWR_OK;
+  };
   while (!done) {
     CKS(A(x, w));
     swr::k_sub<<<grid_for(n), 256, 0, h->st>>>(b, w, V, n);
     CK(cudaGetLastError());
-    CKS(multidot(h, V, 1, V, h->dots));
-    CKS(fetch(h, h->dots, 1, hp));
-    const double beta = std::sqrt(hp[0].x);
+    h->n_launches++;
+    CKS(cgs(h, nullptr, 0, nullptr, V, swr::CGS_NORM, O3(0)));
+    CKS(fetch(h, O3(0), 1, HP(0) + 2 * (m + 2)));
+    const double beta = std::sqrt(HP(0)[2 * (m + 2)].x);
     if (beta <= tol * bnorm) { *converged = 1; break; }
     if (total >= maxit) break;
     swr::k_axpby<<<grid_for(n), 256, 0, h->st>>>(make_double2(0, 0), V, make_double2(1.0 / beta, 0), V, n);
     CK(cudaGetLastError());
+    h->n_launches++;
     std::fill(gam.begin(), gam.end(), cplx(0));
     gam[0] = beta;
     int k, kend = 0;
+    CKS(issue(0));
     for (k = 0; k < m; k++) {
-      const double2 *vk = V + (size_t)k * ldv;
-      double2 *vk1 = V + (size_t)(k + 1) * ldv;
-      int s = A(vk, w);
-      if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
-      if (s) st = s;
+      if (k + 1 < m && total + 1 < maxit) CKS(issue(k + 1));   // speculative next step
+      CK(cudaEventSynchronize(K.ev[k & 1]));
+      const double2 *hp = HP(k & 1);
       total++;
-      // ||w|| before, two CGS passes, ||w|| after — one host round trip
-      CKS(multidot(h, w, 1, w, h->dots));
-      CKS(multidot(h, V, k + 1, w, h->dots + 1));
-      swr::k_multi_axpy<<<grid_for(n), 256, 0, h->st>>>(V, ldv, k + 1, h->dots + 1, w, n);
-      CK(cudaGetLastError());
-      CKS(multidot(h, V, k + 1, w, h->dots + 1 + (m + 1)));
-      swr::k_multi_axpy<<<grid_for(n), 256, 0, h->st>>>(V, ldv, k + 1, h->dots + 1 + (m + 1), w, n);
-      CK(cudaGetLastError());
-      CKS(multidot(h, w, 1, w, h->dots + 2 * (m + 1) + 1));
-      h->n_launches += 3;
-      CKS(fetch(h, h->dots, 2 * (m + 1) + 2, hp));
-      const double wn0 = std::sqrt(hp[0].x);
-      for (int i = 0; i <= k; i++) Hm(i, k) = c2(hp[1 + i]) + c2(hp[1 + (m + 1) + i]);
-      const double hk1 = std::sqrt(hp[2 * (m + 1) + 1].x);
+      const double wn0 = std::sqrt(hp[k + 1].x);
+      for (int i = 0; i <= k; i++) Hm(i, k) = c2(hp[i]) + c2(hp[(m + 2) + i]);
+      const double hk1 = std::sqrt(hp[2 * (m + 2)].x);
       const bool breakdown = hk1 <= 1e-14 * wn0;
-      if (!breakdown) {
-        swr::k_axpby<<<grid_for(n), 256, 0, h->st>>>(make_double2(1.0 / hk1, 0), w, make_double2(0, 0), vk1, n);
-        CK(cudaGetLastError());
-        h->n_launches++;
-      }
       for (int i = 0; i < k; i++) {
         cplx t = cs[i] * Hm(i, k) + sn[i] * Hm(i + 1, k);
         Hm(i + 1, k) = -std::conj(sn[i]) * Hm(i, k) + cs[i] * Hm(i + 1, k);
@@ -403,25 +436,46 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
       for (int qq = i + 1; qq < kend; qq++) acc -= Hm(i, qq) * y[qq];
       y[i] = acc / Hm(i, i);
     }
-    for (int i = 0; i < kend; i++) hp[i] = d2(y[i]);
-    CK(cudaMemcpyAsync(h->ycoef, hp, kend * sizeof(double2), cudaMemcpyHostToDevice, h->st));
-    swr::k_multi_update<<<grid_for(n), 256, 0, h->st>>>(V, ldv, kend, h->ycoef, x, n);
+    CK(cudaStreamSynchronize(h->st));  // retire speculative work before reusing the pinned buffer
+    double2 *hy = HP(0);
+    for (int i = 0; i < kend; i++) hy[i] = d2(y[i]);
+    CK(cudaMemcpyAsync(K.ycoef, hy, kend * sizeof(double2), cudaMemcpyHostToDevice, h->st));
+    swr::k_multi_update<<<grid_for(n), 256, 0, h->st>>>(V, ldv, kend, K.ycoef, x, n);
     CK(cudaGetLastError());
-    CK(cudaStreamSynchronize(h->st));  // hp reused
+    h->n_launches++;
+    CK(cudaStreamSynchronize(h->st));
   }
   *iters = total;
   return st;
 }
 
-// y = (I - L) x or (I - L0) x
+// y = (I - L) x or (I - L0) x: FFT convolution (default when N_T <= 512)
+// or the direct causal-convolution kernel.
 int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
-  const double2 *X = zero ? h->X0 : h->X;
-  const int nslots = 2 * h->N - 2;
-  if (nslots <= 0) return SWR_OK;
+  if (h->N < 2) return SWR_OK;
   CKS(record_pair(h, false, true));
-  swr::k_toeplitz_I_minus_L<<<nslots, 256, 4 * h->NT * sizeof(double2), h->st>>>(X, x, y, h->N, h->NT);
-  CK(cudaGetLastError());
+  if (h->log4) {
+    CK(swr::launch_fft_fwd(h->log4, x, h->NT, 2 * h->N - 2, h->NT, h->tw, h->Fx, h->st));
+    CK(swr::launch_fft_apply(h->log4, zero ? h->FX0 : h->FX, h->Fx, x, y, h->N, h->NT, h->tw, h->st));
+    h->n_launches += 2;
+  } else {
+    const double2 *X = zero ? h->X0 : h->X;
+    const int G = (h->NT + swr::TR - 1) / swr::TR;
+    const int thr = (2 * ((G + 1) / 2) + 31) / 32 * 32;
+    const size_t smem = (4 * ((size_t)h->NT + 3 * swr::TR) + 2 * ((size_t)h->NT + swr::TR)) * sizeof(double2);
+    if (smem > 48 * 1024) CK(cudaFuncSetAttribute(swr::k_toeplitz_I_minus_L, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    swr::k_toeplitz_I_minus_L<<<h->N, thr, smem, h->st>>>(X, x, y, h->N, h->NT);
+    CK(cudaGetLastError());
+    h->n_launches++;
+  }
   CKS(record_pair(h, false, false));
+  return SWR_OK;
+}
+
+// transforms of the first columns, once per build
+int transform_columns(swr_handle *h, bool zero) {
+  if (!h->log4) return SWR_OK;
+  CK(swr::launch_fft_fwd(h->log4, zero ? h->X0 : h->X, h->NT, 4 * h->N, h->NT, h->tw, zero ? h->FX0 : h->FX, h->st));
   h->n_launches++;
   return SWR_OK;
 }
@@ -431,7 +485,7 @@ int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   CKS(fill_zero(h, x, h->ng));
   Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
   int it = 0, conv = 0;
-  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->Vin, h->win, &it, nullptr, &conv);
+  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->kin, &it, nullptr, &conv);
   h->inner_total += it;
   if (!conv) h->inner_fail = true;
   return s;
@@ -481,12 +535,31 @@ int copy_in_r(double *dst, const double *src, size_t n, bool on_dev, cudaStream_
   return SWR_OK;
 }
 
+int alloc_krylov(Krylov &K, size_t mm, size_t ng) {
+  const size_t stride = 3 * (mm + 1) + 8;
+  int s;
+  if ((s = dalloc(&K.V, mm * ng)) || (s = dalloc(&K.w, ng)) || (s = dalloc(&K.dots, 2 * stride)) ||
+      (s = dalloc(&K.ycoef, mm)))
+    return s;
+  if (cudaMallocHost((void **)&K.hp, 2 * stride * sizeof(double2)) != cudaSuccess) return SWR_ERR_OOM;
+  for (int i = 0; i < 2; i++)
+    if (cudaEventCreateWithFlags(&K.ev[i], cudaEventDisableTiming) != cudaSuccess) return SWR_ERR_CUDA;
+  return SWR_OK;
+}
+
 void free_all(swr_handle *h) {
   void *ptrs[] = {h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
-                  h->uloc, h->uT, h->V, h->Vin, h->w, h->win, h->tmp, h->tmp2, h->rhs, h->partial,
-                  h->dots, h->ycoef, h->sys_dev, h->err_dev, h->jobs_dev};
+                  h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
+                  h->sys_dev, h->err_dev, h->jobs_dev, h->counter};
   for (void *p : ptrs)
     if (p) cudaFree(p);
+  for (Krylov *K : {&h->kout, &h->kin}) {
+    for (void *p : {(void *)K->V, (void *)K->w, (void *)K->dots, (void *)K->ycoef})
+      if (p) cudaFree(p);
+    if (K->hp) cudaFreeHost(K->hp);
+    for (int i = 0; i < 2; i++)
+      if (K->ev[i]) cudaEventDestroy(K->ev[i]);
+  }
   if (h->hpin) cudaFreeHost(h->hpin);
   for (auto &e : h->march_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
   for (auto &e : h->intf_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
@@ -582,23 +655,34 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   const bool precond = h->algorithm == SWR_ALG_PRECOND;
   if ((s = dalloc(&h->u0, nx1)) || (s = dalloc(&h->beta, NTt + 1)) || (s = dalloc(&h->q, (size_t)h->N * h->Nj)) ||
       (s = dalloc(&h->er, (size_t)h->N * h->Nj)) || (s = dalloc(&h->uloc, (size_t)h->N * h->Nj)) ||
-      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)3 * h->N + 4)) || (s = dalloc(&h->err_dev, 1)))
+      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)3 * h->N + 4)) || (s = dalloc(&h->err_dev, 1)) ||
+      (s = dalloc(&h->counter, 1)))
     return fail(s);
   if (h->potential == SWR_POT_VX && (s = dalloc(&h->Vx, nx1))) return fail(s);
   if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
   if (ng) {
     const size_t mm = h->restart + 1;
     if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
-        (s = dalloc(&h->V, mm * ng)) || (s = dalloc(&h->w, ng)) || (s = dalloc(&h->tmp, ng)) ||
-        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, 3 * mm * h->N)) ||
-        (s = dalloc(&h->dots, 3 * mm + 4)) || (s = dalloc(&h->ycoef, mm)))
+        (s = alloc_krylov(h->kout, mm, ng)) || (s = dalloc(&h->tmp, ng)) ||
+        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, 4 * (mm + 2) * h->N)) ||
+        false)
       return fail(s);
-    if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->Vin, mm * ng)) ||
-                    (s = dalloc(&h->win, ng))))
+    if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, ng))))
       return fail(s);
     if (cfg->g0 && (s = dalloc(&h->g0, ng))) return fail(s);
+    const char *tmode = getenv("SWR_TOEPLITZ");
+    h->log4 = (tmode && strcmp(tmode, "direct") == 0) ? 0 : swr::fft_log4_for(h->NT);
+    if (h->log4) {
+      const size_t NF = (size_t)1 << (2 * h->log4);
+      if ((s = dalloc(&h->tw, NF)) || (s = dalloc(&h->FX, (size_t)h->N * 4 * NF)) ||
+          (s = dalloc(&h->Fx, (size_t)(2 * h->N - 2) * NF)) || (precond && (s = dalloc(&h->FX0, (size_t)h->N * 4 * NF))))
+        return fail(s);
+      swr::k_twiddles<<<(unsigned)((NF + 255) / 256), 256, 0, h->st>>>(h->tw, (int)NF);
+      if (cudaGetLastError() != cudaSuccess) return fail(SWR_ERR_CUDA);
+    }
   }
-  if (cudaMallocHost((void **)&h->hpin, sizeof(double2) * (3 * (h->restart + 1) + 8)) != cudaSuccess) return fail(SWR_ERR_OOM);
+  if (cudaMallocHost((void **)&h->hpin, sizeof(double2) * (3 * (h->restart + 1) + 16)) != cudaSuccess) return fail(SWR_ERR_OOM);
+  if (h->counter && cudaMemset(h->counter, 0, sizeof(unsigned)) != cudaSuccess) return fail(SWR_ERR_CUDA);
   if (cudaEventCreate(&h->ev_b0) || cudaEventCreate(&h->ev_b1) || cudaEventCreate(&h->ev_s0) || cudaEventCreate(&h->ev_s1))
     return fail(SWR_ERR_CUDA);
   const bool od = cfg->inputs_on_device != 0;
@@ -643,9 +727,11 @@ int swr_build_interface_operator(swr_handle *h) {
   if (h->N > 1) {
     if (h->algorithm == SWR_ALG_NEW) {
       CKS(build_probes(h, false, h->X, h->d));    // 3 RHS per interior subdomain
+      CKS(transform_columns(h, false));
       h->have_L = h->have_d = true;
     } else {
       CKS(build_probes(h, true, h->X0, nullptr));  // L0: 2 RHS per subdomain
+      CKS(transform_columns(h, true));
       h->have_L0 = true;
       if (h->potential != SWR_POT_CUBIC) {
         CKS(sweep_R(h, nullptr, true, false, h->d, nullptr));  // d = R(0; u0)
@@ -678,7 +764,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
     if (h->algorithm == SWR_ALG_NEW) {
       if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
       Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
-      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->V, h->w, &it, &h->hist, &conv);
+      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv);
     } else {
       if (!h->have_L0 || !h->have_d) CKS(swr_build_interface_operator(h));
       CKS(apply_Pinv(h, h->d, h->rhs));
@@ -688,7 +774,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         CK(cudaGetLastError());
         return apply_Pinv(h, h->tmp2, b);
       };
-      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->V, h->w, &it, &h->hist, &conv);
+      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv);
     }
     if (st && st != SWR_ERR_INNER_NOT_CONVERGED) return st;
     h->iterations = it;

@@ -12,6 +12,7 @@ struct FactorJob {
 };
 
 __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0, int *err);
+constexpr int TR = 8;  // outputs per thread of the Toeplitz kernel (N_T = 500: 32 threads per output slot)
 __global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, int N, int NT);
 __global__ void k_multidot_partial(const double2 *V, size_t ldv, int nvec, const double2 *w, double2 *partial,
                                    int N, int NT);
@@ -22,6 +23,18 @@ __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);
 __global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const double2 *y, double2 *x, size_t n);
 __global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, double2 *uT);
 __global__ void k_fill(double2 *x, double2 v, size_t n);
+
+enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };
+cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
+                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st);
+__global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);
+
+int fft_log4_for(int NT);
+__global__ void k_twiddles(double2 *tw, int NF);
+cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int count, int NT, const double2 *tw,
+                           double2 *F, cudaStream_t st);
+cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, const double2 *x, double2 *y, int N,
+                             int NT, const double2 *tw, cudaStream_t st);
 
 struct MarchShape { int M, P, CS; };
 MarchShape choose_march_shape(int Nj);

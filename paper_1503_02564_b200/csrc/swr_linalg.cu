@@ -49,51 +49,205 @@ __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, dou
 // ---------------------------------------------------------------------------
 // y = x - L x with the block pattern of eq. (15)/(16) and
 // causal convolutions (x * y)_n = sum_{s<=n} x_{n-s} y_s (Props. 3-4,
-// P:549-707).  One CTA per output slot; the (<= 2) first columns and input
-// slots are staged in shared memory; thread t computes outputs t and
-// NT-1-t so every thread does NT+1 multiply-adds per pair.
-//   slot r_{j-1} (even 2j-4):  X^{j,1} * l_j + X^{j,2} * r_j
-//   slot l_{j+1} (odd 2j-1):   X^{j,3} * l_j + X^{j,4} * r_j
+// P:549-707).  One CTA per subdomain j: its two input slots l_j, r_j and
+// its four first columns X^{j,1..4} are staged in shared memory (columns
+// zero-padded), and it produces both output slots that read them:
+//   r_{j-1} = X^{j,1} * l_j + X^{j,2} * r_j      (threads [0, T2))
+//   l_{j+1} = X^{j,3} * l_j + X^{j,4} * r_j      (threads [T2, 2 T2))
+// Each thread accumulates TR consecutive outputs over blocks of TR input
+// samples (2TR-1 column values and TR inputs per block in registers) and
+// takes output groups g and G-1-g so the triangular work is balanced.
 // X is [N][4][NT] (subdomain-major), g slot-major.
 // ---------------------------------------------------------------------------
 __global__ void k_toeplitz_I_minus_L(const double2 *__restrict__ X, const double2 *__restrict__ x,
                                      double2 *__restrict__ y, int N, int NT) {
   extern __shared__ double2 ts[];
-  const int o = blockIdx.x;  // output slot
-  double2 *c1 = ts, *c2 = ts + NT, *i1 = ts + 2 * NT, *i2 = ts + 3 * NT;
-  int j, p1, p2, s1, s2;
-  if ((o & 1) == 0) {       // r_{j-1}, j = o/2 + 2
-    j = o / 2 + 2;
-    p1 = 0; s1 = 2 * j - 3;                 // X^{j,1}, l_j
-    p2 = 1; s2 = (j <= N - 1) ? 2 * j - 2 : -1;  // X^{j,2}, r_j
-  } else {                  // l_{j+1}, j = (o+1)/2
-    j = (o + 1) / 2;
-    p1 = 2; s1 = (j >= 2) ? 2 * j - 3 : -1;  // X^{j,3}, l_j
-    p2 = 3; s2 = 2 * j - 2;                  // X^{j,4}, r_j
-  }
-  const double2 *X1 = X + ((size_t)(j - 1) * 4 + p1) * NT, *X2 = X + ((size_t)(j - 1) * 4 + p2) * NT;
-  for (int n = threadIdx.x; n < NT; n += blockDim.x) {
-    c1[n] = (s1 >= 0) ? X1[n] : cz();
-    i1[n] = (s1 >= 0) ? x[(size_t)s1 * NT + n] : cz();
-    c2[n] = (s2 >= 0) ? X2[n] : cz();
-    i2[n] = (s2 >= 0) ? x[(size_t)s2 * NT + n] : cz();
-  }
-  __syncthreads();
-  const double2 *xo = x + (size_t)o * NT;
-  double2 *yo = y + (size_t)o * NT;
-  for (int t = threadIdx.x; t < (NT + 1) / 2; t += blockDim.x) {
-    for (int pass = 0; pass < 2; pass++) {
-      const int n = pass == 0 ? t : NT - 1 - t;
-      if (pass == 1 && n == t) break;
-      double2 a = cz(), b = cz();
-      for (int s = 0; s <= n; s++) {
-        a = cfma(c1[n - s], i1[s], a);
-        b = cfma(c2[n - s], i2[s], b);
-      }
-      const double2 xv = xo[n];
-      yo[n] = make_double2(xv.x - (a.x + b.x), xv.y - (a.y + b.y));
+  const int j = blockIdx.x + 1;
+  const int CL = NT + 3 * TR, IL = NT + TR;
+  double2 *cbase = ts + 2 * TR;                       // 4 columns, stride CL, index range [-2TR, NT+TR)
+  double2 *il = ts + 4 * CL, *ir = il + IL;           // inputs l_j, r_j, index range [0, NT+TR)
+  const int sl = (j >= 2) ? 2 * j - 3 : -1, sr = (j <= N - 1) ? 2 * j - 2 : -1;
+  const double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
+  for (int n = threadIdx.x - 2 * TR; n < NT + TR; n += blockDim.x) {
+    const bool in = n >= 0 && n < NT;
+#pragma unroll
+    for (int pcol = 0; pcol < 4; pcol++) cbase[pcol * CL + n] = in ? Xj[(size_t)pcol * NT + n] : cz();
+    if (n >= 0) {
+      il[n] = (in && sl >= 0) ? x[(size_t)sl * NT + n] : cz();
+      ir[n] = (in && sr >= 0) ? x[(size_t)sr * NT + n] : cz();
     }
   }
+  __syncthreads();
+  const int G = (NT + TR - 1) / TR, T2 = (G + 1) / 2;
+  const int half = threadIdx.x / T2, t = threadIdx.x % T2;
+  if (half > 1) return;
+  const int o = half == 0 ? 2 * j - 4 : 2 * j - 1;    // r_{j-1} or l_{j+1}
+  if ((half == 0 && j < 2) || (half == 1 && j > N - 1)) return;
+  const double2 *c1 = cbase + (half == 0 ? 0 : 2) * CL, *c2 = c1 + CL;   // (X^{j,1},X^{j,2}) or (X^{j,3},X^{j,4})
+  const double2 *xo = x + (size_t)o * NT;
+  double2 *yo = y + (size_t)o * NT;
+  for (int pass = 0; pass < 2; pass++) {
+    const int g = pass == 0 ? t : G - 1 - t;
+    if (pass == 1 && g == t) break;
+    const int n0 = g * TR;
+    double2 acc[TR];
+#pragma unroll
+    for (int r = 0; r < TR; r++) acc[r] = cz();
+    // blocks of TR input samples: acc[r] += c[n0 + r - s] in[s]
+    for (int sb = 0; sb <= n0; sb += TR) {
+      double2 cw[2 * TR - 1], iw[TR];
+#pragma unroll
+      for (int d = 0; d < 2 * TR - 1; d++) cw[d] = c1[n0 - sb + d - (TR - 1)];
+#pragma unroll
+      for (int q = 0; q < TR; q++) iw[q] = il[sb + q];
+#pragma unroll
+      for (int q = 0; q < TR; q++)
+#pragma unroll
+        for (int r = 0; r < TR; r++) acc[r] = cfma(cw[r - q + TR - 1], iw[q], acc[r]);
+#pragma unroll
+      for (int d = 0; d < 2 * TR - 1; d++) cw[d] = c2[n0 - sb + d - (TR - 1)];
+#pragma unroll
+      for (int q = 0; q < TR; q++) iw[q] = ir[sb + q];
+#pragma unroll
+      for (int q = 0; q < TR; q++)
+#pragma unroll
+        for (int r = 0; r < TR; r++) acc[r] = cfma(cw[r - q + TR - 1], iw[q], acc[r]);
+    }
+#pragma unroll
+    for (int r = 0; r < TR; r++) {
+      const int n = n0 + r;
+      if (n < NT) {
+        const double2 xv = xo[n];
+        yo[n] = make_double2(xv.x - acc[r].x, xv.y - acc[r].y);
+      }
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// FFT form of the same operator (the causal convolutions of Props. 3-4 as
+// zero-padded cyclic convolutions of length NF = 4^LOG4 >= 2 N_T - 1).
+// Radix-4 Stockham FFT in shared memory, one CTA per sequence, NF/4 threads.
+//   k_fft_fwd:   F[q] = FFT(pad(src[q]))           (inputs slots; columns at build)
+//   k_fft_apply: y_o  = x_o - IFFT(Fc_a .* Fx_a + Fc_b .* Fx_b)[0:N_T]
+// ---------------------------------------------------------------------------
+template <int LOG4>
+__device__ __forceinline__ void fft4_stockham(double2 *a, double2 *b, const double2 *__restrict__ tw, bool inverse) {
+  constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
+  const int jt = threadIdx.x;  // one radix-4 butterfly per thread and stage
+  double2 *in = a, *out = b;
+#pragma unroll
+  for (int st = 0, Ns = 1; st < LOG4; st++, Ns *= 4) {
+    const int km = jt % Ns;
+    double2 v[4];
+#pragma unroll
+    for (int r = 0; r < 4; r++) {
+      v[r] = in[jt + r * Q];
+      if (r > 0) {
+        double2 wv = tw[(km * r * (NF / (4 * Ns))) & (NF - 1)];
+        if (inverse) wv.y = -wv.y;
+        v[r] = cmul(v[r], wv);
+      }
+    }
+    const double2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]), a2 = cadd(v[1], v[3]);
+    const double2 d13 = csub(v[1], v[3]);
+    const double2 a3 = inverse ? make_double2(-d13.y, d13.x) : make_double2(d13.y, -d13.x);  // (+-i)(v1 - v3)
+    const int od = (jt / Ns) * Ns * 4 + km;
+    out[od] = cadd(a0, a2);
+    out[od + Ns] = cadd(a1, a3);
+    out[od + 2 * Ns] = csub(a0, a2);
+    out[od + 3 * Ns] = csub(a1, a3);
+    __syncthreads();
+    double2 *t = in; in = out; out = t;
+  }
+  if (LOG4 & 1) {  // result is in b: copy back to a
+    for (int i = jt; i < NF; i += Q) a[i] = b[i];
+    __syncthreads();
+  }
+}
+
+template <int LOG4>
+__global__ void k_fft_fwd(const double2 *__restrict__ src, size_t src_stride, int NT, const double2 *__restrict__ tw,
+                          double2 *__restrict__ F) {
+  constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
+  __shared__ double2 a[NF], b[NF];
+  const double2 *s = src + (size_t)blockIdx.x * src_stride;
+  for (int i = threadIdx.x; i < NF; i += Q) a[i] = (i < NT) ? s[i] : cz();
+  __syncthreads();
+  fft4_stockham<LOG4>(a, b, tw, false);
+  double2 *f = F + (size_t)blockIdx.x * NF;
+  for (int i = threadIdx.x; i < NF; i += Q) f[i] = a[i];
+}
+
+// Fx: [2N-2][NF] transforms of the input slots; Fc: [N][4][NF] of the columns.
+template <int LOG4>
+__global__ void k_fft_apply(const double2 *__restrict__ Fc, const double2 *__restrict__ Fx,
+                            const double2 *__restrict__ x, double2 *__restrict__ y, int N, int NT,
+                            const double2 *__restrict__ tw) {
+  constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
+  __shared__ double2 a[NF], b[NF];
+  const int o = blockIdx.x;
+  int j, p1, p2, s1, s2;
+  if ((o & 1) == 0) { j = o / 2 + 2; p1 = 0; s1 = 2 * j - 3; p2 = 1; s2 = (j <= N - 1) ? 2 * j - 2 : -1; }
+  else { j = (o + 1) / 2; p1 = 2; s1 = (j >= 2) ? 2 * j - 3 : -1; p2 = 3; s2 = 2 * j - 2; }
+  const double2 *c1 = Fc + ((size_t)(j - 1) * 4 + p1) * NF, *c2 = Fc + ((size_t)(j - 1) * 4 + p2) * NF;
+  for (int i = threadIdx.x; i < NF; i += Q) {
+    double2 acc = cz();
+    if (s1 >= 0) acc = cmul(c1[i], Fx[(size_t)s1 * NF + i]);
+    if (s2 >= 0) acc = cfma(c2[i], Fx[(size_t)s2 * NF + i], acc);
+    a[i] = acc;
+  }
+  __syncthreads();
+  fft4_stockham<LOG4>(a, b, tw, true);
+  const double inv = 1.0 / NF;
+  const double2 *xo = x + (size_t)o * NT;
+  double2 *yo = y + (size_t)o * NT;
+  for (int n = threadIdx.x; n < NT; n += Q) {
+    const double2 xv = xo[n];
+    yo[n] = make_double2(fma(-inv, a[n].x, xv.x), fma(-inv, a[n].y, xv.y));
+  }
+}
+
+__global__ void k_twiddles(double2 *tw, int NF) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k < NF) {
+    double sn, cs;
+    sincospi(-2.0 * (double)k / (double)NF, &sn, &cs);  // e^{-2 pi i k / NF}
+    tw[k] = make_double2(cs, sn);
+  }
+}
+
+int fft_log4_for(int NT) {
+  for (int l = 2; l <= 5; l++)
+    if ((1 << (2 * l)) >= 2 * NT - 1) return l;
+  return 0;
+}
+
+cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int count, int NT, const double2 *tw,
+                           double2 *F, cudaStream_t st) {
+  if (count <= 0) return cudaSuccess;
+  switch (log4) {
+    case 2: k_fft_fwd<2><<<count, 4, 0, st>>>(src, stride, NT, tw, F); break;
+    case 3: k_fft_fwd<3><<<count, 16, 0, st>>>(src, stride, NT, tw, F); break;
+    case 4: k_fft_fwd<4><<<count, 64, 0, st>>>(src, stride, NT, tw, F); break;
+    case 5: k_fft_fwd<5><<<count, 256, 0, st>>>(src, stride, NT, tw, F); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, const double2 *x, double2 *y, int N,
+                             int NT, const double2 *tw, cudaStream_t st) {
+  if (N < 2) return cudaSuccess;
+  const int nslots = 2 * N - 2;
+  switch (log4) {
+    case 2: k_fft_apply<2><<<nslots, 4, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
+    case 3: k_fft_apply<3><<<nslots, 16, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
+    case 4: k_fft_apply<4><<<nslots, 64, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
+    case 5: k_fft_apply<5><<<nslots, 256, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------
@@ -172,6 +326,171 @@ __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nv
     for (int v = 0; v < nvec; v++) acc = cfma(y[v], V[(size_t)v * ldv + e], acc);
     x[e] = acc;
   }
+}
+
+// ---------------------------------------------------------------------------
+// Fused CGS kernel: one CTA per subdomain j (its owned slots l_j, r_j are
+// contiguous in g), KEPT entries per thread in registers.
+//   mode & CGS_AXPY : w -= sum_v h_v V_v          (h from the device, v < nv)
+//   mode & CGS_DOTS : p_v = <V_v, w>              (v < nv)
+//   mode & CGS_NORM : p_nv = <w, w>
+// Partials per subdomain are reduced in a fixed tree inside the CTA; the last
+// CTA to finish sums them in subdomain order (order-fixed, deterministic) into
+// out[0..nv].  With CGS_SCALE the last CTA also stores 1/sqrt(out[nv]) in
+// out[nv+1] for the normalisation of the next basis vector.
+// ---------------------------------------------------------------------------
+constexpr int CGS_SPLIT = 2;
+
+template <int EPT>
+__global__ void __launch_bounds__(256) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
+                                             const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
+                                             double2 *__restrict__ partial, double2 *__restrict__ out,
+                                             unsigned *counter, int N, int NT) {
+  __shared__ double2 red[33][8];
+  __shared__ bool last;
+  // CTA (j, part): part-th of CGS_SPLIT contiguous pieces of subdomain j's entries
+  const int j = blockIdx.x / CGS_SPLIT + 1, part = blockIdx.x % CGS_SPLIT;
+  const int s_lo = (j >= 2) ? 2 * j - 3 : 0;
+  const int s_hi = (j <= N - 1) ? 2 * j - 2 : 2 * j - 3;
+  const size_t f0 = (size_t)s_lo * NT, f1 = (size_t)(s_hi + 1) * NT;
+  const size_t piece = (f1 - f0 + CGS_SPLIT - 1) / CGS_SPLIT;
+  const size_t e0 = f0 + part * piece, e1 = min(f1, e0 + piece);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  double2 wv[EPT];
+#pragma unroll
+  for (int i = 0; i < EPT; i++) {
+    const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+    wv[i] = (e < e1) ? w[e] : cz();
+  }
+  if (mode & CGS_AXPY) {
+    int v = 0;
+    for (; v + 4 <= nv; v += 4) {      // 4 basis vectors per round trip
+      double2 hv[4], xv[4][EPT];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        hv[u] = hsrc[v + u];
+        const double2 *Vv = V + (size_t)(v + u) * ldv;
+#pragma unroll
+        for (int i = 0; i < EPT; i++) {
+          const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+          xv[u][i] = (e < e1) ? Vv[e] : cz();
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++)
+#pragma unroll
+        for (int i = 0; i < EPT; i++)
+          wv[i] = make_double2(wv[i].x - (hv[u].x * xv[u][i].x - hv[u].y * xv[u][i].y),
+                               wv[i].y - (hv[u].x * xv[u][i].y + hv[u].y * xv[u][i].x));
+    }
+    for (; v < nv; v++) {
+      const double2 hv = hsrc[v];
+      const double2 *Vv = V + (size_t)v * ldv;
+#pragma unroll
+      for (int i = 0; i < EPT; i++) {
+        const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+        if (e < e1) {
+          const double2 x = Vv[e];
+          wv[i] = make_double2(wv[i].x - (hv.x * x.x - hv.y * x.y), wv[i].y - (hv.x * x.y + hv.y * x.x));
+        }
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < EPT; i++) {
+      const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+      if (e < e1) w[e] = wv[i];
+    }
+  }
+  const int nred = ((mode & CGS_DOTS) ? nv : 0) + ((mode & CGS_NORM) ? 1 : 0);
+  if (mode & CGS_DOTS) {
+    int v = 0;
+    for (; v + 4 <= nv; v += 4) {      // 4 basis vectors per round trip
+      double2 acc[4];
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+        const double2 *Vv = V + (size_t)(v + u) * ldv;
+        acc[u] = cz();
+#pragma unroll
+        for (int i = 0; i < EPT; i++) {
+          const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+          if (e < e1) acc[u] = cfmaconj(Vv[e], wv[i], acc[u]);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u++) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc[u] = cadd(acc[u], shfl_down2(acc[u], o));
+        if (lane == 0) red[v + u][wp] = acc[u];
+      }
+    }
+    for (; v < nv; v++) {
+      const double2 *Vv = V + (size_t)v * ldv;
+      double2 acc = cz();
+#pragma unroll
+      for (int i = 0; i < EPT; i++) {
+        const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
+        if (e < e1) acc = cfmaconj(Vv[e], wv[i], acc);
+      }
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_down2(acc, o));
+      if (lane == 0) red[v][wp] = acc;
+    }
+  }
+  if (mode & CGS_NORM) {
+    double2 acc = cz();
+#pragma unroll
+    for (int i = 0; i < EPT; i++) acc.x = fma(wv[i].x, wv[i].x, fma(wv[i].y, wv[i].y, acc.x));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_down2(acc, o));
+    if (lane == 0) red[nred - 1][wp] = acc;
+  }
+  __syncthreads();
+  if ((int)threadIdx.x < nred) {
+    double2 sum = cz();
+    for (int q = 0; q < nwp; q++) sum = cadd(sum, red[threadIdx.x][q]);
+    partial[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // last CTA: one warp per reduced quantity, fixed-order tree over the
+  // (subdomain, piece) partials
+  const int np = gridDim.x;
+  for (int v = wp; v < nred; v += nwp) {
+    double2 sum = cz();
+    for (int q = lane; q < np; q += 32) sum = cadd(sum, __ldcg(partial + (size_t)v * np + q));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
+    if (lane == 0) {
+      out[v] = sum;
+      if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
+    }
+  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// y = s x, s read from the device (the normalisation of a new basis vector)
+__global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__restrict__ sp, double2 *__restrict__ y,
+                            size_t n) {
+  const double sc = sp->x;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    y[e] = make_double2(x[e].x * sc, x[e].y * sc);
+}
+
+cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
+                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st) {
+  const int ent = (2 * NT + CGS_SPLIT - 1) / CGS_SPLIT;
+  if (ent <= 128 * 4) {
+    k_cgs<4><<<N * CGS_SPLIT, 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
+  } else if (ent <= 256 * 8) {
+    k_cgs<8><<<N * CGS_SPLIT, 256, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
+  } else {
+    return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
 }
 
 // ---------------------------------------------------------------------------

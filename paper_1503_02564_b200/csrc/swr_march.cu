@@ -35,9 +35,17 @@ __device__ __forceinline__ void compose(double2 &A, double2 &B, double2 Ae, doub
   A = cmul(A, Ae);
 }
 
-__device__ __forceinline__ void csync(int CS) {
-  if (CS > 1) cg::this_cluster().sync();
-  else __syncthreads();
+// Barrier over the system's CTAs.  Inside a CTA a bar.sync orders shared
+// memory; across the cluster only the threads that wrote data read by other
+// CTAs (halo rows, pushed scan totals) fence, everyone else arrives relaxed
+// (no per-thread membar).
+__device__ __forceinline__ void csync(int CS, bool wrote_remote_visible = false) {
+  __syncthreads();
+  if (CS > 1) {
+    if (wrote_remote_visible) asm volatile("fence.acq_rel.cluster;" ::: "memory");
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+  }
 }
 
 template <typename T>
@@ -46,16 +54,23 @@ __device__ __forceinline__ T *remote(T *p, int rank) {
 }
 
 // c2 * sum_{s=0}^{n-1} beta_{n-s} hv[s]  (S0^2 history),
-// evaluated by one warp; every lane returns the sum.
+// evaluated by one warp from shared memory; every lane returns the sum.
 __device__ __forceinline__ double2 hist_sum(const double2 *hv, const double *beta, int n, int lane, double2 c2) {
-  double2 acc = cz();
+  double2 a0 = cz(), a1 = cz();
+  int s = lane;
 #pragma unroll 1
-  for (int s = lane; s < n; s += 32) {
-    double b = beta[n - s];
-    double2 v = hv[s];
-    acc.x = fma(b, v.x, acc.x);
-    acc.y = fma(b, v.y, acc.y);
+  for (; s + 32 < n; s += 64) {
+    const double b0 = beta[n - s], b1 = beta[n - s - 32];
+    const double2 v0 = hv[s], v1 = hv[s + 32];
+    a0.x = fma(b0, v0.x, a0.x); a0.y = fma(b0, v0.y, a0.y);
+    a1.x = fma(b1, v1.x, a1.x); a1.y = fma(b1, v1.y, a1.y);
   }
+  if (s < n) {
+    const double b0 = beta[n - s];
+    const double2 v0 = hv[s];
+    a0.x = fma(b0, v0.x, a0.x); a0.y = fma(b0, v0.y, a0.y);
+  }
+  double2 acc = cadd(a0, a1);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
   return cmul(c2, acc);
@@ -100,7 +115,7 @@ __device__ __forceinline__ double2 scan_fwd(double2 A, double2 B, const ScanSmem
       }
     }
   }
-  csync(CS);
+  csync(CS, w == 0 && lane == nw - 1);
   double2 val = cz();
 #pragma unroll 1
   for (int c = 0; c < crank; c++) val = cfma(ss.ctot[c], val, ss.ctot[8 + c]);
@@ -139,7 +154,7 @@ __device__ __forceinline__ double2 scan_bwd(double2 A, double2 B, const ScanSmem
       }
     }
   }
-  csync(CS);
+  csync(CS, w == 0 && lane == 0);
   double2 val = cz();
 #pragma unroll 1
   for (int c = CS - 1; c > crank; c--) val = cfma(ss.ctot[16 + c], val, ss.ctot[24 + c]);
@@ -198,9 +213,13 @@ __global__ void __launch_bounds__(PMAX, 1) k_march_resident(const MarchParams p)
   double2 *hva = ss.ctot + 32;
   double2 *hvb = hva + (p.NT + 1);
   BndSmem *bnd = reinterpret_cast<BndSmem *>(hvb + (p.NT + 1));
+  double2 *hred = reinterpret_cast<double2 *>(bnd + 1);   // [64] warp partials of H_a, H_b
+  double *sbeta = reinterpret_cast<double *>(hred + 64);    // [NT+1]
+  for (int i = t; i <= p.NT; i += P) sbeta[i] = p.beta[i];
 
   double2 u[M], q[M];
   double er[M];
+  double er_prev;
   {
     const double2 *u0p = Sp->u0, *qp = Sp->q;
     const double *erp = Sp->er;
@@ -218,7 +237,7 @@ __global__ void __launch_bounds__(PMAX, 1) k_march_resident(const MarchParams p)
       }
     }
     // constant aggregate factors: Af = prod c_k, Ab = prod b_k over the thread's rows
-    const double er_prev = (s0 >= 1 && s0 - 1 < Nj) ? erp[s0 - 1] : 0.0;
+    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? erp[s0 - 1] : 0.0;
     double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
 #pragma unroll
     for (int i = 0; i < M; i++) {
@@ -241,33 +260,74 @@ __global__ void __launch_bounds__(PMAX, 1) k_march_resident(const MarchParams p)
   for (int i = 0; i < M; i++)
     if (s0 + i == Nj - 1) hvb[0] = u[i];
   if (t == 0) { bnd->Ha = cz(); bnd->Hb = cz(); bnd->lin = cz(); bnd->rin = cz(); }
+  // incoming flux of the next step, prefetched by the owning lane
+  auto flux_at = [&](const double2 *ser, int imp, int nn) -> double2 {
+    if (nn > p.NT) return cz();
+    if (imp) return make_double2(nn == 1 ? 1.0 : 0.0, 0.0);
+    return ser ? ser[nn - 1] : cz();
+  };
+  double2 fnext = cz();
+  if ((flags & SYS_HAS_LEFT) && crank == 0 && t == 0) fnext = flux_at(Sp->lin, flags & SYS_LIN_IMPULSE, 1);
+  double2 fnext_b = cz();
+  if ((flags & SYS_HAS_RIGHT) && crank == cb && t == tb) fnext_b = flux_at(Sp->rin, flags & SYS_RIN_IMPULSE, 1);
   __syncthreads();
 
 #pragma unroll 1
   for (int n = 1; n <= p.NT; n++) {
-    // ---- boundary scalars of step n (owning warps) ----
-    if ((flags & SYS_HAS_LEFT) && crank == 0 && w == 0) {
-      __syncwarp();
-      const double2 Ha = p.s02 ? hist_sum(hva, p.beta, n, lane, p.c2) : cz();
-      if (lane == 0) {
-        bnd->Ha = Ha;
-        bnd->lin = (flags & SYS_LIN_IMPULSE) ? make_double2(n == 1 ? 1.0 : 0.0, 0.0)
-                                             : (Sp->lin ? Sp->lin[n - 1] : cz());
+    // ---- boundary scalars of step n ----
+    // S0^2 history H = c2 sum_{s<n} beta_{n-s} v_s: every thread of the CTA
+    // holding the boundary row adds a slice of s <= n-2 (written before the
+    // last barrier), warp partials go to shared memory and the owner of the
+    // row adds them and its own newest term beta_1 v_{n-1} after the halo
+    // barrier.
+    if (p.s02) {
+      if ((flags & SYS_HAS_LEFT) && crank == 0) {
+        double2 acc = cz();
+        for (int q = t; q < n - 1; q += P) {
+          const double b = sbeta[n - q];
+          const double2 v = hva[q];
+          acc.x = fma(b, v.x, acc.x);
+          acc.y = fma(b, v.y, acc.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+        if (lane == 0) hred[w] = acc;
+      }
+      if ((flags & SYS_HAS_RIGHT) && crank == cb) {
+        double2 acc = cz();
+        for (int q = t; q < n - 1; q += P) {
+          const double b = sbeta[n - q];
+          const double2 v = hvb[q];
+          acc.x = fma(b, v.x, acc.x);
+          acc.y = fma(b, v.y, acc.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+        if (lane == 0) hred[32 + w] = acc;
       }
     }
-    if ((flags & SYS_HAS_RIGHT) && crank == cb && w == (tb >> 5)) {
-      __syncwarp();
-      const double2 Hb = p.s02 ? hist_sum(hvb, p.beta, n, lane, p.c2) : cz();
-      if (lane == (tb & 31)) {
-        bnd->Hb = Hb;
-        bnd->rin = (flags & SYS_RIN_IMPULSE) ? make_double2(n == 1 ? 1.0 : 0.0, 0.0)
-                                             : (Sp->rin ? Sp->rin[n - 1] : cz());
-      }
+    if (owns_a) {
+      bnd->lin = fnext;
+      fnext = flux_at(Sp->lin, flags & SYS_LIN_IMPULSE, n + 1);
+    }
+    if (owns_b) {
+      bnd->rin = fnext_b;
+      fnext_b = flux_at(Sp->rin, flags & SYS_RIN_IMPULSE, n + 1);
     }
     // ---- halo: u_{n-1} of the neighbouring rows ----
     hfirst[t] = u[0];
     hlast[t] = u[M - 1];
-    csync(p.CS);
+    csync(p.CS, t == 0 || t == P - 1);
+    if (p.s02 && (owns_a || owns_b)) {
+      double2 ha = owns_a ? cscale(sbeta[1], hva[n - 1]) : cz();
+      double2 hb = owns_b ? cscale(sbeta[1], hvb[n - 1]) : cz();
+      for (int q = 0; q < (P >> 5); q++) {
+        if (owns_a) ha = cadd(ha, hred[q]);
+        if (owns_b) hb = cadd(hb, hred[32 + q]);
+      }
+      if (owns_a) bnd->Ha = cmul(p.c2, ha);
+      if (owns_b) bnd->Hb = cmul(p.c2, hb);
+    }
     double2 uL = cz(), uR = cz();
     if (t > 0) uL = hlast[t - 1];
     else if (crank > 0) uL = *remote(hlast + (P - 1), crank - 1);
@@ -278,7 +338,6 @@ __global__ void __launch_bounds__(PMAX, 1) k_march_resident(const MarchParams p)
     double2 z = cz();
     for (int pass = 0; pass < 2; pass++) {
       launder<M>(q, er);
-      const double er_prev = (s0 >= 1 && s0 - 1 < Nj) ? p.sys[blockIdx.x / p.CS].er[s0 - 1] : 0.0;
 #pragma unroll
       for (int i = 0; i < M; i++) {
         const int k = s0 + i;
@@ -347,7 +406,7 @@ __global__ void __launch_bounds__(PMAX, 1) k_march_resident(const MarchParams p)
 // cap is 65536 / PMAX per thread.
 // ---------------------------------------------------------------------------
 struct Inst { int M, PMAX; };
-static const Inst kInst[] = {{1, 512}, {2, 512}, {4, 512}, {6, 256}, {8, 256}, {11, 256}, {12, 256}, {16, 256}, {17, 256}};
+static const Inst kInst[] = {{1, 512}, {2, 512}, {4, 512}, {6, 256}, {8, 256}, {10, 256}, {11, 256}, {12, 256}};
 
 MarchShape choose_march_shape(int Nj) {
   MarchShape best{0, 0, 0};
@@ -368,7 +427,8 @@ MarchShape choose_march_shape(int Nj) {
 }
 
 size_t march_smem_bytes(const MarchShape &s, int NT) {
-  return sizeof(double2) * ((size_t)s.M * s.P + 4 * (size_t)s.P + 160 + 2 * (size_t)(NT + 1)) + sizeof(BndSmem);
+  return sizeof(double2) * ((size_t)s.M * s.P + 4 * (size_t)s.P + 160 + 2 * (size_t)(NT + 1) + 64) +
+         sizeof(BndSmem) + sizeof(double) * (size_t)(NT + 1);
 }
 
 template <int M, int PMAX>
@@ -409,8 +469,7 @@ cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st) {
     case 8: return launch_m<8, 256>(p, s, smem, st);
     case 11: return launch_m<11, 256>(p, s, smem, st);
     case 12: return launch_m<12, 256>(p, s, smem, st);
-    case 16: return launch_m<16, 256>(p, s, smem, st);
-    case 17: return launch_m<17, 256>(p, s, smem, st);
+    case 10: return launch_m<10, 256>(p, s, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }

@@ -145,3 +145,24 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         # impulse (S0^2 is nearly transparent at dx = 1e-5): compare at the
         # scale of the impulse (parity floor)
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
+
+
+@pytest.mark.parametrize("mode", ["direct", "fft"])
+def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
+    """Both forms of y = (I - L) x (direct causal convolution and FFT
+    convolution) against the oracle's direct convolution."""
+    import torch
+    if mode == "direct":
+        monkeypatch.setenv("SWR_TOEPLITZ", "direct")
+    else:
+        monkeypatch.delenv("SWR_TOEPLITZ", raising=False)
+    for p in (si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX),
+              si.Problem(dx=1e-3, dt=1e-3, N=20, potential=si.POT_VX)):   # N_T = 100 and 500
+        o, g_ = _pair(oracle_mod, gpu, p)
+        g_.build()
+        _, X_g = g_.get_interface(0)
+        rng = np.random.default_rng(9)
+        x = rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng)
+        y_g = g_.apply_I_minus_L(torch.as_tensor(x, device="cuda"), 0).cpu().numpy()
+        y_o = x - o.apply_L(X_g.cpu().numpy(), x)
+        assert rel(y_g, y_o) <= 1e-12, mode

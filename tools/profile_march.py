@@ -1,0 +1,11 @@
+"""One C5 interface-operator build (a single 3-RHS march launch) for ncu."""
+import sys
+sys.path.insert(0, '.')
+import torch
+import swr_inputs as si
+from paper_1503_02564_b200 import SWR
+p = si.config(sys.argv[1] if len(sys.argv) > 1 else "C5")
+s = SWR(p, si.inputs(p))
+s.build()
+torch.cuda.synchronize()
+print("built", p.name)
