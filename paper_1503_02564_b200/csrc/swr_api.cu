@@ -130,7 +130,7 @@ struct swr_handle {
   cudaStream_t st;
   double2 c0, c2v;
   double kappa, eim;
-  MarchShape shape;
+  MarchShape shape[4];                     // launch shape per K = 1..3 RHS per group
   // device data
   double2 *u0 = nullptr;
   double *Vx = nullptr, *beta = nullptr;
@@ -197,8 +197,8 @@ int slot_l(int j) { return 2 * j - 3; }
 int slot_r(int j) { return 2 * j - 2; }
 int zero_matrix_index(swr_handle *h, int j) { return j == 1 ? 0 : (j == h->N ? 2 : 1); }
 
-// ---- one batched march over a list of systems ------------------------------
-int run_march(swr_handle *h, const std::vector<MarchSys> &sys) {
+// ---- one batched march over groups of K systems sharing a matrix --------
+int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal) {
   if (sys.empty()) return SWR_OK;
   CK(cudaMemcpyAsync(h->sys_dev, sys.data(), sys.size() * sizeof(MarchSys), cudaMemcpyHostToDevice, h->st));
   MarchParams p;
@@ -206,20 +206,38 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys) {
   p.nsys = (int)sys.size();
   p.Nj = h->Nj;
   p.NT = h->NT;
-  p.CS = h->shape.CS;
+  p.CS = h->shape[K].CS;
   p.e_im = h->eim;
   p.kappa = h->kappa;
   p.c0 = h->c0;
   p.c2 = h->c2v;
   p.s02 = h->transmission == SWR_TC_S0_2;
+  p.flux_smem = 0;
+  for (const MarchSys &m : sys)
+    if (m.lin || m.rin) p.flux_smem = 1;
   p.beta = h->beta;
+  p.trace = nullptr;
+  if (getenv("SWR_TRACE")) {
+    static long long *tr = nullptr;
+    if (!tr) CK(cudaMalloc(&tr, 64 * sizeof(long long)));
+    CK(cudaMemsetAsync(tr, 0, 64 * sizeof(long long), h->st));
+    p.trace = tr;
+    CK(swr::launch_march(p, h->shape[K], h->st));
+    long long hv[20];
+    CK(cudaMemcpyAsync(hv, tr, 20 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    fprintf(stderr, "march trace (cycles from step start), K=%d M=%d P=%d CS=%d:", K, h->shape[K].M, h->shape[K].P, h->shape[K].CS);
+    for (int i = 1; i < 10; i++) fprintf(stderr, " %lld", hv[i] ? hv[i] - hv[0] : -1);
+    fprintf(stderr, " | next step %lld\n", hv[10] - hv[0]);
+    p.trace = nullptr;
+  }
   CKS(record_pair(h, true, true));
-  CK(swr::launch_march(p, h->shape, h->st));
+  CK(swr::launch_march(p, h->shape[K], h->st));
   CK(cudaGetLastError());
   CKS(record_pair(h, true, false));
   h->n_marches++;
   h->n_launches++;
-  h->cell_steps += (double)sys.size() * h->Nj * h->NT;
+  h->cell_steps += (double)nreal * h->Nj * h->NT;
   return SWR_OK;
 }
 
@@ -259,7 +277,7 @@ int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2
   std::vector<MarchSys> sys;
   for (int j = 1; j <= h->N; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
   if (Rg) CKS(fill_zero(h, Rg, h->ng));
-  return run_march(h, sys);
+  return run_march(h, sys, 1, (int)sys.size());
 }
 
 // ---- assembly + factorisation ----------------------------------------------
@@ -491,31 +509,44 @@ int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   return s;
 }
 
-// the L / L0 first columns by impulse probing, d = R(0; u0)
+// the L / L0 first columns by impulse probing, with d = R(0; u0)
+// in the same launch: one group per subdomain, K = 3 (d, l_j probe, r_j
+// probe; the end subdomains pad with an all-zero RHS) or K = 2 without d.
 int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
   std::vector<MarchSys> sys;
   const int N = h->N, NT = h->NT;
+  const char *kenv = getenv("SWR_BUILD_K");
+  int K = kenv ? atoi(kenv) : 1;
+  if (K < 1 || K > 3 || h->shape[K].M == 0) K = 1;
+  int nreal = 0;
   CKS(fill_zero(h, X, (size_t)N * 4 * NT));
   if (dvec) CKS(fill_zero(h, dvec, h->ng));
   for (int j = 1; j <= N; j++) {
     double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
-    if (dvec) sys.push_back(make_sys(h, j, nullptr, true, zero, dvec, nullptr));
+    const MarchSys blank = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
+    int kk = 0;
+    if (dvec) { sys.push_back(make_sys(h, j, nullptr, true, zero, dvec, nullptr)); kk++; }
     if (j >= 2) {  // l_{j,1} = 1 -> X^{j,1} (out_left), X^{j,3} (out_right)
-      MarchSys s = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
+      MarchSys s = blank;
       s.flags |= swr::SYS_LIN_IMPULSE;
       s.out_left = Xj + 0 * NT;
       s.out_right = (j <= N - 1) ? Xj + 2 * NT : nullptr;
       sys.push_back(s);
+      kk++;
     }
     if (j <= N - 1) {  // r_{j,1} = 1 -> X^{j,2}, X^{j,4}
-      MarchSys s = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
+      MarchSys s = blank;
       s.flags |= swr::SYS_RIN_IMPULSE;
       s.out_left = (j >= 2) ? Xj + 1 * NT : nullptr;
       s.out_right = Xj + 3 * NT;
       sys.push_back(s);
+      kk++;
     }
+    nreal += kk;
+    if (K > 1)
+      for (; kk % K; kk++) sys.push_back(blank);
   }
-  return run_march(h, sys);
+  return run_march(h, sys, K, nreal);
 }
 
 int final_sweep(swr_handle *h, const double2 *g) {
@@ -643,8 +674,13 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->c0 = (h->transmission == SWR_TC_ROBIN) ? make_double2(0.0, -h->robin_p) : h->c2v;  // beta_0 = 1
   h->kappa = (2.0 / h->dt) * (h->dx / 6.0);
   h->eim = (2.0 / h->dt) * (h->dx / 6.0);
-  h->shape = swr::choose_march_shape(h->Nj);
-  if (h->shape.M == 0 || swr::march_smem_bytes(h->shape, h->NT) > 227 * 1024) {
+  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K);
+  h->shape[0] = h->shape[1];
+  bool shapes_ok = true;
+  if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true) > 227 * 1024) shapes_ok = false;
+  for (int K = 2; K <= 3; K++)
+    if (h->shape[K].M == 0 || swr::march_smem_bytes(h->shape[K], h->NT, false) > 227 * 1024) h->shape[K].M = 0;
+  if (!shapes_ok) {
     g_detail = "subdomain too large for the resident march (N_j = " + std::to_string(h->Nj) + ")";
     delete h;
     return SWR_ERR_UNSUPPORTED;
@@ -655,7 +691,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   const bool precond = h->algorithm == SWR_ALG_PRECOND;
   if ((s = dalloc(&h->u0, nx1)) || (s = dalloc(&h->beta, NTt + 1)) || (s = dalloc(&h->q, (size_t)h->N * h->Nj)) ||
       (s = dalloc(&h->er, (size_t)h->N * h->Nj)) || (s = dalloc(&h->uloc, (size_t)h->N * h->Nj)) ||
-      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)3 * h->N + 4)) || (s = dalloc(&h->err_dev, 1)) ||
+      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)4 * h->N + 8)) || (s = dalloc(&h->err_dev, 1)) ||
       (s = dalloc(&h->counter, 1)))
     return fail(s);
   if (h->potential == SWR_POT_VX && (s = dalloc(&h->Vx, nx1))) return fail(s);

@@ -67,7 +67,9 @@ struct MarchParams {
   double2 c0;                // leading coefficient of the transmission operator
   double2 c2;                // e^{-i pi/4} sqrt(2/dt) (S0^2)
   int32_t s02;               // 1: S0^2 history convolution, 0: Robin
+  int32_t flux_smem;         // 1: stage the incoming flux series in shared memory
   const double *beta;        // [N_T+1] beta_s
+  long long *trace;          // optional per-phase clock trace (debug), NULL in production
 };
 
 }  // namespace swr

@@ -36,9 +36,9 @@ cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int coun
 cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, const double2 *x, double2 *y, int N,
                              int NT, const double2 *tw, cudaStream_t st);
 
-struct MarchShape { int M, P, CS; };
-MarchShape choose_march_shape(int Nj);
-size_t march_smem_bytes(const MarchShape &s, int NT);
+struct MarchShape { int M, P, CS, K; };
+MarchShape choose_march_shape(int Nj, int K);
+size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
 
 }  // namespace swr
