@@ -141,6 +141,12 @@ struct swr_handle {
   double2 *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
   // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0, transformed inputs
   int log4 = 0;
+  // V(t,x): per-step pivots [N_T][N][N_j]; f(u): fixed-point stats
+  double *tau = nullptr, *xi = nullptr;
+  double2 *qtd = nullptr;
+  double *ertd = nullptr;
+  int *fp_stat = nullptr;
+  MarchShape shape_nl;
   double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr, *Fx = nullptr;
   double2 *partial = nullptr;
   Krylov kout = {}, kin = {};             // outer / inner (P^{-1}) GMRES workspaces
@@ -198,7 +204,9 @@ int slot_r(int j) { return 2 * j - 2; }
 int zero_matrix_index(swr_handle *h, int j) { return j == 1 ? 0 : (j == h->N ? 2 : 1); }
 
 // ---- one batched march over groups of K systems sharing a matrix --------
-int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal) {
+enum { MARCH_CONST = 0, MARCH_TD = 1, MARCH_NL = 2 };
+
+int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal, int mode = MARCH_CONST) {
   if (sys.empty()) return SWR_OK;
   CK(cudaMemcpyAsync(h->sys_dev, sys.data(), sys.size() * sizeof(MarchSys), cudaMemcpyHostToDevice, h->st));
   MarchParams p;
@@ -217,6 +225,22 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal)
     if (m.lin || m.rin) p.flux_smem = 1;
   p.beta = h->beta;
   p.trace = nullptr;
+  p.td_stride = mode == MARCH_TD ? (size_t)h->N * h->Nj : 0;
+  p.lambda = h->lambda;
+  p.h12 = h->dx / 12.0;
+  p.tol_fp = h->tol_fp;
+  p.maxit_fp = h->maxit_fp;
+  p.fp_stat = h->fp_stat;
+  if (mode == MARCH_NL) {
+    CKS(record_pair(h, true, true));
+    CK(swr::launch_march_nl(p, h->shape_nl, h->st));
+    CK(cudaGetLastError());
+    CKS(record_pair(h, true, false));
+    h->n_marches++;
+    h->n_launches++;
+    h->cell_steps += (double)nreal * h->Nj * h->NT;
+    return SWR_OK;
+  }
   if (getenv("SWR_TRACE")) {
     static long long *tr = nullptr;
     if (!tr) CK(cudaMalloc(&tr, 64 * sizeof(long long)));
@@ -259,6 +283,9 @@ MarchSys make_sys(swr_handle *h, int j, const double2 *g, bool use_u0, bool zero
     const int zi = zero_matrix_index(h, j);
     s.q = h->q0 + (size_t)zi * h->Nj;
     s.er = h->er0 + (size_t)zi * h->Nj;
+  } else if (h->potential == SWR_POT_VTX_SEPARABLE) {
+    s.q = h->qtd + (size_t)(j - 1) * h->Nj;     // step 1; step n at + (n-1) N N_j
+    s.er = h->ertd + (size_t)(j - 1) * h->Nj;
   } else {
     s.q = h->q + (size_t)(j - 1) * h->Nj;
     s.er = h->er + (size_t)(j - 1) * h->Nj;
@@ -277,7 +304,10 @@ int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2
   std::vector<MarchSys> sys;
   for (int j = 1; j <= h->N; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
   if (Rg) CKS(fill_zero(h, Rg, h->ng));
-  return run_march(h, sys, 1, (int)sys.size());
+  int mode = MARCH_CONST;
+  if (!zero_pot && h->potential == SWR_POT_VTX_SEPARABLE) mode = MARCH_TD;
+  if (!zero_pot && h->potential == SWR_POT_CUBIC) mode = MARCH_NL;
+  return run_march(h, sys, 1, (int)sys.size(), mode);
 }
 
 // ---- assembly + factorisation ----------------------------------------------
@@ -290,6 +320,7 @@ int factor_matrices(swr_handle *h) {
       J.W = (h->potential == SWR_POT_VX) ? h->Vx + (size_t)(j - 1) * h->m : nullptr;
       J.has_left = j >= 2;
       J.has_right = j <= h->N - 1;
+      J.g0 = (j - 1) * h->m;
       J.q = h->q + (size_t)(j - 1) * h->Nj;
       J.er = h->er + (size_t)(j - 1) * h->Nj;
       jobs.push_back(J);
@@ -301,11 +332,40 @@ int factor_matrices(swr_handle *h) {
       J.W = nullptr;
       J.has_left = zi >= 1;
       J.has_right = zi <= 1;
+      J.g0 = 0;
       if (h->N == 1) J.has_left = J.has_right = 0;
       J.q = h->q0 + (size_t)zi * h->Nj;
       J.er = h->er0 + (size_t)zi * h->Nj;
       jobs.push_back(J);
     }
+  }
+  if (h->potential == SWR_POT_VTX_SEPARABLE) {
+    std::vector<swr::FactorJob> tj;
+    for (int j = 1; j <= h->N; j++) {
+      swr::FactorJob J;
+      J.W = nullptr;
+      J.has_left = j >= 2;
+      J.has_right = j <= h->N - 1;
+      J.g0 = (j - 1) * h->m;
+      J.q = h->qtd + (size_t)(j - 1) * h->Nj;
+      J.er = h->ertd + (size_t)(j - 1) * h->Nj;
+      tj.push_back(J);
+    }
+    swr::FactorJob *tdev = nullptr;
+    CKS(dalloc(&tdev, tj.size()));
+    CK(cudaMemcpyAsync(tdev, tj.data(), tj.size() * sizeof(tj[0]), cudaMemcpyHostToDevice, h->st));
+    CK(cudaMemsetAsync(h->err_dev, 0, sizeof(int), h->st));
+    const long nth = (long)tj.size() * h->NT;
+    swr::k_factor_td<<<(unsigned)((nth + 127) / 128), 128, 0, h->st>>>(tdev, (int)tj.size(), h->Nj, h->NT, h->dx, h->dt,
+                                                                      h->c0, h->tau, h->xi, h->n_terms, h->Nx, h->m,
+                                                                      (size_t)h->N * h->Nj, h->err_dev);
+    CK(cudaGetLastError());
+    h->n_launches++;
+    int herr = 0;
+    CK(cudaMemcpyAsync(&herr, h->err_dev, sizeof(int), cudaMemcpyDeviceToHost, h->st));
+    CK(cudaStreamSynchronize(h->st));
+    cudaFree(tdev);
+    if (herr) { g_detail = "zero pivot while factoring A_n - B"; return SWR_ERR_ZERO_PIVOT; }
   }
   if (jobs.empty()) return SWR_OK;
   CK(cudaFree(h->jobs_dev));
@@ -357,7 +417,7 @@ int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w
 }
 
 int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, Krylov &K,
-          int *iters, std::vector<double> *hist, int *converged) {
+          int *iters, std::vector<double> *hist, int *converged, bool speculate = true) {
   const size_t n = h->ng;
   const size_t ldv = n;
   double2 *V = K.V, *w = K.w;
@@ -416,7 +476,8 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
     int k, kend = 0;
     CKS(issue(0));
     for (k = 0; k < m; k++) {
-      if (k + 1 < m && total + 1 < maxit) CKS(issue(k + 1));   // speculative next step
+      if (!speculate && k > 0) CKS(issue(k));                             // issue step k now
+      if (speculate && k + 1 < m && total + 1 < maxit) CKS(issue(k + 1));  // or issue the next step ahead
       CK(cudaEventSynchronize(K.ev[k & 1]));
       const double2 *hp = HP(k & 1);
       total++;
@@ -581,6 +642,7 @@ int alloc_krylov(Krylov &K, size_t mm, size_t ng) {
 void free_all(swr_handle *h) {
   void *ptrs[] = {h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
+                  h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev, h->counter};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -650,8 +712,10 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     return SWR_ERR_INVALID_ARG;
   }
   if (cfg->potential == SWR_POT_VX && !cfg->V_x) return SWR_ERR_INVALID_ARG;
-  if (cfg->potential == SWR_POT_VTX_SEPARABLE) { g_detail = "V(t,x) march not enabled yet"; return SWR_ERR_UNSUPPORTED; }
-  if (cfg->potential == SWR_POT_CUBIC) { g_detail = "nonlinear march not enabled yet"; return SWR_ERR_UNSUPPORTED; }
+  if (cfg->potential == SWR_POT_VTX_SEPARABLE && (cfg->n_terms < 1 || !cfg->tau || !cfg->xi)) {
+    g_detail = "V(t,x) needs n_terms >= 1, tau and xi";
+    return SWR_ERR_INVALID_ARG;
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { g_detail = "no CUDA device"; return SWR_ERR_CUDA; }
@@ -695,6 +759,23 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       (s = dalloc(&h->counter, 1)))
     return fail(s);
   if (h->potential == SWR_POT_VX && (s = dalloc(&h->Vx, nx1))) return fail(s);
+  if (h->potential == SWR_POT_VTX_SEPARABLE) {
+    const size_t nt = (size_t)h->n_terms;
+    if ((s = dalloc(&h->tau, nt * (NTt + 1))) || (s = dalloc(&h->xi, nt * nx1)) ||
+        (s = dalloc(&h->qtd, NTt * (size_t)h->N * h->Nj)) || (s = dalloc(&h->ertd, NTt * (size_t)h->N * h->Nj)))
+      return fail(s);
+    if ((s = copy_in_r(h->tau, cfg->tau, nt * (NTt + 1), cfg->inputs_on_device, h->st)) ||
+        (s = copy_in_r(h->xi, cfg->xi, nt * nx1, cfg->inputs_on_device, h->st)))
+      return fail(s);
+  }
+  if ((s = dalloc(&h->fp_stat, 2))) return fail(s);
+  if (cudaMemset(h->fp_stat, 0, 2 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_CUDA);
+  h->shape_nl = swr::choose_march_shape_nl(h->Nj);
+  if (h->potential == SWR_POT_CUBIC &&
+      (h->shape_nl.M == 0 || swr::march_nl_smem_bytes(h->shape_nl, h->NT, true) > 227 * 1024)) {
+    g_detail = "subdomain too large for the resident nonlinear march";
+    return fail(SWR_ERR_UNSUPPORTED);
+  }
   if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
   if (ng) {
     const size_t mm = h->restart + 1;
@@ -792,6 +873,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
   h->iterations = h->inner_total = h->fp_max = 0;
   h->converged = 1;
   h->inner_fail = false;
+  CK(cudaMemsetAsync(h->fp_stat, 0, 2 * sizeof(int), h->st));
   int st = SWR_OK;
   if (h->N > 1) {
     if (h->g0) CK(cudaMemcpyAsync(h->g, h->g0, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
@@ -801,6 +883,28 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
       if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
       Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
       st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv);
+    } else if (h->potential == SWR_POT_CUBIC) {
+      // preconditioned fixed point (eq. chp2_algopd_NL, reading A9):
+      // g <- g - P^{-1}(g - R_nl(g)), stop at ||g^{k+1} - g^k||_2 < tol (A5)
+      if (!h->have_L0) CKS(swr_build_interface_operator(h));
+      double2 *hp = h->hpin;
+      while (it < h->maxit) {
+        CKS(sweep_R(h, h->g, true, false, h->tmp, nullptr));
+        swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(h->g, h->tmp, h->tmp2, h->ng);
+        CK(cudaGetLastError());
+        const int s2 = apply_Pinv(h, h->tmp2, h->tmp);
+        if (s2 && s2 != SWR_ERR_INNER_NOT_CONVERGED) return s2;
+        swr::k_axpby<<<grid_for(h->ng), 256, 0, h->st>>>(make_double2(-1.0, 0.0), h->tmp, make_double2(1.0, 0.0),
+                                                        h->g, h->ng);
+        CK(cudaGetLastError());
+        CKS(cgs(h, nullptr, 0, nullptr, h->tmp, swr::CGS_NORM, h->kout.dots));
+        CKS(fetch(h, h->kout.dots, 1, hp));
+        const double diff = std::sqrt(hp[0].x);
+        h->hist.push_back(diff);
+        it++;
+        h->n_launches += 2;
+        if (diff < h->tol) { conv = 1; break; }
+      }
     } else {
       if (!h->have_L0 || !h->have_d) CKS(swr_build_interface_operator(h));
       CKS(apply_Pinv(h, h->d, h->rhs));
@@ -810,7 +914,9 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         CK(cudaGetLastError());
         return apply_Pinv(h, h->tmp2, b);
       };
-      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv);
+      // the operator runs an inner GMRES (host round trips): no speculation,
+      // which would also run inner solves the oracle does not
+      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, false);
     }
     if (st && st != SWR_ERR_INNER_NOT_CONVERGED) return st;
     h->iterations = it;
@@ -823,6 +929,12 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
     CK(cudaMemcpyAsync(u_T, h->uT, ((size_t)h->Nx + 1) * sizeof(double2),
                        u_T_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
   CK(cudaStreamSynchronize(h->st));
+  {
+    int fs[2] = {0, 0};
+    CK(cudaMemcpy(fs, h->fp_stat, sizeof fs, cudaMemcpyDeviceToHost));
+    h->fp_max = fs[0];
+    if (fs[1]) h->inner_fail = true;
+  }
   if (rep) {
     memset(rep, 0, sizeof(*rep));
     rep->iterations = h->iterations;

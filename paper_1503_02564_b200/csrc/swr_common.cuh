@@ -70,6 +70,12 @@ struct MarchParams {
   int32_t flux_smem;         // 1: stage the incoming flux series in shared memory
   const double *beta;        // [N_T+1] beta_s
   long long *trace;          // optional per-phase clock trace (debug), NULL in production
+  size_t td_stride;          // V(t,x): q/er of step n at q + (n-1) td_stride; 0 = constant matrix
+  // nonlinear f(u) = lambda |u|^2, k_march_nl only
+  double lambda, h12;        // lambda, h/12
+  double tol_fp;
+  int32_t maxit_fp;
+  int32_t *fp_stat;          // [0] max fixed-point iterations (atomicMax), [1] = 1 if a step hit maxit_fp
 };
 
 }  // namespace swr

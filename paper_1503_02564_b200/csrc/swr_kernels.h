@@ -7,6 +7,7 @@ namespace swr {
 struct FactorJob {
   const double *W;   // nodal W on the subdomain [N_j] (NULL = 0)
   int32_t has_left, has_right;
+  int32_t g0, pad_; // global index of local node 0 (V(t,x))
   double2 *q;        // [N_j] out: 1/p_k
   double *er;        // [N_j] out: Re E_k
 };
@@ -40,5 +41,10 @@ struct MarchShape { int M, P, CS, K; };
 MarchShape choose_march_shape(int Nj, int K);
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
+MarchShape choose_march_shape_nl(int Nj);
+size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
+cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st);
+__global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, double h, double dt, double2 c0,
+                            const double *tau, const double *xi, int n_terms, int Nx, int m, size_t stride, int *err);
 
 }  // namespace swr

@@ -46,6 +46,55 @@ __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, dou
   }
 }
 
+// V(t,x) = sum_t tau_t(t) xi_t(x): factorisation of (A_{j,n} - B) for every
+// step n (W_n = (V_n + V_{n-1})/2 enters A_{j,n} through M_{W_n}),
+// one thread per (subdomain, step); step n's pivots at q + (n-1) stride.
+__global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, double h, double dt, double2 c0,
+                            const double *tau, const double *xi, int n_terms, int Nx, int m, size_t stride, int *err) {
+  const long idx = blockIdx.x * (long)blockDim.x + threadIdx.x;
+  if (idx >= (long)njobs * NT) return;
+  const int jb = (int)(idx % njobs), n = (int)(idx / njobs) + 1;
+  const FactorJob J = jobs[jb];
+  (void)Nx; (void)m;
+  const double eim = (2.0 / dt) * (h / 6.0);
+  auto Wat = [&](int k) -> double {       // W_n at local node k
+    double w = 0.0;
+    for (int tt = 0; tt < n_terms; tt++) {
+      const double tb = 0.5 * (tau[(size_t)tt * (NT + 1) + n] + tau[(size_t)tt * (NT + 1) + n - 1]);
+      w += tb * xi[(size_t)tt * (Nx + 1) + J.g0 + k];
+    }
+    return w;
+  };
+  double2 *qo = J.q + (size_t)(n - 1) * stride;
+  double *eo = J.er + (size_t)(n - 1) * stride;
+  double er_prev = 0.0;
+  double2 qprev = cz();
+  double Wl = 0.0, Wk = Wat(0);
+  for (int k = 0; k < Nj; k++) {
+    const double Wr = (k < Nj - 1) ? Wat(k + 1) : 0.0;
+    double Md = 0.0, Sd = 0.0, MWd = 0.0;
+    if (k > 0) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (Wl + 3.0 * Wk) / 12.0; }
+    if (k < Nj - 1) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (3.0 * Wk + Wr) / 12.0; }
+    double2 D = make_double2(-Sd + MWd, (2.0 / dt) * Md);
+    if (k == 0 && J.has_left) D = csub(D, c0);
+    if (k == Nj - 1 && J.has_right) D = csub(D, c0);
+    double2 p = D;
+    if (k > 0) {
+      const double2 E = make_double2(er_prev, eim);
+      p = csub(D, cmul(E, cmul(E, qprev)));
+    }
+    if (!(hypot(p.x, p.y) >= 1e-300)) atomicExch(err, 3);
+    const double2 qk = crcp(p);
+    const double erk = (k < Nj - 1) ? 1.0 / h + h * (Wk + Wr) / 12.0 : 0.0;
+    qo[k] = qk;
+    eo[k] = erk;
+    qprev = qk;
+    er_prev = erk;
+    Wl = Wk;
+    Wk = Wr;
+  }
+}
+
 // ---------------------------------------------------------------------------
 // y = x - L x with the block pattern of eq. (15)/(16) and
 // causal convolutions (x * y)_n = sum_{s<=n} x_{n-s} y_s (Props. 3-4,

@@ -305,6 +305,29 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
+    if (p.td_stride && n > 1) {
+      // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
+      const double2 *qp = G[0].q + (size_t)(n - 1) * p.td_stride;
+      const double *erp = G[0].er + (size_t)(n - 1) * p.td_stride;
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        const int k = s0 + i;
+        q[i] = k < Nj ? __ldg(qp + k) : make_double2(1.0, 0.0);
+        er[i] = k < Nj ? __ldg(erp + k) : 0.0;
+      }
+      er_prev = (s0 >= 1 && s0 - 1 < Nj) ? __ldg(erp + s0 - 1) : 0.0;
+      double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
+#pragma unroll
+      for (int i = 0; i < M; i++) {
+        const int k = s0 + i;
+        const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
+        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+        Af = cmul(Af, c);
+        Ab = cmul(Ab, b);
+      }
+      sAf[t] = Af;
+      sAb[t] = Ab;
+    }
     // ---- S0^2 history H = c2 sum_{s<n} beta_{n-s} v_s:
     // every thread of the CTA holding the boundary row adds a slice of
     // s <= n-2 (written before the last barrier); the owner of the row adds
@@ -483,6 +506,295 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 }
 
 // ---------------------------------------------------------------------------
+// Nonlinear march, f(u) = lambda |u|^2 (Duran-Sanz-Serna midpoint),
+// one RHS per group.  Per step the inner fixed point of eq. (12):
+//   (A_NL - B) z^{s+1} = (2i/dt) M u_{n-1} - M_{f(z^s)} z^s + b_n - Q^T(l_n, r_n)^T
+// from z^0 = v_{n-1}, with the load M_{f(z)} z the weighted mass matrix of the
+// nodal values f(z_k) (reading A3), stopped when
+// max_k |z^{s+1} - z^s| <= tol_fp max_k |z^{s+1}| (reading A4; the maxima are
+// reduced over the cluster so the decision is uniform).  (A_NL - B) is the
+// V = 0 matrix: constant pivots, Re E_k = 1/h.
+// ---------------------------------------------------------------------------
+template <int M, int PMAX>
+__global__ void __launch_bounds__(PMAX, 1) k_march_nl(const MarchParams p) {
+  extern __shared__ double2 sm[];
+  const int P = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = P >> 5;
+  const int CS = p.CS;
+  const int crank = blockIdx.x % CS;
+  const MarchSys *G = p.sys + blockIdx.x / CS;
+  const int Nj = p.Nj, NT = p.NT;
+  const int s0 = (crank * P + t) * M;
+  const double eim = p.e_im;
+
+  double2 *ybuf = sm;                                   // [M][P]
+  double2 *hfirst = ybuf + M * P, *hlast = hfirst + P;  // [P] halo of u_{n-1}
+  double2 *zfirst = hlast + P, *zlast = zfirst + P;     // [P] halo of z^s
+  double2 *sAf = zlast + P, *sAb = sAf + P;             // [P]
+  ScanBuf<1> sf, sbk;
+  sf.wA = sAb + P;            sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32;
+  sbk.wA = sf.ctot + 32;      sbk.wB = sbk.wA + 32;     sbk.ctot = sbk.wB + 32;
+  double2 *hva = sbk.ctot + 32, *hvb = hva + (NT + 1);  // [NT+1]
+  double2 *hred = hvb + (NT + 1);                       // [2][32]
+  double2 *sH = hred + 64;                              // [2]
+  double2 *smax = sH + 2;                               // [32] warp maxima (x: |dz|^2, y: |z|^2); [32+16]: CTA maxima
+  double2 *sflux = smax + 64;                           // [2][NT] if p.flux_smem
+  double *sbeta = reinterpret_cast<double *>(sflux + (p.flux_smem ? 2 * NT : 0));
+
+  const int flags = G->flags;
+  const bool has_left = flags & SYS_HAS_LEFT, has_right = flags & SYS_HAS_RIGHT;
+  const int rows_cta = P * M;
+  const int cb = (Nj - 1) / rows_cta, tb = ((Nj - 1) % rows_cta) / M;
+  const bool owns_a = has_left && s0 == 0;
+  const bool owns_b = has_right && crank == cb && t == tb;
+
+  for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
+  if (p.flux_smem) {
+    for (int i = t; i < NT; i += P) {
+      sflux[i] = G->lin ? G->lin[i] : cz();
+      sflux[NT + i] = G->rin ? G->rin[i] : cz();
+    }
+  }
+  if (t < 2) sH[t] = cz();
+
+  double2 u[M], q[M], ze[M];
+  double er[M];
+  double er_prev;
+  {
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const int k = s0 + i;
+      q[i] = k < Nj ? G->q[k] : make_double2(1.0, 0.0);
+      er[i] = k < Nj ? G->er[k] : 0.0;
+      u[i] = (G->u0 && k < Nj) ? G->u0[k] : cz();
+      ze[i] = u[i];                                   // z^0 of step 1 = v_0 = u_0
+    }
+    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? G->er[s0 - 1] : 0.0;
+    double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const int k = s0 + i;
+      const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
+      const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+      Af = cmul(Af, c);
+      Ab = cmul(Ab, b);
+    }
+    sAf[t] = Af;
+    sAb[t] = Ab;
+  }
+  if (s0 == 0) hva[0] = u[0];
+#pragma unroll
+  for (int i = 0; i < M; i++)
+    if (s0 + i == Nj - 1) hvb[0] = u[i];
+  __syncthreads();
+
+  auto flux = [&](int side, int n) -> double2 {
+    const int imp = side == 0 ? (flags & SYS_LIN_IMPULSE) : (flags & SYS_RIN_IMPULSE);
+    if (imp) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
+    return p.flux_smem ? sflux[side * NT + n - 1] : cz();
+  };
+  int fp_max = 0, fp_fail = 0;
+
+#pragma unroll 1
+  for (int n = 1; n <= NT; n++) {
+    if (p.s02) {
+      if (has_left && crank == 0) {
+        double2 acc = cz();
+        for (int s = t; s < n - 1; s += P) {
+          const double b = sbeta[n - s];
+          acc.x = fma(b, hva[s].x, acc.x);
+          acc.y = fma(b, hva[s].y, acc.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+        if (lane == 0) hred[w] = acc;
+      }
+      if (has_right && crank == cb) {
+        double2 acc = cz();
+        for (int s = t; s < n - 1; s += P) {
+          const double b = sbeta[n - s];
+          acc.x = fma(b, hvb[s].x, acc.x);
+          acc.y = fma(b, hvb[s].y, acc.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+        if (lane == 0) hred[32 + w] = acc;
+      }
+    }
+    hfirst[t] = u[0];
+    hlast[t] = u[M - 1];
+    csync(CS, t == 0 || t == P - 1);
+    if (p.s02 && (owns_a || owns_b)) {
+      if (owns_a) {
+        double2 hh = cscale(sbeta[1], hva[n - 1]);
+        for (int qq = 0; qq < nw; qq++) hh = cadd(hh, hred[qq]);
+        sH[0] = cmul(p.c2, hh);
+      }
+      if (owns_b) {
+        double2 hh = cscale(sbeta[1], hvb[n - 1]);
+        for (int qq = 0; qq < nw; qq++) hh = cadd(hh, hred[32 + qq]);
+        sH[1] = cmul(p.c2, hh);
+      }
+    }
+    double2 uL = cz(), uR = cz();
+    if (t > 0) uL = hlast[t - 1];
+    else if (crank > 0) uL = *remote(hlast + (P - 1), crank - 1);
+    if (t < P - 1) uR = hfirst[t + 1];
+    else if (crank < CS - 1) uR = *remote(hfirst, crank + 1);
+
+    int it;
+    bool conv = false;
+#pragma unroll 1
+    for (it = 1; it <= p.maxit_fp; it++) {
+      // halo of z^s
+      zfirst[t] = ze[0];
+      zlast[t] = ze[M - 1];
+      csync(CS, t == 0 || t == P - 1);
+      double2 zL = cz(), zR = cz();
+      if (t > 0) zL = zlast[t - 1];
+      else if (crank > 0) zL = *remote(zlast + (P - 1), crank - 1);
+      if (t < P - 1) zR = zfirst[t + 1];
+      else if (crank < CS - 1) zR = *remote(zfirst, crank + 1);
+      // forward sweep with rhs = (2i/dt) M u_{n-1} - M_{f(z)} z + b_n - Q^T(l,r)
+      double2 z = cz();
+#pragma unroll 1
+      for (int pass = 0; pass < 2; pass++) {
+        launder<M>(q, er);
+#pragma unroll
+        for (int i = 0; i < M; i++) {
+          const int k = s0 + i;
+          double2 c = cz(), rr = cz();
+          if (k < Nj) {
+            const double2 um = i == 0 ? uL : u[i == 0 ? 0 : i - 1];
+            const double2 up = i == M - 1 ? uR : u[i == M - 1 ? M - 1 : i + 1];
+            rr = rhs_row<true>(k, Nj, um, u[i], up, p.kappa);
+            // weighted mass load (P1 elements, linear interpolant of W = f(z))
+            const double2 zm = i == 0 ? zL : ze[i == 0 ? 0 : i - 1];
+            const double2 zp = i == M - 1 ? zR : ze[i == M - 1 ? M - 1 : i + 1];
+            const double2 zc = ze[i];
+            const double Wc = p.lambda * fma(zc.x, zc.x, zc.y * zc.y);
+            const double Wm = p.lambda * fma(zm.x, zm.x, zm.y * zm.y);
+            const double Wp = p.lambda * fma(zp.x, zp.x, zp.y * zp.y);
+            double2 ld = cz();
+            if (k > 0) {   // element (k-1, k)
+              ld.x += (Wm + 3.0 * Wc) * zc.x + (Wm + Wc) * zm.x;
+              ld.y += (Wm + 3.0 * Wc) * zc.y + (Wm + Wc) * zm.y;
+            }
+            if (k < Nj - 1) {  // element (k, k+1)
+              ld.x += (3.0 * Wc + Wp) * zc.x + (Wc + Wp) * zp.x;
+              ld.y += (3.0 * Wc + Wp) * zc.y + (Wc + Wp) * zp.y;
+            }
+            rr = make_double2(fma(-p.h12, ld.x, rr.x), fma(-p.h12, ld.y, rr.y));
+            if (k == 0 && owns_a) rr = cadd(rr, csub(sH[0], flux(0, n)));
+            if (k == Nj - 1 && owns_b) rr = cadd(rr, csub(sH[1], flux(1, n)));
+            if (k >= 1) c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
+          }
+          z = cfma(c, z, cmul(q[i], rr));
+          if (pass == 1) ybuf[i * P + t] = z;
+        }
+        if (pass == 0) {
+          double2 zz[1] = {z}, carry[1];
+          scan_maps<1, true>(sAf[t], zz, sf, lane, w, nw, CS, crank, carry);
+          z = carry[0];
+        }
+      }
+      double2 x = cz();
+      launder<M>(q, er);
+#pragma unroll
+      for (int i = M - 1; i >= 0; i--) {
+        const int k = s0 + i;
+        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+        x = cfma(b, x, ybuf[i * P + t]);
+      }
+      {
+        double2 xx[1] = {x}, carry[1];
+        scan_maps<1, false>(sAb[t], xx, sbk, lane, w, nw, CS, crank, carry);
+        x = carry[0];
+      }
+      launder<M>(q, er);
+      double dmax = 0.0, nmax = 0.0;
+#pragma unroll
+      for (int i = M - 1; i >= 0; i--) {
+        const int k = s0 + i;
+        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+        x = cfma(b, x, ybuf[i * P + t]);
+        if (k < Nj) {
+          const double dx = x.x - ze[i].x, dy = x.y - ze[i].y;
+          dmax = fmax(dmax, fma(dx, dx, dy * dy));
+          nmax = fmax(nmax, fma(x.x, x.x, x.y * x.y));
+        }
+        ze[i] = x;
+      }
+      // cluster-wide maxima -> uniform convergence decision
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+      }
+      if (lane == 0) smax[w] = make_double2(dmax, nmax);
+      __syncthreads();
+      double2 mm = lane < nw ? smax[lane] : cz();
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        mm.x = fmax(mm.x, __shfl_xor_sync(0xffffffffu, mm.x, o));
+        mm.y = fmax(mm.y, __shfl_xor_sync(0xffffffffu, mm.y, o));
+      }
+      if (CS > 1) {
+        if (t == 0) {
+#pragma unroll 1
+          for (int c = 0; c < CS; c++) *remote(smax + 32 + crank, c) = mm;
+          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+        }
+        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
+        mm = cz();
+        for (int c = 0; c < CS; c++) {
+          const double2 v = smax[32 + c];
+          mm.x = fmax(mm.x, v.x);
+          mm.y = fmax(mm.y, v.y);
+        }
+      }
+      if (sqrt(mm.x) <= p.tol_fp * sqrt(mm.y)) { conv = true; break; }
+    }
+    if (!conv) { it = p.maxit_fp; fp_fail = 1; }
+    if (it > fp_max) fp_max = it;
+    // v_n = z; record S v_n at the interfaces; u_n = 2 v_n - u_{n-1}
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const int k = s0 + i;
+      const double2 x = ze[i];
+      if (k == 0 && owns_a) {
+        hva[n] = x;
+        if (G->out_left) {
+          const double2 sv = cfma(p.c0, x, sH[0]);
+          const double2 l = flux(0, n);
+          G->out_left[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
+        }
+      }
+      if (k == Nj - 1 && owns_b) {
+        hvb[n] = x;
+        if (G->out_right) {
+          const double2 sv = cfma(p.c0, x, sH[1]);
+          const double2 rv = flux(1, n);
+          G->out_right[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
+        }
+      }
+      u[i] = make_double2(fma(2.0, x.x, -u[i].x), fma(2.0, x.y, -u[i].y));
+    }
+    __syncthreads();   // smax and the z halo are rewritten next step
+  }
+  if (G->uT) {
+#pragma unroll
+    for (int i = 0; i < M; i++)
+      if (s0 + i < Nj) G->uT[s0 + i] = u[i];
+  }
+  if (t == 0 && crank == 0 && p.fp_stat) {
+    atomicMax(p.fp_stat, fp_max);
+    if (fp_fail) atomicOr(p.fp_stat + 1, 1);
+  }
+  if (CS > 1) cg::this_cluster().sync();
+}
+
+// ---------------------------------------------------------------------------
 // Launch-shape selection and launcher.  Instantiated (M rows per thread, K
 // RHS per group, PMAX threads per CTA); the register cap is 65536 / PMAX.
 // ---------------------------------------------------------------------------
@@ -511,6 +823,70 @@ MarchShape choose_march_shape(int Nj, int K) {
     }
   }
   return best;
+}
+
+MarchShape choose_march_shape_nl(int Nj) {
+  MarchShape best{0, 0, 0, 1};
+  double best_cost = 1e300;
+  for (int CS = 1; CS <= 16; CS++) {
+    for (int M : {1, 2, 4, 8}) {
+      const int PMAX = M <= 2 ? 512 : 256;
+      long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
+      int P = (int)((per + 31) / 32 * 32);
+      if (P < 32) P = 32;
+      if (P > PMAX) continue;
+      double padded = (double)CS * P * M;
+      double cost = padded * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
+      if (cost < best_cost) { best_cost = cost; best = {M, P, CS, 1}; }
+    }
+  }
+  return best;
+}
+
+size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
+  size_t d2 = (size_t)s.M * s.P + 6 * (size_t)s.P + 4 * 32 + 2 * 32 + 2 * (size_t)(NT + 1) + 64 + 2 + 64 +
+              (flux_smem ? 2 * (size_t)NT : 0);
+  return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
+}
+
+template <int M, int PMAX>
+static cudaError_t launch_nl_m(const MarchParams &p, const MarchShape &s, size_t smem, cudaStream_t st) {
+  auto kern = k_march_nl<M, PMAX>;
+  cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (s.CS > 8) {
+    e = cudaFuncSetAttribute(kern, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(p.nsys * s.CS, 1, 1);
+  cfg.blockDim = dim3(s.P, 1, 1);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  cfg.attrs = attr;
+  cfg.numAttrs = 0;
+  if (s.CS > 1) {
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = s.CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cfg.numAttrs = 1;
+  }
+  return cudaLaunchKernelEx(&cfg, kern, p);
+}
+
+cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st) {
+  p.CS = s.CS;
+  const size_t smem = march_nl_smem_bytes(s, p.NT, p.flux_smem);
+  if (smem > 227 * 1024) return cudaErrorInvalidValue;
+  switch (s.M) {
+    case 1: return launch_nl_m<1, 512>(p, s, smem, st);
+    case 2: return launch_nl_m<2, 512>(p, s, smem, st);
+    case 4: return launch_nl_m<4, 256>(p, s, smem, st);
+    case 8: return launch_nl_m<8, 256>(p, s, smem, st);
+    default: return cudaErrorInvalidValue;
+  }
 }
 
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {

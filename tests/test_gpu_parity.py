@@ -166,3 +166,49 @@ def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
         y_g = g_.apply_I_minus_L(torch.as_tensor(x, device="cuda"), 0).cpu().numpy()
         y_o = x - o.apply_L(X_g.cpu().numpy(), x)
         assert rel(y_g, y_o) <= 1e-12, mode
+
+
+PRECOND_CASES = [
+    ("vtx-s02-N4", si.config("C1", transmission=si.TC_S02, potential=si.POT_VTX, algorithm=si.ALG_PRECOND, N=4)),
+    ("vtx-robin-N5", si.config("C1", transmission=si.TC_ROBIN, potential=si.POT_VTX, algorithm=si.ALG_PRECOND, N=5,
+                               robin_p=5.0)),
+    ("vtx-mid-N20", si.Problem(dx=2e-3, dt=5e-3, N=20, potential=si.POT_VTX, algorithm=si.ALG_PRECOND)),
+    ("nl-s02-N4", si.config("C1", transmission=si.TC_S02, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, N=4,
+                            u0_kind="soliton")),
+    ("nl-robin-N4", si.config("C1", transmission=si.TC_ROBIN, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, N=4,
+                              u0_kind="soliton", robin_p=20.0)),
+    ("nl-mid-N20", si.Problem(dx=2e-3, dt=5e-3, N=20, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND,
+                              u0_kind="soliton")),
+]
+
+
+@pytest.mark.parametrize("name,p", PRECOND_CASES, ids=[c[0] for c in PRECOND_CASES])
+def test_precond_parity(oracle_mod, gpu, name, p):
+    """Preconditioned algorithms: GMRES on P^{-1}(I-L)g = P^{-1}d
+    for V(t,x) and the preconditioned fixed point for |u|^2; equal outer and
+    inner iteration counts and NL fixed-point maxima, u(T) within 1e-10."""
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    info = dict(outer=(rg["iterations"], ro["iterations"]), inner=(rg["inner_iterations"], ro["inner_iterations"]),
+                fp=(rg["fp_max"], ro["fp_max"]), err=rel(uT, ro["uT"]), st=(st, ro["status"]))
+    print(name, info)
+    assert ro["status"] == 0 and st == 0, info
+    assert rg["iterations"] == ro["iterations"], info
+    # the inner P^{-1} solves stop at 1e-12 relative, at the rounding floor of
+    # (I - L0): their counts may differ by a step now and then (DESIGN.md)
+    assert abs(rg["inner_iterations"] - ro["inner_iterations"]) <= max(2, 0.02 * ro["inner_iterations"]), info
+    assert rg["fp_max"] == ro["fp_max"], info
+    assert rel(uT, ro["uT"]) <= 1e-10, info
+
+
+def test_nl_sweep_parity(oracle_mod, gpu):
+    """One nonlinear sweep R_nl(g; u0) with a random g (several CTAs)."""
+    import torch
+    p = si.Problem(dx=1e-3, dt=5e-3, N=20, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, u0_kind="soliton")
+    o, g_ = _pair(oracle_mod, gpu, p)
+    rng = np.random.default_rng(21)
+    g = 0.1 * (rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng))
+    Rg_o = o.apply_R(g, use_u0=True)
+    Rg_g, _ = g_.apply_R(torch.as_tensor(g, device="cuda"), use_u0=True)
+    assert rel(Rg_g.cpu().numpy(), Rg_o) <= 1e-11
