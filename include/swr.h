@@ -95,7 +95,7 @@ typedef struct {
   double tol_fp;              /* NL inner fixed point relative max-norm: 1e-12 */
   int32_t maxit_fp;           /* 50 */
   const double *g0;           /* [2*n_g] initial interface vector, NULL = zero */
-  int32_t rank, world;        /* world = 1: single GPU, no NCCL */
+  int32_t rank, world;        /* world = 1: single GPU, no NCCL; world <= N */
   const void *nccl_unique_id; /* 128-byte ncclUniqueId (world > 1) */
   void *cuda_stream;          /* cudaStream_t owned by the caller (NULL = default stream) */
   int32_t device;             /* CUDA device ordinal for this rank */
@@ -167,6 +167,21 @@ int swr_get_g(swr_handle *h, double *g);
 
 /* Sizes: N_x, N_T, N_j, n_g. */
 int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_t *ng);
+
+/* ---- Multi-GPU (one process per GPU). ----------------------
+ * Subdomains are sharded contiguously: rank r of W owns
+ * j in [floor(rN/W)+1, floor((r+1)N/W)] (P:982-1011 ownership rule).  Each
+ * rank marches only its subdomains; the outputs of eq. (8) that cross a rank
+ * cut, the interface operator d, L (L0) and u(T) are summed over ranks with
+ * ncclAllReduce (disjoint supports: exact), and the interface Krylov solve is
+ * replicated on every rank (identical iteration counts to one GPU).
+ * Pure host function, no GPU needed: */
+int swr_partition(int32_t N, int32_t world, int32_t rank, int32_t *j_lo, int32_t *j_hi);
+
+/* Writes a 128-byte ncclUniqueId (rank 0; broadcast it to the other ranks
+ * and pass it as swr_config.nccl_unique_id).  SWR_ERR_NCCL if libnccl is
+ * not loadable. */
+int swr_nccl_unique_id(void *out128);
 
 #ifdef __cplusplus
 }

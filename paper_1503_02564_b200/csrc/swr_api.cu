@@ -55,6 +55,7 @@ typedef int (*fn_recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_allgather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_group)(void);
+typedef int (*fn_getid)(ncclUniqueId_t *);
 struct Nccl {
   void *lib = nullptr;
   fn_commInitRank commInitRank;
@@ -64,6 +65,7 @@ struct Nccl {
   fn_allreduce allReduce;
   fn_allgather allGather;
   fn_group groupStart, groupEnd;
+  fn_getid getUniqueId;
 };
 Nccl g_nccl;
 enum { nccl_float64 = 8, nccl_sum = 0, nccl_uint8 = 1 };
@@ -84,6 +86,7 @@ int load_nccl() {
   g_nccl.allGather = (fn_allgather)dlsym(g_nccl.lib, "ncclAllGather");
   g_nccl.groupStart = (fn_group)dlsym(g_nccl.lib, "ncclGroupStart");
   g_nccl.groupEnd = (fn_group)dlsym(g_nccl.lib, "ncclGroupEnd");
+  g_nccl.getUniqueId = (fn_getid)dlsym(g_nccl.lib, "ncclGetUniqueId");
   if (!g_nccl.commInitRank || !g_nccl.send || !g_nccl.recv || !g_nccl.allReduce || !g_nccl.groupStart) {
     g_detail = "libnccl is missing symbols";
     return SWR_ERR_NCCL;
@@ -127,6 +130,8 @@ struct swr_handle {
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
+  int j_lo, j_hi;                          // this rank's subdomains (1-based, inclusive)
+  ncclComm_t comm = nullptr;
   cudaStream_t st;
   double2 c0, c2v;
   double kappa, eim;
@@ -299,15 +304,29 @@ int fill_zero(swr_handle *h, double2 *x, size_t n) {
   return SWR_OK;
 }
 
+// Sum over ranks of vectors each rank filled on its own subdomains' slots
+// (disjoint supports, zeros elsewhere: the sum is exact).
+int allreduce_sum(swr_handle *h, double2 *buf, size_t n) {
+  if (h->world <= 1 || n == 0) return SWR_OK;
+  if (g_nccl.allReduce(buf, buf, 2 * n, nccl_float64, nccl_sum, h->comm, h->st) != 0) {
+    g_detail = "ncclAllReduce failed";
+    return SWR_ERR_NCCL;
+  }
+  h->n_launches++;
+  return SWR_OK;
+}
+
 // Rg = R(g; u0?) (eq. 13): every subdomain marches once.
 int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2 *Rg, double2 *uloc) {
   std::vector<MarchSys> sys;
-  for (int j = 1; j <= h->N; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
+  for (int j = h->j_lo; j <= h->j_hi; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
   if (Rg) CKS(fill_zero(h, Rg, h->ng));
   int mode = MARCH_CONST;
   if (!zero_pot && h->potential == SWR_POT_VTX_SEPARABLE) mode = MARCH_TD;
   if (!zero_pot && h->potential == SWR_POT_CUBIC) mode = MARCH_NL;
-  return run_march(h, sys, 1, (int)sys.size(), mode);
+  CKS(run_march(h, sys, 1, (int)sys.size(), mode));
+  if (Rg) CKS(allreduce_sum(h, Rg, h->ng));   // exchange of eq. (8) across rank cuts
+  return SWR_OK;
 }
 
 // ---- assembly + factorisation ----------------------------------------------
@@ -315,7 +334,7 @@ int factor_matrices(swr_handle *h) {
   std::vector<swr::FactorJob> jobs;
   const bool phys_const = h->potential != SWR_POT_VTX_SEPARABLE;
   if (phys_const) {
-    for (int j = 1; j <= h->N; j++) {
+    for (int j = h->j_lo; j <= h->j_hi; j++) {
       swr::FactorJob J;
       J.W = (h->potential == SWR_POT_VX) ? h->Vx + (size_t)(j - 1) * h->m : nullptr;
       J.has_left = j >= 2;
@@ -341,7 +360,7 @@ int factor_matrices(swr_handle *h) {
   }
   if (h->potential == SWR_POT_VTX_SEPARABLE) {
     std::vector<swr::FactorJob> tj;
-    for (int j = 1; j <= h->N; j++) {
+    for (int j = h->j_lo; j <= h->j_hi; j++) {
       swr::FactorJob J;
       J.W = nullptr;
       J.has_left = j >= 2;
@@ -582,7 +601,7 @@ int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
   int nreal = 0;
   CKS(fill_zero(h, X, (size_t)N * 4 * NT));
   if (dvec) CKS(fill_zero(h, dvec, h->ng));
-  for (int j = 1; j <= N; j++) {
+  for (int j = h->j_lo; j <= h->j_hi; j++) {
     double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
     const MarchSys blank = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
     int kk = 0;
@@ -607,14 +626,18 @@ int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
     if (K > 1)
       for (; kk % K; kk++) sys.push_back(blank);
   }
-  return run_march(h, sys, K, nreal);
+  CKS(run_march(h, sys, K, nreal));
+  CKS(allreduce_sum(h, X, (size_t)N * 4 * NT));
+  if (dvec) CKS(allreduce_sum(h, dvec, h->ng));
+  return SWR_OK;
 }
 
 int final_sweep(swr_handle *h, const double2 *g) {
   CKS(sweep_R(h, g, true, false, nullptr, h->uloc));
-  swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->uT);
+  swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->j_lo, h->j_hi, h->uT);
   CK(cudaGetLastError());
   h->n_launches++;
+  CKS(allreduce_sum(h, h->uT, (size_t)h->Nx + 1));
   return SWR_OK;
 }
 
@@ -655,6 +678,7 @@ void free_all(swr_handle *h) {
   }
   if (h->hpin) cudaFreeHost(h->hpin);
   for (auto &e : h->march_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
   for (auto &e : h->intf_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
 }
 
@@ -680,6 +704,23 @@ const char *swr_error_string(int s) {
 
 const char *swr_last_error_detail(void) { return g_detail.c_str(); }
 
+int swr_partition(int32_t N, int32_t world, int32_t rank, int32_t *j_lo, int32_t *j_hi) {
+  if (N < 1 || world < 1 || world > N || rank < 0 || rank >= world || !j_lo || !j_hi) return SWR_ERR_INVALID_ARG;
+  *j_lo = (int32_t)(((int64_t)rank * N) / world) + 1;
+  *j_hi = (int32_t)(((int64_t)(rank + 1) * N) / world);
+  return SWR_OK;
+}
+
+int swr_nccl_unique_id(void *out) {
+  if (!out) return SWR_ERR_INVALID_ARG;
+  CKS(load_nccl());
+  if (!g_nccl.getUniqueId) { g_detail = "ncclGetUniqueId missing"; return SWR_ERR_NCCL; }
+  ncclUniqueId_t id;
+  if (g_nccl.getUniqueId(&id) != 0) { g_detail = "ncclGetUniqueId failed"; return SWR_ERR_NCCL; }
+  memcpy(out, &id, sizeof id);
+  return SWR_OK;
+}
+
 int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_t *ng) {
   if (!h) return SWR_ERR_INVALID_ARG;
   if (Nx) *Nx = h->Nx;
@@ -703,7 +744,6 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     g_detail = "bad rank/world";
     return SWR_ERR_INVALID_ARG;
   }
-  if (cfg->world > 1) { g_detail = "multi-GPU sharding is not enabled in this build"; return SWR_ERR_UNSUPPORTED; }
   if (cfg->transmission == SWR_TC_ROBIN && !(cfg->robin_p > 0)) { g_detail = "Robin needs p > 0"; return SWR_ERR_INVALID_ARG; }
   if (cfg->transmission != SWR_TC_ROBIN && cfg->transmission != SWR_TC_S0_2) return SWR_ERR_INVALID_ARG;
   if (cfg->potential < 0 || cfg->potential > 3) return SWR_ERR_INVALID_ARG;
@@ -731,7 +771,15 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;
   h->ng = (size_t)(2 * h->N - 2) * h->NT;
   h->rank = cfg->rank; h->world = cfg->world; h->device = cfg->device;
+  swr_partition(h->N, h->world, h->rank, &h->j_lo, &h->j_hi);
   h->st = (cudaStream_t)cfg->cuda_stream;
+  if (h->world > 1) {
+    int s0;
+    if ((s0 = load_nccl()) || !cfg->nccl_unique_id) { delete h; g_detail = "NCCL unavailable or no unique id"; return SWR_ERR_NCCL; }
+    ncclUniqueId_t id;
+    memcpy(&id, cfg->nccl_unique_id, sizeof id);
+    if (g_nccl.commInitRank(&h->comm, h->world, id, h->rank) != 0) { delete h; g_detail = "ncclCommInitRank failed"; return SWR_ERR_NCCL; }
+  }
   // transmission constants: c2 = e^{-i pi/4} sqrt(2/dt) = (1-i)/sqrt(dt)
   const double sq = std::sqrt(h->dt);
   h->c2v = make_double2(1.0 / sq, -1.0 / sq);
@@ -972,8 +1020,10 @@ int swr_apply_R(swr_handle *h, const double *g, int32_t use_u0, int32_t force_ze
   CKS(sweep_R(h, (const double2 *)g, use_u0 != 0, force_zero_potential != 0, (double2 *)Rg,
               u_T ? h->uloc : nullptr));
   if (u_T) {
-    swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, (double2 *)u_T);
+    swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->j_lo, h->j_hi,
+                                                             (double2 *)u_T);
     CK(cudaGetLastError());
+    CKS(allreduce_sum(h, (double2 *)u_T, (size_t)h->Nx + 1));
   }
   CK(cudaStreamSynchronize(h->st));
   return SWR_OK;

@@ -22,7 +22,7 @@ __global__ void k_multi_axpy(const double2 *V, size_t ldv, int nvec, const doubl
 __global__ void k_axpby(double2 a, const double2 *x, double2 b, double2 *y, size_t n);
 __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);
 __global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const double2 *y, double2 *x, size_t n);
-__global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, double2 *uT);
+__global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, int j_lo, int j_hi, double2 *uT);
 __global__ void k_fill(double2 *x, double2 v, size_t n);
 
 enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };

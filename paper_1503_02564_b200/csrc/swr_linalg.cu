@@ -546,15 +546,24 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
 // u(T) on the global mesh from the per-subdomain finals; each duplicated
 // interface node is the mean of its two copies (reading A16).
 // ---------------------------------------------------------------------------
-__global__ void k_gather_uT(const double2 *__restrict__ loc, int N, int m, int Nj, double2 *__restrict__ uT) {
+// Multi-GPU: this rank holds subdomains [j_lo, j_hi] (1-based); nodes of
+// other ranks get 0 and a node shared with another rank gets half of the
+// local copy, so the sum over ranks is the mean of the two copies
+// ((a + b)/2 == a/2 + b/2 exactly in binary floating point).
+__global__ void k_gather_uT(const double2 *__restrict__ loc, int N, int m, int Nj, int j_lo, int j_hi,
+                            double2 *__restrict__ uT) {
   const int Nx = N * m;
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i <= Nx; i += gridDim.x * blockDim.x) {
     const int j = (i == Nx) ? N - 1 : i / m;   // 0-based owner with local index i - j m
     const int k = i - j * m;
-    double2 v = loc[(size_t)j * Nj + k];
-    if (k == 0 && j > 0) {
-      const double2 w = loc[(size_t)(j - 1) * Nj + m];
-      v = make_double2((w.x + v.x) / 2.0, (w.y + v.y) / 2.0);
+    const bool own = (j + 1 >= j_lo && j + 1 <= j_hi);
+    double2 v = own ? loc[(size_t)j * Nj + k] : cz();
+    if (k == 0 && j > 0) {                     // interface node: copies in subdomains j-1 and j
+      const bool ownl = (j >= j_lo && j <= j_hi);
+      const double2 w = ownl ? loc[(size_t)(j - 1) * Nj + m] : cz();
+      if (own && ownl) v = make_double2((w.x + v.x) / 2.0, (w.y + v.y) / 2.0);
+      else if (own) v = make_double2(v.x / 2.0, v.y / 2.0);
+      else if (ownl) v = make_double2(w.x / 2.0, w.y / 2.0);
     }
     uT[i] = v;
   }

@@ -75,8 +75,11 @@ def lib():
         L.swr_get_interface.argtypes = [H, i32, vp, vp]
         L.swr_get_g.argtypes = [H, vp]
         L.swr_sizes.argtypes = [H, vp, vp, vp, vp]
+        L.swr_partition.argtypes = [i32, i32, i32, vp, vp]
+        L.swr_nccl_unique_id.argtypes = [vp]
         for f in ("swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_apply_R",
-                  "swr_apply_I_minus_L", "swr_get_interface", "swr_get_g", "swr_sizes"):
+                  "swr_apply_I_minus_L", "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition",
+                  "swr_nccl_unique_id"):
             getattr(L, f).restype = i32
         _lib = L
     return _lib
@@ -84,7 +87,21 @@ def lib():
 
 EXPORTED = ["swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_free",
             "swr_error_string", "swr_last_error_detail", "swr_apply_R", "swr_apply_I_minus_L",
-            "swr_get_interface", "swr_get_g", "swr_sizes"]
+            "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition", "swr_nccl_unique_id"]
+
+
+def partition(N: int, world: int, rank: int):
+    """Subdomains [j_lo, j_hi] (1-based, inclusive) of a rank (swr_partition)."""
+    lo, hi = C.c_int32(), C.c_int32()
+    _check(lib().swr_partition(N, world, rank, C.byref(lo), C.byref(hi)), "swr_partition")
+    return lo.value, hi.value
+
+
+def nccl_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (create on rank 0, broadcast)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().swr_nccl_unique_id(buf), "swr_nccl_unique_id")
+    return buf.raw
 
 
 def _check(st, where, ok=(SWR_OK,)):
@@ -104,7 +121,8 @@ def _ptr(t):
 class SWR:
     """One SWR problem resident on one GPU (world = 1)."""
 
-    def __init__(self, p, arrays: dict, device: int = 0, stream=None, on_device: bool = False):
+    def __init__(self, p, arrays: dict, device: int = 0, stream=None, on_device: bool = False,
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
         import torch
         self.torch = torch
         self.p = p
@@ -136,7 +154,9 @@ class SWR:
         c.tol_inner, c.maxit_inner = p.tol_inner, p.maxit_inner
         c.tol_fp, c.maxit_fp = p.tol_fp, p.maxit_fp
         c.g0 = _ptr(keep.get("g0"))
-        c.rank, c.world, c.nccl_unique_id = 0, 1, None
+        self._nccl_id = C.create_string_buffer(nccl_id, 128) if nccl_id else None
+        c.rank, c.world = rank, world
+        c.nccl_unique_id = C.cast(self._nccl_id, C.c_void_p) if self._nccl_id else None
         c.cuda_stream = self.stream.cuda_stream
         c.device = device
         self.cfg = c
