@@ -146,6 +146,7 @@ struct swr_handle {
   double2 *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
   // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0, transformed inputs
   int log4 = 0;
+  bool fft_fused = true;
   // V(t,x): per-step pivots [N_T][N][N_j]; f(u): fixed-point stats
   double *tau = nullptr, *xi = nullptr;
   double2 *qtd = nullptr;
@@ -552,7 +553,10 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
 int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
   if (h->N < 2) return SWR_OK;
   CKS(record_pair(h, false, true));
-  if (h->log4) {
+  if (h->log4 && h->fft_fused) {
+    CK(swr::launch_fft_conv(h->log4, zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
+    h->n_launches++;
+  } else if (h->log4) {
     CK(swr::launch_fft_fwd(h->log4, x, h->NT, 2 * h->N - 2, h->NT, h->tw, h->Fx, h->st));
     CK(swr::launch_fft_apply(h->log4, zero ? h->FX0 : h->FX, h->Fx, x, y, h->N, h->NT, h->tw, h->st));
     h->n_launches += 2;
@@ -829,7 +833,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     const size_t mm = h->restart + 1;
     if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
         (s = alloc_krylov(h->kout, mm, ng)) || (s = dalloc(&h->tmp, ng)) ||
-        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, 4 * (mm + 2) * h->N)) ||
+        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, (mm + 2) * ((ng + 511) / 512 + 1))) ||
         false)
       return fail(s);
     if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, ng))))
@@ -837,6 +841,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     if (cfg->g0 && (s = dalloc(&h->g0, ng))) return fail(s);
     const char *tmode = getenv("SWR_TOEPLITZ");
     h->log4 = (tmode && strcmp(tmode, "direct") == 0) ? 0 : swr::fft_log4_for(h->NT);
+    h->fft_fused = !(tmode && strcmp(tmode, "fft2") == 0);
     if (h->log4) {
       const size_t NF = (size_t)1 << (2 * h->log4);
       if ((s = dalloc(&h->tw, NF)) || (s = dalloc(&h->FX, (size_t)h->N * 4 * NF)) ||

@@ -31,6 +31,8 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
 __global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);
 
 int fft_log4_for(int NT);
+cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
+                            const double2 *tw, cudaStream_t st);
 __global__ void k_twiddles(double2 *tw, int NF);
 cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int count, int NT, const double2 *tw,
                            double2 *F, cudaStream_t st);

@@ -257,6 +257,64 @@ __global__ void k_fft_apply(const double2 *__restrict__ Fc, const double2 *__res
   }
 }
 
+// Fused form: one CTA per output slot transforms its (<= 2) input slots
+// itself (no transformed-input round trip through HBM), multiplies by the
+// transformed columns, and inverse-transforms.
+template <int LOG4>
+__global__ void k_fft_conv(const double2 *__restrict__ Fc, const double2 *__restrict__ x, double2 *__restrict__ y,
+                           int N, int NT, const double2 *__restrict__ tw) {
+  constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
+  extern __shared__ double2 fs[];
+  double2 *a1 = fs, *a2 = fs + NF, *bb = fs + 2 * NF;   // two transforms + scratch
+  const int o = blockIdx.x;
+  int j, p1, p2, s1, s2;
+  if ((o & 1) == 0) { j = o / 2 + 2; p1 = 0; s1 = 2 * j - 3; p2 = 1; s2 = (j <= N - 1) ? 2 * j - 2 : -1; }
+  else { j = (o + 1) / 2; p1 = 2; s1 = (j >= 2) ? 2 * j - 3 : -1; p2 = 3; s2 = 2 * j - 2; }
+  for (int i = threadIdx.x; i < NF; i += Q) {
+    a1[i] = (s1 >= 0 && i < NT) ? x[(size_t)s1 * NT + i] : cz();
+    a2[i] = (s2 >= 0 && i < NT) ? x[(size_t)s2 * NT + i] : cz();
+  }
+  __syncthreads();
+  fft4_stockham<LOG4>(a1, bb, tw, false);
+  fft4_stockham<LOG4>(a2, bb, tw, false);
+  const double2 *c1 = Fc + ((size_t)(j - 1) * 4 + p1) * NF, *c2 = Fc + ((size_t)(j - 1) * 4 + p2) * NF;
+  for (int i = threadIdx.x; i < NF; i += Q) {
+    double2 acc = cz();
+    if (s1 >= 0) acc = cmul(__ldg(c1 + i), a1[i]);
+    if (s2 >= 0) acc = cfma(__ldg(c2 + i), a2[i], acc);
+    a1[i] = acc;
+  }
+  __syncthreads();
+  fft4_stockham<LOG4>(a1, bb, tw, true);
+  const double inv = 1.0 / NF;
+  const double2 *xo = x + (size_t)o * NT;
+  double2 *yo = y + (size_t)o * NT;
+  for (int n = threadIdx.x; n < NT; n += Q) {
+    const double2 xv = xo[n];
+    yo[n] = make_double2(fma(-inv, a1[n].x, xv.x), fma(-inv, a1[n].y, xv.y));
+  }
+}
+
+cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
+                            const double2 *tw, cudaStream_t st) {
+  if (N < 2) return cudaSuccess;
+  const int nslots = 2 * N - 2;
+  const size_t smem = 3 * ((size_t)1 << (2 * log4)) * sizeof(double2);
+  switch (log4) {
+    case 2: k_fft_conv<2><<<nslots, 4, smem, st>>>(Fc, x, y, N, NT, tw); break;
+    case 3: k_fft_conv<3><<<nslots, 16, smem, st>>>(Fc, x, y, N, NT, tw); break;
+    case 4: k_fft_conv<4><<<nslots, 64, smem, st>>>(Fc, x, y, N, NT, tw); break;
+    case 5: {
+      cudaError_t e = cudaFuncSetAttribute(k_fft_conv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+      if (e != cudaSuccess) return e;
+      k_fft_conv<5><<<nslots, 256, smem, st>>>(Fc, x, y, N, NT, tw);
+      break;
+    }
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 __global__ void k_twiddles(double2 *tw, int NF) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k < NF) {
@@ -388,8 +446,6 @@ __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nv
 // out[0..nv].  With CGS_SCALE the last CTA also stores 1/sqrt(out[nv]) in
 // out[nv+1] for the normalisation of the next basis vector.
 // ---------------------------------------------------------------------------
-constexpr int CGS_SPLIT = 2;
-
 template <int EPT>
 __global__ void __launch_bounds__(256) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
                                              const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
@@ -397,13 +453,10 @@ __global__ void __launch_bounds__(256) k_cgs(const double2 *__restrict__ V, size
                                              unsigned *counter, int N, int NT) {
   __shared__ double2 red[33][8];
   __shared__ bool last;
-  // CTA (j, part): part-th of CGS_SPLIT contiguous pieces of subdomain j's entries
-  const int j = blockIdx.x / CGS_SPLIT + 1, part = blockIdx.x % CGS_SPLIT;
-  const int s_lo = (j >= 2) ? 2 * j - 3 : 0;
-  const int s_hi = (j <= N - 1) ? 2 * j - 2 : 2 * j - 3;
-  const size_t f0 = (size_t)s_lo * NT, f1 = (size_t)(s_hi + 1) * NT;
-  const size_t piece = (f1 - f0 + CGS_SPLIT - 1) / CGS_SPLIT;
-  const size_t e0 = f0 + part * piece, e1 = min(f1, e0 + piece);
+  // CTA b: the contiguous chunk [b EPT P, (b+1) EPT P) of the n_g entries;
+  // partials per CTA are combined in a fixed order (deterministic)
+  const size_t ntot = (size_t)(2 * N - 2) * NT;
+  const size_t e0 = (size_t)blockIdx.x * EPT * blockDim.x, e1 = min(ntot, e0 + (size_t)EPT * blockDim.x);
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
   double2 wv[EPT];
 #pragma unroll
@@ -531,13 +584,15 @@ __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__rest
 
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st) {
-  const int ent = (2 * NT + CGS_SPLIT - 1) / CGS_SPLIT;
-  if (ent <= 128 * 4) {
-    k_cgs<4><<<N * CGS_SPLIT, 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  } else if (ent <= 256 * 8) {
-    k_cgs<8><<<N * CGS_SPLIT, 256, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
+  // one wave of CTAs (148 SMs x 6 resident CTAs of 128 threads), EPT entries per thread
+  const size_t ntot = (size_t)(2 * N - 2) * NT;
+  const size_t per_cta_4 = 4 * 128;
+  const size_t nblk4 = (ntot + per_cta_4 - 1) / per_cta_4;
+  if (nblk4 <= 148 * 6 * 2) {
+    k_cgs<4><<<(unsigned)nblk4, 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
   } else {
-    return cudaErrorInvalidValue;
+    const size_t per = 8 * 128;
+    k_cgs<8><<<(unsigned)((ntot + per - 1) / per), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
   }
   return cudaGetLastError();
 }

@@ -203,6 +203,10 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
   } while (0)
 
 // ---------------------------------------------------------------------------
+// i kappa-fold: the value u* such that i kappa u* = d (a rhs addition d on a
+// row written as an extra neighbour value): u* = -i d / kappa.
+__device__ __forceinline__ double2 ifold(double2 d, double kappa) { return make_double2(d.y / kappa, -d.x / kappa); }
+
 template <int M, int K, int PMAX>
 __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const MarchParams p) {
   extern __shared__ double2 sm[];
@@ -212,7 +216,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   const MarchSys *G = p.sys + (size_t)(blockIdx.x / CS) * K;   // the group's K systems
   const int Nj = p.Nj, NT = p.NT;
   const int s0 = (crank * P + t) * M;                          // first row of this thread
-  const double eim = p.e_im;
+  const double eim = p.e_im, kappa = p.kappa;
 
   // ---- shared memory ----
   double2 *ybuf = sm;                                   // [K][M][P]
@@ -234,8 +238,17 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   const bool has_left = flags & SYS_HAS_LEFT, has_right = flags & SYS_HAS_RIGHT;
   const int rows_cta = P * M;
   const int cb = (Nj - 1) / rows_cta, tb = ((Nj - 1) % rows_cta) / M;
-  const bool owns_a = has_left && s0 == 0;
-  const bool owns_b = has_right && crank == cb && t == tb;
+  const bool first = s0 == 0;                                   // holds row 0
+  const bool last = crank == cb && t == tb;                     // holds row N_j - 1
+  const int ib = (Nj - 1) - s0;                                 // its index in the thread (if last)
+  const bool owns_a = has_left && first;
+  const bool owns_b = has_right && last;
+  int imp[K][2];
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    imp[r][0] = G[r].flags & SYS_LIN_IMPULSE;
+    imp[r][1] = G[r].flags & SYS_RIN_IMPULSE;
+  }
 
   for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
   if (p.flux_smem) {
@@ -249,85 +262,64 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   }
   if (t < 2 * K) sH[t] = cz();
 
+  // Rows beyond N_j (padding) get q = 0: their z, x are 0 and their maps
+  // decouple them, so the row loops need no bounds checks.  The end rows of
+  // the P1 mass matrix and the interface terms b_n - Q^T(l,r) are folded
+  // into the neighbour values u_{-1}, u_{N_j} of the rhs stencil.
   double2 u[K][M], q[M];
   double er[M];
   double er_prev;
-  {
-    const double2 *qp = G[0].q;
-    const double *erp = G[0].er;
+  auto load_factor = [&](const double2 *qp, const double *erp) {
 #pragma unroll
     for (int i = 0; i < M; i++) {
       const int k = s0 + i;
-      q[i] = k < Nj ? qp[k] : make_double2(1.0, 0.0);
-      er[i] = k < Nj ? erp[k] : 0.0;
+      q[i] = k < Nj ? __ldg(qp + k) : cz();
+      er[i] = k < Nj ? __ldg(erp + k) : 0.0;
     }
-#pragma unroll
-    for (int r = 0; r < K; r++) {
-      const double2 *u0p = G[r].u0;
-#pragma unroll
-      for (int i = 0; i < M; i++) {
-        const int k = s0 + i;
-        u[r][i] = (u0p && k < Nj) ? u0p[k] : cz();
-      }
-    }
-    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? erp[s0 - 1] : 0.0;
-    // constant linear parts of the per-thread maps: Af = prod c_k, Ab = prod b_k
+    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? __ldg(erp + s0 - 1) : 0.0;
     double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
 #pragma unroll
     for (int i = 0; i < M; i++) {
-      const int k = s0 + i;
-      const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
-      const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
-      Af = cmul(Af, c);
-      Ab = cmul(Ab, b);
+      Af = cmul(Af, negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim));
+      Ab = cmul(Ab, negqe(q[i], er[i], eim));
     }
     sAf[t] = Af;
     sAb[t] = Ab;
+  };
+  load_factor(G[0].q, G[0].er);
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    const double2 *u0p = G[r].u0;
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const int k = s0 + i;
+      u[r][i] = (u0p && k < Nj) ? u0p[k] : cz();
+    }
   }
-  if (s0 == 0) {
+  if (first) {
 #pragma unroll
     for (int r = 0; r < K; r++) hva[r * (NT + 1)] = u[r][0];
   }
+  if (last) {
 #pragma unroll
-  for (int i = 0; i < M; i++)
-    if (s0 + i == Nj - 1) {
+    for (int i = 0; i < M; i++)
+      if (i == ib) {
 #pragma unroll
-      for (int r = 0; r < K; r++) hvb[r * (NT + 1)] = u[r][i];
-    }
+        for (int r = 0; r < K; r++) hvb[r * (NT + 1)] = u[r][i];
+      }
+  }
   __syncthreads();
 
   auto flux = [&](int r, int side, int n) -> double2 {   // incoming l (side 0) / r (side 1) at step n
-    const int imp = side == 0 ? (G[r].flags & SYS_LIN_IMPULSE) : (G[r].flags & SYS_RIN_IMPULSE);
-    if (imp) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
+    if (imp[r][side]) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
     return p.flux_smem ? sflux[(2 * r + side) * NT + n - 1] : cz();
   };
 
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
-    if (p.td_stride && n > 1) {
-      // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
-      const double2 *qp = G[0].q + (size_t)(n - 1) * p.td_stride;
-      const double *erp = G[0].er + (size_t)(n - 1) * p.td_stride;
-#pragma unroll
-      for (int i = 0; i < M; i++) {
-        const int k = s0 + i;
-        q[i] = k < Nj ? __ldg(qp + k) : make_double2(1.0, 0.0);
-        er[i] = k < Nj ? __ldg(erp + k) : 0.0;
-      }
-      er_prev = (s0 >= 1 && s0 - 1 < Nj) ? __ldg(erp + s0 - 1) : 0.0;
-      double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
-#pragma unroll
-      for (int i = 0; i < M; i++) {
-        const int k = s0 + i;
-        const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
-        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
-        Af = cmul(Af, c);
-        Ab = cmul(Ab, b);
-      }
-      sAf[t] = Af;
-      sAb[t] = Ab;
-    }
+    if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
+      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
     // ---- S0^2 history H = c2 sum_{s<n} beta_{n-s} v_s:
     // every thread of the CTA holding the boundary row adds a slice of
     // s <= n-2 (written before the last barrier); the owner of the row adds
@@ -373,21 +365,6 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     SWR_TRACE(1);
     csync(CS, t == 0 || t == P - 1);
     SWR_TRACE(2);
-    if (p.s02 && (owns_a || owns_b)) {
-#pragma unroll
-      for (int r = 0; r < K; r++) {
-        if (owns_a) {
-          double2 h = cscale(sbeta[1], hva[r * (NT + 1) + n - 1]);
-          for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + qq]);
-          sH[2 * r] = cmul(p.c2, h);
-        }
-        if (owns_b) {
-          double2 h = cscale(sbeta[1], hvb[r * (NT + 1) + n - 1]);
-          for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + 32 + qq]);
-          sH[2 * r + 1] = cmul(p.c2, h);
-        }
-      }
-    }
     double2 uL[K], uR[K];
 #pragma unroll
     for (int r = 0; r < K; r++) {
@@ -398,6 +375,48 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       if (t < P - 1) uR[r] = hfirst[r * P + t + 1];
       else if (crank < CS - 1) uR[r] = *remote(hfirst + r * P, crank + 1);
     }
+    // ---- end rows and interface terms folded into u_{-1} and u_{N_j} ----
+    if (first || last) {
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        if (first) {
+          double2 d = cz();
+          if (owns_a) {
+            double2 h = cz();
+            if (p.s02) {
+              h = cscale(sbeta[1], hva[r * (NT + 1) + n - 1]);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + qq]);
+              h = cmul(p.c2, h);
+            }
+            sH[2 * r] = h;
+            d = csub(h, flux(r, 0, n));                 // b_n - l_n at row 0
+          }
+          const double2 f = ifold(d, kappa);
+          uL[r] = make_double2(fma(-2.0, u[r][0].x, f.x), fma(-2.0, u[r][0].y, f.y));
+        }
+        if (last) {
+          double2 d = cz();
+          if (owns_b) {
+            double2 h = cz();
+            if (p.s02) {
+              h = cscale(sbeta[1], hvb[r * (NT + 1) + n - 1]);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + 32 + qq]);
+              h = cmul(p.c2, h);
+            }
+            sH[2 * r + 1] = h;
+            d = csub(h, flux(r, 1, n));                 // b_n - r_n at row N_j - 1
+          }
+          const double2 f = ifold(d, kappa);
+#pragma unroll
+          for (int i = 0; i < M; i++)
+            if (i == ib) {
+              const double2 un = make_double2(fma(-2.0, u[r][i].x, f.x), fma(-2.0, u[r][i].y, f.y));
+              if (i == M - 1) uR[r] = un;
+              else u[r][i == M - 1 ? M - 1 : i + 1] = un;   // the (padding) row after N_j - 1
+            }
+        }
+      }
+    }
 
     // ---- forward sweep z_k = q_k r_k + c_k z_{k-1}: aggregate, scan, exact ----
     double2 z[K];
@@ -406,23 +425,15 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll 1
     for (int pass = 0; pass < 2; pass++) {
       launder<M>(q, er);
-      {
 #pragma unroll
-        for (int i = 0; i < M; i++) {
-          const int k = s0 + i;
-          const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
+      for (int i = 0; i < M; i++) {
+        const double2 c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
 #pragma unroll
-          for (int r = 0; r < K; r++) {
-            double2 rr = cz();
-            if (k < Nj) {
-              rr = rhs_row<true>(k, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
-                                 i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], p.kappa);
-              if (k == 0 && owns_a) rr = cadd(rr, csub(sH[2 * r], flux(r, 0, n)));
-              if (k == Nj - 1 && owns_b) rr = cadd(rr, csub(sH[2 * r + 1], flux(r, 1, n)));
-            }
-            z[r] = cfma(c, z[r], cmul(q[i], rr));
-            if (pass == 1) ybuf[(r * M + i) * P + t] = z[r];
-          }
+        for (int r = 0; r < K; r++) {
+          const double2 rr = rhs_row<false>(0, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
+                                            i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], kappa);
+          z[r] = cfma(c, z[r], cmul(q[i], rr));
+          if (pass == 1) ybuf[(r * M + i) * P + t] = z[r];
         }
       }
       if (pass == 0) {
@@ -442,8 +453,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     launder<M>(q, er);
 #pragma unroll
     for (int i = M - 1; i >= 0; i--) {
-      const int k = s0 + i;
-      const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+      const double2 b = negqe(q[i], er[i], eim);
 #pragma unroll
       for (int r = 0; r < K; r++) x[r] = cfma(b, x[r], ybuf[(r * M + i) * P + t]);
     }
@@ -456,39 +466,41 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       for (int r = 0; r < K; r++) x[r] = carry[r];
     }
     launder<M>(q, er);
+    double2 xb[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) xb[r] = cz();
 #pragma unroll
     for (int i = M - 1; i >= 0; i--) {
-      const int k = s0 + i;
-      const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
+      const double2 b = negqe(q[i], er[i], eim);
 #pragma unroll
       for (int r = 0; r < K; r++) {
         x[r] = cfma(b, x[r], ybuf[(r * M + i) * P + t]);
+        if (i == ib) xb[r] = x[r];
         u[r][i] = make_double2(fma(2.0, x[r].x, -u[r][i].x), fma(2.0, x[r].y, -u[r][i].y));  // u_n = 2 v_n - u_{n-1}
       }
-      {
-        if (k == 0 && owns_a) {
+    }
+    // ---- record v_n and S v_n at the interfaces (eq. 8) ----
+    if (first) {   // x now holds v_n at row 0
 #pragma unroll
-          for (int r = 0; r < K; r++) {
-            hva[r * (NT + 1) + n] = x[r];
-            double2 *outl = G[r].out_left;
-            if (outl) {
-              const double2 sv = cfma(p.c0, x[r], sH[2 * r]);   // S v_n(a_j) = c0 v_n + H_a
-              const double2 l = flux(r, 0, n);
-              outl[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
-            }
-          }
+      for (int r = 0; r < K; r++) {
+        hva[r * (NT + 1) + n] = x[r];
+        double2 *outl = G[r].out_left;
+        if (owns_a && outl) {
+          const double2 sv = cfma(p.c0, x[r], sH[2 * r]);   // S v_n(a_j) = c0 v_n + H_a
+          const double2 l = flux(r, 0, n);
+          outl[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
         }
-        if (k == Nj - 1 && owns_b) {
+      }
+    }
+    if (last) {
 #pragma unroll
-          for (int r = 0; r < K; r++) {
-            hvb[r * (NT + 1) + n] = x[r];
-            double2 *outr = G[r].out_right;
-            if (outr) {
-              const double2 sv = cfma(p.c0, x[r], sH[2 * r + 1]);
-              const double2 rv = flux(r, 1, n);
-              outr[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
-            }
-          }
+      for (int r = 0; r < K; r++) {
+        hvb[r * (NT + 1) + n] = xb[r];
+        double2 *outr = G[r].out_right;
+        if (owns_b && outr) {
+          const double2 sv = cfma(p.c0, xb[r], sH[2 * r + 1]);
+          const double2 rv = flux(r, 1, n);
+          outr[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
         }
       }
     }

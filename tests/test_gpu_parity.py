@@ -147,13 +147,13 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["direct", "fft"])
+@pytest.mark.parametrize("mode", ["direct", "fft", "fft2"])
 def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
     """Both forms of y = (I - L) x (direct causal convolution and FFT
     convolution) against the oracle's direct convolution."""
     import torch
-    if mode == "direct":
-        monkeypatch.setenv("SWR_TOEPLITZ", "direct")
+    if mode in ("direct", "fft2"):
+        monkeypatch.setenv("SWR_TOEPLITZ", mode)
     else:
         monkeypatch.delenv("SWR_TOEPLITZ", raising=False)
     for p in (si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX),
@@ -212,3 +212,27 @@ def test_nl_sweep_parity(oracle_mod, gpu):
     Rg_o = o.apply_R(g, use_u0=True)
     Rg_g, _ = g_.apply_R(torch.as_tensor(g, device="cuda"), use_u0=True)
     assert rel(Rg_g.cpu().numpy(), Rg_o) <= 1e-11
+
+
+EDGE_CASES = [
+    ("one-cell-subdomains", si.Problem(a0=-1.0, b0=1.0, T=0.05, dx=0.25, dt=0.01, N=8, potential=si.POT_VX)),
+    ("one-step", si.Problem(a0=-2.0, b0=2.0, T=0.01, dx=0.05, dt=0.01, N=4, potential=si.POT_VX)),
+    ("two-steps-robin", si.Problem(a0=-2.0, b0=2.0, T=0.02, dx=0.05, dt=0.01, N=5, potential=si.POT_ZERO,
+                                   transmission=si.TC_ROBIN, robin_p=3.0)),
+    ("N2-fine", si.Problem(a0=-21.0, b0=21.0, T=0.05, dx=1e-2, dt=1e-3, N=2, potential=si.POT_VX)),
+]
+
+
+@pytest.mark.parametrize("name,p", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
+def test_edge_cases(oracle_mod, gpu, name, p):
+    """Degenerate shapes: one-cell subdomains (N_j = 2), a single time step,
+    two steps with Robin, and a long subdomain (N_j = 4201, one CTA) at N = 2."""
+    x = p.nodes()
+    arrays = si.inputs(p)
+    arrays["u0"] = np.exp(-(x * x) + 2j * x)
+    o, g_ = _pair(oracle_mod, gpu, p, arrays)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"]
+    assert rel(uT, ro["uT"]) <= 1e-10
