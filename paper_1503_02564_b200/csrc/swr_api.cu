@@ -405,16 +405,6 @@ int factor_matrices(swr_handle *h) {
 }
 
 // ---- Krylov kernels ----------------------------------------------------------
-// dots[v] = <V_v, w> (order-fixed), v = 0..nvec-1, on the device
-int multidot(swr_handle *h, const double2 *V, int nvec, const double2 *w, double2 *out) {
-  dim3 grid(h->N, nvec);
-  swr::k_multidot_partial<<<grid, 256, 0, h->st>>>(V, h->ng, nvec, w, h->partial, h->N, h->NT);
-  CK(cudaGetLastError());
-  swr::k_multidot_final<<<(nvec + 63) / 64, 64, 0, h->st>>>(h->partial, nvec, h->N, out);
-  CK(cudaGetLastError());
-  h->n_launches += 2;
-  return SWR_OK;
-}
 
 int fetch(swr_handle *h, const double2 *dev, int n, double2 *host) {
   CK(cudaMemcpyAsync(host, dev, n * sizeof(double2), cudaMemcpyDeviceToHost, h->st));
@@ -833,7 +823,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     const size_t mm = h->restart + 1;
     if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
         (s = alloc_krylov(h->kout, mm, ng)) || (s = dalloc(&h->tmp, ng)) ||
-        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, (mm + 2) * ((ng + 511) / 512 + 1))) ||
+        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, (mm + 2) * 148 * 4)) ||
         false)
       return fail(s);
     if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, ng))))

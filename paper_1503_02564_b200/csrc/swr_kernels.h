@@ -15,9 +15,6 @@ struct FactorJob {
 __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0, int *err);
 constexpr int TR = 8;  // outputs per thread of the Toeplitz kernel (N_T = 500: 32 threads per output slot)
 __global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, int N, int NT);
-__global__ void k_multidot_partial(const double2 *V, size_t ldv, int nvec, const double2 *w, double2 *partial,
-                                   int N, int NT);
-__global__ void k_multidot_final(const double2 *partial, int nvec, int N, double2 *out);
 __global__ void k_multi_axpy(const double2 *V, size_t ldv, int nvec, const double2 *h, double2 *w, size_t n);
 __global__ void k_axpby(double2 a, const double2 *x, double2 b, double2 *y, size_t n);
 __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);

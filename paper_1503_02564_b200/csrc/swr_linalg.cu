@@ -377,29 +377,6 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2 *red) {
   return v;
 }
 
-// partial[v * N + (j-1)] = sum over subdomain j's entries of conj(V_v) w
-__global__ void k_multidot_partial(const double2 *__restrict__ V, size_t ldv, int nvec,
-                                   const double2 *__restrict__ w, double2 *partial, int N, int NT) {
-  __shared__ double2 red[32];
-  const int j = blockIdx.x + 1, v = blockIdx.y;
-  const int s_lo = (j >= 2) ? 2 * j - 3 : 0;
-  const int s_hi = (j <= N - 1) ? 2 * j - 2 : 2 * j - 3;
-  const size_t e0 = (size_t)s_lo * NT, e1 = (size_t)(s_hi + 1) * NT;
-  const double2 *Vv = V + (size_t)v * ldv;
-  double2 acc = cz();
-  for (size_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) acc = cfmaconj(Vv[e], w[e], acc);
-  acc = block_reduce(acc, red);
-  if (threadIdx.x == 0) partial[(size_t)v * N + (j - 1)] = acc;
-}
-
-__global__ void k_multidot_final(const double2 *partial, int nvec, int N, double2 *out) {
-  const int v = blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= nvec) return;
-  double2 s = cz();
-  for (int j = 0; j < N; j++) s = cadd(s, partial[(size_t)v * N + j]);
-  out[v] = s;
-}
-
 // w -= sum_v h_v V_v
 __global__ void k_multi_axpy(const double2 *__restrict__ V, size_t ldv, int nvec, const double2 *__restrict__ h,
                              double2 *__restrict__ w, size_t n) {
@@ -436,132 +413,115 @@ __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nv
 }
 
 // ---------------------------------------------------------------------------
-// Fused CGS kernel: one CTA per subdomain j (its owned slots l_j, r_j are
-// contiguous in g), KEPT entries per thread in registers.
+// Fused CGS kernel over the interface vector (n_g complex entries):
 //   mode & CGS_AXPY : w -= sum_v h_v V_v          (h from the device, v < nv)
-//   mode & CGS_DOTS : p_v = <V_v, w>              (v < nv)
+//   mode & CGS_DOTS : p_v = <V_v, w>              (v < nv, after the axpy)
 //   mode & CGS_NORM : p_nv = <w, w>
-// Partials per subdomain are reduced in a fixed tree inside the CTA; the last
-// CTA to finish sums them in subdomain order (order-fixed, deterministic) into
-// out[0..nv].  With CGS_SCALE the last CTA also stores 1/sqrt(out[nv]) in
-// out[nv+1] for the normalisation of the next basis vector.
+// Persistent grid over chunks of 32*KE entries.  The 4 warps of a CTA split
+// the basis vectors (warp q holds v = q, q+4, ...; lane holds entries
+// lane + 32 kk) so each basis value is loaded from HBM exactly once per call
+// and kept in registers between the axpy and the dots; the axpy partials of
+// the 4 warps meet in shared memory (fixed summation order).  Per-CTA dot
+// partials are reduced in a fixed tree; the last CTA sums them over CTAs in a
+// fixed order (deterministic) into out[0..nv]; with CGS_SCALE it also stores
+// 1/sqrt(out[nv]) in out[nv+1].
 // ---------------------------------------------------------------------------
-template <int EPT>
-__global__ void __launch_bounds__(256) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
-                                             const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
-                                             double2 *__restrict__ partial, double2 *__restrict__ out,
-                                             unsigned *counter, int N, int NT) {
-  __shared__ double2 red[33][8];
+template <int VPW, int KE>
+__global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
+                                                const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
+                                                double2 *__restrict__ partial, double2 *__restrict__ out,
+                                                unsigned *counter, int N, int NT) {
+  constexpr int NVMAX = 4 * VPW, CH = 32 * KE;
+  __shared__ double2 red[NVMAX + 1][4];
+  __shared__ double2 sh[NVMAX];
+  __shared__ double2 part[4][CH];
   __shared__ bool last;
-  // CTA b: the contiguous chunk [b EPT P, (b+1) EPT P) of the n_g entries;
-  // partials per CTA are combined in a fixed order (deterministic)
   const size_t ntot = (size_t)(2 * N - 2) * NT;
-  const size_t e0 = (size_t)blockIdx.x * EPT * blockDim.x, e1 = min(ntot, e0 + (size_t)EPT * blockDim.x);
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
-  double2 wv[EPT];
+  const size_t nch = (ntot + CH - 1) / CH;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
+  if (axpy)
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
+  __syncthreads();
+  double2 acc[VPW];
 #pragma unroll
-  for (int i = 0; i < EPT; i++) {
-    const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-    wv[i] = (e < e1) ? w[e] : cz();
-  }
-  if (mode & CGS_AXPY) {
-    int v = 0;
-    for (; v + 4 <= nv; v += 4) {      // 4 basis vectors per round trip
-      double2 hv[4], xv[4][EPT];
+  for (int i = 0; i < VPW; i++) acc[i] = cz();
+  double nacc = 0.0;
+  for (size_t c = blockIdx.x; c < nch; c += gridDim.x) {
+    const size_t base = c * CH + lane;
+    double2 x[VPW][KE], we[KE];
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        hv[u] = hsrc[v + u];
-        const double2 *Vv = V + (size_t)(v + u) * ldv;
+    for (int i = 0; i < VPW; i++) {
+      const int v = wp + 4 * i;
 #pragma unroll
-        for (int i = 0; i < EPT; i++) {
-          const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-          xv[u][i] = (e < e1) ? Vv[e] : cz();
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; u++)
-#pragma unroll
-        for (int i = 0; i < EPT; i++)
-          wv[i] = make_double2(wv[i].x - (hv[u].x * xv[u][i].x - hv[u].y * xv[u][i].y),
-                               wv[i].y - (hv[u].x * xv[u][i].y + hv[u].y * xv[u][i].x));
-    }
-    for (; v < nv; v++) {
-      const double2 hv = hsrc[v];
-      const double2 *Vv = V + (size_t)v * ldv;
-#pragma unroll
-      for (int i = 0; i < EPT; i++) {
-        const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-        if (e < e1) {
-          const double2 x = Vv[e];
-          wv[i] = make_double2(wv[i].x - (hv.x * x.x - hv.y * x.y), wv[i].y - (hv.x * x.y + hv.y * x.x));
-        }
+      for (int k = 0; k < KE; k++) {
+        const size_t e = base + 32 * k;
+        x[i][k] = (v < nv && e < ntot) ? V[(size_t)v * ldv + e] : cz();
       }
     }
 #pragma unroll
-    for (int i = 0; i < EPT; i++) {
-      const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-      if (e < e1) w[e] = wv[i];
+    for (int k = 0; k < KE; k++) {
+      const size_t e = base + 32 * k;
+      we[k] = e < ntot ? w[e] : cz();
     }
-  }
-  const int nred = ((mode & CGS_DOTS) ? nv : 0) + ((mode & CGS_NORM) ? 1 : 0);
-  if (mode & CGS_DOTS) {
-    int v = 0;
-    for (; v + 4 <= nv; v += 4) {      // 4 basis vectors per round trip
-      double2 acc[4];
+    if (axpy) {
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-        const double2 *Vv = V + (size_t)(v + u) * ldv;
-        acc[u] = cz();
+      for (int k = 0; k < KE; k++) {
+        double2 p = cz();
 #pragma unroll
-        for (int i = 0; i < EPT; i++) {
-          const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-          if (e < e1) acc[u] = cfmaconj(Vv[e], wv[i], acc[u]);
-        }
+        for (int i = 0; i < VPW; i++)
+          if (wp + 4 * i < nv) p = cfma(sh[wp + 4 * i], x[i][k], p);
+        part[wp][lane + 32 * k] = p;
       }
+      __syncthreads();
 #pragma unroll
-      for (int u = 0; u < 4; u++) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) acc[u] = cadd(acc[u], shfl_down2(acc[u], o));
-        if (lane == 0) red[v + u][wp] = acc[u];
+      for (int k = 0; k < KE; k++) {
+        const int t = lane + 32 * k;
+        const double2 p = cadd(cadd(cadd(part[0][t], part[1][t]), part[2][t]), part[3][t]);
+        we[k] = csub(we[k], p);
+        const size_t e = base + 32 * k;
+        if (wp == 0 && e < ntot) w[e] = we[k];
       }
+      __syncthreads();
     }
-    for (; v < nv; v++) {
-      const double2 *Vv = V + (size_t)v * ldv;
-      double2 acc = cz();
+    if (dots) {
 #pragma unroll
-      for (int i = 0; i < EPT; i++) {
-        const size_t e = e0 + threadIdx.x + (size_t)i * blockDim.x;
-        if (e < e1) acc = cfmaconj(Vv[e], wv[i], acc);
-      }
+      for (int i = 0; i < VPW; i++)
 #pragma unroll
-      for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_down2(acc, o));
-      if (lane == 0) red[v][wp] = acc;
+        for (int k = 0; k < KE; k++) acc[i] = cfmaconj(x[i][k], we[k], acc[i]);
+    }
+    if (norm && wp == 0) {
+#pragma unroll
+      for (int k = 0; k < KE; k++) nacc = fma(we[k].x, we[k].x, fma(we[k].y, we[k].y, nacc));
     }
   }
-  if (mode & CGS_NORM) {
-    double2 acc = cz();
+  const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
+  if (dots) {
 #pragma unroll
-    for (int i = 0; i < EPT; i++) acc.x = fma(wv[i].x, wv[i].x, fma(wv[i].y, wv[i].y, acc.x));
+    for (int i = 0; i < VPW; i++) {
+      const int v = wp + 4 * i;
+      double2 a = acc[i];
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_down2(acc, o));
-    if (lane == 0) red[nred - 1][wp] = acc;
+      for (int o = 16; o > 0; o >>= 1) a = cadd(a, shfl_down2(a, o));
+      if (lane == 0 && v < nv) red[v][0] = a;
+    }
+  }
+  if (norm && wp == 0) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+    if (lane == 0) red[nred - 1][0] = make_double2(nacc, 0.0);
   }
   __syncthreads();
-  if ((int)threadIdx.x < nred) {
-    double2 sum = cz();
-    for (int q = 0; q < nwp; q++) sum = cadd(sum, red[threadIdx.x][q]);
-    partial[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = sum;
-  }
+  if ((int)threadIdx.x < nred) partial[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = red[threadIdx.x][0];
   __threadfence();
   __syncthreads();
   if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
   __syncthreads();
   if (!last) return;
   __threadfence();
-  // last CTA: one warp per reduced quantity, fixed-order tree over the
-  // (subdomain, piece) partials
+  // last CTA: one warp per reduced quantity, fixed-order tree over the CTAs
   const int np = gridDim.x;
-  for (int v = wp; v < nred; v += nwp) {
+  for (int v = wp; v < nred; v += 4) {
     double2 sum = cz();
     for (int q = lane; q < np; q += 32) sum = cadd(sum, __ldcg(partial + (size_t)v * np + q));
 #pragma unroll
@@ -584,16 +544,14 @@ __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__rest
 
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st) {
-  // one wave of CTAs (148 SMs x 6 resident CTAs of 128 threads), EPT entries per thread
+  // persistent grid: 4 CTAs of 128 threads per SM (148 SMs); the grid only
+  // depends on the sizes, so the reduction order is fixed
   const size_t ntot = (size_t)(2 * N - 2) * NT;
-  const size_t per_cta_4 = 4 * 128;
-  const size_t nblk4 = (ntot + per_cta_4 - 1) / per_cta_4;
-  if (nblk4 <= 148 * 6 * 2) {
-    k_cgs<4><<<(unsigned)nblk4, 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  } else {
-    const size_t per = 8 * 128;
-    k_cgs<8><<<(unsigned)((ntot + per - 1) / per), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  }
+  auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
+  if (nv > 32) return cudaErrorInvalidValue;
+  if (nv <= 8) k_cgs<2, 8><<<grid(256), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
+  else if (nv <= 16) k_cgs<4, 4><<<grid(128), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
+  else k_cgs<8, 2><<<grid(64), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
   return cudaGetLastError();
 }
 

@@ -224,8 +224,9 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   double2 *hlast = hfirst + K * P;                      // [K][P]
   double2 *sAf = hlast + K * P;                         // [P]
   double2 *sAb = sAf + P;                               // [P]
+  double2 *sqlast = sAb + P;                            // [2][P] q of each thread's last row (step parity)
   ScanBuf<K> sf, sbk;
-  sf.wA = sAb + P;            sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32 * K;
+  sf.wA = sqlast + 2 * P;            sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32 * K;
   sbk.wA = sf.ctot + 16 * (1 + K); sbk.wB = sbk.wA + 32; sbk.ctot = sbk.wB + 32 * K;
   double2 *hva = sbk.ctot + 16 * (1 + K);               // [K][NT+1] v_s(a_j)
   double2 *hvb = hva + K * (NT + 1);                    // [K][NT+1] v_s(b_j)
@@ -261,6 +262,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     }
   }
   if (t < 2 * K) sH[t] = cz();
+  for (int i = t; i < 64 * K; i += P) hred[i] = cz();
 
   // Rows beyond N_j (padding) get q = 0: their z, x are 0 and their maps
   // decouple them, so the row loops need no bounds checks.  The end rows of
@@ -269,7 +271,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   double2 u[K][M], q[M];
   double er[M];
   double er_prev;
-  auto load_factor = [&](const double2 *qp, const double *erp) {
+  auto load_factor = [&](const double2 *qp, const double *erp, int par) {
 #pragma unroll
     for (int i = 0; i < M; i++) {
       const int k = s0 + i;
@@ -285,8 +287,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     }
     sAf[t] = Af;
     sAb[t] = Ab;
+    sqlast[par * P + t] = q[M - 1];
   };
-  load_factor(G[0].q, G[0].er);
+  load_factor(G[0].q, G[0].er, 1);
+  sqlast[t] = q[M - 1];
 #pragma unroll
   for (int r = 0; r < K; r++) {
     const double2 *u0p = G[r].u0;
@@ -308,7 +312,24 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         for (int r = 0; r < K; r++) hvb[r * (NT + 1)] = u[r][i];
       }
   }
-  __syncthreads();
+  // halo of u_0; later steps get their neighbour values without a barrier
+  // (end of the step loop)
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    hfirst[r * P + t] = u[r][0];
+    hlast[r * P + t] = u[r][M - 1];
+  }
+  csync(CS, t == 0 || t == P - 1);
+  double2 uL[K], uR[K];
+#pragma unroll
+  for (int r = 0; r < K; r++) {
+    uL[r] = cz();
+    uR[r] = cz();
+    if (t > 0) uL[r] = hlast[r * P + t - 1];
+    else if (crank > 0) uL[r] = *remote(hlast + r * P + (P - 1), crank - 1);
+    if (t < P - 1) uR[r] = hfirst[r * P + t + 1];
+    else if (crank < CS - 1) uR[r] = *remote(hfirst + r * P, crank + 1);
+  }
 
   auto flux = [&](int r, int side, int n) -> double2 {   // incoming l (side 0) / r (side 1) at step n
     if (imp[r][side]) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
@@ -319,63 +340,15 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
     if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
-      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
-    // ---- S0^2 history H = c2 sum_{s<n} beta_{n-s} v_s:
-    // every thread of the CTA holding the boundary row adds a slice of
-    // s <= n-2 (written before the last barrier); the owner of the row adds
-    // the newest term beta_1 v_{n-1} after the halo barrier.
-    if (p.s02) {
-      if (has_left && crank == 0) {
-#pragma unroll
-        for (int r = 0; r < K; r++) {
-          double2 acc = cz();
-          const double2 *hv = hva + r * (NT + 1);
-          for (int s = t; s < n - 1; s += P) {
-            const double b = sbeta[n - s];
-            acc.x = fma(b, hv[s].x, acc.x);
-            acc.y = fma(b, hv[s].y, acc.y);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (lane == 0) hred[r * 64 + w] = acc;
-        }
-      }
-      if (has_right && crank == cb) {
-#pragma unroll
-        for (int r = 0; r < K; r++) {
-          double2 acc = cz();
-          const double2 *hv = hvb + r * (NT + 1);
-          for (int s = t; s < n - 1; s += P) {
-            const double b = sbeta[n - s];
-            acc.x = fma(b, hv[s].x, acc.x);
-            acc.y = fma(b, hv[s].y, acc.y);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (lane == 0) hred[r * 64 + 32 + w] = acc;
-        }
-      }
-    }
-    // ---- halo: u_{n-1} of the neighbouring rows ----
-#pragma unroll
-    for (int r = 0; r < K; r++) {
-      hfirst[r * P + t] = u[r][0];
-      hlast[r * P + t] = u[r][M - 1];
-    }
+      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride, n & 1);
+    // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
+    // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
+    // (hred); the owner of the boundary row adds the newest term below.
     SWR_TRACE(1);
-    csync(CS, t == 0 || t == P - 1);
     SWR_TRACE(2);
-    double2 uL[K], uR[K];
-#pragma unroll
-    for (int r = 0; r < K; r++) {
-      uL[r] = cz();
-      uR[r] = cz();
-      if (t > 0) uL[r] = hlast[r * P + t - 1];
-      else if (crank > 0) uL[r] = *remote(hlast + r * P + (P - 1), crank - 1);
-      if (t < P - 1) uR[r] = hfirst[r * P + t + 1];
-      else if (crank < CS - 1) uR[r] = *remote(hfirst + r * P, crank + 1);
-    }
     // ---- end rows and interface terms folded into u_{-1} and u_{N_j} ----
+    // (uL of the first thread and uR / the row after N_j - 1 of the last
+    // thread are rebuilt here every step)
     if (first || last) {
 #pragma unroll
       for (int r = 0; r < K; r++) {
@@ -446,6 +419,39 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       }
     }
     SWR_TRACE(5);
+    // partial history sums of step n+1: P_{n+1} = sum_{s<=n-1} beta_{n+1-s} v_s
+    if (p.s02 && n < NT) {
+      if (has_left && crank == 0) {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          double2 acc = cz();
+          const double2 *hv = hva + r * (NT + 1);
+          for (int s = t; s <= n - 1; s += P) {
+            const double b = sbeta[n + 1 - s];
+            acc.x = fma(b, hv[s].x, acc.x);
+            acc.y = fma(b, hv[s].y, acc.y);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+          if (lane == 0) hred[r * 64 + w] = acc;
+        }
+      }
+      if (has_right && crank == cb) {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          double2 acc = cz();
+          const double2 *hv = hvb + r * (NT + 1);
+          for (int s = t; s <= n - 1; s += P) {
+            const double b = sbeta[n + 1 - s];
+            acc.x = fma(b, hv[s].x, acc.x);
+            acc.y = fma(b, hv[s].y, acc.y);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+          if (lane == 0) hred[r * 64 + 32 + w] = acc;
+        }
+      }
+    }
     // ---- backward sweep x_k = z_k + b_k x_{k+1}: aggregate, scan, exact ----
     double2 x[K];
 #pragma unroll
@@ -463,7 +469,11 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       scan_maps<K, false>(sAb[t], x, sbk, lane, w, nw, CS, crank, carry);
       SWR_TRACE(7);
 #pragma unroll
-      for (int r = 0; r < K; r++) x[r] = carry[r];
+      for (int r = 0; r < K; r++) {
+        x[r] = carry[r];
+        // u_n at row s+M (the next thread's first row) from the carry x_{s+M}
+        uR[r] = make_double2(fma(2.0, carry[r].x, -uR[r].x), fma(2.0, carry[r].y, -uR[r].y));
+      }
     }
     launder<M>(q, er);
     double2 xb[K];
@@ -477,6 +487,28 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         x[r] = cfma(b, x[r], ybuf[(r * M + i) * P + t]);
         if (i == ib) xb[r] = x[r];
         u[r][i] = make_double2(fma(2.0, x[r].x, -u[r][i].x), fma(2.0, x[r].y, -u[r][i].y));  // u_n = 2 v_n - u_{n-1}
+      }
+    }
+    // u_n at row s-1 (the previous thread's last row): x_{s-1} = z_{s-1} + b_{s-1} x_s
+    // with z_{s-1}, q_{s-1} from the previous thread (shared memory / DSMEM,
+    // written before the backward-scan barrier) and E_{s-1} = er_prev + i eim
+    if (s0 > 0) {
+      double2 qp, zp[K];
+      const int par = p.td_stride ? (n & 1) : 1;
+      if (t > 0) {
+        qp = sqlast[par * P + t - 1];
+#pragma unroll
+        for (int r = 0; r < K; r++) zp[r] = ybuf[(r * M + M - 1) * P + t - 1];
+      } else {
+        qp = *remote(sqlast + par * P + (P - 1), crank - 1);
+#pragma unroll
+        for (int r = 0; r < K; r++) zp[r] = *remote(ybuf + (r * M + M - 1) * P + P - 1, crank - 1);
+      }
+      const double2 bp = negqe(qp, er_prev, eim);
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 xp = cfma(bp, x[r], zp[r]);
+        uL[r] = make_double2(fma(2.0, xp.x, -uL[r].x), fma(2.0, xp.y, -uL[r].y));
       }
     }
     // ---- record v_n and S v_n at the interfaces (eq. 8) ----
@@ -903,7 +935,7 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
 
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
   const size_t K = s.K;
-  size_t d2 = K * s.M * s.P + 2 * K * s.P + 2 * (size_t)s.P + 2 * (32 + 32 * K + 16 * (1 + K)) +
+  size_t d2 = K * s.M * s.P + 2 * K * s.P + 4 * (size_t)s.P + 2 * (32 + 32 * K + 16 * (1 + K)) +
               2 * K * (NT + 1) + 64 * K + 2 * K + (flux_smem ? 2 * K * NT : 0);
   return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
 }
