@@ -248,17 +248,25 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
     return SWR_OK;
   }
   if (getenv("SWR_TRACE")) {
+    // per-CTA phase trace of the first cluster (tools/march_trace.sh)
     static long long *tr = nullptr;
-    if (!tr) CK(cudaMalloc(&tr, 64 * sizeof(long long)));
-    CK(cudaMemsetAsync(tr, 0, 64 * sizeof(long long), h->st));
+    const int ntr = 16 * 32;
+    if (!tr) CK(cudaMalloc(&tr, ntr * sizeof(long long)));
+    CK(cudaMemsetAsync(tr, 0, ntr * sizeof(long long), h->st));
     p.trace = tr;
     CK(swr::launch_march(p, h->shape[K], h->st));
-    long long hv[20];
-    CK(cudaMemcpyAsync(hv, tr, 20 * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
+    std::vector<long long> hv(ntr);
+    CK(cudaMemcpyAsync(hv.data(), tr, ntr * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    fprintf(stderr, "march trace (cycles from step start), K=%d M=%d P=%d CS=%d:", K, h->shape[K].M, h->shape[K].P, h->shape[K].CS);
-    for (int i = 1; i < 10; i++) fprintf(stderr, " %lld", hv[i] ? hv[i] - hv[0] : -1);
-    fprintf(stderr, " | next step %lld\n", hv[10] - hv[0]);
+    const MarchShape &sh = h->shape[K];
+    fprintf(stderr, "march trace K=%d M=%d P=%d CS=%d (cycles from step start)\n", K, sh.M, sh.P, sh.CS);
+    for (int c = 0; c < sh.CS; c++) {
+      const long long *r = hv.data() + c * 32;
+      fprintf(stderr, "  cta %d:", c);
+      for (int i = 1; i < 30; i++)
+        if (r[i]) fprintf(stderr, " %d:%lld", i, r[i] - r[0]);
+      fprintf(stderr, "\n");
+    }
     p.trace = nullptr;
   }
   CKS(record_pair(h, true, true));
@@ -768,8 +776,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   swr_partition(h->N, h->world, h->rank, &h->j_lo, &h->j_hi);
   h->st = (cudaStream_t)cfg->cuda_stream;
   if (h->world > 1) {
-    int s0;
-    if ((s0 = load_nccl()) || !cfg->nccl_unique_id) { delete h; g_detail = "NCCL unavailable or no unique id"; return SWR_ERR_NCCL; }
+    if (load_nccl() != 0 || !cfg->nccl_unique_id) { delete h; g_detail = "NCCL unavailable or no unique id"; return SWR_ERR_NCCL; }
     ncclUniqueId_t id;
     memcpy(&id, cfg->nccl_unique_id, sizeof id);
     if (g_nccl.commInitRank(&h->comm, h->world, id, h->rank) != 0) { delete h; g_detail = "ncclCommInitRank failed"; return SWR_ERR_NCCL; }
@@ -780,7 +787,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->c0 = (h->transmission == SWR_TC_ROBIN) ? make_double2(0.0, -h->robin_p) : h->c2v;  // beta_0 = 1
   h->kappa = (2.0 / h->dt) * (h->dx / 6.0);
   h->eim = (2.0 / h->dt) * (h->dx / 6.0);
-  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K);
+  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K, h->NT);
   h->shape[0] = h->shape[1];
   bool shapes_ok = true;
   if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true) > 227 * 1024) shapes_ok = false;

@@ -37,7 +37,7 @@ cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, con
                              int NT, const double2 *tw, cudaStream_t st);
 
 struct MarchShape { int M, P, CS, K; };
-MarchShape choose_march_shape(int Nj, int K);
+MarchShape choose_march_shape(int Nj, int K, int NT);
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
 MarchShape choose_march_shape_nl(int Nj);

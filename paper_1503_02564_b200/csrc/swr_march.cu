@@ -50,6 +50,32 @@ __device__ __forceinline__ T *remote(T *p, int rank) {
   return cg::this_cluster().map_shared_rank(p, rank);
 }
 
+// mbarrier + st.async exchange between the CTAs of a cluster (no fences:
+// the consumer's phase wait covers the remote stores it counts).
+__device__ __forceinline__ uint32_t smem_u32(const void *ptr) { return (uint32_t)__cvta_generic_to_shared(ptr); }
+__device__ __forceinline__ void mbar_init(unsigned long long *mb, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mb)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(unsigned long long *mb, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(mb)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(unsigned long long *mb, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done)
+    asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                 : "=r"(done) : "r"(smem_u32(mb)), "r"(parity) : "memory");
+}
+__device__ __forceinline__ uint32_t mapa(uint32_t addr, int rank) {
+  uint32_t r;
+  asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(addr), "r"(rank));
+  return r;
+}
+// 16-byte remote store counted by the destination CTA's mbarrier
+__device__ __forceinline__ void st_async(uint32_t raddr, double2 v, uint32_t rmb) {
+  asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.v2.f64 [%0], {%1, %2}, [%3];"
+               ::"r"(raddr), "d"(v.x), "d"(v.y), "r"(rmb) : "memory");
+}
+
 // -q (er + i eim)
 __device__ __forceinline__ double2 negqe(double2 q, double er, double eim) {
   return make_double2(fma(q.y, eim, -q.x * er), -fma(q.x, eim, q.y * er));
@@ -86,9 +112,13 @@ struct ScanBuf {
 // Exclusive scan of the per-thread affine maps z -> A z + B_k (k < K) in row
 // order (FWD) or reverse row order; returns the carries (the composition of
 // all earlier maps applied to 0).  One bar.sync (+ one cluster barrier).
-template <int K, bool FWD>
+// ASYNC: the CTA totals travel by st.async into the parity buffer sb.ctot of
+// every CTA that needs them, counted by that CTA's mbarrier mb (phase parity
+// ph); otherwise by DSMEM stores + fence + cluster barrier.
+template <int K, bool FWD, bool ASYNC = false>
 __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const ScanBuf<K> &sb, int lane, int w, int nw,
-                                          int CS, int crank, double2 (&carry)[K]) {
+                                          int CS, int crank, double2 (&carry)[K], long long *tr = nullptr,
+                                          unsigned long long *mb = nullptr, uint32_t ph = 0) {
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
     const double2 Ae = FWD ? shfl_up2(A, o) : shfl_down2(A, o);
@@ -111,6 +141,7 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
 #pragma unroll
     for (int k = 0; k < K; k++) eB[k] = cz();
   }
+  if (tr) tr[0] = clock64();
   const int tot_lane = FWD ? 31 : 0;
   if (lane == tot_lane) {
     sb.wA[w] = A;
@@ -118,6 +149,7 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
     for (int k = 0; k < K; k++) sb.wB[k * 32 + w] = B[k];
   }
   __syncthreads();
+  if (tr) tr[1] = clock64();
   // every warp scans the warp totals itself (no second CTA barrier)
   double2 a = lane < nw ? sb.wA[lane] : make_double2(1.0, 0.0);
   double2 b[K];
@@ -125,6 +157,7 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
   for (int k = 0; k < K; k++) b[k] = lane < nw ? sb.wB[k * 32 + lane] : cz();
 #pragma unroll
   for (int o = 1; o < 32; o <<= 1) {
+    if (o >= nw) break;   // nw warps: log2(nw) levels
     const double2 ae = FWD ? shfl_up2(a, o) : shfl_down2(a, o);
     const bool take = FWD ? lane >= o : lane + o < 32;
 #pragma unroll
@@ -147,24 +180,46 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
 #pragma unroll
     for (int k = 0; k < K; k++) xb[k] = cz();
   }
+  if (tr) tr[2] = clock64();
   if (CS > 1) {
     // CTA total = inclusive over all warps (lane nw-1 forward, lane 0 backward)
     const int tl = FWD ? nw - 1 : 0;
     const bool pusher = (w == 0) && lane == tl;
-    if (pusher) {
-      const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
+    const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
+    if (ASYNC) {
+      if (pusher) {
+        const uint32_t src = smem_u32(sb.ctot + crank * (1 + K)), lmb = smem_u32(mb);
 #pragma unroll 1
-      for (int c = c0; c < c1; c++) {
-        double2 *dst = remote(sb.ctot + crank * (1 + K), c);
-        dst[0] = a;
+        for (int c = c0; c < c1; c++) {
+          const uint32_t dst = mapa(src, c), rmb = mapa(lmb, c);
+          st_async(dst, a, rmb);
 #pragma unroll
-        for (int k = 0; k < K; k++) dst[1 + k] = b[k];
+          for (int k = 0; k < K; k++) st_async(dst + 16 * (1 + k), b[k], rmb);
+        }
       }
-      asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      if (tr) tr[3] = clock64();
+      const int nin = FWD ? crank : CS - 1 - crank;   // CTAs whose totals this CTA receives
+      if (nin > 0) {
+        if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(nin * 16 * (1 + K)));
+        mbar_wait(mb, ph);
+      }
+    } else {
+      if (pusher) {
+#pragma unroll 1
+        for (int c = c0; c < c1; c++) {
+          double2 *dst = remote(sb.ctot + crank * (1 + K), c);
+          dst[0] = a;
+#pragma unroll
+          for (int k = 0; k < K; k++) dst[1 + k] = b[k];
+        }
+        asm volatile("fence.acq_rel.cluster;" ::: "memory");
+      }
+      if (tr) tr[3] = clock64();
+      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
     }
-    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-    asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
   }
+  if (tr) tr[4] = clock64();
   double2 val[K];
 #pragma unroll
   for (int k = 0; k < K; k++) val[k] = cz();
@@ -194,20 +249,183 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
   }
 }
 
-// Optional per-phase clock64 trace (p.trace != NULL): thread 0 of CTA 0,
-// steps 200..201, 10 timestamps per step.
+// ---------------------------------------------------------------------------
+// Scans with precomputed linear parts.  For a constant matrix the linear
+// part of every partial composition (per thread, per warp, per CTA) is fixed
+// for the whole window, so only the offsets B travel through the shuffles,
+// shared memory and the cluster; the linear factors come from a table built
+// once by scan_tab_init (the same composition tree applied to the A's alone).
+// ---------------------------------------------------------------------------
+struct ScanTab {
+  double2 *lvlA;   // [5][P]  this thread's inclusive A before warp-level step L
+  double2 *eA;     // [P]     lane-exclusive A
+  double2 *lvla;   // [5][32] warp-total A (lane = warp index) before level-2 step L
+  double2 *xa;     // [32]    warp-exclusive A
+  double2 *ctA;    // [16]    CTA totals of the cluster
+};
+__host__ __device__ constexpr int kScanTabD2(int P) { return 6 * P + 5 * 32 + 32 + 16; }
+__device__ __forceinline__ ScanTab scan_tab_at(double2 *base, int P) {
+  ScanTab tb;
+  tb.lvlA = base; tb.eA = base + 5 * P; tb.lvla = tb.eA + P; tb.xa = tb.lvla + 5 * 32; tb.ctA = tb.xa + 32;
+  return tb;
+}
+
+// Build the table of one direction from the per-thread linear parts A; the
+// CTA total is stored into ctA[crank] of every CTA of the cluster (visible
+// after the caller's cluster barrier).  Uses wA as scratch; one bar.sync.
+template <bool FWD>
+__device__ void scan_tab_init(double2 A, double2 *wA, const ScanTab &tb, int t, int P, int lane, int w, int nw,
+                              int CS, int crank) {
+#pragma unroll
+  for (int L = 0; L < 5; L++) {
+    const int o = 1 << L;
+    const double2 Ae = FWD ? shfl_up2(A, o) : shfl_down2(A, o);
+    const bool take = FWD ? lane >= o : lane + o < 32;
+    tb.lvlA[L * P + t] = A;
+    if (take) A = cmul(A, Ae);
+  }
+  double2 eA = FWD ? shfl_up2(A, 1) : shfl_down2(A, 1);
+  if (FWD ? lane == 0 : lane == 31) eA = make_double2(1.0, 0.0);
+  tb.eA[t] = eA;
+  if (lane == (FWD ? 31 : 0)) wA[w] = A;
+  __syncthreads();
+  double2 a = lane < nw ? wA[lane] : make_double2(1.0, 0.0);
+#pragma unroll
+  for (int L = 0; L < 5; L++) {
+    const int o = 1 << L;
+    if (o >= nw) break;
+    const double2 ae = FWD ? shfl_up2(a, o) : shfl_down2(a, o);
+    const bool take = FWD ? lane >= o : lane + o < 32;
+    if (w == 0) tb.lvla[L * 32 + lane] = a;
+    if (take) a = cmul(a, ae);
+  }
+  const bool wfirst = FWD ? w == 0 : w == nw - 1;
+  const int wsrc = wfirst ? 0 : (FWD ? w - 1 : w + 1);
+  double2 xa = make_double2(__shfl_sync(0xffffffffu, a.x, wsrc), __shfl_sync(0xffffffffu, a.y, wsrc));
+  if (wfirst) xa = make_double2(1.0, 0.0);
+  if (lane == 0) tb.xa[w] = xa;
+  if (w == 0 && lane == (FWD ? nw - 1 : 0)) {
+    for (int c = 0; c < CS; c++) *remote(tb.ctA + crank, c) = a;   // CTA total A
+  }
+}
+
+// Exclusive scan of the offsets B_k with the tabulated linear parts; the
+// CTA totals travel by st.async (K values) into the parity buffer sb.ctot of
+// the CTAs that need them, counted by their mbarrier mb (phase parity ph).
+template <int K, bool FWD>
+__device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, const ScanTab &tb, int t, int P,
+                                         int lane, int w, int nw, int CS, int crank, double2 (&carry)[K],
+                                         unsigned long long *mb, uint32_t ph, long long *tr = nullptr) {
+#pragma unroll
+  for (int L = 0; L < 5; L++) {
+    const int o = 1 << L;
+    const bool take = FWD ? lane >= o : lane + o < 32;
+    const double2 Am = tb.lvlA[L * P + t];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const double2 Be = FWD ? shfl_up2(B[k], o) : shfl_down2(B[k], o);
+      if (take) B[k] = cfma(Am, Be, B[k]);
+    }
+  }
+  const bool first = FWD ? lane == 0 : lane == 31;
+  double2 eB[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    eB[k] = FWD ? shfl_up2(B[k], 1) : shfl_down2(B[k], 1);
+    if (first) eB[k] = cz();
+  }
+  if (tr) tr[0] = clock64();
+  if (lane == (FWD ? 31 : 0)) {
+#pragma unroll
+    for (int k = 0; k < K; k++) sb.wB[k * 32 + w] = B[k];
+  }
+  __syncthreads();
+  if (tr) tr[1] = clock64();
+  double2 b[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) b[k] = lane < nw ? sb.wB[k * 32 + lane] : cz();
+#pragma unroll
+  for (int L = 0; L < 5; L++) {
+    const int o = 1 << L;
+    if (o >= nw) break;
+    const bool take = FWD ? lane >= o : lane + o < 32;
+    const double2 am = tb.lvla[L * 32 + lane];
+#pragma unroll
+    for (int k = 0; k < K; k++) {
+      const double2 be = FWD ? shfl_up2(b[k], o) : shfl_down2(b[k], o);
+      if (take) b[k] = cfma(am, be, b[k]);
+    }
+  }
+  const bool wfirst = FWD ? w == 0 : w == nw - 1;
+  const int wsrc = wfirst ? 0 : (FWD ? w - 1 : w + 1);
+  double2 xb[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    xb[k] = make_double2(__shfl_sync(0xffffffffu, b[k].x, wsrc), __shfl_sync(0xffffffffu, b[k].y, wsrc));
+    if (wfirst) xb[k] = cz();
+  }
+  if (tr) tr[2] = clock64();
+  double2 val[K];
+#pragma unroll
+  for (int k = 0; k < K; k++) val[k] = cz();
+  if (CS > 1) {
+    const int tl = FWD ? nw - 1 : 0;
+    const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
+    if (w == 0 && lane == tl) {
+      const uint32_t src = smem_u32(sb.ctot + crank * K), lmb = smem_u32(mb);
+#pragma unroll 1
+      for (int c = c0; c < c1; c++) {
+        const uint32_t dst = mapa(src, c), rmb = mapa(lmb, c);
+#pragma unroll
+        for (int k = 0; k < K; k++) st_async(dst + 16 * k, b[k], rmb);
+      }
+    }
+    if (tr) tr[3] = clock64();
+    const int nin = FWD ? crank : CS - 1 - crank;
+    if (nin > 0) {
+      if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(nin * 16 * K));
+      mbar_wait(mb, ph);
+      if (FWD) {
+#pragma unroll 1
+        for (int c = 0; c < crank; c++) {
+          const double2 ca = tb.ctA[c];
+#pragma unroll
+          for (int k = 0; k < K; k++) val[k] = cfma(ca, val[k], sb.ctot[c * K + k]);
+        }
+      } else {
+#pragma unroll 1
+        for (int c = CS - 1; c > crank; c--) {
+          const double2 ca = tb.ctA[c];
+#pragma unroll
+          for (int k = 0; k < K; k++) val[k] = cfma(ca, val[k], sb.ctot[c * K + k]);
+        }
+      }
+    }
+  }
+  if (tr) tr[4] = clock64();
+  const double2 xa = tb.xa[w], eA = tb.eA[t];
+#pragma unroll
+  for (int k = 0; k < K; k++) {
+    val[k] = cfma(xa, val[k], xb[k]);
+    carry[k] = cfma(eA, val[k], eB[k]);
+  }
+}
+
+// Optional per-phase clock64 trace (p.trace != NULL): thread 0 of each CTA
+// of the first cluster, step 200, 32 slots per CTA (clock64 is per SM: only
+// differences within one CTA are meaningful).
+#define SWR_TRACE_ON (p.trace && blockIdx.x < (unsigned)CS && t == 0 && n == 200)
 #define SWR_TRACE(slot)                                                          \
   do {                                                                           \
-    if (p.trace && blockIdx.x == 0 && t == 0 && (n == 200 || n == 201))          \
-      p.trace[(n - 200) * 10 + (slot)] = clock64();                               \
+    if (SWR_TRACE_ON) p.trace[blockIdx.x * 32 + (slot)] = clock64();             \
   } while (0)
 
 // ---------------------------------------------------------------------------
 // i kappa-fold: the value u* such that i kappa u* = d (a rhs addition d on a
-// row written as an extra neighbour value): u* = -i d / kappa.
-__device__ __forceinline__ double2 ifold(double2 d, double kappa) { return make_double2(d.y / kappa, -d.x / kappa); }
+// row written as an extra neighbour value): u* = -i d / kappa (ikappa = 1/kappa).
+__device__ __forceinline__ double2 ifold(double2 d, double ikappa) { return make_double2(d.y * ikappa, -d.x * ikappa); }
 
-template <int M, int K, int PMAX>
+template <int M, int K, int PMAX, bool TDM>
 __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const MarchParams p) {
   extern __shared__ double2 sm[];
   const int P = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = P >> 5;
@@ -216,24 +434,30 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   const MarchSys *G = p.sys + (size_t)(blockIdx.x / CS) * K;   // the group's K systems
   const int Nj = p.Nj, NT = p.NT;
   const int s0 = (crank * P + t) * M;                          // first row of this thread
-  const double eim = p.e_im, kappa = p.kappa;
+  const double eim = p.e_im, kappa = p.kappa, ikappa = 1.0 / p.kappa;
 
   // ---- shared memory ----
-  double2 *ybuf = sm;                                   // [K][M][P]
+  // mbarriers of the cluster scans: [forward, backward][step parity]
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(sm);
+  double2 *ybuf = sm + 2;                               // [K][M][P]
   double2 *hfirst = ybuf + K * M * P;                   // [K][P]
   double2 *hlast = hfirst + K * P;                      // [K][P]
   double2 *sAf = hlast + K * P;                         // [P]
   double2 *sAb = sAf + P;                               // [P]
-  double2 *sqlast = sAb + P;                            // [2][P] q of each thread's last row (step parity)
-  ScanBuf<K> sf, sbk;
-  sf.wA = sqlast + 2 * P;            sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32 * K;
-  sbk.wA = sf.ctot + 16 * (1 + K); sbk.wB = sbk.wA + 32; sbk.ctot = sbk.wB + 32 * K;
-  double2 *hva = sbk.ctot + 16 * (1 + K);               // [K][NT+1] v_s(a_j)
+  ScanBuf<K> sf, sbk;                                   // ctot: [2 parities][16][1+K]
+  sf.wA = sAb + P;                   sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32 * K;
+  sbk.wA = sf.ctot + 32 * (1 + K); sbk.wB = sbk.wA + 32; sbk.ctot = sbk.wB + 32 * K;
+  double2 *hva = sbk.ctot + 32 * (1 + K);               // [K][NT+1] v_s(a_j)
   double2 *hvb = hva + K * (NT + 1);                    // [K][NT+1] v_s(b_j)
   double2 *hred = hvb + K * (NT + 1);                   // [K][2][32] warp partials of H
   double2 *sH = hred + K * 64;                          // [K][2] H_a, H_b of the current step
   double2 *sflux = sH + 2 * K;                          // [K][2][NT] incoming fluxes (if p.flux_smem)
-  double *sbeta = reinterpret_cast<double *>(sflux + (p.flux_smem ? 2 * K * NT : 0));  // [NT+1]
+  double2 *tabbase = sflux + (p.flux_smem ? 2 * K * NT : 0);
+  const ScanTab tabF = scan_tab_at(tabbase, P);                          // constant matrix only
+  const ScanTab tabB = scan_tab_at(tabbase + kScanTabD2(P), P);
+  double2 *sApre = tabbase + 2 * kScanTabD2(P);         // [M][P] prefix products of the forward maps
+  double2 *sG = sApre + M * P;                          // [P] coupling of the forward carry into x_s
+  double *sbeta = reinterpret_cast<double *>(sG + P);   // [NT+1]
 
   const int flags = G[0].flags;
   const bool has_left = flags & SYS_HAS_LEFT, has_right = flags & SYS_HAS_RIGHT;
@@ -251,6 +475,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     imp[r][1] = G[r].flags & SYS_RIN_IMPULSE;
   }
 
+  if (t == 0) {
+    for (int i = 0; i < 4; i++) mbar_init(mbar + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
   for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
   if (p.flux_smem) {
     for (int k = 0; k < K; k++) {
@@ -271,7 +499,8 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   double2 u[K][M], q[M];
   double er[M];
   double er_prev;
-  auto load_factor = [&](const double2 *qp, const double *erp, int par) {
+  double2 qprev;   // q_{s0-1}, the pivot of the previous thread's last row
+  auto load_factor = [&](const double2 *qp, const double *erp) {
 #pragma unroll
     for (int i = 0; i < M; i++) {
       const int k = s0 + i;
@@ -279,6 +508,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       er[i] = k < Nj ? __ldg(erp + k) : 0.0;
     }
     er_prev = (s0 >= 1 && s0 - 1 < Nj) ? __ldg(erp + s0 - 1) : 0.0;
+    qprev = (s0 >= 1 && s0 - 1 < Nj) ? __ldg(qp + s0 - 1) : cz();
     double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
 #pragma unroll
     for (int i = 0; i < M; i++) {
@@ -287,10 +517,8 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     }
     sAf[t] = Af;
     sAb[t] = Ab;
-    sqlast[par * P + t] = q[M - 1];
   };
-  load_factor(G[0].q, G[0].er, 1);
-  sqlast[t] = q[M - 1];
+  load_factor(G[0].q, G[0].er);
 #pragma unroll
   for (int r = 0; r < K; r++) {
     const double2 *u0p = G[r].u0;
@@ -299,6 +527,21 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       const int k = s0 + i;
       u[r][i] = (u0p && k < Nj) ? u0p[k] : cz();
     }
+  }
+  if constexpr (!TDM) {
+    // constant matrix: z_i = zloc_i + Apre_i z_{s0-1} with Apre_i = prod_{k<=i} c_k,
+    // x_{s0} = xloc_{s0} + Ab x_{s0+M} + G z_{s0-1}, G = sum_i (prod_{k<i} b_k) Apre_i
+    double2 Ap = make_double2(1.0, 0.0), Bp = make_double2(1.0, 0.0), Gt = cz();
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      Ap = cmul(Ap, negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim));
+      sApre[i * P + t] = Ap;
+      Gt = cfma(Bp, Ap, Gt);
+      Bp = cmul(Bp, negqe(q[i], er[i], eim));
+    }
+    sG[t] = Gt;
+    scan_tab_init<true>(sAf[t], sf.wA, tabF, t, P, lane, w, nw, CS, crank);
+    scan_tab_init<false>(sAb[t], sbk.wA, tabB, t, P, lane, w, nw, CS, crank);
   }
   if (first) {
 #pragma unroll
@@ -319,7 +562,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     hfirst[r * P + t] = u[r][0];
     hlast[r * P + t] = u[r][M - 1];
   }
-  csync(CS, t == 0 || t == P - 1);
+  csync(CS, true);
   double2 uL[K], uR[K];
 #pragma unroll
   for (int r = 0; r < K; r++) {
@@ -336,11 +579,12 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     return p.flux_smem ? sflux[(2 * r + side) * NT + n - 1] : cz();
   };
 
+  if constexpr (TDM) {
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
     if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
-      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride, n & 1);
+      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
     // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
     // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
     // (hred); the owner of the boundary row adds the newest term below.
@@ -364,7 +608,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
             sH[2 * r] = h;
             d = csub(h, flux(r, 0, n));                 // b_n - l_n at row 0
           }
-          const double2 f = ifold(d, kappa);
+          const double2 f = ifold(d, ikappa);
           uL[r] = make_double2(fma(-2.0, u[r][0].x, f.x), fma(-2.0, u[r][0].y, f.y));
         }
         if (last) {
@@ -379,7 +623,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
             sH[2 * r + 1] = h;
             d = csub(h, flux(r, 1, n));                 // b_n - r_n at row N_j - 1
           }
-          const double2 f = ifold(d, kappa);
+          const double2 f = ifold(d, ikappa);
 #pragma unroll
           for (int i = 0; i < M; i++)
             if (i == ib) {
@@ -392,7 +636,12 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     }
 
     // ---- forward sweep z_k = q_k r_k + c_k z_{k-1}: aggregate, scan, exact ----
-    double2 z[K];
+    double2 z[K], zc[K];   // zc: the forward carry z_{s0-1}
+    const int pb = (n - 1) & 1;                 // scan buffers / mbarriers of this step
+    const uint32_t ph = ((n - 1) >> 1) & 1;     // their phase parity
+    ScanBuf<K> sfp = sf, sbp = sbk;
+    sfp.ctot += pb * 16 * (1 + K);
+    sbp.ctot += pb * 16 * (1 + K);
 #pragma unroll
     for (int r = 0; r < K; r++) z[r] = cz();
 #pragma unroll 1
@@ -412,10 +661,11 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       if (pass == 0) {
         double2 carry[K];
         SWR_TRACE(3);
-        scan_maps<K, true>(sAf[t], z, sf, lane, w, nw, CS, crank, carry);
+        scan_maps<K, true, true>(sAf[t], z, sfp, lane, w, nw, CS, crank, carry,
+                                 SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr, mbar + pb, ph);
         SWR_TRACE(4);
 #pragma unroll
-        for (int r = 0; r < K; r++) z[r] = carry[r];
+        for (int r = 0; r < K; r++) z[r] = zc[r] = carry[r];
       }
     }
     SWR_TRACE(5);
@@ -466,7 +716,8 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     {
       double2 carry[K];
       SWR_TRACE(6);
-      scan_maps<K, false>(sAb[t], x, sbk, lane, w, nw, CS, crank, carry);
+      scan_maps<K, false, true>(sAb[t], x, sbp, lane, w, nw, CS, crank, carry,
+                                SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr, mbar + 2 + pb, ph);
       SWR_TRACE(7);
 #pragma unroll
       for (int r = 0; r < K; r++) {
@@ -490,27 +741,16 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       }
     }
     // u_n at row s-1 (the previous thread's last row): x_{s-1} = z_{s-1} + b_{s-1} x_s
-    // with z_{s-1}, q_{s-1} from the previous thread (shared memory / DSMEM,
-    // written before the backward-scan barrier) and E_{s-1} = er_prev + i eim
+    // with z_{s-1} the forward carry and b_{s-1} = -q_{s-1} E_{s-1}
     if (s0 > 0) {
-      double2 qp, zp[K];
-      const int par = p.td_stride ? (n & 1) : 1;
-      if (t > 0) {
-        qp = sqlast[par * P + t - 1];
-#pragma unroll
-        for (int r = 0; r < K; r++) zp[r] = ybuf[(r * M + M - 1) * P + t - 1];
-      } else {
-        qp = *remote(sqlast + par * P + (P - 1), crank - 1);
-#pragma unroll
-        for (int r = 0; r < K; r++) zp[r] = *remote(ybuf + (r * M + M - 1) * P + P - 1, crank - 1);
-      }
-      const double2 bp = negqe(qp, er_prev, eim);
+      const double2 bp = negqe(qprev, er_prev, eim);
 #pragma unroll
       for (int r = 0; r < K; r++) {
-        const double2 xp = cfma(bp, x[r], zp[r]);
+        const double2 xp = cfma(bp, x[r], zc[r]);
         uL[r] = make_double2(fma(2.0, xp.x, -uL[r].x), fma(2.0, xp.y, -uL[r].y));
       }
     }
+    SWR_TRACE(8);
     // ---- record v_n and S v_n at the interfaces (eq. 8) ----
     if (first) {   // x now holds v_n at row 0
 #pragma unroll
@@ -536,6 +776,203 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         }
       }
     }
+    SWR_TRACE(9);
+  }
+  } else {
+#pragma unroll 1
+  for (int n = 1; n <= NT; n++) {
+    SWR_TRACE(0);
+    if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
+      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
+    // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
+    // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
+    // (hred); the owner of the boundary row adds the newest term below.
+    SWR_TRACE(1);
+    SWR_TRACE(2);
+    // ---- end rows and interface terms folded into u_{-1} and u_{N_j} ----
+    // (uL of the first thread and uR / the row after N_j - 1 of the last
+    // thread are rebuilt here every step)
+    if (first || last) {
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        if (first) {
+          double2 d = cz();
+          if (owns_a) {
+            double2 h = cz();
+            if (p.s02) {
+              h = cscale(sbeta[1], hva[r * (NT + 1) + n - 1]);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + qq]);
+              h = cmul(p.c2, h);
+            }
+            sH[2 * r] = h;
+            d = csub(h, flux(r, 0, n));                 // b_n - l_n at row 0
+          }
+          const double2 f = ifold(d, ikappa);
+          uL[r] = make_double2(fma(-2.0, u[r][0].x, f.x), fma(-2.0, u[r][0].y, f.y));
+        }
+        if (last) {
+          double2 d = cz();
+          if (owns_b) {
+            double2 h = cz();
+            if (p.s02) {
+              h = cscale(sbeta[1], hvb[r * (NT + 1) + n - 1]);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + 32 + qq]);
+              h = cmul(p.c2, h);
+            }
+            sH[2 * r + 1] = h;
+            d = csub(h, flux(r, 1, n));                 // b_n - r_n at row N_j - 1
+          }
+          const double2 f = ifold(d, ikappa);
+#pragma unroll
+          for (int i = 0; i < M; i++)
+            if (i == ib) {
+              const double2 un = make_double2(fma(-2.0, u[r][i].x, f.x), fma(-2.0, u[r][i].y, f.y));
+              if (i == M - 1) uR[r] = un;
+              else u[r][i == M - 1 ? M - 1 : i + 1] = un;   // the (padding) row after N_j - 1
+            }
+        }
+      }
+    }
+
+    // ---- constant matrix: local forward and backward passes (carries 0), one
+    // scan per direction on the offsets, one exact backward pass ----
+    double2 z[K], zc[K], x[K];
+    const int pb = (n - 1) & 1;                 // scan buffers / mbarriers of this step
+    const uint32_t ph = ((n - 1) >> 1) & 1;     // their phase parity
+    ScanBuf<K> sfp = sf, sbp = sbk;
+    sfp.ctot += pb * 16 * (1 + K);
+    sbp.ctot += pb * 16 * (1 + K);
+#pragma unroll
+    for (int r = 0; r < K; r++) z[r] = x[r] = cz();
+    launder<M>(q, er);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const double2 c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 rr = rhs_row<false>(0, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
+                                          i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], kappa);
+        z[r] = cfma(c, z[r], cmul(q[i], rr));
+        ybuf[(r * M + i) * P + t] = z[r];
+      }
+    }
+    launder<M>(q, er);
+#pragma unroll
+    for (int i = M - 1; i >= 0; i--) {
+      const double2 b = negqe(q[i], er[i], eim);
+#pragma unroll
+      for (int r = 0; r < K; r++) x[r] = cfma(b, x[r], ybuf[(r * M + i) * P + t]);
+    }
+    SWR_TRACE(3);
+    scan_tab<K, true>(z, sfp, tabF, t, P, lane, w, nw, CS, crank, zc, mbar + pb, ph,
+                      SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr);
+    SWR_TRACE(4);
+    // partial history sums of step n+1 (after the forward-scan barrier: hva[n-1] visible): P_{n+1} = sum_{s<=n-1} beta_{n+1-s} v_s
+    if (p.s02 && n < NT) {
+      if (has_left && crank == 0) {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          double2 acc = cz();
+          const double2 *hv = hva + r * (NT + 1);
+          for (int s = t; s <= n - 1; s += P) {
+            const double b = sbeta[n + 1 - s];
+            acc.x = fma(b, hv[s].x, acc.x);
+            acc.y = fma(b, hv[s].y, acc.y);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+          if (lane == 0) hred[r * 64 + w] = acc;
+        }
+      }
+      if (has_right && crank == cb) {
+#pragma unroll
+        for (int r = 0; r < K; r++) {
+          double2 acc = cz();
+          const double2 *hv = hvb + r * (NT + 1);
+          for (int s = t; s <= n - 1; s += P) {
+            const double b = sbeta[n + 1 - s];
+            acc.x = fma(b, hv[s].x, acc.x);
+            acc.y = fma(b, hv[s].y, acc.y);
+          }
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+          if (lane == 0) hred[r * 64 + 32 + w] = acc;
+        }
+      }
+    }
+    SWR_TRACE(5);
+    {
+      const double2 Gt = sG[t];
+#pragma unroll
+      for (int r = 0; r < K; r++) x[r] = cfma(Gt, zc[r], x[r]);
+    }
+    {
+      double2 carry[K];
+      SWR_TRACE(6);
+      scan_tab<K, false>(x, sbp, tabB, t, P, lane, w, nw, CS, crank, carry, mbar + 2 + pb, ph,
+                         SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr);
+      SWR_TRACE(7);
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        x[r] = carry[r];
+        // u_n at row s+M (the next thread's first row) from the carry x_{s+M}
+        uR[r] = make_double2(fma(2.0, carry[r].x, -uR[r].x), fma(2.0, carry[r].y, -uR[r].y));
+      }
+    }
+    launder<M>(q, er);
+    double2 xb[K];
+#pragma unroll
+    for (int r = 0; r < K; r++) xb[r] = cz();
+#pragma unroll
+    for (int i = M - 1; i >= 0; i--) {
+      const double2 b = negqe(q[i], er[i], eim);
+      const double2 Ap = sApre[i * P + t];
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 zi = cfma(Ap, zc[r], ybuf[(r * M + i) * P + t]);
+        x[r] = cfma(b, x[r], zi);
+        if (i == ib) xb[r] = x[r];
+        u[r][i] = make_double2(fma(2.0, x[r].x, -u[r][i].x), fma(2.0, x[r].y, -u[r][i].y));  // u_n = 2 v_n - u_{n-1}
+      }
+    }
+    // u_n at row s-1 (the previous thread's last row): x_{s-1} = z_{s-1} + b_{s-1} x_s
+    // with z_{s-1} the forward carry and b_{s-1} = -q_{s-1} E_{s-1}
+    if (s0 > 0) {
+      const double2 bp = negqe(qprev, er_prev, eim);
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 xp = cfma(bp, x[r], zc[r]);
+        uL[r] = make_double2(fma(2.0, xp.x, -uL[r].x), fma(2.0, xp.y, -uL[r].y));
+      }
+    }
+    SWR_TRACE(8);
+    // ---- record v_n and S v_n at the interfaces (eq. 8) ----
+    if (first) {   // x now holds v_n at row 0
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        hva[r * (NT + 1) + n] = x[r];
+        double2 *outl = G[r].out_left;
+        if (owns_a && outl) {
+          const double2 sv = cfma(p.c0, x[r], sH[2 * r]);   // S v_n(a_j) = c0 v_n + H_a
+          const double2 l = flux(r, 0, n);
+          outl[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
+        }
+      }
+    }
+    if (last) {
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        hvb[r * (NT + 1) + n] = xb[r];
+        double2 *outr = G[r].out_right;
+        if (owns_b && outr) {
+          const double2 sv = cfma(p.c0, xb[r], sH[2 * r + 1]);
+          const double2 rv = flux(r, 1, n);
+          outr[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
+        }
+      }
+    }
+    SWR_TRACE(9);
+  }
   }
 #pragma unroll
   for (int r = 0; r < K; r++) {
@@ -847,20 +1284,24 @@ static const Inst kInst[] = {
     {1, 1, 512}, {2, 1, 512}, {4, 1, 512}, {6, 1, 256}, {8, 1, 256}, {11, 1, 256},
     {3, 2, 256}, {3, 3, 256}};
 
-MarchShape choose_march_shape(int Nj, int K) {
+MarchShape choose_march_shape(int Nj, int K, int NT) {
   MarchShape best{0, 0, 0, 0};
   double best_cost = 1e300;
   const char *pm = getenv("SWR_MARCH_PMAX");
   const int pmax_env = pm ? atoi(pm) : 0;
+  const char *mm = getenv("SWR_MARCH_M");   // experiments: force M rows per thread
+  const int m_env = mm ? atoi(mm) : 0;
   for (int CS = 1; CS <= 16; CS++) {
     for (const Inst &in : kInst) {
       if (in.K != K) continue;
       if (pmax_env && in.PMAX != pmax_env) continue;
+      if (m_env && in.M != m_env) continue;
       const int M = in.M;
       long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
       int P = (int)((per + 31) / 32 * 32);
       if (P < 32) P = 32;
       if (P > in.PMAX) continue;
+      if (march_smem_bytes({M, P, CS, K}, NT, true) > 227 * 1024) continue;
       double padded = (double)CS * P * M;
       double cost = padded * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
       if (cost < best_cost) { best_cost = cost; best = {M, P, CS, K}; }
@@ -935,14 +1376,15 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
 
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
   const size_t K = s.K;
-  size_t d2 = K * s.M * s.P + 2 * K * s.P + 4 * (size_t)s.P + 2 * (32 + 32 * K + 16 * (1 + K)) +
-              2 * K * (NT + 1) + 64 * K + 2 * K + (flux_smem ? 2 * K * NT : 0);
+  size_t d2 = 2 + K * s.M * s.P + 2 * K * s.P + 2 * (size_t)s.P + 2 * (32 + 32 * K + 32 * (1 + K)) +
+              2 * K * (NT + 1) + 64 * K + 2 * K + (flux_smem ? 2 * K * NT : 0) +
+              2 * (6 * (size_t)s.P + 5 * 32 + 32 + 16) + (size_t)s.M * s.P + s.P;   // scan tables, Apre, G
   return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
 }
 
 template <int M, int K, int PMAX>
 static cudaError_t launch_m(const MarchParams &p, const MarchShape &s, size_t smem, cudaStream_t st) {
-  auto kern = k_march<M, K, PMAX>;
+  auto kern = p.td_stride ? k_march<M, K, PMAX, true> : k_march<M, K, PMAX, false>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (s.CS > 8) {
