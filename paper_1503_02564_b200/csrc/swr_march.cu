@@ -81,6 +81,16 @@ __device__ __forceinline__ double2 negqe(double2 q, double er, double eim) {
   return make_double2(fma(q.y, eim, -q.x * er), -fma(q.x, eim, q.y * er));
 }
 
+// -q (er + i eim) in the scaled variables of the constant-matrix path:
+// qk = i kappa q, et = er / kappa, eimt = eim / kappa  ->  qk (-eimt + i et)
+__device__ __forceinline__ double2 ck(double2 qk, double et, double eimt) {
+  return make_double2(fma(-qk.x, eimt, -qk.y * et), fma(qk.x, et, -qk.y * eimt));
+}
+// u_{k-1} + 4 u_k + u_{k+1}
+__device__ __forceinline__ double2 srow(double2 um, double2 uk, double2 up) {
+  return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
+}
+
 // Row k of (2i/dt) M u_{n-1} = i kappa (u_{k-1} + 4u_k + u_{k+1}); end rows
 // of the P1 mass matrix are (h/6)(2, 1).
 template <bool GEN>
@@ -272,7 +282,7 @@ __device__ __forceinline__ ScanTab scan_tab_at(double2 *base, int P) {
 
 // Build the table of one direction from the per-thread linear parts A; the
 // CTA total is stored into ctA[crank] of every CTA of the cluster (visible
-// after the caller's cluster barrier).  Uses wA as scratch; one bar.sync.
+// after the caller's cluster barrier).  One bar.sync.
 template <bool FWD>
 __device__ void scan_tab_init(double2 A, double2 *wA, const ScanTab &tb, int t, int P, int lane, int w, int nw,
                               int CS, int crank) {
@@ -309,13 +319,16 @@ __device__ void scan_tab_init(double2 A, double2 *wA, const ScanTab &tb, int t, 
   }
 }
 
-// Exclusive scan of the offsets B_k with the tabulated linear parts; the
-// CTA totals travel by st.async (K values) into the parity buffer sb.ctot of
-// the CTAs that need them, counted by their mbarrier mb (phase parity ph).
-template <int K, bool FWD>
+// Exclusive scan of the offsets B_k with the tabulated linear parts: warp
+// shuffles, then a serial fold over the other warps' totals, then the CTA
+// totals of the cluster, which travel by st.async (K values) into the parity
+// buffer sb.ctot of the CTAs that need them, counted by their mbarrier mb
+// (phase parity ph).  extra() runs between the pushes and the wait.
+template <int K, bool FWD, typename Extra>
 __device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, const ScanTab &tb, int t, int P,
                                          int lane, int w, int nw, int CS, int crank, double2 (&carry)[K],
-                                         unsigned long long *mb, uint32_t ph, long long *tr = nullptr) {
+                                         unsigned long long *mb, uint32_t ph, Extra &&extra,
+                                         long long *tr = nullptr) {
 #pragma unroll
   for (int L = 0; L < 5; L++) {
     const int o = 1 << L;
@@ -369,7 +382,7 @@ __device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, 
 #pragma unroll
   for (int k = 0; k < K; k++) val[k] = cz();
   if (CS > 1) {
-    const int tl = FWD ? nw - 1 : 0;
+    const int tl = FWD ? nw - 1 : 0;            // lane of warp 0 holding the CTA total
     const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
     if (w == 0 && lane == tl) {
       const uint32_t src = smem_u32(sb.ctot + crank * K), lmb = smem_u32(mb);
@@ -380,6 +393,7 @@ __device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, 
         for (int k = 0; k < K; k++) st_async(dst + 16 * k, b[k], rmb);
       }
     }
+    extra();
     if (tr) tr[3] = clock64();
     const int nin = FWD ? crank : CS - 1 - crank;
     if (nin > 0) {
@@ -401,6 +415,8 @@ __device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, 
         }
       }
     }
+  } else {
+    extra();
   }
   if (tr) tr[4] = clock64();
   const double2 xa = tb.xa[w], eA = tb.eA[t];
@@ -449,8 +465,8 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   sbk.wA = sf.ctot + 32 * (1 + K); sbk.wB = sbk.wA + 32; sbk.ctot = sbk.wB + 32 * K;
   double2 *hva = sbk.ctot + 32 * (1 + K);               // [K][NT+1] v_s(a_j)
   double2 *hvb = hva + K * (NT + 1);                    // [K][NT+1] v_s(b_j)
-  double2 *hred = hvb + K * (NT + 1);                   // [K][2][32] warp partials of H
-  double2 *sH = hred + K * 64;                          // [K][2] H_a, H_b of the current step
+  double2 *hred = hvb + K * (NT + 1);                   // [K][2 par][2 side][32] warp partials of H
+  double2 *sH = hred + K * 128;                         // [K][2] H_a, H_b of the current step
   double2 *sflux = sH + 2 * K;                          // [K][2][NT] incoming fluxes (if p.flux_smem)
   double2 *tabbase = sflux + (p.flux_smem ? 2 * K * NT : 0);
   const ScanTab tabF = scan_tab_at(tabbase, P);                          // constant matrix only
@@ -490,7 +506,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     }
   }
   if (t < 2 * K) sH[t] = cz();
-  for (int i = t; i < 64 * K; i += P) hred[i] = cz();
+  for (int i = t; i < 128 * K; i += P) hred[i] = cz();
 
   // Rows beyond N_j (padding) get q = 0: their z, x are 0 and their maps
   // decouple them, so the row loops need no bounds checks.  The end rows of
@@ -542,7 +558,16 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     sG[t] = Gt;
     scan_tab_init<true>(sAf[t], sf.wA, tabF, t, P, lane, w, nw, CS, crank);
     scan_tab_init<false>(sAb[t], sbk.wA, tabB, t, P, lane, w, nw, CS, crank);
+    // scaled coefficients (see ck): q <- i kappa q, er <- er / kappa
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      q[i] = cimul(kappa, q[i]);
+      er[i] *= ikappa;
+    }
+    qprev = cimul(kappa, qprev);
+    er_prev *= ikappa;
   }
+  const double eimk = eim * ikappa;
   if (first) {
 #pragma unroll
     for (int r = 0; r < K; r++) hva[r * (NT + 1)] = u[r][0];
@@ -583,7 +608,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
-    if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
+    if (TDM && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
       load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
     // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
     // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
@@ -782,11 +807,9 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
-    if (p.td_stride && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
-      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
-    // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
-    // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
-    // (hred); the owner of the boundary row adds the newest term below.
+    // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + beta_2 v_{n-2} + Q_n) (P:218,
+    // P:501-507), Q_n = sum_{s<=n-3} beta_{n-s} v_s summed over the CTA during
+    // step n-2 (hred); the owner of the boundary row adds the two newest terms.
     SWR_TRACE(1);
     SWR_TRACE(2);
     // ---- end rows and interface terms folded into u_{-1} and u_{N_j} ----
@@ -800,8 +823,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
           if (owns_a) {
             double2 h = cz();
             if (p.s02) {
-              h = cscale(sbeta[1], hva[r * (NT + 1) + n - 1]);
-              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + qq]);
+              const double2 *hv = hva + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 0) * 32;
+              h = cscale(sbeta[1], hv[n - 1]);
+              if (n >= 2) h = cadd(h, cscale(sbeta[2], hv[n - 2]));
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hq[qq]);
               h = cmul(p.c2, h);
             }
             sH[2 * r] = h;
@@ -815,8 +840,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
           if (owns_b) {
             double2 h = cz();
             if (p.s02) {
-              h = cscale(sbeta[1], hvb[r * (NT + 1) + n - 1]);
-              for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[r * 64 + 32 + qq]);
+              const double2 *hv = hvb + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 1) * 32;
+              h = cscale(sbeta[1], hv[n - 1]);
+              if (n >= 2) h = cadd(h, cscale(sbeta[2], hv[n - 2]));
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hq[qq]);
               h = cmul(p.c2, h);
             }
             sH[2 * r + 1] = h;
@@ -847,59 +874,46 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     launder<M>(q, er);
 #pragma unroll
     for (int i = 0; i < M; i++) {
-      const double2 c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
+      const double2 c = ck(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eimk);
 #pragma unroll
       for (int r = 0; r < K; r++) {
-        const double2 rr = rhs_row<false>(0, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
-                                          i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], kappa);
-        z[r] = cfma(c, z[r], cmul(q[i], rr));
+        const double2 sr = srow(i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
+                                i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1]);
+        z[r] = cfma(c, z[r], cmul(q[i], sr));
         ybuf[(r * M + i) * P + t] = z[r];
       }
     }
     launder<M>(q, er);
 #pragma unroll
     for (int i = M - 1; i >= 0; i--) {
-      const double2 b = negqe(q[i], er[i], eim);
+      const double2 b = ck(q[i], er[i], eimk);
 #pragma unroll
       for (int r = 0; r < K; r++) x[r] = cfma(b, x[r], ybuf[(r * M + i) * P + t]);
     }
     SWR_TRACE(3);
+    // Q_{n+2} = sum_{s<=n-1} beta_{n+2-s} v_s of one side (v_{n-1} is visible
+    // after the forward-scan barrier), reduced per warp into hred; run by the
+    // CTA holding that side while it waits for the other CTAs' totals
+    auto history = [&](int side) {
+      if (!(p.s02 && n + 2 <= NT)) return;
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        double2 acc = cz();
+        const double2 *hv = (side ? hvb : hva) + r * (NT + 1);
+        for (int s = t; s <= n - 1; s += P) {
+          const double b = sbeta[n + 2 - s];
+          acc.x = fma(b, hv[s].x, acc.x);
+          acc.y = fma(b, hv[s].y, acc.y);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+        if (lane == 0) hred[((r * 2 + (n & 1)) * 2 + side) * 32 + w] = acc;
+      }
+    };
     scan_tab<K, true>(z, sfp, tabF, t, P, lane, w, nw, CS, crank, zc, mbar + pb, ph,
+                      [&] { if (has_right && crank == cb) history(1); },
                       SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr);
     SWR_TRACE(4);
-    // partial history sums of step n+1 (after the forward-scan barrier: hva[n-1] visible): P_{n+1} = sum_{s<=n-1} beta_{n+1-s} v_s
-    if (p.s02 && n < NT) {
-      if (has_left && crank == 0) {
-#pragma unroll
-        for (int r = 0; r < K; r++) {
-          double2 acc = cz();
-          const double2 *hv = hva + r * (NT + 1);
-          for (int s = t; s <= n - 1; s += P) {
-            const double b = sbeta[n + 1 - s];
-            acc.x = fma(b, hv[s].x, acc.x);
-            acc.y = fma(b, hv[s].y, acc.y);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (lane == 0) hred[r * 64 + w] = acc;
-        }
-      }
-      if (has_right && crank == cb) {
-#pragma unroll
-        for (int r = 0; r < K; r++) {
-          double2 acc = cz();
-          const double2 *hv = hvb + r * (NT + 1);
-          for (int s = t; s <= n - 1; s += P) {
-            const double b = sbeta[n + 1 - s];
-            acc.x = fma(b, hv[s].x, acc.x);
-            acc.y = fma(b, hv[s].y, acc.y);
-          }
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
-          if (lane == 0) hred[r * 64 + 32 + w] = acc;
-        }
-      }
-    }
     SWR_TRACE(5);
     {
       const double2 Gt = sG[t];
@@ -910,6 +924,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       double2 carry[K];
       SWR_TRACE(6);
       scan_tab<K, false>(x, sbp, tabB, t, P, lane, w, nw, CS, crank, carry, mbar + 2 + pb, ph,
+                         [&] { if (has_left && crank == 0) history(0); },
                          SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr);
       SWR_TRACE(7);
 #pragma unroll
@@ -925,7 +940,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     for (int r = 0; r < K; r++) xb[r] = cz();
 #pragma unroll
     for (int i = M - 1; i >= 0; i--) {
-      const double2 b = negqe(q[i], er[i], eim);
+      const double2 b = ck(q[i], er[i], eimk);
       const double2 Ap = sApre[i * P + t];
 #pragma unroll
       for (int r = 0; r < K; r++) {
@@ -938,7 +953,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     // u_n at row s-1 (the previous thread's last row): x_{s-1} = z_{s-1} + b_{s-1} x_s
     // with z_{s-1} the forward carry and b_{s-1} = -q_{s-1} E_{s-1}
     if (s0 > 0) {
-      const double2 bp = negqe(qprev, er_prev, eim);
+      const double2 bp = ck(qprev, er_prev, eimk);
 #pragma unroll
       for (int r = 0; r < K; r++) {
         const double2 xp = cfma(bp, x[r], zc[r]);
@@ -1377,8 +1392,8 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
   const size_t K = s.K;
   size_t d2 = 2 + K * s.M * s.P + 2 * K * s.P + 2 * (size_t)s.P + 2 * (32 + 32 * K + 32 * (1 + K)) +
-              2 * K * (NT + 1) + 64 * K + 2 * K + (flux_smem ? 2 * K * NT : 0) +
-              2 * (6 * (size_t)s.P + 5 * 32 + 32 + 16) + (size_t)s.M * s.P + s.P;   // scan tables, Apre, G
+              2 * K * (NT + 1) + 128 * K + 2 * K + (flux_smem ? 2 * K * NT : 0) +
+              2 * (size_t)kScanTabD2(s.P) + (size_t)s.M * s.P + s.P;   // scan tables, Apre, G
   return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
 }
 
