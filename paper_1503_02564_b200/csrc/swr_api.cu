@@ -147,6 +147,7 @@ struct swr_handle {
   // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0, transformed inputs
   int log4 = 0;
   bool fft_fused = true;
+  bool fft_reg = false;   // register four-step FFT kernel (NF = 1024)
   // V(t,x): per-step pivots [N_T][N][N_j]; f(u): fixed-point stats
   double *tau = nullptr, *xi = nullptr;
   double2 *qtd = nullptr;
@@ -551,7 +552,10 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
 int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
   if (h->N < 2) return SWR_OK;
   CKS(record_pair(h, false, true));
-  if (h->log4 && h->fft_fused) {
+  if (h->log4 && h->fft_reg) {
+    CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
+    h->n_launches++;
+  } else if (h->log4 && h->fft_fused) {
     CK(swr::launch_fft_conv(h->log4, zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
     h->n_launches++;
   } else if (h->log4) {
@@ -839,6 +843,8 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     const char *tmode = getenv("SWR_TOEPLITZ");
     h->log4 = (tmode && strcmp(tmode, "direct") == 0) ? 0 : swr::fft_log4_for(h->NT);
     h->fft_fused = !(tmode && strcmp(tmode, "fft2") == 0);
+    // register FFT for NF = 1024 unless a Stockham form is requested
+    h->fft_reg = h->log4 == 5 && !(tmode && (strcmp(tmode, "fft2") == 0 || strcmp(tmode, "fftsm") == 0));
     if (h->log4) {
       const size_t NF = (size_t)1 << (2 * h->log4);
       if ((s = dalloc(&h->tw, NF)) || (s = dalloc(&h->FX, (size_t)h->N * 4 * NF)) ||

@@ -23,6 +23,8 @@ __global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, int j_lo, 
 __global__ void k_fill(double2 *x, double2 v, size_t n);
 
 enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };
+cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
+                                cudaStream_t st);
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st);
 __global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);

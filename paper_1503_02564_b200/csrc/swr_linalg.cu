@@ -295,6 +295,160 @@ __global__ void k_fft_conv(const double2 *__restrict__ Fc, const double2 *__rest
   }
 }
 
+// ---------------------------------------------------------------------------
+// Register FFT form for NF = 1024 (N_T <= 512): four-step 1024 = 32 x 32
+// FFTs, one warp per transform, 32 values per thread.  A thread holds the
+// column n1 = lane (values x[n1 + 32 n2], n2 = register), runs a 32-point
+// radix-2 DIF in registers, multiplies by W_1024^{n1 k2}, the warp
+// transposes through padded shared memory (conflict-free), and a second
+// 32-point DIF finishes: lane l ends up holding X[l + 32 k1] in register
+// bitrev(k1), the same lane/register layout the inverse transform reads.
+// Shared-memory traffic is one transpose per transform (the radix-4
+// Stockham kernel above moves the whole sequence through shared memory at
+// each of its five stages).  One CTA (2 warps) per subdomain j: both input
+// slots (l_j, r_j) are transformed once, exchanged, and each warp forms one
+// output slot (the X^{j,1..2} and X^{j,3..4} pairs) and inverts it.
+// ---------------------------------------------------------------------------
+namespace fftr {
+// cos / sin (2 pi k / 32), k = 0..8 (first octant + pi/4); the rest by symmetry
+__device__ __forceinline__ constexpr double c32(int k) {
+  return k == 0 ? 1.0 : k == 1 ? 0.98078528040323043 : k == 2 ? 0.92387953251128674 : k == 3 ? 0.83146961230254524
+       : k == 4 ? 0.70710678118654752 : k == 5 ? 0.55557023301960218 : k == 6 ? 0.38268343236508977
+       : k == 7 ? 0.19509032201612826 : 0.0;
+}
+// e^{-+ 2 pi i k / 32} times d (k in [0, 16), constant after unrolling)
+template <bool INV>
+__device__ __forceinline__ double2 tw32(double2 d, int k) {
+  if (k == 0) return d;
+  if (k == 8) return INV ? make_double2(-d.y, d.x) : make_double2(d.y, -d.x);   // * (+-i)
+  const double c = k < 8 ? c32(k) : -c32(16 - k);
+  const double sn = k < 8 ? c32(8 - k) : c32(k - 8);                             // sin(2 pi k / 32) >= 0
+  const double s = INV ? sn : -sn;
+  return make_double2(fma(d.x, c, -d.y * s), fma(d.x, s, d.y * c));
+}
+__device__ __forceinline__ constexpr int br5(int k) {
+  return ((k & 1) << 4) | ((k & 2) << 2) | (k & 4) | ((k & 8) >> 2) | ((k & 16) >> 4);
+}
+// 32-point radix-2 DIF in registers; output X[k] in v[br5(k)].  HALF: v[16..31] = 0 on input.
+template <bool INV, bool HALF>
+__device__ __forceinline__ void dif32(double2 (&v)[32]) {
+#pragma unroll
+  for (int m = 32; m >= 2; m >>= 1) {
+#pragma unroll
+    for (int b = 0; b < 32; b += m) {
+#pragma unroll
+      for (int i = 0; i < m / 2; i++) {
+        const double2 a = v[b + i];
+        if (HALF && m == 32) {
+          v[b + i + m / 2] = tw32<INV>(a, i * (32 / m));
+        } else {
+          const double2 c = v[b + i + m / 2];
+          v[b + i] = cadd(a, c);
+          v[b + i + m / 2] = tw32<INV>(csub(a, c), i * (32 / m));
+        }
+      }
+    }
+  }
+}
+// 1024-point transform of the warp's sequence: on entry lane n1 holds
+// x[n1 + 32 n2] in v[n2]; on exit X[lane + 32 k1] in v[br5(k1)].  T: [32][33].
+template <bool INV, bool HALF>
+__device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const double2 *__restrict__ tw, int lane) {
+  dif32<INV, HALF>(v);                                  // Y[k2] = v[br5(k2)]
+  // W^{n1 k2} = W^{n1 a} W^{8 n1 b}, k2 = a + 8 b: W^{n1 a} by a short product
+  // chain, W^{8 n1 b} from the table (4 loads per thread instead of 31 gathers)
+  double2 wa[8], wb[4];
+  wa[0] = make_double2(1.0, 0.0);
+  wa[1] = __ldg(tw + lane);
+#pragma unroll
+  for (int a = 2; a < 8; a++) wa[a] = cmul(wa[a - 1], wa[1]);
+  wb[0] = make_double2(1.0, 0.0);
+#pragma unroll
+  for (int b = 1; b < 4; b++) wb[b] = __ldg(tw + ((8 * b * lane) & 1023));
+#pragma unroll
+  for (int r = 1; r < 32; r++) {
+    const int k2 = br5(r), a = k2 & 7, b = k2 >> 3;
+    double2 w = b == 0 ? wa[a] : (a == 0 ? wb[b] : cmul(wa[a], wb[b]));
+    if (INV) w.y = -w.y;
+    v[r] = cmul(v[r], w);
+  }
+#pragma unroll
+  for (int r = 0; r < 32; r++) T[lane * 33 + br5(r)] = v[r];
+  __syncwarp();
+#pragma unroll
+  for (int n1 = 0; n1 < 32; n1++) v[n1] = T[n1 * 33 + lane];
+  __syncwarp();
+  dif32<INV, false>(v);
+}
+}  // namespace fftr
+
+__global__ void __launch_bounds__(64) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
+                                                     double2 *__restrict__ y, int N, int NT,
+                                                     const double2 *__restrict__ tw) {
+  constexpr int NF = 1024;
+  extern __shared__ double2 fsm[];
+  const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double2 *T = fsm + q * (32 * 33);        // per-warp transpose buffer, also the spectrum exchange
+  const int j = blockIdx.x + 1;
+  const int sidx = q == 0 ? 2 * j - 3 : 2 * j - 2;
+  const bool has_in = q == 0 ? j >= 2 : j <= N - 1;
+  double2 v[32];
+#pragma unroll
+  for (int n2 = 0; n2 < 32; n2++) {
+    const int n = lane + 32 * n2;
+    v[n2] = (n2 < 16 && has_in && n < NT) ? x[(size_t)sidx * NT + n] : cz();
+  }
+  fftr::fft1024<false, true>(v, T, tw, lane);
+  // spectra of l_j (warp 0) and r_j (warp 1) in the own buffer (natural
+  // order k = lane + 32 k1), read by both warps
+#pragma unroll
+  for (int k1 = 0; k1 < 32; k1++) T[k1 * 32 + lane] = v[fftr::br5(k1)];
+  __syncthreads();
+  // warp 0: output slot 2j-4 (l_j side, columns X^{j,1}, X^{j,2}); warp 1: 2j-1 (X^{j,3}, X^{j,4})
+  const bool has_out = q == 0 ? j >= 2 : j <= N - 1;
+  const int o = q == 0 ? 2 * j - 4 : 2 * j - 1;
+  const double2 *c1 = Fc + ((size_t)(j - 1) * 4 + 2 * q) * NF, *c2 = c1 + NF;
+  const double2 *other = fsm + (1 - q) * (32 * 33);
+  const bool hA = j >= 2, hB = j <= N - 1;
+  if (has_out) {
+#pragma unroll
+    for (int k1 = 0; k1 < 32; k1++) {
+      const int k = lane + 32 * k1;
+      const double2 own = T[k1 * 32 + lane], oth = other[k1 * 32 + lane];
+      const double2 A = q == 0 ? own : oth, B = q == 0 ? oth : own;
+      double2 acc = cz();
+      if (hA) acc = cmul(__ldg(c1 + k), A);
+      if (hB) acc = cfma(__ldg(c2 + k), B, acc);
+      v[k1] = acc;
+    }
+  }
+  __syncthreads();   // the other warp has read this warp's buffer
+  if (!has_out) return;
+  fftr::fft1024<true, false>(v, T, tw, lane);
+  const double inv = 1.0 / NF;
+  const double2 *xo = x + (size_t)o * NT;
+  double2 *yo = y + (size_t)o * NT;
+#pragma unroll
+  for (int k1 = 0; k1 < 16; k1++) {
+    const int n = lane + 32 * k1;
+    if (n < NT) {
+      const double2 xv = xo[n], a = v[fftr::br5(k1)];
+      yo[n] = make_double2(fma(-inv, a.x, xv.x), fma(-inv, a.y, xv.y));
+    }
+  }
+}
+
+cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
+                                cudaStream_t st) {
+  if (N < 2) return cudaSuccess;
+  if (NT > 512) return cudaErrorInvalidValue;
+  const size_t smem = (2 * 32 * 33) * sizeof(double2);
+  cudaError_t e = cudaFuncSetAttribute(k_fft_conv_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  k_fft_conv_reg<<<N, 64, smem, st>>>(Fc, x, y, N, NT, tw);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
                             const double2 *tw, cudaStream_t st) {
   if (N < 2) return cudaSuccess;

@@ -147,12 +147,13 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["direct", "fft", "fft2"])
+@pytest.mark.parametrize("mode", ["direct", "fft", "fft2", "fftsm"])
 def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
-    """Both forms of y = (I - L) x (direct causal convolution and FFT
-    convolution) against the oracle's direct convolution."""
+    """All forms of y = (I - L) x (direct causal convolution; FFT convolution:
+    register four-step for NF = 1024 (default), fused or two-kernel radix-4
+    Stockham) against the oracle's direct convolution."""
     import torch
-    if mode in ("direct", "fft2"):
+    if mode in ("direct", "fft2", "fftsm"):
         monkeypatch.setenv("SWR_TOEPLITZ", mode)
     else:
         monkeypatch.delenv("SWR_TOEPLITZ", raising=False)
