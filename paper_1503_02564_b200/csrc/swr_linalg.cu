@@ -3,6 +3,9 @@
 // gather (PAPER.md = Besse & Xing, arXiv:1503.02564).
 #include "swr_common.cuh"
 #include "swr_kernels.h"
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
 
 namespace swr {
 
@@ -696,13 +699,199 @@ __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__rest
     y[e] = make_double2(x[e].x * sc, x[e].y * sc);
 }
 
+// ---------------------------------------------------------------------------
+// Same CGS kernel, bulk-copy pipeline form.  One persistent CTA per SM
+// streams chunks of CH = 128 EPT entries of the nv basis vectors and of w
+// into shared memory with cp.async.bulk (TMA, one 1-D copy per vector row,
+// completion counted on a per-stage mbarrier), NS stages deep, so HBM reads
+// run ahead of the arithmetic without any thread holding them in registers.
+// Thread t owns entries t + 128 k of each chunk: the axpy and the dots of an
+// entry are thread-local (no cross-warp reduction per chunk, one CTA barrier
+// per chunk to release the stage).  Dot partials: registers over the CTA's
+// chunks (fixed order), warp shuffles + shared memory, the last CTA sums the
+// per-CTA partials in CTA order.
+// ---------------------------------------------------------------------------
+__device__ __forceinline__ uint32_t cgs_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int NVMAX>
+__global__ void __launch_bounds__(256, 1) k_cgs_tma(const double2 *__restrict__ V, size_t ldv, int nv,
+                                                    const double2 *__restrict__ hsrc, double2 *__restrict__ w,
+                                                    int mode, double2 *__restrict__ partial, double2 *__restrict__ out,
+                                                    unsigned *counter, size_t ntot, int EPT, int NS) {
+  constexpr int NH = NVMAX / 2;   // basis vectors per thread (v = 2 i + hf)
+  extern __shared__ __align__(128) unsigned char smraw[];
+  __shared__ double2 red[NVMAX + 1][8];
+  __shared__ double2 sh[NVMAX];
+  __shared__ bool last;
+  unsigned long long *mb = reinterpret_cast<unsigned long long *>(smraw);   // [NS]
+  double2 *stg = reinterpret_cast<double2 *>(smraw + 128);                  // [NS][nv + 1][CH]
+  const int t = threadIdx.x, lane = t & 31, wp = t >> 5, hf = t & 1, el0 = t >> 1;
+  const int CH = 128 * EPT, nrow = nv + 1;
+  const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
+  const size_t nch = (ntot + CH - 1) / CH;
+  const int mine = blockIdx.x < nch ? (int)((nch - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
+  if (axpy)
+    for (int v = t; v < nv; v += blockDim.x) sh[v] = hsrc[v];
+  if (t == 0) {
+    for (int i = 0; i < NS; i++)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cgs_smem_u32(mb + i)) : "memory");
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  auto issue = [&](int i) {   // chunk i of this CTA into stage i % NS (warp 0, one row per lane)
+    const int sgi = i % NS;
+    const size_t base = (blockIdx.x + (size_t)i * gridDim.x) * CH;
+    const uint32_t bytes = (uint32_t)(min((size_t)CH, ntot - base) * sizeof(double2));
+    const uint32_t mbar = cgs_smem_u32(mb + sgi);
+    if (lane == 0)
+      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes * nrow) : "memory");
+    double2 *dst = stg + (size_t)sgi * nrow * CH;
+    for (int v = lane; v <= nv; v += 32) {
+      const double2 *src = v < nv ? V + (size_t)v * ldv + base : w + base;
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(cgs_smem_u32(dst + (size_t)v * CH)), "l"(src), "r"(bytes), "r"(mbar) : "memory");
+    }
+  };
+  if (wp == 0)
+    for (int i = 0; i < NS - 1 && i < mine; i++) issue(i);
+  double2 acc[NH];
+#pragma unroll
+  for (int v = 0; v < NH; v++) acc[v] = cz();
+  double nacc = 0.0;
+  for (int i = 0; i < mine; i++) {
+    if (wp == 0 && i + NS - 1 < mine) issue(i + NS - 1);   // its stage was released at the end of i - 1
+    const int sgi = i % NS;
+    {
+      const uint32_t mbar = cgs_smem_u32(mb + sgi), par = (uint32_t)((i / NS) & 1);
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(mbar), "r"(par) : "memory");
+    }
+    const double2 *st = stg + (size_t)sgi * nrow * CH;
+    const size_t base = (blockIdx.x + (size_t)i * gridDim.x) * CH;
+    const int n = (int)min((size_t)CH, ntot - base);
+    // lanes 2e, 2e + 1 share entry e (even / odd v); the loop bound is warp-uniform
+    // (CH is a multiple of 128) so the pair shuffle always sees the full warp
+    for (int e = el0; e < CH; e += 128) {
+      const bool ok = e < n;
+      double2 we = ok ? st[(size_t)nv * CH + e] : cz();
+      if (axpy) {
+        double2 p0 = cz(), p1 = cz();
+        if (ok) {
+#pragma unroll 4
+          for (int v = hf; v < nv; v += 4) {
+            p0 = cfma(sh[v], st[(size_t)v * CH + e], p0);
+            if (v + 2 < nv) p1 = cfma(sh[v + 2], st[(size_t)(v + 2) * CH + e], p1);
+          }
+        }
+        const double2 pm = cadd(p0, p1), po = shfl_xor2(pm, 1);
+        const double2 tot = hf == 0 ? cadd(pm, po) : cadd(po, pm);   // (even + odd), same on both lanes
+        we = csub(we, tot);
+        if (ok && hf == 0) w[base + e] = we;
+      }
+      if (ok) {
+        if (dots) {
+#pragma unroll
+          for (int k = 0; k < NH; k++)
+            if (2 * k + hf < nv) acc[k] = cfmaconj(st[(size_t)(2 * k + hf) * CH + e], we, acc[k]);
+        }
+        if (norm && hf == 0) nacc = fma(we.x, we.x, fma(we.y, we.y, nacc));
+      }
+    }
+    __syncthreads();   // stage sgi free for chunk i + NS
+  }
+  const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
+  if (dots) {
+#pragma unroll
+    for (int k = 0; k < NH; k++) {
+      if (2 * k < nv) {
+        double2 a = acc[k];
+#pragma unroll
+        for (int o = 16; o > 1; o >>= 1) a = cadd(a, shfl_xor2(a, o));   // lanes of the same parity
+        if (lane < 2 && 2 * k + lane < nv) red[2 * k + lane][wp] = a;
+      }
+    }
+  }
+  if (norm) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
+    if (lane == 0) red[nred - 1][wp] = make_double2(nacc, 0.0);
+  }
+  __syncthreads();
+  if (t < nred) {
+    double2 sum = red[t][0];
+#pragma unroll
+    for (int q = 1; q < 8; q++) sum = cadd(sum, red[t][q]);
+    partial[(size_t)t * gridDim.x + blockIdx.x] = sum;
+  }
+  __threadfence();
+  __syncthreads();
+  if (t == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  const int np = gridDim.x;
+  for (int v = wp; v < nred; v += 8) {
+    double2 sum = cz();
+    for (int q = lane; q < np; q += 32) sum = cadd(sum, __ldcg(partial + (size_t)v * np + q));
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
+    if (lane == 0) {
+      out[v] = sum;
+      if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
+    }
+  }
+  if (t == 0) *counter = 0u;
+}
+
+template <int NVMAX>
+static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
+                                    double2 *partial, double2 *out, unsigned *counter, size_t ntot, cudaStream_t st) {
+  // stage = (nv + 1) rows of CH = 128 EPT entries, about 48 KB; up to 4 stages in 200 KB
+  const int nrow = nv + 1;
+  int EPT = (int)((48 * 1024) / ((size_t)nrow * 128 * sizeof(double2)));
+  EPT = EPT < 1 ? 1 : (EPT > 16 ? 16 : EPT);
+  const size_t stage = (size_t)nrow * 128 * EPT * sizeof(double2);
+  const int NS = (int)std::min<size_t>(4, (200 * 1024) / stage);
+  const size_t smem = 128 + (size_t)NS * stage;
+  static bool attr_set = false;
+  if (!attr_set) {
+    cudaError_t e = cudaFuncSetAttribute(k_cgs_tma<NVMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+    if (e != cudaSuccess) {
+      fprintf(stderr, "k_cgs_tma<%d>: cudaFuncSetAttribute: %s\n", NVMAX, cudaGetErrorString(e));
+      return e;
+    }
+    attr_set = true;
+  }
+  const size_t nch = (ntot + 128 * EPT - 1) / (128 * EPT);
+  const unsigned grid = (unsigned)std::min<size_t>(nch, 148);
+  k_cgs_tma<NVMAX><<<grid, 256, smem, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, EPT, NS);
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) {
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, k_cgs_tma<NVMAX>);
+    fprintf(stderr, "k_cgs_tma<%d>: launch grid %u smem %zu (max dyn %d, static %zu, regs %d, maxthr %d): %s\n", NVMAX, grid,
+            smem, fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes, fa.numRegs, fa.maxThreadsPerBlock, cudaGetErrorString(e));
+  }
+  return e;
+}
+
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st) {
-  // persistent grid: 4 CTAs of 128 threads per SM (148 SMs); the grid only
-  // depends on the sizes, so the reduction order is fixed
   const size_t ntot = (size_t)(2 * N - 2) * NT;
-  auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
   if (nv > 32) return cudaErrorInvalidValue;
+  // default: register form below; SWR_CGS=tma selects the bulk-copy pipeline
+  // form (measured slower at C5: 190 vs 147 ms per solve)
+  const char *cgs_env = getenv("SWR_CGS");
+  if (cgs_env && strcmp(cgs_env, "tma") == 0) {
+    if (nv <= 8) return launch_cgs_tma_t<8>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
+    if (nv <= 16) return launch_cgs_tma_t<16>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
+    return launch_cgs_tma_t<32>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
+  }
+  // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
+  // grid only depends on the sizes, so the reduction order is fixed
+  auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
   if (nv <= 8) k_cgs<2, 8><<<grid(256), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
   else if (nv <= 16) k_cgs<4, 4><<<grid(128), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
   else k_cgs<8, 2><<<grid(64), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);

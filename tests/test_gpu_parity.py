@@ -147,6 +147,20 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
 
 
+@pytest.mark.parametrize("cgs", ["reg", "tma"])
+def test_cgs_kernel_forms(oracle_mod, gpu, cgs, monkeypatch):
+    """Both CGS kernel forms (register; bulk-copy pipeline) give the oracle's
+    GMRES iteration count and u(T) on a NEW solve whose Krylov vectors span
+    several chunks with a ragged tail."""
+    monkeypatch.setenv("SWR_CGS", cgs)
+    p = si.Problem(dx=1e-3, dt=1e-3, N=20, potential=si.POT_VX)
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert st == 0 and rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
 @pytest.mark.parametrize("mode", ["direct", "fft", "fft2", "fftsm"])
 def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
     """All forms of y = (I - L) x (direct causal convolution; FFT convolution:
