@@ -429,8 +429,9 @@ typedef std::function<int(const double2 *, double2 *)> Op;
 // per Arnoldi step: the operator, three fused CGS kernels (dots; axpy+dots;
 // axpy+norm) and the normalisation; one host round trip for the Givens
 // update.
-int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w, int mode, double2 *out) {
-  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st));
+int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w, int mode, double2 *out,
+        double2 *out_host = nullptr) {
+  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st, out_host));
   h->n_launches++;
   return SWR_OK;
 }
@@ -467,28 +468,28 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
     int s = A(V + (size_t)k * ldv, w);
     if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
     if (s) st = s;
-    CKS(cgs(h, V, k + 1, nullptr, w, swr::CGS_DOTS | swr::CGS_NORM, O1(par)));                 // h1, ||w||^2
-    CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_DOTS, O2(par)));                // w -= V h1; h2
-    CKS(cgs(h, V, k + 1, O2(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par)));  // w -= V h2
-    swr::k_scale_dev<<<grid_for(n), 256, 0, h->st>>>(w, O3(par) + 1, V + (size_t)(k + 1) * ldv, n);
-    CK(cudaGetLastError());
+    // scalars also go straight to the pinned mirror HP(par) (no copy node)
+    CKS(cgs(h, V, k + 1, nullptr, w, swr::CGS_DOTS | swr::CGS_NORM, O1(par), HP(par)));              // h1, ||w||^2
+    CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_DOTS, O2(par), HP(par) + (m + 2)));   // w -= V h1; h2
+    CKS(cgs(h, V, k + 1, O2(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par),
+            HP(par) + 2 * (m + 2)));                                                                 // w -= V h2
+    CK(swr::launch_pdl(swr::k_scale_dev, dim3(grid_for(n)), dim3(256), 0, h->st, (const double2 *)w,
+                       (const double2 *)(O3(par) + 1), V + (size_t)(k + 1) * ldv, n));
     h->n_launches++;
-    CK(cudaMemcpyAsync(HP(par), O1(par), stride * sizeof(double2), cudaMemcpyDeviceToHost, h->st));
     CK(cudaEventRecord(K.ev[par], h->st));
     return SWR_OK;
   };
   while (!done) {
     CKS(A(x, w));
-    swr::k_sub<<<grid_for(n), 256, 0, h->st>>>(b, w, V, n);
-    CK(cudaGetLastError());
+    CK(swr::launch_pdl(swr::k_sub, dim3(grid_for(n)), dim3(256), 0, h->st, b, (const double2 *)w, V, n));
     h->n_launches++;
     CKS(cgs(h, nullptr, 0, nullptr, V, swr::CGS_NORM, O3(0)));
     CKS(fetch(h, O3(0), 1, HP(0) + 2 * (m + 2)));
     const double beta = std::sqrt(HP(0)[2 * (m + 2)].x);
     if (beta <= tol * bnorm) { *converged = 1; break; }
     if (total >= maxit) break;
-    swr::k_axpby<<<grid_for(n), 256, 0, h->st>>>(make_double2(0, 0), V, make_double2(1.0 / beta, 0), V, n);
-    CK(cudaGetLastError());
+    CK(swr::launch_pdl(swr::k_axpby, dim3(grid_for(n)), dim3(256), 0, h->st, make_double2(0, 0), (const double2 *)V,
+                       make_double2(1.0 / beta, 0), V, n));
     h->n_launches++;
     std::fill(gam.begin(), gam.end(), cplx(0));
     gam[0] = beta;
@@ -538,8 +539,8 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
     double2 *hy = HP(0);
     for (int i = 0; i < kend; i++) hy[i] = d2(y[i]);
     CK(cudaMemcpyAsync(K.ycoef, hy, kend * sizeof(double2), cudaMemcpyHostToDevice, h->st));
-    swr::k_multi_update<<<grid_for(n), 256, 0, h->st>>>(V, ldv, kend, K.ycoef, x, n);
-    CK(cudaGetLastError());
+    CK(swr::launch_pdl(swr::k_multi_update, dim3(grid_for(n)), dim3(256), 0, h->st, (const double2 *)V, ldv, kend,
+                       (const double2 *)K.ycoef, x, n));
     h->n_launches++;
     CK(cudaStreamSynchronize(h->st));
   }

@@ -1,8 +1,27 @@
 // swr_kernels.h — kernel declarations shared by the host orchestration.
 #pragma once
 #include "swr_common.cuh"
+#include <utility>
 
 namespace swr {
+
+// Launch with programmatic stream serialization (the kernel must call
+// pdl_wait() before reading what earlier work in the stream wrote).
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
 
 struct FactorJob {
   const double *W;   // nodal W on the subdomain [N_j] (NULL = 0)
@@ -26,7 +45,8 @@ enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
                                 cudaStream_t st);
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st);
+                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
+                       double2 *out_host = nullptr);
 __global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);
 
 int fft_log4_for(int NT);

@@ -266,6 +266,8 @@ __global__ void k_fft_apply(const double2 *__restrict__ Fc, const double2 *__res
 template <int LOG4>
 __global__ void k_fft_conv(const double2 *__restrict__ Fc, const double2 *__restrict__ x, double2 *__restrict__ y,
                            int N, int NT, const double2 *__restrict__ tw) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
   extern __shared__ double2 fs[];
   double2 *a1 = fs, *a2 = fs + NF, *bb = fs + 2 * NF;   // two transforms + scratch
@@ -388,6 +390,8 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const doub
 __global__ void __launch_bounds__(64) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
                                                      double2 *__restrict__ y, int N, int NT,
                                                      const double2 *__restrict__ tw) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NF = 1024;
   extern __shared__ double2 fsm[];
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -448,8 +452,7 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   const size_t smem = (2 * 32 * 33) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_fft_conv_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  k_fft_conv_reg<<<N, 64, smem, st>>>(Fc, x, y, N, NT, tw);
-  return cudaGetLastError();
+  return launch_pdl(k_fft_conv_reg, dim3(N), dim3(64), smem, st, Fc, x, y, N, NT, tw);
 }
 
 cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
@@ -549,12 +552,16 @@ __global__ void k_multi_axpy(const double2 *__restrict__ V, size_t ldv, int nvec
 
 // y = a * x + b * y (complex a, b)
 __global__ void k_axpby(double2 a, const double2 *__restrict__ x, double2 b, double2 *__restrict__ y, size_t n) {
+  pdl_wait();
+  pdl_trigger();
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     y[e] = cfma(a, x[e], cmul(b, y[e]));
 }
 
 // z = x - y
 __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n) {
+  pdl_wait();
+  pdl_trigger();
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     z[e] = csub(x[e], y[e]);
 }
@@ -562,6 +569,8 @@ __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n) 
 // x += sum_v y_v V_v  (GMRES update)
 __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nvec, const double2 *__restrict__ y,
                                double2 *__restrict__ x, size_t n) {
+  pdl_wait();
+  pdl_trigger();
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
     double2 acc = x[e];
     for (int v = 0; v < nvec; v++) acc = cfma(y[v], V[(size_t)v * ldv + e], acc);
@@ -587,7 +596,9 @@ template <int VPW, int KE>
 __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
                                                 const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
                                                 double2 *__restrict__ partial, double2 *__restrict__ out,
-                                                unsigned *counter, int N, int NT) {
+                                                unsigned *counter, int N, int NT, double2 *__restrict__ out_host) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NVMAX = 4 * VPW, CH = 32 * KE;
   __shared__ double2 red[NVMAX + 1][4];
   __shared__ double2 sh[NVMAX];
@@ -685,6 +696,7 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
     for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
     if (lane == 0) {
       out[v] = sum;
+      if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
       if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
     }
   }
@@ -694,6 +706,8 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
 // y = s x, s read from the device (the normalisation of a new basis vector)
 __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__restrict__ sp, double2 *__restrict__ y,
                             size_t n) {
+  pdl_wait();
+  pdl_trigger();
   const double sc = sp->x;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
     y[e] = make_double2(x[e].x * sc, x[e].y * sc);
@@ -717,7 +731,10 @@ template <int NVMAX>
 __global__ void __launch_bounds__(256, 1) k_cgs_tma(const double2 *__restrict__ V, size_t ldv, int nv,
                                                     const double2 *__restrict__ hsrc, double2 *__restrict__ w,
                                                     int mode, double2 *__restrict__ partial, double2 *__restrict__ out,
-                                                    unsigned *counter, size_t ntot, int EPT, int NS) {
+                                                    unsigned *counter, size_t ntot, int EPT, int NS,
+                                                    double2 *__restrict__ out_host) {
+  pdl_wait();
+  pdl_trigger();
   constexpr int NH = NVMAX / 2;   // basis vectors per thread (v = 2 i + hf)
   extern __shared__ __align__(128) unsigned char smraw[];
   __shared__ double2 red[NVMAX + 1][8];
@@ -839,6 +856,7 @@ __global__ void __launch_bounds__(256, 1) k_cgs_tma(const double2 *__restrict__ 
     for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
     if (lane == 0) {
       out[v] = sum;
+      if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
       if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
     }
   }
@@ -847,7 +865,8 @@ __global__ void __launch_bounds__(256, 1) k_cgs_tma(const double2 *__restrict__ 
 
 template <int NVMAX>
 static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                                    double2 *partial, double2 *out, unsigned *counter, size_t ntot, cudaStream_t st) {
+                                    double2 *partial, double2 *out, unsigned *counter, size_t ntot, cudaStream_t st,
+                                    double2 *out_host) {
   // stage = (nv + 1) rows of CH = 128 EPT entries, about 48 KB; up to 4 stages in 200 KB
   const int nrow = nv + 1;
   int EPT = (int)((48 * 1024) / ((size_t)nrow * 128 * sizeof(double2)));
@@ -866,8 +885,8 @@ static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const 
   }
   const size_t nch = (ntot + 128 * EPT - 1) / (128 * EPT);
   const unsigned grid = (unsigned)std::min<size_t>(nch, 148);
-  k_cgs_tma<NVMAX><<<grid, 256, smem, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, EPT, NS);
-  cudaError_t e = cudaGetLastError();
+  cudaError_t e = launch_pdl(k_cgs_tma<NVMAX>, dim3(grid), dim3(256), smem, st, V, ldv, nv, hsrc, w, mode, partial, out,
+                             counter, ntot, EPT, NS, out_host);
   if (e != cudaSuccess) {
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, k_cgs_tma<NVMAX>);
@@ -878,24 +897,24 @@ static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const 
 }
 
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st) {
+                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
+                       double2 *out_host) {
   const size_t ntot = (size_t)(2 * N - 2) * NT;
   if (nv > 32) return cudaErrorInvalidValue;
   // default: register form below; SWR_CGS=tma selects the bulk-copy pipeline
   // form (measured slower at C5: 190 vs 147 ms per solve)
   const char *cgs_env = getenv("SWR_CGS");
   if (cgs_env && strcmp(cgs_env, "tma") == 0) {
-    if (nv <= 8) return launch_cgs_tma_t<8>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
-    if (nv <= 16) return launch_cgs_tma_t<16>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
-    return launch_cgs_tma_t<32>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st);
+    if (nv <= 8) return launch_cgs_tma_t<8>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
+    if (nv <= 16) return launch_cgs_tma_t<16>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
+    return launch_cgs_tma_t<32>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
   }
   // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
   // grid only depends on the sizes, so the reduction order is fixed
   auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
-  if (nv <= 8) k_cgs<2, 8><<<grid(256), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  else if (nv <= 16) k_cgs<4, 4><<<grid(128), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  else k_cgs<8, 2><<<grid(64), 128, 0, st>>>(V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT);
-  return cudaGetLastError();
+  if (nv <= 8) return launch_pdl(k_cgs<2, 8>, dim3(grid(256)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  if (nv <= 16) return launch_pdl(k_cgs<4, 4>, dim3(grid(128)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  return launch_pdl(k_cgs<8, 2>, dim3(grid(64)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
 }
 
 // ---------------------------------------------------------------------------
