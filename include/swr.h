@@ -99,6 +99,10 @@ typedef struct {
   const void *nccl_unique_id; /* 128-byte ncclUniqueId (world > 1) */
   void *cuda_stream;          /* cudaStream_t owned by the caller (NULL = default stream) */
   int32_t device;             /* CUDA device ordinal for this rank */
+  int32_t gs_passes;          /* GMRES Gram-Schmidt passes per Arnoldi step: 1 = classical
+                                 Gram-Schmidt, PETSc's default KSPGMRES orthogonalization
+                                 (the paper's solver library; reading A6);
+                                 2 = CGS2 (one reorthogonalization); 0 = 1 */
 } swr_config;
 
 typedef struct {

@@ -405,8 +405,9 @@ typedef ocplx (*or_dotfn)(const void *ctx, const ocplx *x, const ocplx *y);
 static double vnorm(or_dotfn dot, const void *dctx, const ocplx *x) { return sqrt(creal(dot(dctx, x, x))); }
 
 static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const void *dctx,
-                          const ocplx *b, ocplx *x, double tol, int32_t m, int32_t maxit,
+                          const ocplx *b, ocplx *x, double tol, int32_t m, int32_t maxit, int32_t npass,
                           int32_t *iters, double *hist, int32_t *converged) {
+  if (npass < 1) npass = 1;
   *iters = 0;
   *converged = 0;
   double bnorm = vnorm(dot, dctx, b);
@@ -446,7 +447,7 @@ static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const v
       total++;
       double wn0 = vnorm(dot, dctx, w);
       for (int32_t i = 0; i <= k; i++) Hm(i, k) = 0.0;
-      for (int pass = 0; pass < 2; pass++) {        /* CGS2 */
+      for (int pass = 0; pass < npass; pass++) {    /* classical Gram-Schmidt, npass times */
         for (int32_t i = 0; i <= k; i++) hc[i] = dot(dctx, V + (size_t)i * n, w);
         for (int32_t i = 0; i <= k; i++) {
           const ocplx *vi = V + (size_t)i * n;
@@ -515,12 +516,13 @@ static ocplx seq_dot(const void *c, const ocplx *x, const ocplx *y) {
   for (size_t i = 0; i < s->n; i++) acc += conj(x[i]) * y[i];
   return acc;
 }
-int32_t or_gmres_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x, double tol,
+int32_t or_gmres_dense(int32_t n, int32_t gs_passes, const ocplx *A, const ocplx *b, ocplx *x, double tol,
                        int32_t restart, int32_t maxit, int32_t *iters, double *hist) {
   dense_ctx d = {n, A};
   seq_ctx s = {(size_t)n};
   int32_t conv = 0;
-  int32_t st = gmres_core((size_t)n, dense_op, &d, seq_dot, &s, b, x, tol, restart, maxit, iters, hist, &conv);
+  int32_t st = gmres_core((size_t)n, dense_op, &d, seq_dot, &s, b, x, tol, restart, maxit, gs_passes, iters, hist,
+                          &conv);
   if (st) return st;
   return conv ? OR_OK : OR_NOT_CONVERGED;
 }
@@ -554,7 +556,7 @@ static int32_t apply_Pinv(drv_ctx *d, const ocplx *y, ocplx *x) {
   for (size_t i = 0; i < d->ng; i++) x[i] = 0.0;
   int32_t it = 0, conv = 0;
   int32_t st = gmres_core(d->ng, op_I_minus_L, d, drv_dot, d, y, x, d->P->tol_inner,
-                          d->P->restart, d->P->maxit_inner, &it, NULL, &conv);
+                          d->P->restart, d->P->maxit_inner, d->P->gs_passes, &it, NULL, &conv);
   d->inner_total += it;
   if (!conv) d->inner_fail = 1;
   return st;
@@ -633,7 +635,7 @@ int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
     if (st) goto out;
     st = or_build_L(P, 0, X);
     if (st) goto out;
-    st = gmres_core(ng, op_I_minus_L, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit,
+    st = gmres_core(ng, op_I_minus_L, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit, P->gs_passes,
                     &it, rep->history, &conv);
     if (st) goto out;
     rep->n_history = it;
@@ -645,7 +647,7 @@ int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
     if (st) goto out;
     st = apply_Pinv(&d, d.tmp2, rhs);               /* P^{-1} d */
     if (st && st != OR_INNER_NOT_CONVERGED) goto out;
-    st = gmres_core(ng, op_precond, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit,
+    st = gmres_core(ng, op_precond, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit, P->gs_passes,
                     &it, rep->history, &conv);
     if (st && st != OR_INNER_NOT_CONVERGED) goto out;
     rep->n_history = it;

@@ -44,6 +44,8 @@ typedef struct {
   double tol_inner; int32_t maxit_inner;         /* P^{-1} inner GMRES: 1e-12, 2000 */
   double tol_fp; int32_t maxit_fp;               /* NL inner fixed point: 1e-12, 50 */
   const ocplx *g0;            /* [(2N-2) N_T] initial interface vector, NULL = zero */
+  int32_t gs_passes;          /* GMRES Gram-Schmidt passes: 1 = classical (PETSc's default
+                                 KSPGMRES orthogonalization, reading A6), 2 = CGS2; 0 = 1 */
 } or_problem;
 
 typedef struct {
@@ -105,7 +107,7 @@ ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y);
 
 /* GMRES(m) with CGS2 on a dense n x n matrix (row-major); dot is plain
  * sequential.  Used by tests to pin the Krylov driver. */
-int32_t or_gmres_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x,
+int32_t or_gmres_dense(int32_t n, int32_t gs_passes, const ocplx *A, const ocplx *b, ocplx *x,
                        double tol, int32_t restart, int32_t maxit,
                        int32_t *iters, double *hist);
 

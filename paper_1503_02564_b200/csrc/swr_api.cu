@@ -127,6 +127,7 @@ struct swr_handle {
   // problem
   double a0, b0, T, dx, dt, lambda, robin_p, tol, tol_inner, tol_fp;
   int N, potential, transmission, algorithm, restart, maxit, maxit_inner, maxit_fp, n_terms;
+  int gs_passes = 1;   // Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
@@ -470,9 +471,14 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
     if (s) st = s;
     // scalars also go straight to the pinned mirror HP(par) (no copy node)
     CKS(cgs(h, V, k + 1, nullptr, w, swr::CGS_DOTS | swr::CGS_NORM, O1(par), HP(par)));              // h1, ||w||^2
-    CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_DOTS, O2(par), HP(par) + (m + 2)));   // w -= V h1; h2
-    CKS(cgs(h, V, k + 1, O2(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par),
-            HP(par) + 2 * (m + 2)));                                                                 // w -= V h2
+    if (h->gs_passes == 2) {
+      CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_DOTS, O2(par), HP(par) + (m + 2))); // w -= V h1; h2
+      CKS(cgs(h, V, k + 1, O2(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par),
+              HP(par) + 2 * (m + 2)));                                                               // w -= V h2
+    } else {
+      CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par),
+              HP(par) + 2 * (m + 2)));                                                               // w -= V h1
+    }
     CK(swr::launch_pdl(swr::k_scale_dev, dim3(grid_for(n)), dim3(256), 0, h->st, (const double2 *)w,
                        (const double2 *)(O3(par) + 1), V + (size_t)(k + 1) * ldv, n));
     h->n_launches++;
@@ -502,7 +508,7 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
       const double2 *hp = HP(k & 1);
       total++;
       const double wn0 = std::sqrt(hp[k + 1].x);
-      for (int i = 0; i <= k; i++) Hm(i, k) = c2(hp[i]) + c2(hp[(m + 2) + i]);
+      for (int i = 0; i <= k; i++) Hm(i, k) = h->gs_passes == 2 ? c2(hp[i]) + c2(hp[(m + 2) + i]) : c2(hp[i]);
       const double hk1 = std::sqrt(hp[2 * (m + 2)].x);
       const bool breakdown = hk1 <= 1e-14 * wn0;
       for (int i = 0; i < k; i++) {
@@ -773,6 +779,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->tol_inner = cfg->tol_inner > 0 ? cfg->tol_inner : 1e-12; h->tol_fp = cfg->tol_fp > 0 ? cfg->tol_fp : 1e-12;
   h->N = cfg->N; h->potential = cfg->potential; h->transmission = cfg->transmission; h->algorithm = cfg->algorithm;
   h->restart = cfg->restart > 0 ? cfg->restart : 30; h->maxit = cfg->maxit > 0 ? cfg->maxit : 2000;
+  h->gs_passes = cfg->gs_passes == 2 ? 2 : 1;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;

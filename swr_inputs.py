@@ -48,6 +48,7 @@ class Problem:
     tol_fp: float = 1e-12
     maxit_fp: int = 50
     g0_random: bool = False
+    gs_passes: int = 1          # Gram-Schmidt passes in GMRES: 1 = CGS (PETSc default, reading A6), 2 = CGS2
     seed: int = 7
     name: str = ""
 

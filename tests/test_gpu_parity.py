@@ -104,6 +104,19 @@ def test_new_algorithm_parity(oracle_mod, gpu, name, p):
     assert rel(g_.get_g().cpu().numpy(), ro["g"]) <= 1e-9
 
 
+@pytest.mark.parametrize("name,p", [CASES[2], CASES[4]], ids=[CASES[2][0], CASES[4][0]])
+def test_new_algorithm_parity_cgs2(oracle_mod, gpu, name, p):
+    """The CGS2 option (gs_passes = 2) on both sides: equal counts, u(T)."""
+    import dataclasses
+    p = dataclasses.replace(p, gs_passes=2)
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"]
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)

@@ -115,20 +115,40 @@ def test_thomas_vs_lapack(oracle_mod):
 
 
 # ---------------------------------------------------------------- GMRES driver
-def test_gmres_dense(oracle_mod):
+@pytest.mark.parametrize("gs", [1, 2])
+def test_gmres_dense(oracle_mod, gs):
     b = np.array([1, 2, 3], np.complex128)
-    st, x, it, _ = oracle_mod.gmres_dense(np.eye(3), b)
+    st, x, it, _ = oracle_mod.gmres_dense(np.eye(3), b, gs_passes=gs)
     assert st == 0 and it == 1 and np.allclose(x, b, rtol=1e-15)
-    st, x, it, _ = oracle_mod.gmres_dense(np.diag([1.0, 2, 3]), b)
+    st, x, it, _ = oracle_mod.gmres_dense(np.diag([1.0, 2, 3]), b, gs_passes=gs)
     assert st == 0 and np.allclose(x, 1, rtol=1e-10)
     rng = np.random.default_rng(2)
     A = np.eye(40) * 3 + (rng.standard_normal((40, 40)) + 1j * rng.standard_normal((40, 40))) / 8
     b = rng.standard_normal(40) + 1j * rng.standard_normal(40)
-    st, x, it, hist = oracle_mod.gmres_dense(A, b, tol=1e-12, restart=7)
+    st, x, it, hist = oracle_mod.gmres_dense(A, b, tol=1e-12, restart=7, gs_passes=gs)
     xs = np.linalg.solve(A, b)
     assert st == 0 and np.linalg.norm(x - xs) < 1e-10 * np.linalg.norm(xs)
     assert np.linalg.norm(b - A @ x) <= 1.01e-12 * np.linalg.norm(b) * 10
     assert len(hist) == it and hist[-1] <= 1e-12 * np.linalg.norm(b)
+
+
+@pytest.mark.parametrize("gs", [1, 2])
+def test_gmres_minimal_residual(oracle_mod, gs):
+    """Unrestarted GMRES minimises ||b - A x|| over the Krylov space: the
+    residual estimate after k steps equals min_y ||b - A K_k y|| with K_k an
+    orthonormal basis of span{b, Ab, ..., A^{k-1} b} from numpy's QR of the
+    explicit power basis (independent of the Arnoldi/Givens code)."""
+    rng = np.random.default_rng(11)
+    n = 12
+    A = np.eye(n) * 2 + (rng.standard_normal((n, n)) + 1j * rng.standard_normal((n, n))) / 6
+    b = rng.standard_normal(n) + 1j * rng.standard_normal(n)
+    st, x, it, hist = oracle_mod.gmres_dense(A, b, tol=1e-13, restart=n, maxit=n, gs_passes=gs)
+    for k in range(1, min(it, 8) + 1):
+        P = np.stack([np.linalg.matrix_power(A, i) @ b for i in range(k)], axis=1)
+        Q, _ = np.linalg.qr(P)
+        y, *_ = np.linalg.lstsq(A @ Q, b, rcond=None)
+        rmin = np.linalg.norm(b - A @ Q @ y)
+        assert abs(hist[k - 1] - rmin) <= 1e-9 * np.linalg.norm(b), (k, hist[k - 1], rmin)
 
 
 # ---------------------------------------------------------------- monodomain
