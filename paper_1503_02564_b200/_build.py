@@ -16,8 +16,21 @@ FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=s
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
 
 
+STAMP = os.path.join(PKG, "build", "flags.txt")
+
+
+def _extra_flags() -> list:
+    # SWR_TRACE_BUILD=1: compile the march phase-trace points in (tools/march_trace.sh)
+    return ["-DSWR_MARCH_TRACE=1"] if os.environ.get("SWR_TRACE_BUILD") == "1" else []
+
+
 def _stale() -> bool:
     if not os.path.exists(SO):
+        return True
+    try:
+        if open(STAMP).read() != " ".join(_extra_flags()):
+            return True
+    except OSError:
         return True
     t = os.path.getmtime(SO)
     deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "swr.h")]
@@ -32,7 +45,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
 
     def comp(src):
         obj = os.path.join(objdir, src.replace(".cu", ".o"))
-        cmd = [NVCC, *FLAGS, "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src), "-o", obj]
+        cmd = [NVCC, *FLAGS, *_extra_flags(), "-Xptxas", "-v" if verbose else "-O3", "-c", os.path.join(CSRC, src),
+               "-o", obj]
         r = subprocess.run(cmd, capture_output=True, text=True)
         if r.returncode != 0:
             raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
@@ -48,6 +62,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", tmp, *objs,
                            "-ldl"])
     os.replace(tmp, SO)
+    with open(STAMP, "w") as f:
+        f.write(" ".join(_extra_flags()))
     return SO
 
 

@@ -430,7 +430,10 @@ __device__ __forceinline__ void scan_tab(double2 (&B)[K], const ScanBuf<K> &sb, 
 // Optional per-phase clock64 trace (p.trace != NULL): thread 0 of each CTA
 // of the first cluster, step 200, 32 slots per CTA (clock64 is per SM: only
 // differences within one CTA are meaningful).
-#define SWR_TRACE_ON (p.trace && blockIdx.x < (unsigned)CS && t == 0 && n == 200)
+#ifndef SWR_MARCH_TRACE
+#define SWR_MARCH_TRACE 0   // build with SWR_TRACE_BUILD=1 to compile the trace points in
+#endif
+#define SWR_TRACE_ON (SWR_MARCH_TRACE && p.trace && blockIdx.x < (unsigned)CS && t == 0 && n == 200)
 #define SWR_TRACE(slot)                                                          \
   do {                                                                           \
     if (SWR_TRACE_ON) p.trace[blockIdx.x * 32 + (slot)] = clock64();             \

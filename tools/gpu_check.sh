@@ -1,4 +1,4 @@
 # GPU tests (short) + C5 timing + C5 per-CTA phase trace
 timeout 600 python -m pytest tests -q -m gpu -x 2>&1 | tail -4
 timeout 120 python tools/quick_c5.py C5 2>&1
-SWR_TRACE=1 timeout 120 python tools/march_scan.py 500 2>&1 | head -5
+bash tools/march_trace.sh 2>&1 | head -5
