@@ -858,6 +858,18 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       if ((s = dalloc(&h->tw, NF)) || (s = dalloc(&h->FX, (size_t)h->N * 4 * NF)) ||
           (s = dalloc(&h->Fx, (size_t)(2 * h->N - 2) * NF)) || (precond && (s = dalloc(&h->FX0, (size_t)h->N * 4 * NF))))
         return fail(s);
+      // set aside L2 for the transformed columns re-read by every (I - L) apply
+      // (device-wide limit, raised only; SWR_L2_PERSIST=0 leaves it alone)
+      const char *pe = getenv("SWR_L2_PERSIST");
+      if (!(pe && strcmp(pe, "0") == 0)) {
+        int maxp = 0;
+        size_t cur = 0;
+        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+        const size_t want = std::min((size_t)maxp, (size_t)h->N * 4 * NF * sizeof(double2));
+        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+        cudaGetLastError();
+      }
       swr::k_twiddles<<<(unsigned)((NF + 255) / 256), 256, 0, h->st>>>(h->tw, (int)NF);
       if (cudaGetLastError() != cudaSuccess) return fail(SWR_ERR_CUDA);
     }

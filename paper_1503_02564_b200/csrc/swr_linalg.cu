@@ -445,6 +445,19 @@ __global__ void __launch_bounds__(64) k_fft_conv_reg(const double2 *__restrict__
   }
 }
 
+// Bytes of L2 set aside for persisting accesses on the current device (0: none;
+// SWR_L2_PERSIST=0 disables the window).
+static size_t l2_persist_bytes() {
+  static size_t v = [] {
+    const char *e = getenv("SWR_L2_PERSIST");
+    if (e && strcmp(e, "0") == 0) return (size_t)0;
+    size_t lim = 0;
+    if (cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize) != cudaSuccess) return (size_t)0;
+    return lim;
+  }();
+  return v;
+}
+
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
                                 cudaStream_t st) {
   if (N < 2) return cudaSuccess;
@@ -452,7 +465,29 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   const size_t smem = (2 * 32 * 33) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_fft_conv_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
-  return launch_pdl(k_fft_conv_reg, dim3(N), dim3(64), smem, st, Fc, x, y, N, NT, tw);
+  // the transformed columns (N x 4 x NF complex, 32 MB at C5) are re-read by
+  // every apply: ask L2 to keep them (persisting window; the Krylov vectors
+  // streamed between applies are normal accesses and do not evict them)
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(N);
+  cfg.blockDim = dim3(64);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[1].val.accessPolicyWindow.base_ptr = const_cast<double2 *>(Fc);
+  at[1].val.accessPolicyWindow.num_bytes = (size_t)N * 4 * 1024 * sizeof(double2);
+  at[1].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = l2_persist_bytes() > 0 ? 2 : 1;
+  if (cfg.numAttrs == 2 && at[1].val.accessPolicyWindow.num_bytes > l2_persist_bytes()) {
+    at[1].val.accessPolicyWindow.hitRatio = (float)l2_persist_bytes() / (float)at[1].val.accessPolicyWindow.num_bytes;
+  }
+  return cudaLaunchKernelEx(&cfg, k_fft_conv_reg, Fc, x, y, N, NT, tw);
 }
 
 cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
