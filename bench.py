@@ -294,7 +294,7 @@ def main():
     bytes_apply = 16 * (2 * p.ng + (4 * (p.N - 2) + 2) * nf)
     if t_intf > 0:
         ach = bytes_apply / (t_intf / 1e3 / n_apply) / 1e9
-        line["roofline_interface"] = {"bound": "hbm", "kernel": "k_fft_fwd + k_fft_apply", "achieved": ach,
+        line["roofline_interface"] = {"bound": "hbm", "kernel": "k_fft_conv_reg (register four-step FFT convolution)", "achieved": ach,
                                       "peak": hbm, "unit": "GB/s", "frac": ach / hbm,
                                       "algorithmic": f"{bytes_apply} B per apply x {n_apply} applies"}
     # e2e: host buffers through the public API, H2D of the inputs and D2H of u(T)

@@ -387,7 +387,7 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const doub
 }
 }  // namespace fftr
 
-__global__ void __launch_bounds__(64) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
+__global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
                                                      double2 *__restrict__ y, int N, int NT,
                                                      const double2 *__restrict__ tw) {
   pdl_wait();
