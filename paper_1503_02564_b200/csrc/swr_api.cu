@@ -115,6 +115,7 @@ inline unsigned grid_for(size_t n, int bs = 256) {
 // have their own, so the outer speculation never races the inner solve).
 struct Krylov {
   double2 *V, *w;
+  double2 *w2;          // second work vector (fused normalisation path)
   double2 *dots;        // device [2][3(m+2)+8]: per-iteration scalars, double-buffered
   double2 *hp;          // pinned mirror, same layout
   double2 *ycoef;       // device [m]
@@ -423,6 +424,9 @@ int fetch(swr_handle *h, const double2 *dev, int n, double2 *host) {
 }
 
 typedef std::function<int(const double2 *, double2 *)> Op;
+// Fused form of a linear operator for GMRES: y = A(s x) and vcopy = s x,
+// s = sp->x on the device (the new basis vector is normalised on load).
+typedef std::function<int(const double2 *x, const double2 *sp, double2 *vcopy, double2 *y)> OpScaled;
 
 // GMRES(m) with CGS2 and complex Givens rotations, the same algorithm as the
 // oracle (reading A5/A6): stop at |gamma_{k+1}| <= tol ||b||, true residual
@@ -438,7 +442,8 @@ int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w
 }
 
 int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, Krylov &K,
-          int *iters, std::vector<double> *hist, int *converged, bool speculate = true) {
+          int *iters, std::vector<double> *hist, int *converged, bool speculate = true,
+          const OpScaled *AS = nullptr) {
   const size_t n = h->ng;
   const size_t ldv = n;
   double2 *V = K.V, *w = K.w;
@@ -464,9 +469,16 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
   // device work of Arnoldi step k: w = A v_k, CGS2, v_{k+1} = w/||w||,
   // scalars -> pinned buffer (k & 1), event.  No host dependency, so step
   // k+1 is issued before the host reads step k's scalars.
+  // fused path (AS): step k reads the raw vector left by step k-1 (or the
+  // restart) in buf[(k + 1) & 1] with its 1/norm at sptr(k), writes
+  // v_k = V_k = s x on the fly and w = A v_k into buf[k & 1]; no separate
+  // normalisation pass
+  double2 *buf[2] = {K.w, K.w2};
+  auto sptr = [&](int k) -> const double2 * { return k == 0 ? O3(1) + 1 : O3((k - 1) & 1) + 1; };
   auto issue = [&](int k) -> int {
     const int par = k & 1;
-    int s = A(V + (size_t)k * ldv, w);
+    if (AS) w = buf[k & 1];
+    int s = AS ? (*AS)(buf[(k + 1) & 1], sptr(k), V + (size_t)k * ldv, w) : A(V + (size_t)k * ldv, w);
     if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
     if (s) st = s;
     // scalars also go straight to the pinned mirror HP(par) (no copy node)
@@ -479,24 +491,30 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
       CKS(cgs(h, V, k + 1, O1(par), w, swr::CGS_AXPY | swr::CGS_NORM | swr::CGS_SCALE, O3(par),
               HP(par) + 2 * (m + 2)));                                                               // w -= V h1
     }
-    CK(swr::launch_pdl(swr::k_scale_dev, dim3(grid_for(n)), dim3(256), 0, h->st, (const double2 *)w,
-                       (const double2 *)(O3(par) + 1), V + (size_t)(k + 1) * ldv, n));
-    h->n_launches++;
+    if (!AS) {
+      CK(swr::launch_pdl(swr::k_scale_dev, dim3(grid_for(n)), dim3(256), 0, h->st, (const double2 *)w,
+                         (const double2 *)(O3(par) + 1), V + (size_t)(k + 1) * ldv, n));
+      h->n_launches++;
+    }
     CK(cudaEventRecord(K.ev[par], h->st));
     return SWR_OK;
   };
   while (!done) {
-    CKS(A(x, w));
-    CK(swr::launch_pdl(swr::k_sub, dim3(grid_for(n)), dim3(256), 0, h->st, b, (const double2 *)w, V, n));
+    CKS(A(x, K.w));
+    double2 *r0 = AS ? buf[1] : V;   // fused: raw r in buf[1], 1/beta at O3(1)+1 (sptr(0))
+    CK(swr::launch_pdl(swr::k_sub, dim3(grid_for(n)), dim3(256), 0, h->st, b, (const double2 *)K.w, r0, n));
     h->n_launches++;
-    CKS(cgs(h, nullptr, 0, nullptr, V, swr::CGS_NORM, O3(0)));
-    CKS(fetch(h, O3(0), 1, HP(0) + 2 * (m + 2)));
+    const int rp = AS ? 1 : 0;
+    CKS(cgs(h, nullptr, 0, nullptr, r0, swr::CGS_NORM | (AS ? swr::CGS_SCALE : 0), O3(rp)));
+    CKS(fetch(h, O3(rp), 1, HP(0) + 2 * (m + 2)));
     const double beta = std::sqrt(HP(0)[2 * (m + 2)].x);
     if (beta <= tol * bnorm) { *converged = 1; break; }
     if (total >= maxit) break;
-    CK(swr::launch_pdl(swr::k_axpby, dim3(grid_for(n)), dim3(256), 0, h->st, make_double2(0, 0), (const double2 *)V,
-                       make_double2(1.0 / beta, 0), V, n));
-    h->n_launches++;
+    if (!AS) {
+      CK(swr::launch_pdl(swr::k_axpby, dim3(grid_for(n)), dim3(256), 0, h->st, make_double2(0, 0), (const double2 *)V,
+                         make_double2(1.0 / beta, 0), V, n));
+      h->n_launches++;
+    }
     std::fill(gam.begin(), gam.end(), cplx(0));
     gam[0] = beta;
     int k, kend = 0;
@@ -583,6 +601,15 @@ int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
   return SWR_OK;
 }
 
+// Fused GMRES operator (register FFT path only): y = (I - L)(s x), vcopy = s x.
+int apply_I_minus_L_scaled(swr_handle *h, bool zero, const double2 *x, const double2 *sp, double2 *vcopy, double2 *y) {
+  CKS(record_pair(h, false, true));
+  CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy));
+  h->n_launches++;
+  CKS(record_pair(h, false, false));
+  return SWR_OK;
+}
+
 // transforms of the first columns, once per build
 int transform_columns(swr_handle *h, bool zero) {
   if (!h->log4) return SWR_OK;
@@ -595,8 +622,12 @@ int transform_columns(swr_handle *h, bool zero) {
 int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   CKS(fill_zero(h, x, h->ng));
   Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
+  OpScaled A0s = [h](const double2 *a, const double2 *sp, double2 *vc, double2 *b) {
+    return apply_I_minus_L_scaled(h, true, a, sp, vc, b);
+  };
   int it = 0, conv = 0;
-  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->kin, &it, nullptr, &conv);
+  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->kin, &it, nullptr, &conv, true,
+                h->N >= 2 && h->log4 && h->fft_reg ? &A0s : nullptr);
   h->inner_total += it;
   if (!conv) h->inner_fail = true;
   return s;
@@ -667,7 +698,7 @@ int alloc_krylov(Krylov &K, size_t mm, size_t ng) {
   const size_t stride = 3 * (mm + 1) + 8;
   int s;
   if ((s = dalloc(&K.V, mm * ng)) || (s = dalloc(&K.w, ng)) || (s = dalloc(&K.dots, 2 * stride)) ||
-      (s = dalloc(&K.ycoef, mm)))
+      (s = dalloc(&K.ycoef, mm)) || (s = dalloc(&K.w2, ng)))
     return s;
   if (cudaMallocHost((void **)&K.hp, 2 * stride * sizeof(double2)) != cudaSuccess) return SWR_ERR_OOM;
   for (int i = 0; i < 2; i++)
@@ -683,7 +714,7 @@ void free_all(swr_handle *h) {
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
-    for (void *p : {(void *)K->V, (void *)K->w, (void *)K->dots, (void *)K->ycoef})
+    for (void *p : {(void *)K->V, (void *)K->w, (void *)K->dots, (void *)K->ycoef, (void *)K->w2})
       if (p) cudaFree(p);
     if (K->hp) cudaFreeHost(K->hp);
     for (int i = 0; i < 2; i++)
@@ -958,7 +989,11 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
     if (h->algorithm == SWR_ALG_NEW) {
       if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
       Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
-      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv);
+      OpScaled As = [h](const double2 *a, const double2 *sp, double2 *vc, double2 *b) {
+        return apply_I_minus_L_scaled(h, false, a, sp, vc, b);
+      };
+      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, true,
+                 h->N >= 2 && h->log4 && h->fft_reg ? &As : nullptr);
     } else if (h->potential == SWR_POT_CUBIC) {
       // preconditioned fixed point (eq. chp2_algopd_NL, reading A9):
       // g <- g - P^{-1}(g - R_nl(g)), stop at ||g^{k+1} - g^k||_2 < tol (A5)

@@ -43,7 +43,7 @@ __global__ void k_fill(double2 *x, double2 v, size_t n);
 
 enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
-                                cudaStream_t st);
+                                cudaStream_t st, const double2 *xs = nullptr, double2 *xcopy = nullptr);
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
                        double2 *out_host = nullptr);

@@ -387,9 +387,13 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const doub
 }
 }  // namespace fftr
 
+// xs (optional, device): the input is s * x with s = xs->x, and xcopy
+// (optional) receives s * x — the GMRES step normalises its new basis vector
+// here instead of in a separate pass.
 __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
                                                      double2 *__restrict__ y, int N, int NT,
-                                                     const double2 *__restrict__ tw) {
+                                                     const double2 *__restrict__ tw, const double2 *__restrict__ xs,
+                                                     double2 *__restrict__ xcopy) {
   pdl_wait();
   pdl_trigger();
   constexpr int NF = 1024;
@@ -399,11 +403,13 @@ __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restric
   const int j = blockIdx.x + 1;
   const int sidx = q == 0 ? 2 * j - 3 : 2 * j - 2;
   const bool has_in = q == 0 ? j >= 2 : j <= N - 1;
+  const double sx = xs ? xs->x : 1.0;
   double2 v[32];
 #pragma unroll
   for (int n2 = 0; n2 < 32; n2++) {
     const int n = lane + 32 * n2;
-    v[n2] = (n2 < 16 && has_in && n < NT) ? x[(size_t)sidx * NT + n] : cz();
+    v[n2] = (n2 < 16 && has_in && n < NT) ? cscale(sx, x[(size_t)sidx * NT + n]) : cz();
+    if (xcopy && n2 < 16 && has_in && n < NT) xcopy[(size_t)sidx * NT + n] = v[n2];
   }
   fftr::fft1024<false, true>(v, T, tw, lane);
   // spectra of l_j (warp 0) and r_j (warp 1) in the own buffer (natural
@@ -439,7 +445,7 @@ __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restric
   for (int k1 = 0; k1 < 16; k1++) {
     const int n = lane + 32 * k1;
     if (n < NT) {
-      const double2 xv = xo[n], a = v[fftr::br5(k1)];
+      const double2 xv = cscale(sx, xo[n]), a = v[fftr::br5(k1)];
       yo[n] = make_double2(fma(-inv, a.x, xv.x), fma(-inv, a.y, xv.y));
     }
   }
@@ -459,7 +465,7 @@ static size_t l2_persist_bytes() {
 }
 
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
-                                cudaStream_t st) {
+                                cudaStream_t st, const double2 *xs, double2 *xcopy) {
   if (N < 2) return cudaSuccess;
   if (NT > 512) return cudaErrorInvalidValue;
   const size_t smem = (2 * 32 * 33) * sizeof(double2);
@@ -487,7 +493,7 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   if (cfg.numAttrs == 2 && at[1].val.accessPolicyWindow.num_bytes > l2_persist_bytes()) {
     at[1].val.accessPolicyWindow.hitRatio = (float)l2_persist_bytes() / (float)at[1].val.accessPolicyWindow.num_bytes;
   }
-  return cudaLaunchKernelEx(&cfg, k_fft_conv_reg, Fc, x, y, N, NT, tw);
+  return cudaLaunchKernelEx(&cfg, k_fft_conv_reg, Fc, x, y, N, NT, tw, xs, xcopy);
 }
 
 cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
