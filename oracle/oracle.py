@@ -37,7 +37,7 @@ class _Problem(C.Structure):
         ("tol", C.c_double), ("restart", C.c_int32), ("maxit", C.c_int32),
         ("tol_inner", C.c_double), ("maxit_inner", C.c_int32),
         ("tol_fp", C.c_double), ("maxit_fp", C.c_int32),
-        ("g0", C.c_void_p), ("gs_passes", C.c_int32),
+        ("g0", C.c_void_p), ("gs_passes", C.c_int32), ("krylov", C.c_int32),
     ]
 
 
@@ -72,10 +72,11 @@ def lib():
         _lib.or_dot.argtypes = [P, vp, vp]
         _lib.or_dot.restype = _Cplx
         _lib.or_gmres_dense.argtypes = [i32, i32, vp, vp, vp, C.c_double, i32, i32, vp, vp]
+        _lib.or_bicgstab_dense.argtypes = [i32, vp, vp, vp, C.c_double, i32, vp, vp]
         _lib.or_solve.argtypes = [P, vp, C.POINTER(_Report), vp]
         _lib.or_monodomain.argtypes = [P, vp, vp]
         for f in ("or_sizes", "or_thomas", "or_subdomain_matrix", "or_march", "or_apply_R",
-                  "or_build_L", "or_gmres_dense", "or_solve", "or_monodomain"):
+                  "or_build_L", "or_gmres_dense", "or_bicgstab_dense", "or_solve", "or_monodomain"):
             getattr(_lib, f).restype = i32
         _lib.or_coeffs.restype = None
         _lib.or_fem.restype = None
@@ -115,6 +116,7 @@ class Oracle:
         s.tol_fp, s.maxit_fp = p.tol_fp, p.maxit_fp
         s.g0 = _ptr(self.keep.get("g0"))
         s.gs_passes = p.gs_passes
+        s.krylov = p.krylov
         self.s = s
         self.L = lib()
         self.Nx, self.NT, self.Nj = p.Nx, p.NT, p.Nj
@@ -207,4 +209,14 @@ def gmres_dense(A, b, tol=1e-10, restart=30, maxit=2000, x0=None, gs_passes=1):
     it = np.zeros(1, np.int32)
     hist = np.zeros(maxit + 1)
     st = lib().or_gmres_dense(n, gs_passes, _ptr(A), _ptr(b), _ptr(x), tol, restart, maxit, _ptr(it), _ptr(hist))
+    return st, x, int(it[0]), hist[: int(it[0])]
+
+
+def bicgstab_dense(A, b, tol=1e-10, maxit=2000, x0=None):
+    A, b = _c128(A), _c128(b)
+    n = len(b)
+    x = np.zeros(n, np.complex128) if x0 is None else _c128(x0).copy()
+    it = np.zeros(1, np.int32)
+    hist = np.zeros(maxit + 1)
+    st = lib().or_bicgstab_dense(n, _ptr(A), _ptr(b), _ptr(x), tol, maxit, _ptr(it), _ptr(hist))
     return st, x, int(it[0]), hist[: int(it[0])]

@@ -498,6 +498,81 @@ out:
   return st;
 }
 
+/* BiCGStab (van der Vorst 1992; Saad, Iterative Methods, Alg. 7.7), the
+ * paper's other Krylov solver (reading A20).  From x0:
+ *   r = b - A x, rh = r, p = r;  per iteration: rho = <rh, r>,
+ *   p = r + (rho/rho_old)(alpha/omega)(p - omega v) (i > 1), v = A p,
+ *   alpha = rho / <rh, v>, s = r - alpha v  [stop if ||s|| <= tol ||b||:
+ *   x += alpha p], t = A s, omega = <t, s>/<t, t>, x += alpha p + omega s,
+ *   r = s - omega t  [stop if ||r|| <= tol ||b||].
+ * One iteration = two operator applications; hist[i] = the stopping norm.
+ * rho = 0, <rh, v> = 0 or omega = 0 before convergence: OR_BREAKDOWN. */
+static int32_t bicgstab_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const void *dctx,
+                             const ocplx *b, ocplx *x, double tol, int32_t maxit,
+                             int32_t *iters, double *hist, int32_t *converged) {
+  *iters = 0;
+  *converged = 0;
+  double bnorm = vnorm(dot, dctx, b);
+  if (bnorm == 0.0) {
+    for (size_t i = 0; i < n; i++) x[i] = 0.0;
+    *converged = 1;
+    return OR_OK;
+  }
+  ocplx *r = (ocplx *)calloc(n, sizeof(ocplx)), *rh = (ocplx *)calloc(n, sizeof(ocplx));
+  ocplx *p = (ocplx *)calloc(n, sizeof(ocplx)), *v = (ocplx *)calloc(n, sizeof(ocplx));
+  ocplx *sv = (ocplx *)calloc(n, sizeof(ocplx)), *t = (ocplx *)calloc(n, sizeof(ocplx));
+  int32_t st = OR_OK;
+  if (!r || !rh || !p || !v || !sv || !t) { st = OR_OOM; goto out; }
+  st = A(actx, x, r);
+  if (st && st != OR_INNER_NOT_CONVERGED) goto out;
+  for (size_t i = 0; i < n; i++) { r[i] = b[i] - r[i]; rh[i] = r[i]; }
+  if (vnorm(dot, dctx, r) <= tol * bnorm) { *converged = 1; goto out; }
+  ocplx rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  for (int32_t it = 0; it < maxit; it++) {
+    ocplx rho = dot(dctx, rh, r);
+    if (rho == 0.0) { st = OR_BREAKDOWN; break; }
+    if (it == 0) {
+      for (size_t i = 0; i < n; i++) p[i] = r[i];
+    } else {
+      ocplx beta = (rho / rho_old) * (alpha / omega);
+      for (size_t i = 0; i < n; i++) p[i] = r[i] + beta * (p[i] - omega * v[i]);
+    }
+    int32_t s = A(actx, p, v);
+    if (s && s != OR_INNER_NOT_CONVERGED) { st = s; break; }
+    if (s) st = s;
+    ocplx rv = dot(dctx, rh, v);
+    if (rv == 0.0) { st = OR_BREAKDOWN; break; }
+    alpha = rho / rv;
+    for (size_t i = 0; i < n; i++) sv[i] = r[i] - alpha * v[i];
+    *iters = it + 1;
+    double sn = vnorm(dot, dctx, sv);
+    if (sn <= tol * bnorm) {
+      for (size_t i = 0; i < n; i++) x[i] += alpha * p[i];
+      if (hist) hist[it] = sn;
+      *converged = 1;
+      break;
+    }
+    s = A(actx, sv, t);
+    if (s && s != OR_INNER_NOT_CONVERGED) { st = s; break; }
+    if (s) st = s;
+    ocplx ts = dot(dctx, t, sv), tt = dot(dctx, t, t);
+    if (tt == 0.0) { st = OR_BREAKDOWN; break; }
+    omega = ts / tt;
+    for (size_t i = 0; i < n; i++) { x[i] += alpha * p[i] + omega * sv[i]; r[i] = sv[i] - omega * t[i]; }
+    double rn = vnorm(dot, dctx, r);
+    if (hist) hist[it] = rn;
+    if (rn <= tol * bnorm) { *converged = 1; break; }
+    if (omega == 0.0) { st = OR_BREAKDOWN; break; }
+    rho_old = rho;
+  }
+out:
+  free(r); free(rh); free(p); free(v); free(sv); free(t);
+  return st;
+}
+
+int32_t or_bicgstab_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x, double tol, int32_t maxit,
+                          int32_t *iters, double *hist);
+
 /* Dense GMRES (test pin of the Krylov driver). */
 typedef struct { int32_t n; const ocplx *A; } dense_ctx;
 static int32_t dense_op(void *c, const ocplx *x, ocplx *y) {
@@ -516,6 +591,16 @@ static ocplx seq_dot(const void *c, const ocplx *x, const ocplx *y) {
   for (size_t i = 0; i < s->n; i++) acc += conj(x[i]) * y[i];
   return acc;
 }
+int32_t or_bicgstab_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x, double tol, int32_t maxit,
+                          int32_t *iters, double *hist) {
+  dense_ctx d = {n, A};
+  seq_ctx s = {(size_t)n};
+  int32_t conv = 0;
+  int32_t st = bicgstab_core((size_t)n, dense_op, &d, seq_dot, &s, b, x, tol, maxit, iters, hist, &conv);
+  if (st) return st;
+  return conv ? OR_OK : OR_NOT_CONVERGED;
+}
+
 int32_t or_gmres_dense(int32_t n, int32_t gs_passes, const ocplx *A, const ocplx *b, ocplx *x, double tol,
                        int32_t restart, int32_t maxit, int32_t *iters, double *hist) {
   dense_ctx d = {n, A};
@@ -552,14 +637,33 @@ static int32_t op_I_minus_L(void *c, const ocplx *x, ocplx *y) {
 
 /* x = P^{-1} y: GMRES on (I - L0) x = y from x = 0 (eq. Pxg, P:1054-1059,
  * reading A8). */
+/* The Krylov solver of the problem (reading A20): BiCGStab if requested,
+ * GMRES(restart) otherwise (also for the inner P^{-1} of a fixed point). */
+static int32_t krylov_solve(const or_problem *P, size_t n, or_opfn A, void *actx, const void *dctx,
+                            const ocplx *b, ocplx *x, double tol, int32_t maxit, int32_t *iters, double *hist,
+                            int32_t *conv) {
+  if (P->krylov == OR_KRY_BICGSTAB)
+    return bicgstab_core(n, A, actx, drv_dot, dctx, b, x, tol, maxit, iters, hist, conv);
+  return gmres_core(n, A, actx, drv_dot, dctx, b, x, tol, P->restart, maxit, P->gs_passes, iters, hist, conv);
+}
+
 static int32_t apply_Pinv(drv_ctx *d, const ocplx *y, ocplx *x) {
   for (size_t i = 0; i < d->ng; i++) x[i] = 0.0;
   int32_t it = 0, conv = 0;
-  int32_t st = gmres_core(d->ng, op_I_minus_L, d, drv_dot, d, y, x, d->P->tol_inner,
-                          d->P->restart, d->P->maxit_inner, d->P->gs_passes, &it, NULL, &conv);
+  int32_t st = krylov_solve(d->P, d->ng, op_I_minus_L, d, d, y, x, d->P->tol_inner, d->P->maxit_inner, &it, NULL,
+                            &conv);
   d->inner_total += it;
   if (!conv) d->inner_fail = 1;
   return st;
+}
+
+/* y = (I - L) x = x - R_0(x) matrix-free (Algorithm 2, reading A22). */
+static int32_t op_I_minus_L_mf(void *c, const ocplx *x, ocplx *y) {
+  drv_ctx *d = (drv_ctx *)c;
+  int32_t st = or_apply_R(d->P, x, 0, 0, d->tmp, &d->fp_max);
+  if (st) return st;
+  for (size_t i = 0; i < d->ng; i++) y[i] = x[i] - d->tmp[i];
+  return OR_OK;
 }
 
 /* y = P^{-1} (x - R_0(x)), R_0(x) = R(x; u0 = 0) with the true potential
@@ -635,24 +739,63 @@ int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
     if (st) goto out;
     st = or_build_L(P, 0, X);
     if (st) goto out;
-    st = gmres_core(ng, op_I_minus_L, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit, P->gs_passes,
-                    &it, rep->history, &conv);
-    if (st) goto out;
+    if (P->krylov == OR_KRY_FIXED_POINT) {
+      /* fixed point g^{k+1} = d + L g^k (reading A21) */
+      while (it < P->maxit) {
+        or_apply_L(P, X, g, d.tmp);
+        double diff2 = 0.0;
+        for (size_t i = 0; i < ng; i++) {
+          const ocplx gn = rhs[i] + d.tmp[i];
+          d.tmp2[i] = gn - g[i];
+          g[i] = gn;
+        }
+        diff2 = creal(or_dot(P, d.tmp2, d.tmp2));
+        if (rep->history) rep->history[it] = sqrt(diff2);
+        it++;
+        if (sqrt(diff2) < P->tol) { conv = 1; break; }
+      }
+    } else {
+      st = krylov_solve(P, ng, op_I_minus_L, &d, &d, rhs, g, P->tol, P->maxit, &it, rep->history, &conv);
+      if (st) goto out;
+    }
     rep->n_history = it;
-  } else if (linear) {
-    /* Preconditioned GMRES for V(t,x). */
+  } else if (P->algorithm == OR_ALG_CLASSICAL) {
+    if (P->krylov == OR_KRY_FIXED_POINT) {
+      /* Algorithm 1: g^{k+1} = R(g^k), stop ||g^{k+1} - g^k|| < tol */
+      while (it < P->maxit) {
+        int32_t s = or_apply_R(P, g, 1, 0, d.tmp, &d.fp_max);
+        if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
+        for (size_t i = 0; i < ng; i++) { d.tmp2[i] = d.tmp[i] - g[i]; g[i] = d.tmp[i]; }
+        double diff = sqrt(creal(or_dot(P, d.tmp2, d.tmp2)));
+        if (rep->history) rep->history[it] = diff;
+        it++;
+        if (diff < P->tol) { conv = 1; break; }
+      }
+      st = OR_OK;
+    } else {
+      /* Algorithm 2: Krylov on (I - L) g = d, (I - L) g = g - R_0(g)
+       * matrix-free, d = R(0; u0); linear potentials only */
+      if (!linear) { st = OR_UNSUPPORTED; goto out; }
+      st = or_apply_R(P, NULL, 1, 0, rhs, &d.fp_max);
+      if (st) goto out;
+      st = krylov_solve(P, ng, op_I_minus_L_mf, &d, &d, rhs, g, P->tol, P->maxit, &it, rep->history, &conv);
+      if (st && st != OR_INNER_NOT_CONVERGED) goto out;
+    }
+    rep->n_history = it;
+  } else if (linear && P->krylov != OR_KRY_FIXED_POINT) {
+    /* Preconditioned Krylov for V(t,x). */
     st = or_build_L(P, 1, X);                       /* L0: V = 0 probes */
     if (st) goto out;
     st = or_apply_R(P, NULL, 1, 0, d.tmp2, &d.fp_max); /* d = R(0; u0) */
     if (st) goto out;
     st = apply_Pinv(&d, d.tmp2, rhs);               /* P^{-1} d */
     if (st && st != OR_INNER_NOT_CONVERGED) goto out;
-    st = gmres_core(ng, op_precond, &d, drv_dot, &d, rhs, g, P->tol, P->restart, P->maxit, P->gs_passes,
-                    &it, rep->history, &conv);
+    st = krylov_solve(P, ng, op_precond, &d, &d, rhs, g, P->tol, P->maxit, &it, rep->history, &conv);
     if (st && st != OR_INNER_NOT_CONVERGED) goto out;
     rep->n_history = it;
   } else {
-    /* Preconditioned fixed point for f(u) (eq. chp2_algopd_NL, reading A9):
+    /* Preconditioned fixed point for f(u) (eq. chp2_algopd_NL, reading A9),
+     * also for V(t,x) when the fixed point is requested:
      * g^{k+1} = g^k - P^{-1}(g^k - R_nl(g^k)), stop ||g^{k+1}-g^k||_2 < tol. */
     st = or_build_L(P, 1, X);
     if (st) goto out;

@@ -25,7 +25,10 @@ enum { OR_OK = 0, OR_ERR_ARG = 1, OR_NOT_CONVERGED = 2, OR_ZERO_PIVOT = 3,
        OR_OOM = 9 };
 enum { OR_POT_ZERO = 0, OR_POT_VX = 1, OR_POT_VTX = 2, OR_POT_CUBIC = 3 };
 enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1 };
-enum { OR_ALG_NEW = 0, OR_ALG_PRECOND = 1 };
+enum { OR_ALG_NEW = 0, OR_ALG_PRECOND = 1, OR_ALG_CLASSICAL = 2 };
+/* Interface solver (reading A20/A21): GMRES(restart), BiCGStab, or the fixed
+ * point of the algorithm (NEW: g <- d + L g; CLASSICAL: g <- R(g), Algorithm 1). */
+enum { OR_KRY_GMRES = 0, OR_KRY_BICGSTAB = 1, OR_KRY_FIXED_POINT = 2 };
 
 typedef struct {
   double a0, b0, T, dx, dt;   /* domain (a0,b0), final time, mesh, time step */
@@ -46,6 +49,8 @@ typedef struct {
   const ocplx *g0;            /* [(2N-2) N_T] initial interface vector, NULL = zero */
   int32_t gs_passes;          /* GMRES Gram-Schmidt passes: 1 = classical (PETSc's default
                                  KSPGMRES orthogonalization, reading A6), 2 = CGS2; 0 = 1 */
+  int32_t krylov;             /* OR_KRY_*: interface solver (outer, and the inner P^{-1} solve
+                                 for GMRES / BiCGStab; P^{-1} is never a fixed point) */
 } or_problem;
 
 typedef struct {
@@ -104,6 +109,10 @@ void or_apply_L(const or_problem *P, const ocplx *X, const ocplx *g, ocplx *Lg);
 /* Order-fixed inner product over the interface vector: partial per
  * subdomain (its own slots, sequential), partials summed in j order. */
 ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y);
+
+/* BiCGStab on a dense n x n matrix (row-major), same driver as or_solve. */
+int32_t or_bicgstab_dense(int32_t n, const ocplx *A, const ocplx *b, ocplx *x, double tol, int32_t maxit,
+                          int32_t *iters, double *hist);
 
 /* GMRES(m) with CGS2 on a dense n x n matrix (row-major); dot is plain
  * sequential.  Used by tests to pin the Krylov driver. */

@@ -20,7 +20,8 @@ import numpy as np
 # oracle/swr_oracle.h); they are the ABI's argument codes, not arithmetic.
 POT_ZERO, POT_VX, POT_VTX, POT_CUBIC = 0, 1, 2, 3
 TC_ROBIN, TC_S02 = 0, 1
-ALG_NEW, ALG_PRECOND = 0, 1
+ALG_NEW, ALG_PRECOND, ALG_CLASSICAL = 0, 1, 2
+KRY_GMRES, KRY_BICGSTAB, KRY_FIXED_POINT = 0, 1, 2
 
 
 @dataclasses.dataclass
@@ -49,6 +50,7 @@ class Problem:
     maxit_fp: int = 50
     g0_random: bool = False
     gs_passes: int = 1          # Gram-Schmidt passes in GMRES: 1 = CGS (PETSc default, reading A6), 2 = CGS2
+    krylov: int = KRY_GMRES     # interface solver: GMRES, BiCGStab or the algorithm's fixed point (A20/A21)
     seed: int = 7
     name: str = ""
 

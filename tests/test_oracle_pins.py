@@ -132,6 +132,28 @@ def test_gmres_dense(oracle_mod, gs):
     assert len(hist) == it and hist[-1] <= 1e-12 * np.linalg.norm(b)
 
 
+def test_bicgstab_dense(oracle_mod):
+    """BiCGStab converges to numpy's solution.  Finite termination: its
+    residual is Q_k(A) P_k(A) r0 with P_k the BiCG polynomial, which
+    annihilates r0 once k reaches the number of distinct eigenvalues of a
+    normal A: one iteration (at the half step) for A = 2I, two for two
+    distinct eigenvalues."""
+    rng = np.random.default_rng(4)
+    A = np.eye(30) * 3 + (rng.standard_normal((30, 30)) + 1j * rng.standard_normal((30, 30))) / 6
+    b = rng.standard_normal(30) + 1j * rng.standard_normal(30)
+    st, x, it, hist = oracle_mod.bicgstab_dense(A, b, tol=1e-12)
+    xs = np.linalg.solve(A, b)
+    assert st == 0 and np.linalg.norm(x - xs) < 1e-10 * np.linalg.norm(xs)
+    assert np.linalg.norm(b - A @ x) <= 1e-11 * np.linalg.norm(b)
+    assert len(hist) == it and hist[-1] <= 1e-12 * np.linalg.norm(b)
+    d = np.array([1.0] * 5 + [2.0] * 5)
+    b2 = rng.standard_normal(10) + 1j * rng.standard_normal(10)
+    st, x, it, _ = oracle_mod.bicgstab_dense(np.diag(d), b2, tol=1e-13)
+    assert st == 0 and it == 2 and np.allclose(x, b2 / d, rtol=1e-12)
+    st, x, it, _ = oracle_mod.bicgstab_dense(2 * np.eye(10), b2, tol=1e-13)
+    assert st == 0 and it == 1 and np.allclose(x, b2 / 2, rtol=1e-14)
+
+
 @pytest.mark.parametrize("gs", [1, 2])
 def test_gmres_minimal_residual(oracle_mod, gs):
     """Unrestarted GMRES minimises ||b - A x|| over the Krylov space: the
@@ -308,6 +330,35 @@ def test_new_algorithm_equals_monodomain(oracle_mod, tc, pot):
     st, um, _ = o.monodomain()
     assert r["status"] == 0 and r["converged"]
     assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+@pytest.mark.parametrize("alg,kry", [(si.ALG_NEW, si.KRY_BICGSTAB), (si.ALG_NEW, si.KRY_FIXED_POINT),
+                                     (si.ALG_CLASSICAL, si.KRY_FIXED_POINT), (si.ALG_CLASSICAL, si.KRY_GMRES),
+                                     (si.ALG_CLASSICAL, si.KRY_BICGSTAB), (si.ALG_PRECOND, si.KRY_BICGSTAB)])
+def test_solver_variants_equal_monodomain(oracle_mod, alg, kry):
+    """Every interface solver of the paper (Algorithms 1-3 with fixed point,
+    GMRES or BiCGStab) converges to the single-domain
+    solution (V(x) for NEW/CLASSICAL, V(t,x) for PRECOND)."""
+    pot = si.POT_VTX if alg == si.ALG_PRECOND else si.POT_VX
+    p = si.config("C1", transmission=si.TC_S02, potential=pot, N=4, algorithm=alg, krylov=kry)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    r = o.solve()
+    st, um, _ = o.monodomain()
+    assert r["status"] == 0 and r["converged"], r["status"]
+    assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+def test_fixed_point_iterations_agree(oracle_mod):
+    """The fixed points of Algorithm 1 (g <- R(g)) and of the new algorithm
+    (g <- d + L g) are the same iteration in exact arithmetic (R(g) = L g + d,
+    Props 1-4): equal iteration counts and histories to rounding."""
+    ps = [si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=4, algorithm=a,
+                    krylov=si.KRY_FIXED_POINT) for a in (si.ALG_NEW, si.ALG_CLASSICAL)]
+    rs = [oracle_mod.Oracle(q, si.inputs(q)).solve() for q in ps]
+    assert rs[0]["iterations"] == rs[1]["iterations"]
+    h0, h1 = rs[0]["history"], rs[1]["history"]
+    # the two evaluations of R differ by rounding only: |diff| at the scale of the first step
+    assert np.abs(h0 - h1).max() <= 1e-12 * h0[0]
 
 
 def test_precond_exact_for_zero_potential(oracle_mod):
