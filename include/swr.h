@@ -72,7 +72,17 @@ enum swr_potential {
 };
 
 enum swr_transmission { SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1 };
-enum swr_algorithm { SWR_ALG_NEW = 0, SWR_ALG_PRECOND = 1 };
+enum swr_algorithm {
+  SWR_ALG_NEW = 0,       /* Algorithm 3 */
+  SWR_ALG_PRECOND = 1,   /* preconditioned algorithms */
+  SWR_ALG_CLASSICAL = 2  /* Algorithm 1 (fixed point g <- R(g)) or
+                            Algorithm 2 (Krylov on g - R_0(g) = R(0; u0)) */
+};
+/* Interface solver (readings A20, A21).  GMRES / BiCGStab also serve the
+ * inner P^{-1} solve of SWR_ALG_PRECOND (GMRES when the outer solver is the
+ * fixed point); the fixed point is g <- d + L g for NEW, g <- R(g) for
+ * CLASSICAL and g <- g - P^{-1}(g - R(g)) for PRECOND. */
+enum swr_krylov { SWR_KRY_GMRES = 0, SWR_KRY_BICGSTAB = 1, SWR_KRY_FIXED_POINT = 2 };
 
 typedef struct {
   double a0, b0, T, dx, dt;   /* domain, final time, mesh size, time step */
@@ -103,6 +113,7 @@ typedef struct {
                                  Gram-Schmidt, PETSc's default KSPGMRES orthogonalization
                                  (the paper's solver library; reading A6);
                                  2 = CGS2 (one reorthogonalization); 0 = 1 */
+  int32_t krylov;             /* swr_krylov: interface solver (0 = GMRES) */
 } swr_config;
 
 typedef struct {
@@ -124,7 +135,8 @@ typedef struct {
 /* Validate the configuration, copy the inputs to the GPU, assemble and
  * factor the subdomain matrices (A - B), eq. (9).
  * Returns SWR_ERR_INVALID_ARG for: N not dividing N_x, world > N, Robin with
- * p <= 0, NEW with a time-dependent or nonlinear potential, NULL u0.
+ * p <= 0, NEW with a time-dependent or nonlinear potential, CLASSICAL with a
+ * Krylov solver and f(u) (R is not affine), NULL u0.
  * *out receives the handle (NULL on failure).  Collective. */
 int swr_setup(const swr_config *cfg, swr_handle **out);
 

@@ -129,6 +129,7 @@ struct swr_handle {
   double a0, b0, T, dx, dt, lambda, robin_p, tol, tol_inner, tol_fp;
   int N, potential, transmission, algorithm, restart, maxit, maxit_inner, maxit_fp, n_terms;
   int gs_passes = 1;   // Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
+  int krylov = 0;      // swr_krylov
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
@@ -619,6 +620,91 @@ int transform_columns(swr_handle *h, bool zero) {
 }
 
 // x = P^{-1} y: GMRES on (I - L0) x = y from x = 0 (eq. Pxg, reading A8)
+// BiCGStab in the oracle's order (van der Vorst; reading A20): r, rh, p, v,
+// s, t live in basis slots 0..5 of K; the scalars come back to the host at
+// each half step (the method's own decisions: alpha, omega, the stops).
+int bicgstab(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int maxit, Krylov &K, int *iters,
+             std::vector<double> *hist, int *converged) {
+  const size_t n = h->ng;
+  double2 *r = K.V, *rh = K.V + n, *p = K.V + 2 * n, *v = K.V + 3 * n, *sv = K.V + 4 * n, *t = K.V + 5 * n;
+  double2 *dv = K.dots, *hp = K.hp;
+  const dim3 g(grid_for(n)), bl(256);
+  *iters = 0;
+  *converged = 0;
+  CKS(cgs(h, nullptr, 0, nullptr, const_cast<double2 *>(b), swr::CGS_NORM, dv));
+  CKS(fetch(h, dv, 1, hp));
+  const double bnorm = std::sqrt(hp[0].x);
+  if (bnorm == 0.0) {
+    CKS(fill_zero(h, x, n));
+    *converged = 1;
+    return SWR_OK;
+  }
+  int st = SWR_OK;
+  auto op = [&](const double2 *in, double2 *out) -> int {
+    int s = A(in, out);
+    if (s && s != SWR_ERR_INNER_NOT_CONVERGED) return s;
+    if (s) st = s;
+    return SWR_OK;
+  };
+  CKS(op(x, r));
+  CK(swr::launch_pdl(swr::k_lin2, g, bl, 0, h->st, r, make_double2(1, 0), b, make_double2(-1, 0), (const double2 *)r, n));
+  CK(cudaMemcpyAsync(rh, r, n * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  h->n_launches++;
+  // rho = <rh, r>, ||r||^2
+  CKS(cgs(h, rh, 1, nullptr, r, swr::CGS_DOTS | swr::CGS_NORM, dv));
+  CKS(fetch(h, dv, 2, hp));
+  if (std::sqrt(hp[1].x) <= tol * bnorm) { *converged = 1; return st; }
+  cplx rho = c2(hp[0]), rho_old = 1.0, alpha = 1.0, omega = 1.0;
+  for (int it = 0; it < maxit; it++) {
+    if (rho == 0.0) return SWR_ERR_BREAKDOWN;
+    if (it == 0) {
+      CK(cudaMemcpyAsync(p, r, n * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+    } else {
+      const cplx beta = (rho / rho_old) * (alpha / omega);
+      CK(swr::launch_pdl(swr::k_bicg_p, g, bl, 0, h->st, p, (const double2 *)r, (const double2 *)v, d2(beta), d2(omega), n));
+      h->n_launches++;
+    }
+    CKS(op(p, v));
+    CKS(cgs(h, rh, 1, nullptr, v, swr::CGS_DOTS, dv));                 // <rh, v>
+    CKS(fetch(h, dv, 1, hp));
+    const cplx rv = c2(hp[0]);
+    if (rv == 0.0) return SWR_ERR_BREAKDOWN;
+    alpha = rho / rv;
+    CK(swr::launch_pdl(swr::k_lin2, g, bl, 0, h->st, sv, make_double2(1, 0), (const double2 *)r, d2(-alpha),
+                       (const double2 *)v, n));                             // s = r - alpha v
+    h->n_launches++;
+    CKS(cgs(h, nullptr, 0, nullptr, sv, swr::CGS_NORM, dv));
+    CKS(fetch(h, dv, 1, hp));
+    *iters = it + 1;
+    const double sn = std::sqrt(hp[0].x);
+    if (sn <= tol * bnorm) {
+      CK(swr::launch_pdl(swr::k_axpby, g, bl, 0, h->st, d2(alpha), (const double2 *)p, make_double2(1, 0), x, n));
+      h->n_launches++;
+      if (hist) hist->push_back(sn);
+      *converged = 1;
+      break;
+    }
+    CKS(op(sv, t));
+    CKS(cgs(h, sv, 2, nullptr, t, swr::CGS_DOTS, dv));                 // <s, t>, <t, t> (s, t adjacent)
+    CKS(fetch(h, dv, 2, hp));
+    const cplx ts = std::conj(c2(hp[0])), tt = c2(hp[1]);
+    if (tt == 0.0) return SWR_ERR_BREAKDOWN;
+    omega = ts / tt;
+    CK(swr::launch_pdl(swr::k_bicg_xr, g, bl, 0, h->st, x, r, (const double2 *)p, (const double2 *)sv,
+                       (const double2 *)t, d2(alpha), d2(omega), n));
+    h->n_launches++;
+    rho_old = rho;
+    CKS(cgs(h, rh, 1, nullptr, r, swr::CGS_DOTS | swr::CGS_NORM, dv));  // next rho, ||r||^2
+    CKS(fetch(h, dv, 2, hp));
+    const double rn = std::sqrt(hp[1].x);
+    if (hist) hist->push_back(rn);
+    if (rn <= tol * bnorm) { *converged = 1; break; }
+    if (omega == 0.0) return SWR_ERR_BREAKDOWN;
+    rho = c2(hp[0]);
+  }
+  return st;
+}
+
 int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   CKS(fill_zero(h, x, h->ng));
   Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
@@ -626,8 +712,10 @@ int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
     return apply_I_minus_L_scaled(h, true, a, sp, vc, b);
   };
   int it = 0, conv = 0;
-  int s = gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->kin, &it, nullptr, &conv, true,
-                h->N >= 2 && h->log4 && h->fft_reg ? &A0s : nullptr);
+  int s = h->krylov == SWR_KRY_BICGSTAB
+              ? bicgstab(h, A0, y, x, h->tol_inner, h->maxit_inner, h->kin, &it, nullptr, &conv)
+              : gmres(h, A0, y, x, h->tol_inner, h->restart, h->maxit_inner, h->kin, &it, nullptr, &conv, true,
+                      h->N >= 2 && h->log4 && h->fft_reg ? &A0s : nullptr);
   h->inner_total += it;
   if (!conv) h->inner_fail = true;
   return s;
@@ -795,6 +883,11 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     g_detail = "NEW needs a time-independent linear potential (P:1015)";
     return SWR_ERR_INVALID_ARG;
   }
+  if (cfg->krylov < 0 || cfg->krylov > 2 || cfg->algorithm < 0 || cfg->algorithm > 2) return SWR_ERR_INVALID_ARG;
+  if (cfg->algorithm == SWR_ALG_CLASSICAL && cfg->potential == SWR_POT_CUBIC && cfg->krylov != SWR_KRY_FIXED_POINT) {
+    g_detail = "the classical Krylov algorithm needs an affine R (linear potential, P:734)";
+    return SWR_ERR_INVALID_ARG;
+  }
   if (cfg->potential == SWR_POT_VX && !cfg->V_x) return SWR_ERR_INVALID_ARG;
   if (cfg->potential == SWR_POT_VTX_SEPARABLE && (cfg->n_terms < 1 || !cfg->tau || !cfg->xi)) {
     g_detail = "V(t,x) needs n_terms >= 1, tau and xi";
@@ -811,6 +904,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->N = cfg->N; h->potential = cfg->potential; h->transmission = cfg->transmission; h->algorithm = cfg->algorithm;
   h->restart = cfg->restart > 0 ? cfg->restart : 30; h->maxit = cfg->maxit > 0 ? cfg->maxit : 2000;
   h->gs_passes = cfg->gs_passes == 2 ? 2 : 1;
+  h->krylov = cfg->krylov;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;
@@ -870,7 +964,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   }
   if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
   if (ng) {
-    const size_t mm = h->restart + 1;
+    const size_t mm = std::max(h->restart + 1, 6);   // BiCGStab uses 6 of the basis slots
     if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
         (s = alloc_krylov(h->kout, mm, ng)) || (s = dalloc(&h->tmp, ng)) ||
         (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, (mm + 2) * 148 * 4)) ||
@@ -953,6 +1047,11 @@ int swr_build_interface_operator(swr_handle *h) {
       CKS(build_probes(h, false, h->X, h->d));    // 3 RHS per interior subdomain
       CKS(transform_columns(h, false));
       h->have_L = h->have_d = true;
+    } else if (h->algorithm == SWR_ALG_CLASSICAL) {
+      if (h->krylov != SWR_KRY_FIXED_POINT) {      // Algorithm 2: d = R(0; u0)
+        CKS(sweep_R(h, nullptr, true, false, h->d, nullptr));
+        h->have_d = true;
+      }
     } else {
       CKS(build_probes(h, true, h->X0, nullptr));  // L0: 2 RHS per subdomain
       CKS(transform_columns(h, true));
@@ -986,36 +1085,88 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
     if (h->g0) CK(cudaMemcpyAsync(h->g, h->g0, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
     else CKS(fill_zero(h, h->g, h->ng));
     int it = 0, conv = 0;
+    double2 *hp = h->hpin;
+    // fixed point driver: g <- next(g), stop at ||g^{k+1} - g^k||_2 < tol (A5, A21);
+    // next() leaves the increment g^{k+1} - g^k in h->tmp2
+    auto fixed_point = [&](const std::function<int()> &next) -> int {
+      while (it < h->maxit) {
+        const int s2 = next();
+        if (s2 && s2 != SWR_ERR_INNER_NOT_CONVERGED) return s2;
+        CKS(cgs(h, nullptr, 0, nullptr, h->tmp2, swr::CGS_NORM, h->kout.dots));
+        CKS(fetch(h, h->kout.dots, 1, hp));
+        const double diff = std::sqrt(hp[0].x);
+        h->hist.push_back(diff);
+        it++;
+        if (diff < h->tol) { conv = 1; break; }
+      }
+      return SWR_OK;
+    };
+    const dim3 gg(grid_for(h->ng)), bb(256);
     if (h->algorithm == SWR_ALG_NEW) {
       if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
       Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
       OpScaled As = [h](const double2 *a, const double2 *sp, double2 *vc, double2 *b) {
         return apply_I_minus_L_scaled(h, false, a, sp, vc, b);
       };
-      st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, true,
-                 h->N >= 2 && h->log4 && h->fft_reg ? &As : nullptr);
-    } else if (h->potential == SWR_POT_CUBIC) {
+      if (h->krylov == SWR_KRY_FIXED_POINT) {
+        // g <- d + L g = g + (d - (I - L) g)
+        st = fixed_point([&]() -> int {
+          CKS(apply_I_minus_L(h, false, h->g, h->tmp));
+          CK(swr::launch_pdl(swr::k_lin2, gg, bb, 0, h->st, h->tmp2, make_double2(1, 0), (const double2 *)h->d,
+                             make_double2(-1, 0), (const double2 *)h->tmp, h->ng));
+          CK(swr::launch_pdl(swr::k_axpby, gg, bb, 0, h->st, make_double2(1, 0), (const double2 *)h->tmp2,
+                             make_double2(1, 0), h->g, h->ng));
+          h->n_launches += 2;
+          return SWR_OK;
+        });
+      } else if (h->krylov == SWR_KRY_BICGSTAB) {
+        st = bicgstab(h, A, h->d, h->g, h->tol, h->maxit, h->kout, &it, &h->hist, &conv);
+      } else {
+        st = gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, true,
+                   h->N >= 2 && h->log4 && h->fft_reg ? &As : nullptr);
+      }
+    } else if (h->algorithm == SWR_ALG_CLASSICAL) {
+      if (h->krylov == SWR_KRY_FIXED_POINT) {
+        // Algorithm 1: g <- R(g) (with u0; R_nl for f(u))
+        st = fixed_point([&]() -> int {
+          CKS(sweep_R(h, h->g, true, false, h->tmp, nullptr));
+          swr::k_sub<<<gg, bb, 0, h->st>>>(h->tmp, h->g, h->tmp2, h->ng);
+          CK(cudaGetLastError());
+          CK(cudaMemcpyAsync(h->g, h->tmp, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+          h->n_launches++;
+          return SWR_OK;
+        });
+      } else {
+        // Algorithm 2: Krylov on (I - L) g = d, (I - L) g = g - R_0(g) matrix-free
+        if (!h->have_d) CKS(swr_build_interface_operator(h));
+        Op A = [h](const double2 *a, double2 *b) -> int {
+          CKS(sweep_R(h, a, false, false, h->tmp, nullptr));
+          swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(a, h->tmp, b, h->ng);
+          CK(cudaGetLastError());
+          h->n_launches++;
+          return SWR_OK;
+        };
+        st = h->krylov == SWR_KRY_BICGSTAB
+                 ? bicgstab(h, A, h->d, h->g, h->tol, h->maxit, h->kout, &it, &h->hist, &conv)
+                 : gmres(h, A, h->d, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, true);
+      }
+    } else if (h->potential == SWR_POT_CUBIC || h->krylov == SWR_KRY_FIXED_POINT) {
       // preconditioned fixed point (eq. chp2_algopd_NL, reading A9):
-      // g <- g - P^{-1}(g - R_nl(g)), stop at ||g^{k+1} - g^k||_2 < tol (A5)
+      // g <- g - P^{-1}(g - R(g)), stop at ||g^{k+1} - g^k||_2 < tol (A5)
       if (!h->have_L0) CKS(swr_build_interface_operator(h));
-      double2 *hp = h->hpin;
-      while (it < h->maxit) {
+      st = fixed_point([&]() -> int {
         CKS(sweep_R(h, h->g, true, false, h->tmp, nullptr));
-        swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(h->g, h->tmp, h->tmp2, h->ng);
+        swr::k_sub<<<gg, bb, 0, h->st>>>(h->g, h->tmp, h->tmp2, h->ng);
         CK(cudaGetLastError());
         const int s2 = apply_Pinv(h, h->tmp2, h->tmp);
         if (s2 && s2 != SWR_ERR_INNER_NOT_CONVERGED) return s2;
-        swr::k_axpby<<<grid_for(h->ng), 256, 0, h->st>>>(make_double2(-1.0, 0.0), h->tmp, make_double2(1.0, 0.0),
-                                                        h->g, h->ng);
+        swr::k_axpby<<<gg, bb, 0, h->st>>>(make_double2(-1.0, 0.0), h->tmp, make_double2(1.0, 0.0), h->g, h->ng);
         CK(cudaGetLastError());
-        CKS(cgs(h, nullptr, 0, nullptr, h->tmp, swr::CGS_NORM, h->kout.dots));
-        CKS(fetch(h, h->kout.dots, 1, hp));
-        const double diff = std::sqrt(hp[0].x);
-        h->hist.push_back(diff);
-        it++;
+        // increment g^{k+1} - g^k = -P^{-1}(...): same norm as h->tmp
+        CK(cudaMemcpyAsync(h->tmp2, h->tmp, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
         h->n_launches += 2;
-        if (diff < h->tol) { conv = 1; break; }
-      }
+        return s2;
+      });
     } else {
       if (!h->have_L0 || !h->have_d) CKS(swr_build_interface_operator(h));
       CKS(apply_Pinv(h, h->d, h->rhs));
@@ -1025,9 +1176,11 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         CK(cudaGetLastError());
         return apply_Pinv(h, h->tmp2, b);
       };
-      // the operator runs an inner GMRES (host round trips): no speculation,
-      // which would also run inner solves the oracle does not
-      st = gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, false);
+      // the operator runs an inner Krylov solve (host round trips): no
+      // speculation, which would also run inner solves the oracle does not
+      st = h->krylov == SWR_KRY_BICGSTAB
+               ? bicgstab(h, A, h->rhs, h->g, h->tol, h->maxit, h->kout, &it, &h->hist, &conv)
+               : gmres(h, A, h->rhs, h->g, h->tol, h->restart, h->maxit, h->kout, &it, &h->hist, &conv, false);
     }
     if (st && st != SWR_ERR_INNER_NOT_CONVERGED) return st;
     h->iterations = it;

@@ -599,6 +599,35 @@ __global__ void k_axpby(double2 a, const double2 *__restrict__ x, double2 b, dou
     y[e] = cfma(a, x[e], cmul(b, y[e]));
 }
 
+// z = a x + b y (z may alias x or y)
+__global__ void k_lin2(double2 *z, double2 a, const double2 *x, double2 b, const double2 *y, size_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    z[e] = cfma(a, x[e], cmul(b, y[e]));
+}
+
+// BiCGStab updates in the oracle's order (reading A20):
+//   p = r + beta (p - omega v)
+__global__ void k_bicg_p(double2 *__restrict__ p, const double2 *__restrict__ r, const double2 *__restrict__ v,
+                         double2 beta, double2 omega, size_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    p[e] = cadd(r[e], cmul(beta, csub(p[e], cmul(omega, v[e]))));
+}
+//   x += alpha p + omega s;  r = s - omega t
+__global__ void k_bicg_xr(double2 *__restrict__ x, double2 *__restrict__ r, const double2 *__restrict__ p,
+                          const double2 *__restrict__ sv, const double2 *__restrict__ t, double2 alpha, double2 omega,
+                          size_t n) {
+  pdl_wait();
+  pdl_trigger();
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
+    x[e] = cadd(x[e], cadd(cmul(alpha, p[e]), cmul(omega, sv[e])));
+    r[e] = csub(sv[e], cmul(omega, t[e]));
+  }
+}
+
 // z = x - y
 __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n) {
   pdl_wait();

@@ -117,6 +117,36 @@ def test_new_algorithm_parity_cgs2(oracle_mod, gpu, name, p):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
+SOLVER_CASES = [
+    ("new-bicgstab", si.ALG_NEW, si.KRY_BICGSTAB, si.POT_VX),
+    ("new-fixed-point", si.ALG_NEW, si.KRY_FIXED_POINT, si.POT_VX),
+    ("classical-fixed-point", si.ALG_CLASSICAL, si.KRY_FIXED_POINT, si.POT_VX),
+    ("classical-gmres", si.ALG_CLASSICAL, si.KRY_GMRES, si.POT_VX),
+    ("classical-bicgstab", si.ALG_CLASSICAL, si.KRY_BICGSTAB, si.POT_VX),
+    ("classical-fp-cubic", si.ALG_CLASSICAL, si.KRY_FIXED_POINT, si.POT_CUBIC),
+    ("precond-bicgstab", si.ALG_PRECOND, si.KRY_BICGSTAB, si.POT_VTX),
+    ("precond-fixed-point", si.ALG_PRECOND, si.KRY_FIXED_POINT, si.POT_VTX),
+]
+
+
+@pytest.mark.parametrize("name,alg,kry,pot", SOLVER_CASES, ids=[c[0] for c in SOLVER_CASES])
+def test_solver_variant_parity(oracle_mod, gpu, name, alg, kry, pot):
+    """The paper's other interface solvers (Algorithms 1-2, fixed points,
+    BiCGStab, readings A20-A22): equal iteration counts, u(T)
+    within 1e-10 of the oracle."""
+    p = si.config("C1", transmission=si.TC_S02, potential=pot, N=4, algorithm=alg, krylov=kry,
+                  u0_kind="soliton" if pot == si.POT_CUBIC else "gaussian")
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    info = dict(it=(rg["iterations"], ro["iterations"]), inner=(rg["inner_iterations"], ro["inner_iterations"]),
+                st=(st, ro["status"]), err=rel(uT, ro["uT"]))
+    print(name, info)
+    assert ro["status"] == 0 and st == 0, info
+    assert rg["iterations"] == ro["iterations"], info
+    assert rel(uT, ro["uT"]) <= 1e-10, info
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)
