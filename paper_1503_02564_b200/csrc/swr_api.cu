@@ -159,6 +159,11 @@ struct swr_handle {
   MarchShape shape_nl;
   double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr, *Fx = nullptr;
   double2 *partial = nullptr;
+  // streaming march (subdomains too large for the resident kernel)
+  bool stream_march = false;
+  double2 *sst_u = nullptr, *sst_z = nullptr, *sst_vals = nullptr;
+  int *sst_flags = nullptr;
+  int sst_cap = 0;   // systems the scratch holds
   Krylov kout = {}, kin = {};             // outer / inner (P^{-1}) GMRES workspaces
   double2 *hpin = nullptr;                 // pinned scalars for restarts and norms
   MarchSys *sys_dev = nullptr;
@@ -274,7 +279,14 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
     p.trace = nullptr;
   }
   CKS(record_pair(h, true, true));
-  CK(swr::launch_march(p, h->shape[K], h->st));
+  if (h->stream_march) {
+    // one system per group (K = 1), in batches of co-resident chains
+    if (K != 1) { g_detail = "streaming march takes K = 1"; return SWR_ERR_UNSUPPORTED; }
+    if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
+    CK(swr::launch_march_stream(p, (int)sys.size(), h->sst_u, h->sst_z, h->sst_flags, h->sst_vals, h->st));
+  } else {
+    CK(swr::launch_march(p, h->shape[K], h->st));
+  }
   CK(cudaGetLastError());
   CKS(record_pair(h, true, false));
   h->n_marches++;
@@ -798,7 +810,8 @@ void free_all(swr_handle *h) {
   void *ptrs[] = {h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
-                  h->sys_dev, h->err_dev, h->jobs_dev, h->counter};
+                  h->sys_dev, h->err_dev, h->jobs_dev, h->counter,
+                  h->sst_u, h->sst_z, h->sst_vals, h->sst_flags};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
@@ -930,10 +943,13 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true) > 227 * 1024) shapes_ok = false;
   for (int K = 2; K <= 3; K++)
     if (h->shape[K].M == 0 || swr::march_smem_bytes(h->shape[K], h->NT, false) > 227 * 1024) h->shape[K].M = 0;
-  if (!shapes_ok) {
-    g_detail = "subdomain too large for the resident march (N_j = " + std::to_string(h->Nj) + ")";
-    delete h;
-    return SWR_ERR_UNSUPPORTED;
+  {
+    const char *me = getenv("SWR_MARCH");
+    if (!shapes_ok || (me && strcmp(me, "stream") == 0)) {
+      // too large for a resident cluster (or forced): stream the state through HBM
+      h->stream_march = true;
+      for (int K = 0; K <= 3; K++) h->shape[K] = {1, 256, 1, 1};
+    }
   }
   auto fail = [&](int s) { free_all(h); delete h; return s; };
   int s;
@@ -953,6 +969,14 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     if ((s = copy_in_r(h->tau, cfg->tau, nt * (NTt + 1), cfg->inputs_on_device, h->st)) ||
         (s = copy_in_r(h->xi, cfg->xi, nt * nx1, cfg->inputs_on_device, h->st)))
       return fail(s);
+  }
+  if (h->stream_march) {
+    h->sst_cap = 3 * h->N + 2;   // the largest batched march (3 RHS per subdomain in the build)
+    const size_t nslot = 148 * 32;   // chain CTAs of one launch, upper bound
+    if ((s = dalloc(&h->sst_u, (size_t)h->sst_cap * h->Nj)) || (s = dalloc(&h->sst_z, (size_t)h->sst_cap * h->Nj)) ||
+        (s = dalloc(&h->sst_vals, nslot * 8)))
+      return fail(s);
+    if (cudaMalloc((void **)&h->sst_flags, nslot * 3 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_OOM);
   }
   if ((s = dalloc(&h->fp_stat, 2))) return fail(s);
   if (cudaMemset(h->fp_stat, 0, 2 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_CUDA);

@@ -66,6 +66,9 @@ struct MarchShape { int M, P, CS, K; };
 MarchShape choose_march_shape(int Nj, int K, int NT);
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
+size_t march_stream_smem_bytes(int NT);
+cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, double2 *zst, int *flags, double2 *vals,
+                                cudaStream_t st);
 MarchShape choose_march_shape_nl(int Nj);
 size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st);

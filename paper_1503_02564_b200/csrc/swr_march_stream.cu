@@ -1,0 +1,299 @@
+// swr_march_stream.cu — the whole-window march for subdomains too large to
+// keep resident on one thread-block cluster (N_j beyond ~45K rows, e.g. C2:
+// N = 10 at dx = 1e-5, N_j = 420,001).  Same arithmetic as k_march (P:193-198,
+// P:305-330; readings A3-A16): per step (A - B) v_n = rhs, u_n = 2 v_n - u_{n-1},
+// S v_n recorded at the interfaces.
+//
+// B200 mapping.  The state u_{n-1} and the forward values z streams through HBM
+// (the march is then HBM-bound, the regime of SURVEY 8(d) "B1 streaming").
+// A system is a chain of nc co-resident CTAs (cooperative launch); CTA c owns
+// the contiguous rows [c Rc, (c+1) Rc) and thread t of it a contiguous block
+// of Rt rows, so each thread streams whole 128-byte lines of its own rows and
+// keeps the Thomas recurrence in registers.  Per step:
+//   pass 1  forward from carry 0 over the thread's rows -> affine map (A, F)
+//   scan    CTA scan of the maps; the CTA totals are published in global
+//           memory (value + step flag, release/acquire) and folded by the
+//           later CTAs of the chain
+//   pass 2  forward again from the exact carry, z stored
+//   pass 3  backward from carry 0 over z -> (Ab, B); scan and chain fold in
+//           reverse order
+//   pass 4  backward from the exact carry: v = x, u_n = 2 v - u_{n-1}
+// The boundary rows fold b_n - l_n / b_n - r_n into the stencil as in k_march;
+// the S0^2 history sum of an end row is reduced by the CTA holding it.
+#include "swr_common.cuh"
+#include "swr_kernels.h"
+#include <cooperative_groups.h>
+
+namespace swr {
+
+namespace {
+
+__device__ __forceinline__ double2 negqe_s(double2 q, double er, double eim) {
+  return make_double2(fma(q.y, eim, -q.x * er), -fma(q.x, eim, q.y * er));
+}
+
+__device__ __forceinline__ void st_release(int *p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int ld_acquire(const int *p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void wait_flag(const int *p, int v) {
+  while (ld_acquire(p) < v) __nanosleep(64);
+}
+
+// Exclusive scan of per-thread affine maps x -> A x + B over the CTA in
+// thread order (FWD) or reverse; returns the exclusive (eA, eB) of this
+// thread and, in every thread, the CTA total (tA, tB).
+template <bool FWD>
+__device__ void cta_scan(double2 A, double2 B, double2 *sm, double2 &eA, double2 &eB, double2 &tA, double2 &tB) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5, nw = blockDim.x >> 5;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const double2 Ae = FWD ? shfl_up2(A, o) : shfl_down2(A, o), Be = FWD ? shfl_up2(B, o) : shfl_down2(B, o);
+    if (FWD ? lane >= o : lane + o < 32) {
+      B = cfma(A, Be, B);
+      A = cmul(A, Ae);
+    }
+  }
+  double2 xA = FWD ? shfl_up2(A, 1) : shfl_down2(A, 1), xB = FWD ? shfl_up2(B, 1) : shfl_down2(B, 1);
+  if (FWD ? lane == 0 : lane == 31) { xA = make_double2(1.0, 0.0); xB = cz(); }
+  double2 *wA = sm, *wB = sm + 32;
+  if (lane == (FWD ? 31 : 0)) { wA[w] = A; wB[w] = B; }
+  __syncthreads();
+  // warp prefix: fold of the other warps' totals (<= 16 warps)
+  double2 pA = make_double2(1.0, 0.0), pB = cz(), aA = make_double2(1.0, 0.0), aB = cz();
+  for (int i = 0; i < nw; i++) {
+    const int q = FWD ? i : nw - 1 - i;
+    const double2 qa = wA[q], qb = wB[q];
+    if (FWD ? q < w : q > w) { pB = cfma(qa, pB, qb); pA = cmul(qa, pA); }
+    aB = cfma(qa, aB, qb);
+    aA = cmul(qa, aA);
+  }
+  __syncthreads();
+  eB = cfma(xA, pB, xB);
+  eA = cmul(xA, pA);
+  tA = aA;
+  tB = aB;
+}
+
+}  // namespace
+
+// One CTA per (system, chain index).  scratch: u [nsys][Nj], z [nsys][Nj];
+// sync: done/fwd/bwd flags [nsys][nc] (int), values fv/bv [nsys][nc][2 parity][2].
+__global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int nc, double2 *ust, double2 *zst,
+                                                      int *flags, double2 *vals) {
+  extern __shared__ double2 ssm[];
+  double2 *scanbuf = ssm;                      // [64]
+  double2 *red = scanbuf + 64;                 // [32] block reduction
+  double2 *hvL = red + 32;                     // [NT+1] v_s at row 0 (CTA 0 of a system with a left interface)
+  double2 *hvR = hvL + (p.NT + 1);             // [NT+1] v_s at row N_j - 1 (last CTA, right interface)
+  __shared__ double2 sHL, sHR;                 // H_n of the end rows this CTA holds
+  const int t = threadIdx.x, P = blockDim.x;
+  const int sidx = blockIdx.x / nc, c = blockIdx.x % nc;
+  const MarchSys &S = p.sys[sidx];
+  const int Nj = p.Nj, NT = p.NT;
+  const double eim = p.e_im, kappa = p.kappa, ikappa = 1.0 / p.kappa;
+  const int Rc = (Nj + nc - 1) / nc;
+  const int rc0 = min(Nj, c * Rc), rc1 = min(Nj, (c + 1) * Rc);
+  const int Rt = (rc1 - rc0 + P - 1) / P;
+  const int rt0 = min(rc1, rc0 + t * Rt), rt1 = min(rc1, rc0 + (t + 1) * Rt);
+  double2 *u = ust + (size_t)sidx * Nj, *z = zst + (size_t)sidx * Nj;
+  int *fdone = flags + (size_t)sidx * nc * 3, *ffwd = fdone + nc, *fbwd = ffwd + nc;
+  double2 *fv = vals + (size_t)sidx * nc * 8, *bv = fv + nc * 4;   // [nc][parity][A, B]
+  const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
+  const bool first_cta = c == 0, last_cta = rc1 == Nj && rc0 < Nj;
+  const bool own0 = first_cta && t == 0 && rt0 == 0 && rt1 > 0;          // holds row 0
+  const bool ownL = rt1 == Nj && rt0 < Nj;                                 // holds row N_j - 1
+  const bool histL = first_cta && has_left, histR = last_cta && has_right;
+
+  // initial state
+  for (int k = rc0 + t; k < rc1; k += P) u[k] = S.u0 ? S.u0[k] : cz();
+  if (histL && t == 0) hvL[0] = S.u0 ? S.u0[0] : cz();
+  if (histR && t == 0) hvR[0] = S.u0 ? S.u0[Nj - 1] : cz();
+  __syncthreads();
+  __threadfence();
+  if (t == 0) st_release(fdone + c, 0);
+
+  auto flux = [&](int sd, int n) -> double2 {
+    if (S.flags & (sd == 0 ? SYS_LIN_IMPULSE : SYS_RIN_IMPULSE)) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
+    const double2 *f = sd == 0 ? S.lin : S.rin;
+    return f ? f[n - 1] : cz();
+  };
+
+  for (int n = 1; n <= NT; n++) {
+    const size_t toff = p.td_stride ? (size_t)(n - 1) * p.td_stride : 0;
+    const double2 *q = S.q + toff;
+    const double *er = S.er + toff;
+    // neighbours' u_{n-1} (halo rows) are final once they reported step n-1
+    if (t == 0) {
+      if (c > 0) wait_flag(fdone + c - 1, n - 1);
+      if (c < nc - 1) wait_flag(fdone + c + 1, n - 1);
+    }
+    // S0^2 history of the end rows this CTA holds: H_n = c2 sum_{s<n} beta_{n-s} v_s
+    for (int sd = 0; sd < 2; sd++) {
+      if (!(sd == 0 ? histL : histR)) continue;
+      const double2 *hv = sd == 0 ? hvL : hvR;
+      double2 acc = cz();
+      if (p.s02)
+        for (int s = t; s <= n - 1; s += P)
+          acc = make_double2(fma(p.beta[n - s], hv[s].x, acc.x), fma(p.beta[n - s], hv[s].y, acc.y));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+      if ((t & 31) == 0) red[t >> 5] = acc;
+      __syncthreads();
+      if (t == 0) {
+        double2 hs = cz();
+        for (int w = 0; w < (P >> 5); w++) hs = cadd(hs, red[w]);
+        (sd == 0 ? sHL : sHR) = p.s02 ? cmul(p.c2, hs) : cz();
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    // end-row folds (k_march): d = H_n - l_n at row 0, H_n - r_n at row N_j - 1
+    const double2 dL = (own0 && has_left) ? csub(sHL, flux(0, n)) : cz();
+    const double2 dR = (ownL && has_right) ? csub(sHR, flux(1, n)) : cz();
+    auto sval = [&](int k, double2 um, double2 uk, double2 up) -> double2 {
+      // u_{k-1} + 4 u_k + u_{k+1} with the P1 end rows (h/6)(2, 1) and the folds
+      if (k == 0) {
+        const double2 f = make_double2(dL.y * ikappa, -dL.x * ikappa);
+        return make_double2(fma(2.0, uk.x, up.x) + f.x, fma(2.0, uk.y, up.y) + f.y);
+      }
+      if (k == Nj - 1) {
+        const double2 f = make_double2(dR.y * ikappa, -dR.x * ikappa);
+        return make_double2(fma(2.0, uk.x, um.x) + f.x, fma(2.0, uk.y, um.y) + f.y);
+      }
+      return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
+    };
+    // ---- forward: z_k = c_k z_{k-1} + q_k (i kappa s_k), c_k = -q_k E_{k-1} ----
+    auto fwd_pass = [&](double2 zin, bool store, double2 &Aout) -> double2 {
+      double2 zz = zin, A = make_double2(1.0, 0.0);
+      double2 um = rt0 > 0 ? __ldcg(u + rt0 - 1) : cz(), uk = rt0 < rt1 ? __ldcg(u + rt0) : cz();
+      double erp = rt0 > 0 ? er[rt0 - 1] : 0.0;
+#pragma unroll 4
+      for (int k = rt0; k < rt1; k++) {
+        const double2 up = k + 1 < Nj ? __ldcg(u + k + 1) : cz();
+        const double2 qk = __ldg(q + k);
+        const double2 ck = negqe_s(qk, erp, eim);
+        const double2 rr = cimul(kappa, sval(k, um, uk, up));
+        zz = cfma(ck, zz, cmul(qk, rr));
+        if (store) z[k] = zz;
+        else A = cmul(ck, A);
+        erp = __ldg(er + k);
+        um = uk;
+        uk = up;
+      }
+      Aout = A;
+      return zz;
+    };
+    const int par = n & 1;
+    double2 A1, F1 = fwd_pass(cz(), false, A1);
+    double2 eA, eB, tA, tB;
+    cta_scan<true>(A1, F1, scanbuf, eA, eB, tA, tB);
+    if (t == 0) {
+      fv[(c * 2 + par) * 2 + 0] = tA;
+      fv[(c * 2 + par) * 2 + 1] = tB;
+      __threadfence();
+      st_release(ffwd + c, n);
+    }
+    // carry into the CTA: fold of the earlier CTAs' totals
+    double2 zc = cz();
+    if (c > 0) {
+      if (t == 0)
+        for (int cc = 0; cc < c; cc++) wait_flag(ffwd + cc, n);
+      __syncthreads();
+      for (int cc = 0; cc < c; cc++)
+        zc = cfma(__ldcg(fv + (cc * 2 + par) * 2 + 0), zc, __ldcg(fv + (cc * 2 + par) * 2 + 1));
+    }
+    double2 dummy;
+    fwd_pass(cfma(eA, zc, eB), true, dummy);
+    // ---- backward: x_k = z_k + b_k x_{k+1}, b_k = -q_k E_k ----
+    double2 Ab = make_double2(1.0, 0.0), xb = cz();
+    for (int k = rt1 - 1; k >= rt0; k--) {
+      const double2 bk = negqe_s(__ldg(q + k), __ldg(er + k), eim);
+      xb = cfma(bk, xb, z[k]);
+      Ab = cmul(bk, Ab);
+    }
+    cta_scan<false>(Ab, xb, scanbuf, eA, eB, tA, tB);
+    if (t == 0) {
+      bv[(c * 2 + par) * 2 + 0] = tA;
+      bv[(c * 2 + par) * 2 + 1] = tB;
+      __threadfence();
+      st_release(fbwd + c, n);
+    }
+    double2 xc = cz();
+    if (c < nc - 1) {
+      if (t == 0)
+        for (int cc = nc - 1; cc > c; cc--) wait_flag(fbwd + cc, n);
+      __syncthreads();
+      for (int cc = nc - 1; cc > c; cc--)
+        xc = cfma(__ldcg(bv + (cc * 2 + par) * 2 + 0), xc, __ldcg(bv + (cc * 2 + par) * 2 + 1));
+    }
+    double2 x = cfma(eA, xc, eB), x0v = cz(), xLv = cz();
+    for (int k = rt1 - 1; k >= rt0; k--) {
+      const double2 bk = negqe_s(__ldg(q + k), __ldg(er + k), eim);
+      x = cfma(bk, x, z[k]);
+      const double2 uo = __ldcg(u + k);
+      u[k] = make_double2(fma(2.0, x.x, -uo.x), fma(2.0, x.y, -uo.y));   // u_n = 2 v_n - u_{n-1}
+      if (k == Nj - 1) xLv = x;
+      if (k == 0) x0v = x;
+    }
+    // record v_n and S v_n at the interfaces (eq. 8)
+    if (own0) {
+      if (histL) hvL[n] = x0v;
+      if (has_left && S.out_left) {
+        const double2 sv = cfma(p.c0, x0v, sHL), l = flux(0, n);
+        S.out_left[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
+      }
+    }
+    if (ownL) {
+      if (histR) hvR[n] = xLv;
+      if (has_right && S.out_right) {
+        const double2 sv = cfma(p.c0, xLv, sHR), r = flux(1, n);
+        S.out_right[n - 1] = make_double2(fma(2.0, sv.x, -r.x), fma(2.0, sv.y, -r.y));
+      }
+    }
+    __syncthreads();
+    __threadfence();
+    if (t == 0) st_release(fdone + c, n);
+  }
+  if (S.uT)
+    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
+}
+
+size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1)) * sizeof(double2); }
+
+// Streams the systems in batches whose chains are all co-resident.
+cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, double2 *zst, int *flags, double2 *vals,
+                                cudaStream_t st) {
+  const size_t smem = march_stream_smem_bytes(p.NT);
+  cudaError_t e = cudaFuncSetAttribute(k_march_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_stream, 256, smem);
+  if (e != cudaSuccess) return e;
+  const int cap = nsm * per_sm;
+  if (cap < 1) return cudaErrorInvalidConfiguration;
+  const MarchSys *all = p.sys;
+  for (int s0 = 0; s0 < nsys_total;) {
+    const int nb = std::min(nsys_total - s0, cap);
+    int nc = std::max(1, cap / nb);
+    nc = std::min(nc, std::max(1, p.Nj / 256));   // at least a row per thread
+    MarchParams q = p;
+    q.sys = all + s0;
+    q.nsys = nb;
+    e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 3 * sizeof(int), st);   // -1: nothing reported yet
+    if (e != cudaSuccess) return e;
+    void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
+    e = cudaLaunchCooperativeKernel((const void *)k_march_stream, dim3(nb * nc), dim3(256), args, smem, st);
+    if (e != cudaSuccess) return e;
+    s0 += nb;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace swr

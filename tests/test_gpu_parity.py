@@ -190,6 +190,45 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
 
 
+STREAM_CASES = [
+    ("new-s02-N4", si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=4)),
+    ("new-robin-N5", si.config("C1", transmission=si.TC_ROBIN, potential=si.POT_VX, N=5, robin_p=19.0)),
+    ("new-mid-N42", si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX, transmission=si.TC_S02)),
+    ("precond-vtx-N4", si.config("C1", transmission=si.TC_S02, potential=si.POT_VTX, algorithm=si.ALG_PRECOND, N=4)),
+]
+
+
+@pytest.mark.parametrize("name,p", STREAM_CASES, ids=[c[0] for c in STREAM_CASES])
+def test_streaming_march_parity(oracle_mod, gpu, name, p, monkeypatch):
+    """The streaming march (state through HBM, chains of co-resident CTAs;
+    used when a subdomain does not fit a resident cluster, e.g. C2 at
+    dx = 1e-5) forced on problems the oracle solves: equal counts, u(T)."""
+    monkeypatch.setenv("SWR_MARCH", "stream")
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
+def test_streaming_sweep_matches_resident(gpu, monkeypatch):
+    """One sweep R(g) through both march kernels on a 3-CTA-per-chain
+    problem: equal to rounding."""
+    import torch
+    p = si.Problem(dx=1e-3, dt=5e-3, N=10, potential=si.POT_VX, transmission=si.TC_S02)
+    arr = si.inputs(p)
+    g = torch.randn(p.ng, dtype=torch.complex128, device="cuda")
+    monkeypatch.delenv("SWR_MARCH", raising=False)
+    a = gpu.SWR(p, arr)
+    ra, ua = a.apply_R(g, use_u0=True, want_uT=True)
+    monkeypatch.setenv("SWR_MARCH", "stream")
+    b = gpu.SWR(p, arr)
+    rb, ub = b.apply_R(g, use_u0=True, want_uT=True)
+    assert rel(rb.cpu().numpy(), ra.cpu().numpy()) <= 1e-12
+    assert rel(ub.cpu().numpy(), ua.cpu().numpy()) <= 1e-12
+
+
 @pytest.mark.parametrize("cgs", ["reg", "tma"])
 def test_cgs_kernel_forms(oracle_mod, gpu, cgs, monkeypatch):
     """Both CGS kernel forms (register; bulk-copy pipeline) give the oracle's
