@@ -190,6 +190,26 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
         assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
 
 
+def test_c2_full_size_sampled(oracle_mod, gpu):
+    """C2 at full size (N = 10, dx = 1e-5: N_j = 420,001, the streaming march)
+    in the launch shape the timing uses: d = R(0) traces of subdomains 1, 5
+    (the Gaussian's support) against the oracle's marches."""
+    p = si.config("C2")
+    arrays = si.inputs(p)
+    g_ = gpu.SWR(p, arrays)
+    g_.build()
+    d_g, _ = g_.get_interface(0)
+    d_g = d_g.cpu().numpy()
+    o = oracle_mod.Oracle(p, arrays)
+    NT = p.NT
+    for j in (1, 5):
+        st, ol, orr, _, _ = o.march(j, None, None, use_u0=True)
+        if j >= 2:
+            assert rel(d_g[(2 * j - 4) * NT:(2 * j - 3) * NT], ol, 1.0) <= 1e-10
+        if j <= p.N - 1:
+            assert rel(d_g[(2 * j - 1) * NT:(2 * j) * NT], orr, 1.0) <= 1e-10
+
+
 STREAM_CASES = [
     ("new-s02-N4", si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=4)),
     ("new-robin-N5", si.config("C1", transmission=si.TC_ROBIN, potential=si.POT_VX, N=5, robin_p=19.0)),
