@@ -417,7 +417,7 @@ int factor_matrices(swr_handle *h) {
   CKS(dalloc(&h->jobs_dev, jobs.size()));
   CK(cudaMemcpyAsync(h->jobs_dev, jobs.data(), jobs.size() * sizeof(jobs[0]), cudaMemcpyHostToDevice, h->st));
   CK(cudaMemsetAsync(h->err_dev, 0, sizeof(int), h->st));
-  swr::k_factor<<<(unsigned)((jobs.size() + 63) / 64), 64, 0, h->st>>>(h->jobs_dev, (int)jobs.size(), h->Nj, h->dx,
+  swr::k_factor<<<(unsigned)((jobs.size() + 3) / 4), 128, 0, h->st>>>(h->jobs_dev, (int)jobs.size(), h->Nj, h->dx,
                                                                         h->dt, h->c0, h->err_dev);
   CK(cudaGetLastError());
   h->n_launches++;

@@ -13,40 +13,62 @@ namespace swr {
 // Assembly + LU pivots of (A_{j} - B_{j}) (eq. 9):
 //   A = (2i/dt) M - S + M_W, P1 elements on a uniform mesh,
 //   M_W the weighted mass of the linear interpolant of W (reading A2),
-//   B subtracts c0 on interface rows.  One thread factors one matrix
+//   B subtracts c0 on interface rows.  One warp factors one matrix
 //   (sequential Thomas pivots p_k = D_k - E_{k-1}^2 / p_{k-1}, q_k = 1/p_k).
 // ---------------------------------------------------------------------------
 __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0,
                          int *err) {
-  const int jb = blockIdx.x * blockDim.x + threadIdx.x;
+  // one warp per matrix: the lanes assemble 32 rows at a time (diagonal D_k,
+  // Re E_k) and store the results coalesced; lane 0 runs the pivot
+  // recurrence p_k = D_k - E_{k-1}^2 / p_{k-1} from shared memory
+  __shared__ double2 sD[4][32], sQ[4][32];
+  __shared__ double sE[4][32];
+  const int wl = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int jb = blockIdx.x * (blockDim.x >> 5) + wl;
   if (jb >= njobs) return;
   const FactorJob J = jobs[jb];
   const double eim = (2.0 / dt) * (h / 6.0);
   double er_prev = 0.0;
   double2 qprev = cz();
-  for (int k = 0; k < Nj; k++) {
-    const double Wk = J.W ? J.W[k] : 0.0;
-    const double Wl = (J.W && k > 0) ? J.W[k - 1] : 0.0;
-    const double Wr = (J.W && k < Nj - 1) ? J.W[k + 1] : 0.0;
-    double Md = 0.0, Sd = 0.0, MWd = 0.0;
-    if (k > 0) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (Wl + 3.0 * Wk) / 12.0; }
-    if (k < Nj - 1) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (3.0 * Wk + Wr) / 12.0; }
-    double2 D = make_double2(-Sd + MWd, (2.0 / dt) * Md);
-    if (k == 0 && J.has_left) D = csub(D, c0);
-    if (k == Nj - 1 && J.has_right) D = csub(D, c0);
-    double2 p = D;
-    if (k > 0) {
-      const double2 E = make_double2(er_prev, eim);
-      p = csub(D, cmul(E, cmul(E, qprev)));
+  bool bad = false;
+  for (int k0 = 0; k0 < Nj; k0 += 32) {
+    const int k = k0 + lane;
+    if (k < Nj) {
+      const double Wk = J.W ? J.W[k] : 0.0;
+      const double Wl = (J.W && k > 0) ? J.W[k - 1] : 0.0;
+      const double Wr = (J.W && k < Nj - 1) ? J.W[k + 1] : 0.0;
+      double Md = 0.0, Sd = 0.0, MWd = 0.0;
+      if (k > 0) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (Wl + 3.0 * Wk) / 12.0; }
+      if (k < Nj - 1) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (3.0 * Wk + Wr) / 12.0; }
+      double2 D = make_double2(-Sd + MWd, (2.0 / dt) * Md);
+      if (k == 0 && J.has_left) D = csub(D, c0);
+      if (k == Nj - 1 && J.has_right) D = csub(D, c0);
+      sD[wl][lane] = D;
+      sE[wl][lane] = (k < Nj - 1) ? 1.0 / h + h * (Wk + Wr) / 12.0 : 0.0;
     }
-    if (!(hypot(p.x, p.y) >= 1e-300)) atomicExch(err, 3);  // zero pivot
-    const double2 qk = crcp(p);
-    const double erk = (k < Nj - 1) ? 1.0 / h + h * (Wk + Wr) / 12.0 : 0.0;
-    J.q[k] = qk;
-    J.er[k] = erk;
-    qprev = qk;
-    er_prev = erk;
+    __syncwarp();
+    if (lane == 0) {
+      const int kn = min(32, Nj - k0);
+      for (int i = 0; i < kn; i++) {
+        double2 p = sD[wl][i];
+        if (k0 + i > 0) {
+          const double2 E = make_double2(er_prev, eim);
+          p = csub(p, cmul(E, cmul(E, qprev)));
+        }
+        if (!(hypot(p.x, p.y) >= 1e-300)) bad = true;   // zero pivot
+        qprev = crcp(p);
+        sQ[wl][i] = qprev;
+        er_prev = sE[wl][i];
+      }
+    }
+    __syncwarp();
+    if (k < Nj) {
+      J.q[k] = sQ[wl][lane];
+      J.er[k] = sE[wl][lane];
+    }
+    __syncwarp();
   }
+  if (lane == 0 && bad) atomicExch(err, 3);
 }
 
 // V(t,x) = sum_t tau_t(t) xi_t(x): factorisation of (A_{j,n} - B) for every
