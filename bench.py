@@ -164,9 +164,17 @@ def run_reference(args, p, arrays):
     print(json.dumps(line), flush=True)
 
 
+POT_NAME = {si.POT_ZERO: "V=0", si.POT_VX: "V=-x^2", si.POT_VTX: "V=5tx", si.POT_CUBIC: "f(u)=|u|^2"}
+ALG_NAME = {si.ALG_NEW: "NEW", si.ALG_PRECOND: "PRECOND", si.ALG_CLASSICAL: "CLASSICAL"}
+KRY_NAME = {si.KRY_GMRES: "GMRES(30)", si.KRY_BICGSTAB: "BiCGStab", si.KRY_FIXED_POINT: "fixed point"}
+
+
 def workload_config(p):
-    return {"workload": f"{p.name}: V=-x^2 NEW+GMRES(30) CGS2, N={p.N}, dx={p.dx:g}, dt={p.dt:g}, T={p.T:g}, "
-                        f"S0^2, Gaussian u0, zero g0 (BASELINE configs[4] at N=500)",
+    gs = "CGS" if p.gs_passes == 1 else "CGS2"
+    return {"workload": f"{p.name}: {POT_NAME[p.potential]} {ALG_NAME[p.algorithm]}+{KRY_NAME[p.krylov]} {gs}, "
+                        f"N={p.N}, dx={p.dx:g}, dt={p.dt:g}, T={p.T:g}, "
+                        f"{'S0^2' if p.transmission == si.TC_S02 else 'Robin'}, {p.u0_kind} u0, zero g0"
+                        + (" (BASELINE configs[4] at N=500)" if p.name == "C5" else ""),
             "N_subdomains": p.N, "N_x": p.Nx, "N_T": p.NT, "N_j": p.Nj,
             "cell_steps_per_step": (3 * p.N - 2 + p.N) * p.Nj * p.NT,
             "parallelism": None, "l2": "flushed before every timed step (256 MiB write)"}
