@@ -115,9 +115,67 @@ static ocplx or_c2(const or_problem *P) {
   return (1.0 - I_) / sqrt(P->dt);
 }
 
+/* Interface data of one side of subdomain j for the higher-order operators
+ * (time-independent potential): W at the interface node, its outward normal
+ * derivative dnW (reading A23: central difference of the nodal W on the
+ * global mesh, n = -x at a_j, +x at b_j) and the gauge phase rate:
+ * calV_n = t_n W, calW_n = (calV_n + calV_{n-1})/2 = W dt (n - 1/2) for
+ * n >= 1, calW_0 = 0 (reading A24). */
+typedef struct { double W, dnW; int32_t fz; } tc_side;
+
+static tc_side or_tc_side(const or_problem *P, int32_t j, int32_t side, int32_t fz) {
+  tc_side t = {0.0, 0.0, fz};
+  if (fz || P->potential != OR_POT_VX) return t;
+  int32_t Nx, NT, Nj;
+  or_sizes(P, &Nx, &NT, &Nj);
+  int32_t m = Nx / P->N, i = side == 0 ? (j - 1) * m : j * m;
+  t.W = P->V_x[i];
+  double dx = (i > 0 && i < Nx) ? (P->V_x[i + 1] - P->V_x[i - 1]) / (2.0 * P->dx) : 0.0;
+  t.dnW = side == 0 ? -dx : dx;
+  return t;
+}
+
+static double or_calW(const tc_side *t, int32_t n, double dt) { return n == 0 ? 0.0 : t->W * dt * (n - 0.5); }
+
+/* Kernel K(n, s) of the discrete transmission operator S v_n = sum_{s<=n}
+ * K(n, s) v_s, alpha/beta/gamma from or_coeffs. */
+static ocplx or_tcK(const or_problem *P, const tc_side *t, int32_t n, int32_t s, const double *alpha,
+                    const double *beta, const double *gamma) {
+  const double dt = P->dt;
+  const ocplx c2 = or_c2(P);                                  /* e^{-i pi/4} sqrt(2/dt) */
+  const ocplx e3 = (1.0 + I_) / sqrt(2.0) * sqrt(dt / 2.0);   /* e^{i pi/4} sqrt(dt/2) */
+  const int32_t d = n - s;
+  switch (P->transmission) {
+    case OR_TC_ROBIN: return d == 0 ? -I_ * P->robin_p : 0.0;
+    case OR_TC_S02: return c2 * beta[d];
+    case OR_TC_S03: return c2 * beta[d] - e3 * (t->W / 2.0) * alpha[d];
+    case OR_TC_S04: return c2 * beta[d] - e3 * (t->W / 2.0) * alpha[d] - I_ * (t->dnW / 4.0) * (dt / 2.0) * gamma[d];
+    case OR_TC_S12:
+    case OR_TC_S14: {
+      const double ph = or_calW(t, n, dt) - or_calW(t, s, dt);
+      const ocplx e = cexp(I_ * ph);
+      ocplx k = c2 * e * beta[d];
+      if (P->transmission == OR_TC_S14) {
+        const double sg = t->dnW > 0 ? 1.0 : (t->dnW < 0 ? -1.0 : 0.0), r = sqrt(fabs(t->dnW)) / 2.0;
+        k -= I_ * sg * r * e * (dt / 2.0) * gamma[d] * r;
+      }
+      return k;
+    }
+  }
+  return 0.0;
+}
+
 static ocplx or_c0(const or_problem *P) {
   if (P->transmission == OR_TC_ROBIN) return -I_ * P->robin_p;
   return or_c2(P) * 1.0; /* beta_0 = 1 */
+}
+
+/* Leading coefficient K(n, n) of side `side` of subdomain j. */
+static ocplx or_c0_side(const or_problem *P, int32_t j, int32_t side, int32_t fz) {
+  if (P->transmission == OR_TC_ROBIN || P->transmission == OR_TC_S02) return or_c0(P);
+  tc_side t = or_tc_side(P, j, side, fz);
+  double a[1] = {1.0}, b[1] = {1.0}, g[1] = {1.0};
+  return or_tcK(P, &t, 1, 1, a, b, g);
 }
 
 /* Nodal W_n on subdomain j: W_n = (V_n + V_{n-1})/2. */
@@ -161,9 +219,8 @@ int32_t or_subdomain_matrix(const or_problem *P, int32_t j, int32_t n, int32_t f
   }
   lo[0] = 0.0;
   up[Nj - 1] = 0.0;
-  ocplx c0 = or_c0(P);
-  if (j >= 2) di[0] -= c0;
-  if (j <= P->N - 1) di[Nj - 1] -= c0;
+  if (j >= 2) di[0] -= or_c0_side(P, j, 0, fz);
+  if (j <= P->N - 1) di[Nj - 1] -= or_c0_side(P, j, 1, fz);
   free(W);
   return OR_OK;
 }
@@ -190,7 +247,12 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
   int32_t N = P->N, m = Nx / N, g0 = (j - 1) * m;
   int32_t has_left = (j >= 2), has_right = (j <= N - 1);
   int32_t pot = fz ? OR_POT_ZERO : P->potential;
-  int32_t s02 = (P->transmission == OR_TC_S02);
+  int32_t hist = (P->transmission != OR_TC_ROBIN);
+  tc_side tL = or_tc_side(P, j, 0, fz), tR = or_tc_side(P, j, 1, fz);
+  /* the neighbour's operator at the same interface node: opposite normal */
+  tc_side tLo = tL, tRo = tR;
+  tLo.dnW = -tL.dnW;
+  tRo.dnW = -tR.dnW;
   size_t nb = (size_t)Nj;
   ocplx *u = (ocplx *)calloc(nb, sizeof(ocplx));
   ocplx *v = (ocplx *)calloc(nb, sizeof(ocplx));
@@ -204,6 +266,7 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
   ocplx *vb = (ocplx *)calloc((size_t)NT + 1, sizeof(ocplx));
   double *beta = (double *)calloc((size_t)NT + 1, sizeof(double));
   double *alpha = (double *)calloc((size_t)NT + 1, sizeof(double));
+  double *gamma = (double *)calloc((size_t)NT + 1, sizeof(double));
   double *Md = (double *)calloc(nb, sizeof(double));
   double *Mo = (double *)calloc(nb, sizeof(double));
   double *Wz = (double *)calloc(nb, sizeof(double));
@@ -211,11 +274,18 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
   double *Wo = (double *)calloc(nb, sizeof(double));
   int32_t st = OR_OK;
   if (!u || !v || !vprev || !rhs || !rhs2 || !lo || !di || !up || !va || !vb ||
-      !beta || !alpha || !Md || !Mo || !Wz || !Wd || !Wo) { st = OR_OOM; goto done; }
+      !beta || !alpha || !gamma || !Md || !Mo || !Wz || !Wd || !Wo) { st = OR_OOM; goto done; }
 
-  or_coeffs(NT + 1, alpha, beta, NULL);
+  or_coeffs(NT + 1, alpha, beta, gamma);
   or_fem(Nj, P->dx, NULL, Md, Mo, NULL, NULL, NULL, NULL);
-  ocplx c2 = or_c2(P), c0 = or_c0(P);
+  ocplx c0L = or_c0_side(P, j, 0, fz), c0R = or_c0_side(P, j, 1, fz);
+  /* leading coefficients of the neighbour's operators at a_j, b_j */
+  ocplx c0Lo = c0L, c0Ro = c0R;
+  if (P->transmission >= OR_TC_S03) {
+    double a1[1] = {1.0}, b1[1] = {1.0}, g1[1] = {1.0};
+    c0Lo = or_tcK(P, &tLo, 1, 1, a1, b1, g1);
+    c0Ro = or_tcK(P, &tRo, 1, 1, a1, b1, g1);
+  }
   ocplx s2 = 2.0 * I_ / P->dt;
   if (use_u0)
     for (int32_t k = 0; k < Nj; k++) u[k] = P->u0[g0 + k];
@@ -237,14 +307,26 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
       if (k + 1 < Nj) mu += Mo[k] * u[k + 1];
       rhs[k] = s2 * mu;
     }
-    ocplx Ha = 0.0, Hb = 0.0;
-    if (s02) {
-      for (int32_t s = 0; s < n; s++) {
-        Ha += beta[n - s] * va[s];
-        Hb += beta[n - s] * vb[s];
+    /* history H_n = sum_{s<n} K(n, s) v_s of each side */
+    ocplx Ha = 0.0, Hb = 0.0, Hao = 0.0, Hbo = 0.0;   /* own side; neighbour's operator */
+    if (hist) {
+      if (P->transmission == OR_TC_S02) {   /* c2 factored out */
+        for (int32_t s = 0; s < n; s++) {
+          Ha += beta[n - s] * va[s];
+          Hb += beta[n - s] * vb[s];
+        }
+        Ha = or_c2(P) * Ha;
+        Hb = or_c2(P) * Hb;
+        Hao = Ha;
+        Hbo = Hb;
+      } else {
+        for (int32_t s = 0; s < n; s++) {
+          Ha += or_tcK(P, &tL, n, s, alpha, beta, gamma) * va[s];
+          Hb += or_tcK(P, &tR, n, s, alpha, beta, gamma) * vb[s];
+          Hao += or_tcK(P, &tLo, n, s, alpha, beta, gamma) * va[s];
+          Hbo += or_tcK(P, &tRo, n, s, alpha, beta, gamma) * vb[s];
+        }
       }
-      Ha = c2 * Ha;
-      Hb = c2 * Hb;
     }
     if (has_left) rhs[0] += Ha - (lin ? lin[n - 1] : 0.0);
     if (has_right) rhs[Nj - 1] += Hb - (rin ? rin[n - 1] : 0.0);
@@ -285,15 +367,20 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
     }
     va[n] = v[0];
     vb[n] = v[Nj - 1];
-    if (has_left && out_left) out_left[n - 1] = -(lin ? lin[n - 1] : 0.0) + 2.0 * (c0 * v[0] + Ha);
-    if (has_right && out_right) out_right[n - 1] = -(rin ? rin[n - 1] : 0.0) + 2.0 * (c0 * v[Nj - 1] + Hb);
+    /* eq. (8) with the neighbour's operator: r_{j-1} = -l_j +
+     * (S_{a_j} + S_{b_{j-1}}) v(a_j); the two coincide except for the terms
+     * odd in the normal derivative of W (S0^4, S1^4, reading A25) */
+    if (has_left && out_left)
+      out_left[n - 1] = -(lin ? lin[n - 1] : 0.0) + (c0L * v[0] + Ha) + (c0Lo * v[0] + Hao);
+    if (has_right && out_right)
+      out_right[n - 1] = -(rin ? rin[n - 1] : 0.0) + (c0R * v[Nj - 1] + Hb) + (c0Ro * v[Nj - 1] + Hbo);
   }
   if (uT) for (int32_t k = 0; k < Nj; k++) uT[k] = u[k];
   if (fp_max && fpm > *fp_max) *fp_max = fpm;
   if (fp_fail) st = OR_INNER_NOT_CONVERGED;
 done:
   free(u); free(v); free(vprev); free(rhs); free(rhs2); free(lo); free(di); free(up);
-  free(va); free(vb); free(beta); free(alpha); free(Md); free(Mo); free(Wz); free(Wd); free(Wo);
+  free(va); free(vb); free(beta); free(alpha); free(gamma); free(Md); free(Mo); free(Wz); free(Wd); free(Wo);
   return st;
 }
 
@@ -711,6 +798,9 @@ int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
   if (P->transmission == OR_TC_ROBIN && !(P->robin_p > 0)) return OR_ERR_ARG;
+  if (P->transmission < OR_TC_ROBIN || P->transmission > OR_TC_S14) return OR_ERR_ARG;
+  if (P->transmission >= OR_TC_S03 && !(P->potential == OR_POT_ZERO || P->potential == OR_POT_VX))
+    return OR_UNSUPPORTED;   /* higher orders: time-independent potentials */
   int32_t N = P->N;
   or_report dummy;
   if (!rep) rep = &dummy;

@@ -24,7 +24,10 @@ enum { OR_OK = 0, OR_ERR_ARG = 1, OR_NOT_CONVERGED = 2, OR_ZERO_PIVOT = 3,
        OR_BREAKDOWN = 4, OR_INNER_NOT_CONVERGED = 5, OR_UNSUPPORTED = 6,
        OR_OOM = 9 };
 enum { OR_POT_ZERO = 0, OR_POT_VX = 1, OR_POT_VTX = 2, OR_POT_CUBIC = 3 };
-enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1 };
+/* Transmission operators (P:146-170 continuous, P:218-238 discrete):
+ * Robin -ip; potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4.
+ * Orders above 2 need a time-independent potential here (V = 0 or V(x)). */
+enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1, OR_TC_S03 = 2, OR_TC_S04 = 3, OR_TC_S12 = 4, OR_TC_S14 = 5 };
 enum { OR_ALG_NEW = 0, OR_ALG_PRECOND = 1, OR_ALG_CLASSICAL = 2 };
 /* Interface solver (reading A20/A21): GMRES(restart), BiCGStab, or the fixed
  * point of the algorithm (NEW: g <- d + L g; CLASSICAL: g <- R(g), Algorithm 1). */

@@ -19,7 +19,7 @@ import numpy as np
 # enum values mirrored by both sides' own headers (include/swr.h and
 # oracle/swr_oracle.h); they are the ABI's argument codes, not arithmetic.
 POT_ZERO, POT_VX, POT_VTX, POT_CUBIC = 0, 1, 2, 3
-TC_ROBIN, TC_S02 = 0, 1
+TC_ROBIN, TC_S02, TC_S03, TC_S04, TC_S12, TC_S14 = 0, 1, 2, 3, 4, 5
 ALG_NEW, ALG_PRECOND, ALG_CLASSICAL = 0, 1, 2
 KRY_GMRES, KRY_BICGSTAB, KRY_FIXED_POINT = 0, 1, 2
 
@@ -101,6 +101,8 @@ def make_vx(p: Problem) -> np.ndarray:
         return -(x * x)
     if p.vx_kind == "zero":
         return np.zeros_like(x)
+    if p.vx_kind == "const":           # V = 5 (gauge-strategy pins)
+        return np.full_like(x, 5.0)
     raise ValueError(p.vx_kind)
 
 

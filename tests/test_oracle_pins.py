@@ -386,6 +386,55 @@ def test_new_rejects_time_dependent(oracle_mod):
     assert o.solve()["status"] == 6
 
 
+HIGHER_TC = [si.TC_S03, si.TC_S04, si.TC_S12, si.TC_S14]
+
+
+@pytest.mark.parametrize("tc", HIGHER_TC)
+def test_higher_order_tc_reduce_to_s02_for_zero_potential(oracle_mod, tc):
+    """With V = 0 the potential and gauge operators of every order reduce to
+    S0^2 (the extra terms carry V, d_n V or the phase int V):
+    the interface operator d, L of the new algorithm agree to rounding."""
+    p = si.config("C1", transmission=si.TC_S02, potential=si.POT_ZERO, N=4)
+    q = si.config("C1", transmission=tc, potential=si.POT_ZERO, N=4)
+    o, oq = oracle_mod.Oracle(p, si.inputs(p)), oracle_mod.Oracle(q, si.inputs(q))
+    d0, dq = o.apply_R(np.zeros(o.ng), use_u0=True), oq.apply_R(np.zeros(oq.ng), use_u0=True)
+    assert np.linalg.norm(dq - d0) <= 1e-13 * np.linalg.norm(d0)
+    X0, Xq = o.build_L(), oq.build_L()
+    assert np.abs(Xq - X0).max() <= 1e-13 * np.abs(X0).max()
+
+
+@pytest.mark.parametrize("tc", HIGHER_TC)
+def test_higher_order_tc_converge_to_monodomain(oracle_mod, tc):
+    """Whatever the transmission operator, the converged SWR solution is the
+    single-domain one (the operator only changes the convergence): pins that
+    the leading coefficient on the matrix row, the history and the emitted
+    traces of eq. (8) are the same operator."""
+    p = si.config("C1", transmission=tc, potential=si.POT_VX, N=4)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    r = o.solve()
+    st, um, _ = o.monodomain()
+    assert r["status"] == 0 and r["converged"]
+    assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+def test_gauge_tc_is_transparent_for_constant_potential(oracle_mod):
+    """For a constant potential V0 the solution is e^{i V0 t} times a free one
+    and the gauge operator S1^2 = e^{-i pi/4} e^{i calV} d_t^{1/2} e^{-i calV}
+     absorbs a packet as well as S0^2 does without a potential,
+    while S0^2, blind to V0, reflects more (same set-up as the S0^2 pin)."""
+    out = {}
+    for tc in (si.TC_S12, si.TC_S02):
+        p = si.Problem(a0=-16, b0=4, T=0.2, dx=2e-3, dt=2e-4, N=2, potential=si.POT_VX, vx_kind="const",
+                       transmission=tc)
+        o = oracle_mod.Oracle(p, si.inputs(p))
+        st, _, _, uT, _ = o.march(1, None, None, use_u0=True)
+        q = si.Problem(a0=-16, b0=24, T=0.2, dx=2e-3, dt=2e-4, N=1, potential=si.POT_VX, vx_kind="const")
+        st2, ub, _ = oracle_mod.Oracle(q, si.inputs(q)).monodomain()
+        out[tc] = np.abs(uT - ub[: p.Nj]).max()
+    assert out[si.TC_S12] <= 1e-4, out
+    assert out[si.TC_S02] >= 10 * out[si.TC_S12], out
+
+
 def test_s02_transmission_is_transparent(oracle_mod):
     """S0^2 is the discrete transparent condition of the free equation
     (P:146-159): a Gaussian packet leaving subdomain 1 through b_1
