@@ -71,7 +71,13 @@ enum swr_potential {
   SWR_POT_CUBIC = 3            /* f(u) = lambda |u|^2 */
 };
 
-enum swr_transmission { SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1 };
+/* Transmission operators (discrete P:218-238): Robin -ip;
+ * potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4.  Orders
+ * above S0^2 need a time-independent potential (V = 0 or V(x)) and the NEW or
+ * CLASSICAL algorithm (readings A23-A25). */
+enum swr_transmission {
+  SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1, SWR_TC_S0_3 = 2, SWR_TC_S0_4 = 3, SWR_TC_S1_2 = 4, SWR_TC_S1_4 = 5
+};
 enum swr_algorithm {
   SWR_ALG_NEW = 0,       /* Algorithm 3 */
   SWR_ALG_PRECOND = 1,   /* preconditioned algorithms */

@@ -137,6 +137,10 @@ struct swr_handle {
   ncclComm_t comm = nullptr;
   cudaStream_t st;
   double2 c0, c2v;
+  // higher-order transmission operators (tc_hi): per subdomain side
+  bool tc_hi = false;
+  double2 *kap = nullptr;                 // device [N][2][N_T+1] even kernels
+  std::vector<double2> tc_c0, tc_c0e, tc_dlt, tc_rho, tc_f0;   // [N][2]
   double kappa, eim;
   MarchShape shape[4];                     // launch shape per K = 1..3 RHS per group
   // device data
@@ -233,6 +237,7 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
   p.e_im = h->eim;
   p.kappa = h->kappa;
   p.c0 = h->c0;
+  p.tc_hi = h->tc_hi ? 1 : 0;
   p.c2 = h->c2v;
   p.s02 = h->transmission == SWR_TC_S0_2;
   p.flux_smem = 0;
@@ -320,6 +325,16 @@ MarchSys make_sys(swr_handle *h, int j, const double2 *g, bool use_u0, bool zero
     s.q = h->q + (size_t)(j - 1) * h->Nj;
     s.er = h->er + (size_t)(j - 1) * h->Nj;
   }
+  if (h->tc_hi && !zero_pot) {
+    for (int side = 0; side < 2; side++) {
+      const size_t o = (size_t)(j - 1) * 2 + side;
+      s.kap[side] = h->kap + o * (h->NT + 1);
+      s.c0e[side] = h->tc_c0e[o];
+      s.dlt[side] = h->tc_dlt[o];
+      s.rho[side] = h->tc_rho[o];
+      s.f0[side] = h->tc_f0[o];
+    }
+  }
   return s;
 }
 
@@ -354,8 +369,66 @@ int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2
   return SWR_OK;
 }
 
+// ---- higher-order transmission operators -----------
+// Per subdomain side: W at the interface node, dnW by the central difference
+// on the global mesh with the outward normal (A23), gauge phase rate
+// theta = W dt (A24).  Even kernel (emitted through eq. 8, A25):
+//   S0^3, S0^4: kap_m = c2 beta_m - e^{i pi/4} sqrt(dt/2) (W/2) alpha_m
+//   S1^2, S1^4: kap_m = c2 beta_m e^{i theta m},   v_0 term times e^{-i theta/2}
+// odd part (S0^4, S1^4): dlt gamma_m rho^m, dlt = -i (dnW/4)(dt/2), rho = 1 or
+// e^{i theta}; leading coefficient of the local condition kap_0 + dlt.
+int setup_tc(swr_handle *h) {
+  const int N = h->N, NT = h->NT;
+  h->tc_c0.assign(2 * N, h->c0);
+  h->tc_c0e.assign(2 * N, h->c0);
+  h->tc_dlt.assign(2 * N, make_double2(0, 0));
+  h->tc_rho.assign(2 * N, make_double2(1, 0));
+  h->tc_f0.assign(2 * N, make_double2(1, 0));
+  if (!h->tc_hi) return SWR_OK;
+  std::vector<double> V((size_t)h->Nx + 1, 0.0);
+  if (h->Vx) {
+    CK(cudaStreamSynchronize(h->st));
+    CK(cudaMemcpy(V.data(), h->Vx, V.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  }
+  std::vector<double> al(NT + 1), be(NT + 1);
+  for (int m = 0; m <= NT; m++) {
+    const double a = m == 0 ? 1.0 : (m % 2 ? al[m - 1] : al[m - 2] * (double)(m - 1) / (double)m);
+    al[m] = a;
+    be[m] = (m % 2) ? -a : a;
+  }
+  const cplx cc2 = c2(h->c2v), e3 = cplx(1.0, 1.0) / std::sqrt(2.0) * std::sqrt(h->dt / 2.0);
+  const int tc = h->transmission;
+  const bool gauge = tc == SWR_TC_S1_2 || tc == SWR_TC_S1_4, order4 = tc == SWR_TC_S0_4 || tc == SWR_TC_S1_4;
+  std::vector<double2> K((size_t)N * 2 * (NT + 1));
+  for (int j = 1; j <= N; j++) {
+    for (int side = 0; side < 2; side++) {
+      const int i = side == 0 ? (j - 1) * h->m : j * h->m;
+      const double W = V[i];
+      const double dxW = (i > 0 && i < h->Nx) ? (V[i + 1] - V[i - 1]) / (2.0 * h->dx) : 0.0;
+      const double dnW = side == 0 ? -dxW : dxW;
+      const double th = W * h->dt;
+      double2 *k = K.data() + ((size_t)(j - 1) * 2 + side) * (NT + 1);
+      for (int m = 0; m <= NT; m++) {
+        cplx v = gauge ? cc2 * be[m] * std::exp(cplx(0.0, th * m)) : cc2 * be[m] - e3 * (W / 2.0) * al[m];
+        k[m] = d2(v);
+      }
+      const size_t o = (size_t)(j - 1) * 2 + side;
+      const cplx dlt = order4 ? cplx(0.0, -1.0) * (dnW / 4.0) * (h->dt / 2.0) : cplx(0.0);
+      h->tc_c0e[o] = k[0];
+      h->tc_dlt[o] = d2(dlt);
+      h->tc_c0[o] = d2(c2(k[0]) + dlt);
+      h->tc_rho[o] = gauge ? d2(std::exp(cplx(0.0, th))) : make_double2(1, 0);
+      h->tc_f0[o] = gauge ? d2(std::exp(cplx(0.0, -th / 2.0))) : make_double2(1, 0);
+    }
+  }
+  if (!h->kap) CKS(dalloc(&h->kap, K.size()));
+  CK(cudaMemcpy(h->kap, K.data(), K.size() * sizeof(double2), cudaMemcpyHostToDevice));
+  return SWR_OK;
+}
+
 // ---- assembly + factorisation ----------------------------------------------
 int factor_matrices(swr_handle *h) {
+  CKS(setup_tc(h));
   std::vector<swr::FactorJob> jobs;
   const bool phys_const = h->potential != SWR_POT_VTX_SEPARABLE;
   if (phys_const) {
@@ -367,6 +440,8 @@ int factor_matrices(swr_handle *h) {
       J.g0 = (j - 1) * h->m;
       J.q = h->q + (size_t)(j - 1) * h->Nj;
       J.er = h->er + (size_t)(j - 1) * h->Nj;
+      J.c0L = h->tc_c0[(size_t)(j - 1) * 2 + 0];
+      J.c0R = h->tc_c0[(size_t)(j - 1) * 2 + 1];
       jobs.push_back(J);
     }
   }
@@ -380,6 +455,7 @@ int factor_matrices(swr_handle *h) {
       if (h->N == 1) J.has_left = J.has_right = 0;
       J.q = h->q0 + (size_t)zi * h->Nj;
       J.er = h->er0 + (size_t)zi * h->Nj;
+      J.c0L = J.c0R = h->c0;
       jobs.push_back(J);
     }
   }
@@ -393,6 +469,7 @@ int factor_matrices(swr_handle *h) {
       J.g0 = (j - 1) * h->m;
       J.q = h->qtd + (size_t)(j - 1) * h->Nj;
       J.er = h->ertd + (size_t)(j - 1) * h->Nj;
+      J.c0L = J.c0R = h->c0;
       tj.push_back(J);
     }
     swr::FactorJob *tdev = nullptr;
@@ -811,7 +888,7 @@ void free_all(swr_handle *h) {
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev, h->counter,
-                  h->sst_u, h->sst_z, h->sst_vals, h->sst_flags};
+                  h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
@@ -890,7 +967,12 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     return SWR_ERR_INVALID_ARG;
   }
   if (cfg->transmission == SWR_TC_ROBIN && !(cfg->robin_p > 0)) { g_detail = "Robin needs p > 0"; return SWR_ERR_INVALID_ARG; }
-  if (cfg->transmission != SWR_TC_ROBIN && cfg->transmission != SWR_TC_S0_2) return SWR_ERR_INVALID_ARG;
+  if (cfg->transmission < SWR_TC_ROBIN || cfg->transmission > SWR_TC_S1_4) return SWR_ERR_INVALID_ARG;
+  if (cfg->transmission >= SWR_TC_S0_3 &&
+      (!(cfg->potential == SWR_POT_ZERO || cfg->potential == SWR_POT_VX) || cfg->algorithm == SWR_ALG_PRECOND)) {
+    g_detail = "orders above S0^2 need a time-independent potential and the NEW or CLASSICAL algorithm";
+    return SWR_ERR_INVALID_ARG;
+  }
   if (cfg->potential < 0 || cfg->potential > 3) return SWR_ERR_INVALID_ARG;
   if (cfg->algorithm == SWR_ALG_NEW && !(cfg->potential == SWR_POT_ZERO || cfg->potential == SWR_POT_VX)) {
     g_detail = "NEW needs a time-independent linear potential (P:1015)";
@@ -935,14 +1017,15 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   const double sq = std::sqrt(h->dt);
   h->c2v = make_double2(1.0 / sq, -1.0 / sq);
   h->c0 = (h->transmission == SWR_TC_ROBIN) ? make_double2(0.0, -h->robin_p) : h->c2v;  // beta_0 = 1
+  h->tc_hi = h->transmission >= SWR_TC_S0_3;
   h->kappa = (2.0 / h->dt) * (h->dx / 6.0);
   h->eim = (2.0 / h->dt) * (h->dx / 6.0);
-  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K, h->NT);
+  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K, h->NT, h->tc_hi);
   h->shape[0] = h->shape[1];
   bool shapes_ok = true;
-  if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true) > 227 * 1024) shapes_ok = false;
+  if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true, h->tc_hi) > 227 * 1024) shapes_ok = false;
   for (int K = 2; K <= 3; K++)
-    if (h->shape[K].M == 0 || swr::march_smem_bytes(h->shape[K], h->NT, false) > 227 * 1024) h->shape[K].M = 0;
+    if (h->shape[K].M == 0 || swr::march_smem_bytes(h->shape[K], h->NT, false, h->tc_hi) > 227 * 1024) h->shape[K].M = 0;
   {
     const char *me = getenv("SWR_MARCH");
     if (!shapes_ok || (me && strcmp(me, "stream") == 0)) {

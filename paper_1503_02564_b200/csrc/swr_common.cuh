@@ -65,6 +65,13 @@ struct MarchSys {
   const double *er;        // [N_j] Re E_k, E_k = (A-B)_{k,k+1}
   int32_t flags;
   int32_t pad_;
+  // higher-order transmission operators (MarchParams::tc_hi), side 0 = a_j, 1 = b_j:
+  // S v_n = sum_{s<=n} K(n,s) v_s = even part (kernel kap, emitted by eq. 8)
+  // + odd part dlt gamma_{n-s} rho^{n-s} (local condition only); the v_0 term
+  // carries the factor f0 (gauge phase), A23-A25
+  const double2 *kap[2];   // [N_T+1] even kernels
+  double2 c0e[2];          // kap[side][0]
+  double2 dlt[2], rho[2], f0[2];
 };
 
 struct MarchParams {
@@ -75,6 +82,7 @@ struct MarchParams {
   double2 c0;                // leading coefficient of the transmission operator
   double2 c2;                // e^{-i pi/4} sqrt(2/dt) (S0^2)
   int32_t s02;               // 1: S0^2 history convolution, 0: Robin
+  int32_t tc_hi;             // 1: higher-order operator (per-system kernels in MarchSys)
   int32_t flux_smem;         // 1: stage the incoming flux series in shared memory
   const double *beta;        // [N_T+1] beta_s
   long long *trace;          // optional per-phase clock trace (debug), NULL in production

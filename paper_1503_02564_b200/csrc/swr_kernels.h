@@ -29,6 +29,7 @@ struct FactorJob {
   int32_t g0, pad_; // global index of local node 0 (V(t,x))
   double2 *q;        // [N_j] out: 1/p_k
   double *er;        // [N_j] out: Re E_k
+  double2 c0L, c0R;  // leading coefficients of the transmission operator at a_j, b_j
 };
 
 __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0, int *err);
@@ -63,8 +64,8 @@ cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, con
                              int NT, const double2 *tw, cudaStream_t st);
 
 struct MarchShape { int M, P, CS, K; };
-MarchShape choose_march_shape(int Nj, int K, int NT);
-size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
+MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi = false);
+size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem, bool tc_hi = false);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
 size_t march_stream_smem_bytes(int NT);
 cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, double2 *zst, int *flags, double2 *vals,

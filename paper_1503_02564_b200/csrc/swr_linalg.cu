@@ -41,8 +41,8 @@ __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, dou
       if (k > 0) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (Wl + 3.0 * Wk) / 12.0; }
       if (k < Nj - 1) { Md += h / 3.0; Sd += 1.0 / h; MWd += h * (3.0 * Wk + Wr) / 12.0; }
       double2 D = make_double2(-Sd + MWd, (2.0 / dt) * Md);
-      if (k == 0 && J.has_left) D = csub(D, c0);
-      if (k == Nj - 1 && J.has_right) D = csub(D, c0);
+      if (k == 0 && J.has_left) D = csub(D, J.c0L);
+      if (k == Nj - 1 && J.has_right) D = csub(D, J.c0R);
       sD[wl][lane] = D;
       sE[wl][lane] = (k < Nj - 1) ? 1.0 / h + h * (Wk + Wr) / 12.0 : 0.0;
     }

@@ -477,6 +477,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   double2 *sApre = tabbase + 2 * kScanTabD2(P);         // [M][P] prefix products of the forward maps
   double2 *sG = sApre + M * P;                          // [P] coupling of the forward carry into x_s
   double *sbeta = reinterpret_cast<double *>(sG + P);   // [NT+1]
+  double2 *kapS = reinterpret_cast<double2 *>(sbeta + ((NT + 2) & ~1));   // tc_hi: [K][2][NT+1] even kernels
 
   const int flags = G[0].flags;
   const bool has_left = flags & SYS_HAS_LEFT, has_right = flags & SYS_HAS_RIGHT;
@@ -499,6 +500,13 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
+  if (!TDM && p.tc_hi) {
+    for (int k = 0; k < K; k++)
+      for (int sd = 0; sd < 2; sd++) {
+        const double2 *kp = G[k].kap[sd];
+        for (int i = t; i <= NT; i += P) kapS[(k * 2 + sd) * (NT + 1) + i] = kp ? kp[i] : cz();
+      }
+  }
   if (p.flux_smem) {
     for (int k = 0; k < K; k++) {
       const double2 *l = G[k].lin, *r = G[k].rin;
@@ -571,16 +579,26 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     er_prev *= ikappa;
   }
   const double eimk = eim * ikappa;
+  // odd part of order-4 operators: B_n = sum_{s<n} rho^{n-s} v'_s (owner registers)
+  double2 Bodd[K][2];
+#pragma unroll
+  for (int r = 0; r < K; r++) Bodd[r][0] = Bodd[r][1] = cz();
   if (first) {
 #pragma unroll
-    for (int r = 0; r < K; r++) hva[r * (NT + 1)] = u[r][0];
+    for (int r = 0; r < K; r++) {
+      hva[r * (NT + 1)] = (!TDM && p.tc_hi) ? cmul(G[r].f0[0], u[r][0]) : u[r][0];   // v'_0
+      if (!TDM && p.tc_hi) Bodd[r][0] = cmul(G[r].rho[0], hva[r * (NT + 1)]);
+    }
   }
   if (last) {
 #pragma unroll
     for (int i = 0; i < M; i++)
       if (i == ib) {
 #pragma unroll
-        for (int r = 0; r < K; r++) hvb[r * (NT + 1)] = u[r][i];
+        for (int r = 0; r < K; r++) {
+          hvb[r * (NT + 1)] = (!TDM && p.tc_hi) ? cmul(G[r].f0[1], u[r][i]) : u[r][i];
+          if (!TDM && p.tc_hi) Bodd[r][1] = cmul(G[r].rho[1], hvb[r * (NT + 1)]);
+        }
       }
   }
   // halo of u_0; later steps get their neighbour values without a barrier
@@ -825,6 +843,16 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
           double2 d = cz();
           if (owns_a) {
             double2 h = cz();
+            if (p.tc_hi) {
+              // even history (emitted) + odd part (local condition only), A25
+              const double2 *hv = hva + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 0) * 32;
+              const double2 *kp = kapS + (r * 2 + 0) * (NT + 1);
+              h = cmul(kp[1], hv[n - 1]);
+              if (n >= 2) h = cfma(kp[2], hv[n - 2], h);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hq[qq]);
+              sH[2 * r] = h;
+              d = csub(cfma(cscale(2.0, G[r].dlt[0]), Bodd[r][0], h), flux(r, 0, n));
+            } else {
             if (p.s02) {
               const double2 *hv = hva + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 0) * 32;
               h = cscale(sbeta[1], hv[n - 1]);
@@ -834,6 +862,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
             }
             sH[2 * r] = h;
             d = csub(h, flux(r, 0, n));                 // b_n - l_n at row 0
+            }
           }
           const double2 f = ifold(d, ikappa);
           uL[r] = make_double2(fma(-2.0, u[r][0].x, f.x), fma(-2.0, u[r][0].y, f.y));
@@ -842,6 +871,15 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
           double2 d = cz();
           if (owns_b) {
             double2 h = cz();
+            if (p.tc_hi) {
+              const double2 *hv = hvb + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 1) * 32;
+              const double2 *kp = kapS + (r * 2 + 1) * (NT + 1);
+              h = cmul(kp[1], hv[n - 1]);
+              if (n >= 2) h = cfma(kp[2], hv[n - 2], h);
+              for (int qq = 0; qq < nw; qq++) h = cadd(h, hq[qq]);
+              sH[2 * r + 1] = h;
+              d = csub(cfma(cscale(2.0, G[r].dlt[1]), Bodd[r][1], h), flux(r, 1, n));
+            } else {
             if (p.s02) {
               const double2 *hv = hvb + r * (NT + 1), *hq = hred + ((r * 2 + (n & 1)) * 2 + 1) * 32;
               h = cscale(sbeta[1], hv[n - 1]);
@@ -851,6 +889,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
             }
             sH[2 * r + 1] = h;
             d = csub(h, flux(r, 1, n));                 // b_n - r_n at row N_j - 1
+            }
           }
           const double2 f = ifold(d, ikappa);
 #pragma unroll
@@ -898,11 +937,15 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     // after the forward-scan barrier), reduced per warp into hred; run by the
     // CTA holding that side while it waits for the other CTAs' totals
     auto history = [&](int side) {
-      if (!(p.s02 && n + 2 <= NT)) return;
+      if (!((p.s02 || p.tc_hi) && n + 2 <= NT)) return;
 #pragma unroll
       for (int r = 0; r < K; r++) {
         double2 acc = cz();
         const double2 *hv = (side ? hvb : hva) + r * (NT + 1);
+        if (p.tc_hi) {
+          const double2 *kp = kapS + (r * 2 + side) * (NT + 1);
+          for (int s = t; s <= n - 1; s += P) acc = cfma(kp[n + 2 - s], hv[s], acc);
+        } else
         for (int s = t; s <= n - 1; s += P) {
           const double b = sbeta[n + 2 - s];
           acc.x = fma(b, hv[s].x, acc.x);
@@ -969,9 +1012,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll
       for (int r = 0; r < K; r++) {
         hva[r * (NT + 1) + n] = x[r];
+        if (p.tc_hi) Bodd[r][0] = cmul(G[r].rho[0], cadd(Bodd[r][0], x[r]));
         double2 *outl = G[r].out_left;
         if (owns_a && outl) {
-          const double2 sv = cfma(p.c0, x[r], sH[2 * r]);   // S v_n(a_j) = c0 v_n + H_a
+          const double2 sv = cfma(p.tc_hi ? G[r].c0e[0] : p.c0, x[r], sH[2 * r]);   // S v_n(a_j) = c0 v_n + H_a
           const double2 l = flux(r, 0, n);
           outl[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
         }
@@ -981,9 +1025,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll
       for (int r = 0; r < K; r++) {
         hvb[r * (NT + 1) + n] = xb[r];
+        if (p.tc_hi) Bodd[r][1] = cmul(G[r].rho[1], cadd(Bodd[r][1], xb[r]));
         double2 *outr = G[r].out_right;
         if (owns_b && outr) {
-          const double2 sv = cfma(p.c0, xb[r], sH[2 * r + 1]);
+          const double2 sv = cfma(p.tc_hi ? G[r].c0e[1] : p.c0, xb[r], sH[2 * r + 1]);
           const double2 rv = flux(r, 1, n);
           outr[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
         }
@@ -1302,7 +1347,7 @@ static const Inst kInst[] = {
     {1, 1, 512}, {2, 1, 512}, {4, 1, 512}, {6, 1, 256}, {8, 1, 256}, {11, 1, 256},
     {3, 2, 256}, {3, 3, 256}};
 
-MarchShape choose_march_shape(int Nj, int K, int NT) {
+MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi) {
   MarchShape best{0, 0, 0, 0};
   double best_cost = 1e300;
   const char *pm = getenv("SWR_MARCH_PMAX");
@@ -1319,7 +1364,7 @@ MarchShape choose_march_shape(int Nj, int K, int NT) {
       int P = (int)((per + 31) / 32 * 32);
       if (P < 32) P = 32;
       if (P > in.PMAX) continue;
-      if (march_smem_bytes({M, P, CS, K}, NT, true) > 227 * 1024) continue;
+      if (march_smem_bytes({M, P, CS, K}, NT, true, tc_hi) > 227 * 1024) continue;
       double padded = (double)CS * P * M;
       double cost = padded * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
       if (cost < best_cost) { best_cost = cost; best = {M, P, CS, K}; }
@@ -1392,12 +1437,13 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
   }
 }
 
-size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
+size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem, bool tc_hi) {
   const size_t K = s.K;
   size_t d2 = 2 + K * s.M * s.P + 2 * K * s.P + 2 * (size_t)s.P + 2 * (32 + 32 * K + 32 * (1 + K)) +
               2 * K * (NT + 1) + 128 * K + 2 * K + (flux_smem ? 2 * K * NT : 0) +
               2 * (size_t)kScanTabD2(s.P) + (size_t)s.M * s.P + s.P;   // scan tables, Apre, G
-  return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
+  return d2 * sizeof(double2) + sizeof(double) * (size_t)((NT + 2) & ~1) +
+         (tc_hi ? (size_t)2 * K * (NT + 1) * sizeof(double2) : 0);
 }
 
 template <int M, int K, int PMAX>
@@ -1429,7 +1475,7 @@ static cudaError_t launch_m(const MarchParams &p, const MarchShape &s, size_t sm
 
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st) {
   p.CS = s.CS;
-  const size_t smem = march_smem_bytes(s, p.NT, p.flux_smem);
+  const size_t smem = march_smem_bytes(s, p.NT, p.flux_smem, p.tc_hi != 0);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
 #define SWR_CASE(MM, KK, PP) \
   if (s.M == MM && s.K == KK && s.P <= PP) return launch_m<MM, KK, PP>(p, s, smem, st);

@@ -111,8 +111,15 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 
   // initial state
   for (int k = rc0 + t; k < rc1; k += P) u[k] = S.u0 ? S.u0[k] : cz();
-  if (histL && t == 0) hvL[0] = S.u0 ? S.u0[0] : cz();
-  if (histR && t == 0) hvR[0] = S.u0 ? S.u0[Nj - 1] : cz();
+  // v'_0 (times the gauge factor f0 for the higher-order operators)
+  if (histL && t == 0) hvL[0] = p.tc_hi ? cmul(S.f0[0], S.u0 ? S.u0[0] : cz()) : (S.u0 ? S.u0[0] : cz());
+  if (histR && t == 0) hvR[0] = p.tc_hi ? cmul(S.f0[1], S.u0 ? S.u0[Nj - 1] : cz()) : (S.u0 ? S.u0[Nj - 1] : cz());
+  // odd part of order-4 operators, B_n = sum_{s<n} rho^{n-s} v'_s (held by the end-row threads)
+  double2 BoL = cz(), BoR = cz();
+  if (p.tc_hi) {
+    if (own0) BoL = cmul(S.rho[0], cmul(S.f0[0], S.u0 ? S.u0[0] : cz()));
+    if (ownL) BoR = cmul(S.rho[1], cmul(S.f0[1], S.u0 ? S.u0[Nj - 1] : cz()));
+  }
   __syncthreads();
   __threadfence();
   if (t == 0) st_release(fdone + c, 0);
@@ -137,7 +144,10 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       if (!(sd == 0 ? histL : histR)) continue;
       const double2 *hv = sd == 0 ? hvL : hvR;
       double2 acc = cz();
-      if (p.s02)
+      if (p.tc_hi) {
+        const double2 *kp = S.kap[sd];
+        for (int s = t; s <= n - 1; s += P) acc = cfma(__ldg(kp + n - s), hv[s], acc);
+      } else if (p.s02)
         for (int s = t; s <= n - 1; s += P)
           acc = make_double2(fma(p.beta[n - s], hv[s].x, acc.x), fma(p.beta[n - s], hv[s].y, acc.y));
 #pragma unroll
@@ -147,14 +157,15 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       if (t == 0) {
         double2 hs = cz();
         for (int w = 0; w < (P >> 5); w++) hs = cadd(hs, red[w]);
-        (sd == 0 ? sHL : sHR) = p.s02 ? cmul(p.c2, hs) : cz();
+        (sd == 0 ? sHL : sHR) = p.tc_hi ? hs : (p.s02 ? cmul(p.c2, hs) : cz());
       }
       __syncthreads();
     }
     __syncthreads();
     // end-row folds (k_march): d = H_n - l_n at row 0, H_n - r_n at row N_j - 1
-    const double2 dL = (own0 && has_left) ? csub(sHL, flux(0, n)) : cz();
-    const double2 dR = (ownL && has_right) ? csub(sHR, flux(1, n)) : cz();
+    // (the odd part of order-4 operators enters the local condition only, A25)
+    const double2 dL = (own0 && has_left) ? csub(cfma(cscale(2.0, S.dlt[0]), BoL, sHL), flux(0, n)) : cz();
+    const double2 dR = (ownL && has_right) ? csub(cfma(cscale(2.0, S.dlt[1]), BoR, sHR), flux(1, n)) : cz();
     auto sval = [&](int k, double2 um, double2 uk, double2 up) -> double2 {
       // u_{k-1} + 4 u_k + u_{k+1} with the P1 end rows (h/6)(2, 1) and the folds
       if (k == 0) {
@@ -243,15 +254,17 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
     // record v_n and S v_n at the interfaces (eq. 8)
     if (own0) {
       if (histL) hvL[n] = x0v;
+      if (p.tc_hi) BoL = cmul(S.rho[0], cadd(BoL, x0v));
       if (has_left && S.out_left) {
-        const double2 sv = cfma(p.c0, x0v, sHL), l = flux(0, n);
+        const double2 sv = cfma(p.tc_hi ? S.c0e[0] : p.c0, x0v, sHL), l = flux(0, n);
         S.out_left[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
       }
     }
     if (ownL) {
       if (histR) hvR[n] = xLv;
+      if (p.tc_hi) BoR = cmul(S.rho[1], cadd(BoR, xLv));
       if (has_right && S.out_right) {
-        const double2 sv = cfma(p.c0, xLv, sHR), r = flux(1, n);
+        const double2 sv = cfma(p.tc_hi ? S.c0e[1] : p.c0, xLv, sHR), r = flux(1, n);
         S.out_right[n - 1] = make_double2(fma(2.0, sv.x, -r.x), fma(2.0, sv.y, -r.y));
       }
     }

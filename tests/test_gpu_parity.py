@@ -147,6 +147,31 @@ def test_solver_variant_parity(oracle_mod, gpu, name, alg, kry, pot):
     assert rel(uT, ro["uT"]) <= 1e-10, info
 
 
+TC_CASES = [("s03", si.TC_S03), ("s04", si.TC_S04), ("s12", si.TC_S12), ("s14", si.TC_S14)]
+
+
+@pytest.mark.parametrize("name,tc", TC_CASES, ids=[c[0] for c in TC_CASES])
+@pytest.mark.parametrize("march", ["resident", "stream"])
+def test_higher_order_tc_parity(oracle_mod, gpu, name, tc, march, monkeypatch):
+    """Potential (S0^3, S0^4) and gauge (S1^2, S1^4) transmission operators
+    (readings A23-A25) through the new algorithm on
+    V(x) = -x^2, both march kernels: equal GMRES counts, u(T) within 1e-10."""
+    if march == "stream":
+        monkeypatch.setenv("SWR_MARCH", "stream")
+    else:
+        monkeypatch.delenv("SWR_MARCH", raising=False)
+    p = si.config("C1", transmission=tc, potential=si.POT_VX, N=4)
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert rel(uT, ro["uT"]) <= 1e-10
+    d_g, X_g = g_.get_interface(0)
+    assert rel(d_g.cpu().numpy(), o.apply_R(np.zeros(o.ng), use_u0=True), 1.0) <= 1e-12
+    assert rel(X_g.cpu().numpy(), o.build_L(), 1.0) <= 1e-12
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)

@@ -11,7 +11,7 @@ t0 = time.time()
 r = oracle.Oracle(p, arr).solve()
 t1 = time.time()
 print(f"oracle C5: status {r['status']} iterations {r['iterations']} time {t1 - t0:.0f} s", flush=True)
-np.save("gpurun_out/oracle_c5_uT.npy", r["uT"])
+np.save("/tmp/oracle_c5_uT.npy", r["uT"])   # 67 MB: kept off gpurun_out (64 MiB limit)
 np.save("gpurun_out/oracle_c5_hist.npy", np.array(r["history"]))
 try:
     import torch
