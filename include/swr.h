@@ -71,12 +71,14 @@ enum swr_potential {
   SWR_POT_CUBIC = 3            /* f(u) = lambda |u|^2 */
 };
 
-/* Transmission operators (discrete P:218-238): Robin -ip;
- * potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4.  Orders
- * above S0^2 need a time-independent potential (V = 0 or V(x)) and the NEW or
- * CLASSICAL algorithm (readings A23-A25). */
+/* Transmission operators (discrete P:218-267): Robin -ip;
+ * potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4; Pade
+ * strategy S2^{2,m}, S2^{4,m} with m = pade_m poles (coefficients: reading
+ * A26).  Operators other than Robin / S0^2 need a time-independent potential
+ * (V = 0 or V(x)) and the NEW or CLASSICAL algorithm (readings A23-A26). */
 enum swr_transmission {
-  SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1, SWR_TC_S0_3 = 2, SWR_TC_S0_4 = 3, SWR_TC_S1_2 = 4, SWR_TC_S1_4 = 5
+  SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1, SWR_TC_S0_3 = 2, SWR_TC_S0_4 = 3, SWR_TC_S1_2 = 4, SWR_TC_S1_4 = 5,
+  SWR_TC_S2_2 = 6, SWR_TC_S2_4 = 7
 };
 enum swr_algorithm {
   SWR_ALG_NEW = 0,       /* Algorithm 3 */
@@ -120,6 +122,7 @@ typedef struct {
                                  (the paper's solver library; reading A6);
                                  2 = CGS2 (one reorthogonalization); 0 = 1 */
   int32_t krylov;             /* swr_krylov: interface solver (0 = GMRES) */
+  int32_t pade_m;             /* Pade poles m >= 1 for SWR_TC_S2_2 / SWR_TC_S2_4 (else ignored) */
 } swr_config;
 
 typedef struct {

@@ -38,6 +38,7 @@ class _Problem(C.Structure):
         ("tol_inner", C.c_double), ("maxit_inner", C.c_int32),
         ("tol_fp", C.c_double), ("maxit_fp", C.c_int32),
         ("g0", C.c_void_p), ("gs_passes", C.c_int32), ("krylov", C.c_int32),
+        ("pade_m", C.c_int32),
     ]
 
 
@@ -75,8 +76,12 @@ def lib():
         _lib.or_bicgstab_dense.argtypes = [i32, vp, vp, vp, C.c_double, i32, vp, vp]
         _lib.or_solve.argtypes = [P, vp, C.POINTER(_Report), vp]
         _lib.or_monodomain.argtypes = [P, vp, vp]
+        _lib.or_pade_coeffs.argtypes = [i32, vp, vp]
+        _lib.or_pade_coeffs.restype = None
+        _lib.or_tc_apply.argtypes = [P, C.c_double, C.c_double, i32, vp, vp]
         for f in ("or_sizes", "or_thomas", "or_subdomain_matrix", "or_march", "or_apply_R",
-                  "or_build_L", "or_gmres_dense", "or_bicgstab_dense", "or_solve", "or_monodomain"):
+                  "or_build_L", "or_gmres_dense", "or_bicgstab_dense", "or_solve", "or_monodomain",
+                  "or_tc_apply"):
             getattr(_lib, f).restype = i32
         _lib.or_coeffs.restype = None
         _lib.or_fem.restype = None
@@ -117,6 +122,7 @@ class Oracle:
         s.g0 = _ptr(self.keep.get("g0"))
         s.gs_passes = p.gs_passes
         s.krylov = p.krylov
+        s.pade_m = getattr(p, "pade_m", 0)
         self.s = s
         self.L = lib()
         self.Nx, self.NT, self.Nj = p.Nx, p.NT, p.Nj
@@ -128,6 +134,14 @@ class Oracle:
         st = self.L.or_subdomain_matrix(C.byref(self.s), j, n, int(force_zero), _ptr(lo), _ptr(di), _ptr(up))
         assert st == 0, st
         return lo, di, up
+
+    def tc_apply(self, v, W=0.0, dnW=0.0):
+        """S v_n, n = 1..len(v)-1, of the configured operator at one boundary point."""
+        v = _c128(v)
+        out = np.zeros(len(v) - 1, np.complex128)
+        st = self.L.or_tc_apply(C.byref(self.s), float(W), float(dnW), len(v) - 1, _ptr(v), _ptr(out))
+        assert st == 0, st
+        return out
 
     def march(self, j, lin=None, rin=None, use_u0=True, force_zero=False):
         lin, rin = _c128(lin), _c128(rin)
@@ -193,6 +207,12 @@ def fem(nn, h, W=None):
     arrs = [np.zeros(nn) if i % 2 == 0 else np.zeros(max(nn - 1, 1)) for i in range(6)]
     lib().or_fem(nn, h, _ptr(W), *[_ptr(a) for a in arrs])
     return arrs  # Mdiag, Moff, Sdiag, Soff, MWdiag, MWoff
+
+
+def pade_coeffs(m):
+    a, d = np.zeros(m + 1), np.zeros(m + 1)
+    lib().or_pade_coeffs(m, _ptr(a), _ptr(d))
+    return a, d
 
 
 def thomas(lo, di, up, rhs):

@@ -170,12 +170,131 @@ static ocplx or_c0(const or_problem *P) {
   return or_c2(P) * 1.0; /* beta_0 = 1 */
 }
 
+/* ------------------------------------------------------------------ */
+/* Pade strategy S2^{2,m}, S2^{4,m} (P:173-177 continuous, P:241-267     */
+/* discrete).  sqrt(z) ~ sum_{s=0}^m a_s - sum_{s=1}^m a_s d_s/(z + d_s). */
+/* The paper does not give a_s^m, d_s^m (reading A26): the rational       */
+/* approximation of the cited ABC literature, a_0 = 0,                    */
+/* a_s = 1/(m cos^2 th_s), d_s = tan^2 th_s, th_s = (2s-1) pi/(4m).       */
+/* In S2^2 the paper writes d_k^m in one denominator; read as d_s^m.      */
+/* ------------------------------------------------------------------ */
+static int or_is_pade(const or_problem *P) {
+  return P->transmission == OR_TC_S22 || P->transmission == OR_TC_S24;
+}
+
+void or_pade_coeffs(int32_t m, double *a, double *d) {
+  a[0] = 0.0;
+  d[0] = 0.0;
+  for (int32_t s = 1; s <= m; s++) {
+    const double th = (2.0 * s - 1.0) * acos(-1.0) / (4.0 * m);
+    const double c = cos(th);
+    a[s] = 1.0 / (m * c * c);
+    d[s] = tan(th) * tan(th);
+  }
+}
+
+/* State of the auxiliary functions phi^s_{j,n-1} (s = 1..m) and psi_{j,n-1}
+ * of one boundary point, both zero at n = 0. */
+typedef struct { int32_t m; double *a, *d; ocplx *phi; ocplx psi; } pade_state;
+
+static int32_t pade_init(const or_problem *P, pade_state *S) {
+  S->m = P->pade_m;
+  S->a = (double *)calloc((size_t)S->m + 1, sizeof(double));
+  S->d = (double *)calloc((size_t)S->m + 1, sizeof(double));
+  S->phi = (ocplx *)calloc((size_t)S->m + 1, sizeof(ocplx));
+  S->psi = 0.0;
+  if (!S->a || !S->d || !S->phi) return OR_OOM;
+  or_pade_coeffs(S->m, S->a, S->d);
+  return OR_OK;
+}
+
+static void pade_free(pade_state *S) { free(S->a); free(S->d); free(S->phi); }
+
+/* Coefficient of v_{j,n} in S2 v_{j,n}:
+ *   -i (sum_{s=0}^m a_s) + i sum_{s=1}^m a_s d_s / (2i/dt + W + d_s)
+ *   [+ (dnW/4) / (2i/dt + W) for S2^4]. */
+static ocplx pade_c0(const or_problem *P, const tc_side *t, const pade_state *S) {
+  const ocplx s2 = 2.0 * I_ / P->dt;
+  ocplx sa = 0.0, c = 0.0;
+  for (int32_t s = 0; s <= S->m; s++) sa += S->a[s];
+  c = -I_ * sa;
+  for (int32_t s = 1; s <= S->m; s++) c += I_ * S->a[s] * S->d[s] / (s2 + t->W + S->d[s]);
+  if (P->transmission == OR_TC_S24) c += (t->dnW / 4.0) / (s2 + t->W);
+  return c;
+}
+
+/* The rest of S2 v_{j,n}: terms in phi^s_{j,n-1}, psi_{j,n-1}. */
+static ocplx pade_hist(const or_problem *P, const tc_side *t, const pade_state *S) {
+  const ocplx s2 = 2.0 * I_ / P->dt;
+  ocplx h = 0.0;
+  for (int32_t s = 1; s <= S->m; s++) h += I_ * S->a[s] * S->d[s] * (s2 / (s2 + t->W + S->d[s])) * S->phi[s];
+  if (P->transmission == OR_TC_S24) {
+    const double sg = t->dnW > 0 ? 1.0 : (t->dnW < 0 ? -1.0 : 0.0);
+    h += sg * (sqrt(fabs(t->dnW)) / 2.0) * (s2 / (s2 + t->W)) * S->psi;
+  }
+  return h;
+}
+
+/* phi^s_{n-1/2} = v_n/(2i/dt + W + d_s) + (2i/dt)/(2i/dt + W + d_s) phi^s_{n-1},
+ * phi^s_n = 2 phi^s_{n-1/2} - phi^s_{n-1}; psi likewise.
+ * phi, psi depend on |dnW| only, so one state serves both normals. */
+static void pade_advance(const or_problem *P, const tc_side *t, pade_state *S, ocplx vn) {
+  const ocplx s2 = 2.0 * I_ / P->dt;
+  for (int32_t s = 1; s <= S->m; s++) {
+    const ocplx D = s2 + t->W + S->d[s];
+    const ocplx half = vn / D + (s2 / D) * S->phi[s];
+    S->phi[s] = 2.0 * half - S->phi[s];
+  }
+  const ocplx D0 = s2 + t->W;
+  const ocplx half = (sqrt(fabs(t->dnW)) / 2.0) * vn / D0 + (s2 / D0) * S->psi;
+  S->psi = 2.0 * half - S->psi;
+}
+
 /* Leading coefficient K(n, n) of side `side` of subdomain j. */
 static ocplx or_c0_side(const or_problem *P, int32_t j, int32_t side, int32_t fz) {
   if (P->transmission == OR_TC_ROBIN || P->transmission == OR_TC_S02) return or_c0(P);
   tc_side t = or_tc_side(P, j, side, fz);
+  if (or_is_pade(P)) {
+    pade_state S;
+    ocplx c = 0.0;
+    if (pade_init(P, &S) == OR_OK) c = pade_c0(P, &t, &S);
+    pade_free(&S);
+    return c;
+  }
   double a[1] = {1.0}, b[1] = {1.0}, g[1] = {1.0};
   return or_tcK(P, &t, 1, 1, a, b, g);
+}
+
+/* S v_n, n = 1..nsteps, of the discrete transmission operator of one
+ * boundary point with interface data (W, dnW) applied to the trace sequence
+ * v_0..v_nsteps (test hook for the operator pins; same code as the march). */
+int32_t or_tc_apply(const or_problem *P, double W, double dnW, int32_t nsteps, const ocplx *v, ocplx *Sv) {
+  if (nsteps < 1) return OR_ERR_ARG;
+  tc_side t = {W, dnW, 0};
+  if (or_is_pade(P)) {
+    pade_state S;
+    int32_t st = pade_init(P, &S);
+    if (st) { pade_free(&S); return st; }
+    const ocplx c0 = pade_c0(P, &t, &S);
+    for (int32_t n = 1; n <= nsteps; n++) {
+      Sv[n - 1] = c0 * v[n] + pade_hist(P, &t, &S);
+      pade_advance(P, &t, &S, v[n]);
+    }
+    pade_free(&S);
+    return OR_OK;
+  }
+  double *al = (double *)calloc((size_t)nsteps + 1, sizeof(double));
+  double *be = (double *)calloc((size_t)nsteps + 1, sizeof(double));
+  double *ga = (double *)calloc((size_t)nsteps + 1, sizeof(double));
+  if (!al || !be || !ga) { free(al); free(be); free(ga); return OR_OOM; }
+  or_coeffs(nsteps + 1, al, be, ga);
+  for (int32_t n = 1; n <= nsteps; n++) {
+    ocplx acc = 0.0;
+    for (int32_t s = 0; s <= n; s++) acc += or_tcK(P, &t, n, s, al, be, ga) * v[s];
+    Sv[n - 1] = acc;
+  }
+  free(al); free(be); free(ga);
+  return OR_OK;
 }
 
 /* Nodal W_n on subdomain j: W_n = (V_n + V_{n-1})/2. */
@@ -273,15 +392,22 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
   double *Wd = (double *)calloc(nb, sizeof(double));
   double *Wo = (double *)calloc(nb, sizeof(double));
   int32_t st = OR_OK;
+  pade_state pL, pR;
+  memset(&pL, 0, sizeof pL);
+  memset(&pR, 0, sizeof pR);
   if (!u || !v || !vprev || !rhs || !rhs2 || !lo || !di || !up || !va || !vb ||
       !beta || !alpha || !gamma || !Md || !Mo || !Wz || !Wd || !Wo) { st = OR_OOM; goto done; }
+  if (or_is_pade(P) && ((st = pade_init(P, &pL)) || (st = pade_init(P, &pR)))) goto done;
 
   or_coeffs(NT + 1, alpha, beta, gamma);
   or_fem(Nj, P->dx, NULL, Md, Mo, NULL, NULL, NULL, NULL);
   ocplx c0L = or_c0_side(P, j, 0, fz), c0R = or_c0_side(P, j, 1, fz);
   /* leading coefficients of the neighbour's operators at a_j, b_j */
   ocplx c0Lo = c0L, c0Ro = c0R;
-  if (P->transmission >= OR_TC_S03) {
+  if (or_is_pade(P)) {
+    c0Lo = pade_c0(P, &tLo, &pL);
+    c0Ro = pade_c0(P, &tRo, &pR);
+  } else if (P->transmission >= OR_TC_S03) {
     double a1[1] = {1.0}, b1[1] = {1.0}, g1[1] = {1.0};
     c0Lo = or_tcK(P, &tLo, 1, 1, a1, b1, g1);
     c0Ro = or_tcK(P, &tRo, 1, 1, a1, b1, g1);
@@ -319,6 +445,11 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
         Hb = or_c2(P) * Hb;
         Hao = Ha;
         Hbo = Hb;
+      } else if (or_is_pade(P)) {   /* auxiliary recursions */
+        Ha = pade_hist(P, &tL, &pL);
+        Hb = pade_hist(P, &tR, &pR);
+        Hao = pade_hist(P, &tLo, &pL);
+        Hbo = pade_hist(P, &tRo, &pR);
       } else {
         for (int32_t s = 0; s < n; s++) {
           Ha += or_tcK(P, &tL, n, s, alpha, beta, gamma) * va[s];
@@ -367,6 +498,10 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
     }
     va[n] = v[0];
     vb[n] = v[Nj - 1];
+    if (or_is_pade(P)) {
+      pade_advance(P, &tL, &pL, v[0]);
+      pade_advance(P, &tR, &pR, v[Nj - 1]);
+    }
     /* eq. (8) with the neighbour's operator: r_{j-1} = -l_j +
      * (S_{a_j} + S_{b_{j-1}}) v(a_j); the two coincide except for the terms
      * odd in the normal derivative of W (S0^4, S1^4, reading A25) */
@@ -381,6 +516,7 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
 done:
   free(u); free(v); free(vprev); free(rhs); free(rhs2); free(lo); free(di); free(up);
   free(va); free(vb); free(beta); free(alpha); free(gamma); free(Md); free(Mo); free(Wz); free(Wd); free(Wo);
+  pade_free(&pL); pade_free(&pR);
   return st;
 }
 
@@ -798,7 +934,8 @@ int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep, ocplx *g_out) {
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
   if (P->transmission == OR_TC_ROBIN && !(P->robin_p > 0)) return OR_ERR_ARG;
-  if (P->transmission < OR_TC_ROBIN || P->transmission > OR_TC_S14) return OR_ERR_ARG;
+  if (P->transmission < OR_TC_ROBIN || P->transmission > OR_TC_S24) return OR_ERR_ARG;
+  if ((P->transmission == OR_TC_S22 || P->transmission == OR_TC_S24) && P->pade_m < 1) return OR_ERR_ARG;
   if (P->transmission >= OR_TC_S03 && !(P->potential == OR_POT_ZERO || P->potential == OR_POT_VX))
     return OR_UNSUPPORTED;   /* higher orders: time-independent potentials */
   int32_t N = P->N;

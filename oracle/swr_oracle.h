@@ -25,9 +25,12 @@ enum { OR_OK = 0, OR_ERR_ARG = 1, OR_NOT_CONVERGED = 2, OR_ZERO_PIVOT = 3,
        OR_OOM = 9 };
 enum { OR_POT_ZERO = 0, OR_POT_VX = 1, OR_POT_VTX = 2, OR_POT_CUBIC = 3 };
 /* Transmission operators (P:146-170 continuous, P:218-238 discrete):
- * Robin -ip; potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4.
- * Orders above 2 need a time-independent potential here (V = 0 or V(x)). */
-enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1, OR_TC_S03 = 2, OR_TC_S04 = 3, OR_TC_S12 = 4, OR_TC_S14 = 5 };
+ * Robin -ip; potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4;
+ * Pade strategy S2^{2,m}, S2^{4,m} (m = pade_m poles).
+ * Operators other than Robin / S0^2 need a time-independent potential here
+ * (V = 0 or V(x)). */
+enum { OR_TC_ROBIN = 0, OR_TC_S02 = 1, OR_TC_S03 = 2, OR_TC_S04 = 3, OR_TC_S12 = 4, OR_TC_S14 = 5,
+       OR_TC_S22 = 6, OR_TC_S24 = 7 };
 enum { OR_ALG_NEW = 0, OR_ALG_PRECOND = 1, OR_ALG_CLASSICAL = 2 };
 /* Interface solver (reading A20/A21): GMRES(restart), BiCGStab, or the fixed
  * point of the algorithm (NEW: g <- d + L g; CLASSICAL: g <- R(g), Algorithm 1). */
@@ -54,6 +57,7 @@ typedef struct {
                                  KSPGMRES orthogonalization, reading A6), 2 = CGS2; 0 = 1 */
   int32_t krylov;             /* OR_KRY_*: interface solver (outer, and the inner P^{-1} solve
                                  for GMRES / BiCGStab; P^{-1} is never a fixed point) */
+  int32_t pade_m;             /* number of Pade poles m >= 1 for OR_TC_S22 / OR_TC_S24 */
 } or_problem;
 
 typedef struct {
@@ -69,6 +73,11 @@ typedef struct {
 void or_coeffs(int32_t n, double *alpha, double *beta, double *gamma);
 
 /* Mesh / partition sizes. */
+/* Pade coefficients a_s^m, d_s^m, s = 0..m (reading A26, a_0 = d_0 = 0). */
+void or_pade_coeffs(int32_t m, double *a, double *d);
+/* S v_n (n = 1..nsteps) of the configured transmission operator at one
+ * boundary point with interface data W, dnW, applied to v_0..v_nsteps. */
+int32_t or_tc_apply(const or_problem *P, double W, double dnW, int32_t nsteps, const ocplx *v, ocplx *Sv);
 int32_t or_sizes(const or_problem *P, int32_t *Nx, int32_t *NT, int32_t *Nj);
 
 /* P1 FEM matrices on a uniform mesh of nn nodes, spacing h, nodal weight W

@@ -130,6 +130,7 @@ struct swr_handle {
   int N, potential, transmission, algorithm, restart, maxit, maxit_inner, maxit_fp, n_terms;
   int gs_passes = 1;   // Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
   int krylov = 0;      // swr_krylov
+  int pade_m = 0;      // Pade poles (SWR_TC_S2_*)
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
@@ -398,6 +399,15 @@ int setup_tc(swr_handle *h) {
   }
   const cplx cc2 = c2(h->c2v), e3 = cplx(1.0, 1.0) / std::sqrt(2.0) * std::sqrt(h->dt / 2.0);
   const int tc = h->transmission;
+  const bool pade = tc == SWR_TC_S2_2 || tc == SWR_TC_S2_4;
+  // Pade poles (reading A26): a_s = 1/(m cos^2 th_s), d_s = tan^2 th_s, th_s = (2s-1) pi/(4m), a_0 = 0
+  const int pm = h->pade_m;
+  std::vector<double> pa(pade ? pm + 1 : 0, 0.0), pd(pade ? pm + 1 : 0, 0.0);
+  for (int s = 1; pade && s <= pm; s++) {
+    const double th = (2.0 * s - 1.0) * M_PI / (4.0 * pm), c = std::cos(th), t = std::tan(th);
+    pa[s] = 1.0 / (pm * c * c);
+    pd[s] = t * t;
+  }
   const bool gauge = tc == SWR_TC_S1_2 || tc == SWR_TC_S1_4, order4 = tc == SWR_TC_S0_4 || tc == SWR_TC_S1_4;
   std::vector<double2> K((size_t)N * 2 * (NT + 1));
   for (int j = 1; j <= N; j++) {
@@ -408,11 +418,51 @@ int setup_tc(swr_handle *h) {
       const double dnW = side == 0 ? -dxW : dxW;
       const double th = W * h->dt;
       double2 *k = K.data() + ((size_t)(j - 1) * 2 + side) * (NT + 1);
+      const size_t o = (size_t)(j - 1) * 2 + side;
+      if (pade) {
+        // Eliminating phi^s, psi from S2: with
+        // D_s = 2i/dt + W + d_s and rho_s = (2i/dt - W - d_s)/D_s,
+        //   phi^s_n = (2/D_s) v_n + rho_s phi^s_{n-1}   (v_0 never enters)
+        // so S2 v_n = kap_0 v_n + sum_{t=1}^{n-1} kap_{n-t} v_t with
+        //   kap_0 = -i sum_s a_s + i sum_s a_s d_s / D_s,
+        //   kap_k = sum_s i a_s d_s (2i/dt) (2/D_s^2) rho_s^{k-1}   (k >= 1);
+        // S2^4 adds (dnW/4)/D_0 v_n and sum_t (dnW/4)(2i/dt)(2/D_0^2) rho_0^{n-1-t} v_t,
+        // i.e. the odd part 2 dlt rho_0^{n-t} with dlt = (dnW/4)(2i/dt)/(D_0^2 rho_0).
+        const cplx s2(0.0, 2.0 / h->dt);
+        cplx k0(0.0, 0.0);
+        for (int s = 1; s <= pm; s++) k0 += cplx(0.0, -1.0) * pa[s];
+        for (int m = 1; m <= NT; m++) k[m] = make_double2(0, 0);
+        std::vector<cplx> acc(NT + 1, cplx(0.0, 0.0));
+        for (int s = 1; s <= pm; s++) {
+          const cplx D = s2 + W + pd[s], rho = (s2 - W - pd[s]) / D;
+          k0 += cplx(0.0, 1.0) * pa[s] * pd[s] / D;
+          const cplx w = cplx(0.0, 1.0) * pa[s] * pd[s] * s2 * 2.0 / (D * D);
+          cplx r(1.0, 0.0);
+          for (int m = 1; m <= NT; m++) {
+            acc[m] += w * r;
+            r *= rho;
+          }
+        }
+        acc[0] = k0;
+        for (int m = 0; m <= NT; m++) k[m] = d2(acc[m]);
+        cplx c0o(0.0), dlt(0.0), rho0(1.0, 0.0);
+        if (tc == SWR_TC_S2_4) {
+          const cplx D0 = s2 + W;
+          rho0 = (s2 - W) / D0;
+          c0o = (dnW / 4.0) / D0;
+          dlt = (dnW / 4.0) * s2 / (D0 * D0 * rho0);
+        }
+        h->tc_c0e[o] = k[0];
+        h->tc_dlt[o] = d2(dlt);
+        h->tc_c0[o] = d2(k0 + c0o);
+        h->tc_rho[o] = d2(rho0);
+        h->tc_f0[o] = make_double2(0, 0);
+        continue;
+      }
       for (int m = 0; m <= NT; m++) {
         cplx v = gauge ? cc2 * be[m] * std::exp(cplx(0.0, th * m)) : cc2 * be[m] - e3 * (W / 2.0) * al[m];
         k[m] = d2(v);
       }
-      const size_t o = (size_t)(j - 1) * 2 + side;
       const cplx dlt = order4 ? cplx(0.0, -1.0) * (dnW / 4.0) * (h->dt / 2.0) : cplx(0.0);
       h->tc_c0e[o] = k[0];
       h->tc_dlt[o] = d2(dlt);
@@ -967,7 +1017,11 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     return SWR_ERR_INVALID_ARG;
   }
   if (cfg->transmission == SWR_TC_ROBIN && !(cfg->robin_p > 0)) { g_detail = "Robin needs p > 0"; return SWR_ERR_INVALID_ARG; }
-  if (cfg->transmission < SWR_TC_ROBIN || cfg->transmission > SWR_TC_S1_4) return SWR_ERR_INVALID_ARG;
+  if (cfg->transmission < SWR_TC_ROBIN || cfg->transmission > SWR_TC_S2_4) return SWR_ERR_INVALID_ARG;
+  if ((cfg->transmission == SWR_TC_S2_2 || cfg->transmission == SWR_TC_S2_4) && cfg->pade_m < 1) {
+    g_detail = "the Pade operators need pade_m >= 1";
+    return SWR_ERR_INVALID_ARG;
+  }
   if (cfg->transmission >= SWR_TC_S0_3 &&
       (!(cfg->potential == SWR_POT_ZERO || cfg->potential == SWR_POT_VX) || cfg->algorithm == SWR_ALG_PRECOND)) {
     g_detail = "orders above S0^2 need a time-independent potential and the NEW or CLASSICAL algorithm";
@@ -1000,6 +1054,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->restart = cfg->restart > 0 ? cfg->restart : 30; h->maxit = cfg->maxit > 0 ? cfg->maxit : 2000;
   h->gs_passes = cfg->gs_passes == 2 ? 2 : 1;
   h->krylov = cfg->krylov;
+  h->pade_m = cfg->pade_m;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;

@@ -19,7 +19,7 @@ import numpy as np
 # enum values mirrored by both sides' own headers (include/swr.h and
 # oracle/swr_oracle.h); they are the ABI's argument codes, not arithmetic.
 POT_ZERO, POT_VX, POT_VTX, POT_CUBIC = 0, 1, 2, 3
-TC_ROBIN, TC_S02, TC_S03, TC_S04, TC_S12, TC_S14 = 0, 1, 2, 3, 4, 5
+TC_ROBIN, TC_S02, TC_S03, TC_S04, TC_S12, TC_S14, TC_S22, TC_S24 = 0, 1, 2, 3, 4, 5, 6, 7
 ALG_NEW, ALG_PRECOND, ALG_CLASSICAL = 0, 1, 2
 KRY_GMRES, KRY_BICGSTAB, KRY_FIXED_POINT = 0, 1, 2
 
@@ -51,6 +51,7 @@ class Problem:
     g0_random: bool = False
     gs_passes: int = 1          # Gram-Schmidt passes in GMRES: 1 = CGS (PETSc default, reading A6), 2 = CGS2
     krylov: int = KRY_GMRES     # interface solver: GMRES, BiCGStab or the algorithm's fixed point (A20/A21)
+    pade_m: int = 20            # Pade poles m for TC_S22 / TC_S24 (the paper tabulates m = 20, 50, 100)
     seed: int = 7
     name: str = ""
 

@@ -62,6 +62,12 @@ def test_setup_rejects_bad_config_without_gpu_work():
     c.algorithm = si.ALG_NEW
     c.potential = si.POT_CUBIC          # NEW needs V(x)
     assert L.swr_setup(C.byref(c), C.byref(h)) == 1
+    c.potential = si.POT_VX
+    c.transmission = si.TC_S22
+    c.pade_m = 0                        # Pade needs m >= 1
+    assert L.swr_setup(C.byref(c), C.byref(h)) == 1
+    c.transmission = 8                  # no such operator
+    assert L.swr_setup(C.byref(c), C.byref(h)) == 1
     assert not h.value
     del np
 

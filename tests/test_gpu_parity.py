@@ -147,14 +147,16 @@ def test_solver_variant_parity(oracle_mod, gpu, name, alg, kry, pot):
     assert rel(uT, ro["uT"]) <= 1e-10, info
 
 
-TC_CASES = [("s03", si.TC_S03), ("s04", si.TC_S04), ("s12", si.TC_S12), ("s14", si.TC_S14)]
+TC_CASES = [("s03", si.TC_S03), ("s04", si.TC_S04), ("s12", si.TC_S12), ("s14", si.TC_S14),
+            ("s22", si.TC_S22), ("s24", si.TC_S24)]
 
 
 @pytest.mark.parametrize("name,tc", TC_CASES, ids=[c[0] for c in TC_CASES])
 @pytest.mark.parametrize("march", ["resident", "stream"])
 def test_higher_order_tc_parity(oracle_mod, gpu, name, tc, march, monkeypatch):
-    """Potential (S0^3, S0^4) and gauge (S1^2, S1^4) transmission operators
-    (readings A23-A25) through the new algorithm on
+    """Potential (S0^3, S0^4), gauge (S1^2, S1^4) and Pade (S2^{2,20},
+    S2^{4,20}) transmission operators (readings
+    A23-A26) through the new algorithm on
     V(x) = -x^2, both march kernels: equal GMRES counts, u(T) within 1e-10."""
     if march == "stream":
         monkeypatch.setenv("SWR_MARCH", "stream")

@@ -9,6 +9,8 @@ import math
 import os
 from fractions import Fraction
 
+import dataclasses
+
 import numpy as np
 import pytest
 
@@ -415,6 +417,87 @@ def test_higher_order_tc_converge_to_monodomain(oracle_mod, tc):
     st, um, _ = o.monodomain()
     assert r["status"] == 0 and r["converged"]
     assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
+PADE_TC = [si.TC_S22, si.TC_S24]
+
+
+@pytest.mark.parametrize("m", [1, 5, 20, 100])
+def test_pade_coefficients_approximate_sqrt(oracle_mod, m):
+    """Reading A26: sqrt(z) ~ R_m(z) = sum_s a_s - sum_s a_s d_s/(z + d_s)
+    (the form of P:243-247).  R_m(1) = 1 exactly for every m, and R_m
+    converges to numpy's sqrt on the right half plane as m grows."""
+    a, d = oracle_mod.pade_coeffs(m)
+    assert a[0] == 0.0 and np.all(a[1:] > 0) and np.all(np.diff(d[1:]) > 0)
+
+    def R(z):
+        return a.sum() - np.sum(a[1:] * d[1:] / (z + d[1:]))
+
+    assert abs(R(1.0) - 1.0) <= 1e-14
+    z = np.array([0.3, 2.0, 1 + 3j, 5j, 0.5 - 2j])
+    err = max(abs(R(zz) - np.sqrt(zz)) / abs(np.sqrt(zz)) for zz in z)
+    assert err <= {1: 1.0, 5: 2e-2, 20: 1e-6, 100: 1e-13}[m], err
+
+
+@pytest.mark.parametrize("tc", PADE_TC)
+@pytest.mark.parametrize("m", [3, 20])
+def test_pade_operator_symbol(oracle_mod, tc, m):
+    """The auxiliary recursions of P:248-265 are Crank-Nicolson for
+    (i d_t + W + d_s) phi = v on the v-form (midpoint) sequence, so in the
+    z-transform (tau = one-step delay, z_d = (2i/dt)(1 - tau)/(1 + tau)):
+    S2^2 = -i R_m(z_d + W) and S2^4 = S2^2 + (d_n W/4)/(z_d + W).
+    The impulse response of the oracle's operator, summed as a power series,
+    matches the rational symbol evaluated directly (pins D_s, the 2i/dt
+    factors, the phi/psi updates and the sign conventions)."""
+    p = si.config("C1", transmission=tc, potential=si.POT_VX, pade_m=m)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    a, d = oracle_mod.pade_coeffs(m)
+    nst = 300
+    v = np.zeros(nst + 1, np.complex128)
+    v[1] = 1.0
+    for W, dnW in ((0.0, 0.0), (-3.0, 1.7), (2.0, -0.8)):
+        k = o.tc_apply(v, W, dnW)
+        for tau in (0.3, -0.5, 0.4j):
+            zd = (2j / p.dt) * (1 - tau) / (1 + tau) + W
+            ref = -1j * (a.sum() - np.sum(a[1:] * d[1:] / (zd + d[1:])))
+            if tc == si.TC_S24:
+                ref += (dnW / 4.0) / zd
+            got = np.sum(k * tau ** np.arange(nst))
+            assert abs(got - ref) <= 1e-13 * abs(ref), (W, dnW, tau)
+
+
+def test_pade_tends_to_s02_without_potential(oracle_mod):
+    """With W = 0, S2^{2,m} -> S0^2 = -i sqrt(z_d) (the beta
+    convolution) as m grows, wherever the Pade approximant of sqrt converges
+    on the symbol's range (dt = 1 keeps z_d = O(1)); m = 100 agrees to
+    rounding on a random trace sequence, m = 20 does not."""
+    base = si.config("C1", T=40.0, dt=1.0)
+    rng = np.random.default_rng(1)
+    v = rng.standard_normal(41) + 1j * rng.standard_normal(41)
+    v[0] = 0.0   # v_0 enters S0^2 but not the Pade recursions (phi_0 = 0)
+    ref = oracle_mod.Oracle(dataclasses.replace(base, transmission=si.TC_S02), si.inputs(base)).tc_apply(v)
+    err = {}
+    for m in (20, 100):
+        q = dataclasses.replace(base, transmission=si.TC_S22, pade_m=m)
+        err[m] = np.abs(oracle_mod.Oracle(q, si.inputs(q)).tc_apply(v) - ref).max() / np.abs(ref).max()
+    assert err[100] <= 1e-12 and err[20] >= 1e-2, err
+
+
+@pytest.mark.parametrize("tc", PADE_TC)
+def test_pade_tc_converges_to_monodomain(oracle_mod, tc):
+    """The Pade operators change the convergence, not the limit: the SWR
+    solution equals the single-domain one; and the iteration count falls as
+    m grows (the paper's observation)."""
+    its = []
+    for m in (5, 20, 50):
+        p = si.config("C1", transmission=tc, potential=si.POT_VX, N=4, pade_m=m)
+        o = oracle_mod.Oracle(p, si.inputs(p))
+        r = o.solve()
+        st, um, _ = o.monodomain()
+        assert r["status"] == 0 and r["converged"]
+        assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+        its.append(r["iterations"])
+    assert its[0] > its[1] > its[2], its
 
 
 def test_gauge_tc_is_transparent_for_constant_potential(oracle_mod):
