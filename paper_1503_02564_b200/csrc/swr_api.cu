@@ -131,6 +131,8 @@ struct swr_handle {
   int gs_passes = 1;   // Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
   int krylov = 0;      // swr_krylov
   int pade_m = 0;      // Pade poles (SWR_TC_S2_*)
+  bool cgs_alt = true; // alternate CGS traversal direction (SWR_CGS_ALT=0 disables)
+  int cgs_dir = 0;
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
@@ -576,6 +578,11 @@ typedef std::function<int(const double2 *x, const double2 *sp, double2 *vcopy, d
 // update.
 int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w, int mode, double2 *out,
         double2 *out_host = nullptr) {
+  // alternate the traversal direction pass to pass (L2 reuse of V's tail)
+  if (h->cgs_alt) {
+    h->cgs_dir ^= 1;
+    if (h->cgs_dir) mode |= swr::CGS_REV;
+  }
   CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st, out_host));
   h->n_launches++;
   return SWR_OK;
@@ -1055,6 +1062,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->gs_passes = cfg->gs_passes == 2 ? 2 : 1;
   h->krylov = cfg->krylov;
   h->pade_m = cfg->pade_m;
+  if (const char *e = getenv("SWR_CGS_ALT")) h->cgs_alt = atoi(e) != 0;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;
@@ -1238,6 +1246,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
   }
   CK(cudaEventRecord(h->ev_s0, h->st));
   h->hist.clear();
+  h->cgs_dir = 0;   // the same pass directions (and rounding) on every solve
   h->iterations = h->inner_total = h->fp_max = 0;
   h->converged = 1;
   h->inner_fail = false;

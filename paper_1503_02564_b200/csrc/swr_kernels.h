@@ -46,7 +46,9 @@ __global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const dou
 __global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, int j_lo, int j_hi, double2 *uT);
 __global__ void k_fill(double2 *x, double2 v, size_t n);
 
-enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8 };
+// CGS_REV: walk the element chunks from the end (alternating directions
+// between consecutive passes keeps the last-read part of V hot in L2)
+enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8, CGS_REV = 16 };
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
                                 cudaStream_t st, const double2 *xs = nullptr, double2 *xcopy = nullptr);
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,

@@ -707,7 +707,9 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
 #pragma unroll
   for (int i = 0; i < VPW; i++) acc[i] = cz();
   double nacc = 0.0;
-  for (size_t c = blockIdx.x; c < nch; c += gridDim.x) {
+  const bool rev = mode & CGS_REV;
+  for (size_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
+    const size_t c = rev ? nch - 1 - ci : ci;
     const size_t base = c * CH + lane;
     double2 x[VPW][KE], we[KE];
 #pragma unroll
