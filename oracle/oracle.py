@@ -38,7 +38,7 @@ class _Problem(C.Structure):
         ("tol_inner", C.c_double), ("maxit_inner", C.c_int32),
         ("tol_fp", C.c_double), ("maxit_fp", C.c_int32),
         ("g0", C.c_void_p), ("gs_passes", C.c_int32), ("krylov", C.c_int32),
-        ("pade_m", C.c_int32),
+        ("pade_m", C.c_int32), ("pinv_exact", C.c_int32),
     ]
 
 
@@ -79,9 +79,10 @@ def lib():
         _lib.or_pade_coeffs.argtypes = [i32, vp, vp]
         _lib.or_pade_coeffs.restype = None
         _lib.or_tc_apply.argtypes = [P, C.c_double, C.c_double, i32, vp, vp]
+        _lib.or_pinv_causal.argtypes = [P, vp, vp, vp]
         for f in ("or_sizes", "or_thomas", "or_subdomain_matrix", "or_march", "or_apply_R",
                   "or_build_L", "or_gmres_dense", "or_bicgstab_dense", "or_solve", "or_monodomain",
-                  "or_tc_apply"):
+                  "or_tc_apply", "or_pinv_causal"):
             getattr(_lib, f).restype = i32
         _lib.or_coeffs.restype = None
         _lib.or_fem.restype = None
@@ -123,6 +124,7 @@ class Oracle:
         s.gs_passes = p.gs_passes
         s.krylov = p.krylov
         s.pade_m = getattr(p, "pade_m", 0)
+        s.pinv_exact = getattr(p, "pinv_exact", 0)
         self.s = s
         self.L = lib()
         self.Nx, self.NT, self.Nj = p.Nx, p.NT, p.Nj
@@ -134,6 +136,14 @@ class Oracle:
         st = self.L.or_subdomain_matrix(C.byref(self.s), j, n, int(force_zero), _ptr(lo), _ptr(di), _ptr(up))
         assert st == 0, st
         return lo, di, up
+
+    def pinv_causal(self, X, y):
+        """x = (I - L0)^{-1} y by causal forward substitution (X: first columns)."""
+        X, y = _c128(X), _c128(y)
+        x = np.zeros(self.ng, np.complex128)
+        st = self.L.or_pinv_causal(C.byref(self.s), _ptr(X), _ptr(y), _ptr(x))
+        assert st == 0, st
+        return x
 
     def tc_apply(self, v, W=0.0, dnW=0.0):
         """S v_n, n = 1..len(v)-1, of the configured operator at one boundary point."""

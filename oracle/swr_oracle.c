@@ -599,6 +599,87 @@ void or_apply_L(const or_problem *P, const ocplx *X, const ocplx *g, ocplx *Lg) 
   }
 }
 
+/* Exact P^{-1} = (I - L0)^{-1} (P:1041-1059 define P as
+ * I - L0, L0 lower block triangular in time with Toeplitz blocks, Props.
+ * 3-4).  Row n of (I - L0)x = y reads
+ *   x[n] - L0_0 x[n] = y[n] + sum_{k=1}^{n} L0_k x[n-k],
+ * L0_k the lag-k matrix of the block pattern of eq. (15)/(16).  The lag-0
+ * matrix T0 = I - L0_0 is assembled densely and LU-factored (partial
+ * pivoting) once; every step solves T0 x[n] = (history + y[n]). */
+int32_t or_pinv_causal(const or_problem *P, const ocplx *X, const ocplx *y, ocplx *x) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  const int32_t N = P->N, ns = 2 * N - 2;
+  if (ns < 1) return OR_OK;
+  ocplx *T = (ocplx *)calloc((size_t)ns * ns, sizeof(ocplx));
+  ocplx *h = (ocplx *)calloc((size_t)ns, sizeof(ocplx));
+  int32_t *piv = (int32_t *)calloc((size_t)ns, sizeof(int32_t));
+  if (!T || !h || !piv) { free(T); free(h); free(piv); return OR_OOM; }
+  /* T0 = I - L0_0: the couplings of or_apply_L at lag 0 */
+  for (int32_t s = 0; s < ns; s++) T[(size_t)s * ns + s] = 1.0;
+  for (int32_t j = 1; j <= N; j++) {
+    const ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+    if (j >= 2) {
+      T[(size_t)slot_r(j - 1) * ns + slot_l(j)] -= X1[0];
+      if (j <= N - 1) T[(size_t)slot_r(j - 1) * ns + slot_r(j)] -= X2[0];
+    }
+    if (j <= N - 1) {
+      if (j >= 2) T[(size_t)slot_l(j + 1) * ns + slot_l(j)] -= X3[0];
+      T[(size_t)slot_l(j + 1) * ns + slot_r(j)] -= X4[0];
+    }
+  }
+  /* LU with partial pivoting, in place (Doolittle; L unit lower) */
+  for (int32_t c = 0; c < ns; c++) {
+    int32_t pr = c;
+    for (int32_t r = c + 1; r < ns; r++)
+      if (cabs(T[(size_t)r * ns + c]) > cabs(T[(size_t)pr * ns + c])) pr = r;
+    piv[c] = pr;
+    if (pr != c)
+      for (int32_t k = 0; k < ns; k++) {
+        ocplx t = T[(size_t)c * ns + k];
+        T[(size_t)c * ns + k] = T[(size_t)pr * ns + k];
+        T[(size_t)pr * ns + k] = t;
+      }
+    if (T[(size_t)c * ns + c] == 0.0) { free(T); free(h); free(piv); return OR_ERR_ARG; }
+    for (int32_t r = c + 1; r < ns; r++) {
+      const ocplx f = T[(size_t)r * ns + c] / T[(size_t)c * ns + c];
+      T[(size_t)r * ns + c] = f;
+      for (int32_t k = c + 1; k < ns; k++) T[(size_t)r * ns + k] -= f * T[(size_t)c * ns + k];
+    }
+  }
+  for (int32_t n = 0; n < NT; n++) {
+    /* h = y[n] + sum_{k=1}^{n} L0_k x[n-k] */
+    for (int32_t s = 0; s < ns; s++) h[s] = y[(size_t)s * NT + n];
+    for (int32_t j = 1; j <= N; j++) {
+      const ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+      const ocplx *xl = (j >= 2) ? x + (size_t)slot_l(j) * NT : NULL;
+      const ocplx *xr = (j <= N - 1) ? x + (size_t)slot_r(j) * NT : NULL;
+      for (int32_t k = 1; k <= n; k++) {
+        if (j >= 2) {
+          h[slot_r(j - 1)] += X1[k] * xl[n - k];
+          if (j <= N - 1) h[slot_r(j - 1)] += X2[k] * xr[n - k];
+        }
+        if (j <= N - 1) {
+          if (j >= 2) h[slot_l(j + 1)] += X3[k] * xl[n - k];
+          h[slot_l(j + 1)] += X4[k] * xr[n - k];
+        }
+      }
+    }
+    /* T0 x[n] = h: permute, forward (unit L), backward (U) */
+    for (int32_t c = 0; c < ns; c++)
+      if (piv[c] != c) { ocplx t = h[c]; h[c] = h[piv[c]]; h[piv[c]] = t; }
+    for (int32_t r = 0; r < ns; r++)
+      for (int32_t k = 0; k < r; k++) h[r] -= T[(size_t)r * ns + k] * h[k];
+    for (int32_t r = ns - 1; r >= 0; r--) {
+      for (int32_t k = r + 1; k < ns; k++) h[r] -= T[(size_t)r * ns + k] * h[k];
+      h[r] /= T[(size_t)r * ns + r];
+    }
+    for (int32_t s = 0; s < ns; s++) x[(size_t)s * NT + n] = h[s];
+  }
+  free(T); free(h); free(piv);
+  return OR_OK;
+}
+
 /* Order-fixed inner product <x, y> = sum conj(x) y: one partial per
  * subdomain over the slots it owns (l_j, r_j), partials summed in
  * subdomain order. */
@@ -871,6 +952,7 @@ static int32_t krylov_solve(const or_problem *P, size_t n, or_opfn A, void *actx
 }
 
 static int32_t apply_Pinv(drv_ctx *d, const ocplx *y, ocplx *x) {
+  if (d->P->pinv_exact) return or_pinv_causal(d->P, d->X, y, x);
   for (size_t i = 0; i < d->ng; i++) x[i] = 0.0;
   int32_t it = 0, conv = 0;
   int32_t st = krylov_solve(d->P, d->ng, op_I_minus_L, d, d, y, x, d->P->tol_inner, d->P->maxit_inner, &it, NULL,

@@ -58,6 +58,8 @@ typedef struct {
   int32_t krylov;             /* OR_KRY_*: interface solver (outer, and the inner P^{-1} solve
                                  for GMRES / BiCGStab; P^{-1} is never a fixed point) */
   int32_t pade_m;             /* number of Pade poles m >= 1 for OR_TC_S22 / OR_TC_S24 */
+  int32_t pinv_exact;         /* P^{-1} of OR_ALG_PRECOND: 0 = inner Krylov on (I - L0),
+                                 1 = exact causal block forward substitution */
 } or_problem;
 
 typedef struct {
@@ -78,6 +80,10 @@ void or_pade_coeffs(int32_t m, double *a, double *d);
 /* S v_n (n = 1..nsteps) of the configured transmission operator at one
  * boundary point with interface data W, dnW, applied to v_0..v_nsteps. */
 int32_t or_tc_apply(const or_problem *P, double W, double dnW, int32_t nsteps, const ocplx *v, ocplx *Sv);
+/* x = (I - L0)^{-1} y exactly, by forward substitution in time: at each
+ * step n the history convolution of L0 (lags >= 1) is moved to the right
+ * side and the (2N-2)x(2N-2) lag-0 system is solved (factored once). */
+int32_t or_pinv_causal(const or_problem *P, const ocplx *X, const ocplx *y, ocplx *x);
 int32_t or_sizes(const or_problem *P, int32_t *Nx, int32_t *NT, int32_t *Nj);
 
 /* P1 FEM matrices on a uniform mesh of nn nodes, spacing h, nodal weight W

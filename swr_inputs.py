@@ -52,6 +52,7 @@ class Problem:
     gs_passes: int = 1          # Gram-Schmidt passes in GMRES: 1 = CGS (PETSc default, reading A6), 2 = CGS2
     krylov: int = KRY_GMRES     # interface solver: GMRES, BiCGStab or the algorithm's fixed point (A20/A21)
     pade_m: int = 20            # Pade poles m for TC_S22 / TC_S24 (the paper tabulates m = 20, 50, 100)
+    pinv_exact: int = 0         # PRECOND: 0 = inner Krylov P^{-1} (paper), 1 = exact causal solve (8(f)-4)
     seed: int = 7
     name: str = ""
 

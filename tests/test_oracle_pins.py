@@ -419,6 +419,38 @@ def test_higher_order_tc_converge_to_monodomain(oracle_mod, tc):
     assert np.linalg.norm(r["uT"] - um) <= 1e-8 * np.linalg.norm(um)
 
 
+@pytest.mark.parametrize("tc", [si.TC_ROBIN, si.TC_S02])
+def test_pinv_causal_inverts_I_minus_L0(oracle_mod, tc):
+    """the causal forward substitution is the exact inverse of
+    P = I - L0: applying I - L0 by the independent convolution
+    of or_apply_L to its output returns the input to rounding."""
+    p = si.config("C1", N=5, potential=si.POT_VTX, algorithm=si.ALG_PRECOND, transmission=tc)
+    o = oracle_mod.Oracle(p, si.inputs(p))
+    X = o.build_L(force_zero=True)
+    rng = np.random.default_rng(3)
+    y = rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng)
+    x = o.pinv_causal(X, y)
+    assert np.linalg.norm(x - o.apply_L(X, x) - y) <= 1e-13 * np.linalg.norm(y)
+
+
+@pytest.mark.parametrize("pot,kry", [(si.POT_VTX, si.KRY_GMRES), (si.POT_VTX, si.KRY_BICGSTAB),
+                                     (si.POT_CUBIC, si.KRY_FIXED_POINT)])
+def test_pinv_exact_equals_inner_krylov(oracle_mod, pot, kry):
+    """The exact P^{-1} changes rounding only: the preconditioned algorithms
+    take the same outer iterations as with the inner Krylov P^{-1} (tolerance
+    1e-12), no inner iterations, and reach the monodomain solution."""
+    p = si.config("C1", N=5, potential=pot, algorithm=si.ALG_PRECOND, transmission=si.TC_S02, krylov=kry)
+    q = dataclasses.replace(p, pinv_exact=1)
+    ra = oracle_mod.Oracle(p, si.inputs(p)).solve()
+    oq = oracle_mod.Oracle(q, si.inputs(q))
+    rb = oq.solve()
+    assert ra["status"] == 0 and rb["status"] == 0 and rb["converged"]
+    assert rb["iterations"] == ra["iterations"] and rb["inner_iterations"] == 0 < ra["inner_iterations"]
+    assert np.linalg.norm(rb["uT"] - ra["uT"]) <= 1e-10 * np.linalg.norm(ra["uT"])
+    st, um, _ = oq.monodomain()
+    assert np.linalg.norm(rb["uT"] - um) <= 1e-8 * np.linalg.norm(um)
+
+
 PADE_TC = [si.TC_S22, si.TC_S24]
 
 
