@@ -123,6 +123,10 @@ typedef struct {
                                  2 = CGS2 (one reorthogonalization); 0 = 1 */
   int32_t krylov;             /* swr_krylov: interface solver (0 = GMRES) */
   int32_t pade_m;             /* Pade poles m >= 1 for SWR_TC_S2_2 / SWR_TC_S2_4 (else ignored) */
+  int32_t pinv_exact;         /* SWR_ALG_PRECOND: 0 = P^{-1} by the inner Krylov solve on (I - L0)
+                                 (P:1059); 1 = exact causal forward substitution in time (reading
+                                 A27); fails with SWR_ERR_UNSUPPORTED when the lag-0 interface
+                                 coupling is too strong for the bounded sweep count */
 } swr_config;
 
 typedef struct {

@@ -131,6 +131,10 @@ struct swr_handle {
   int gs_passes = 1;   // Gram-Schmidt passes per Arnoldi step (1: CGS, 2: CGS2)
   int krylov = 0;      // swr_krylov
   int pade_m = 0;      // Pade poles (SWR_TC_S2_*)
+  int pinv_exact = 0;  // exact causal P^{-1} (A27)
+  int pinv_sweeps = 0; // block-Jacobi sweeps of its lag-0 solve
+  double pinv_rho = 0.0;
+  double2 *pinvF = nullptr;   // [2N-2][PINV_B] far-history scratch
   bool cgs_alt = true; // alternate CGS traversal direction (SWR_CGS_ALT=0 disables)
   int cgs_dir = 0;
   int Nx, NT, Nj, m;
@@ -851,7 +855,44 @@ int bicgstab(swr_handle *h, const Op &A, const double2 *b, double2 *x, double to
   return st;
 }
 
+// Exact P^{-1} (reading A27): block-Jacobi sweeps on the lag-0 system of
+// every step.  rho = max_i ||D_i^{-1} C_i||_inf over the interfaces bounds
+// the contraction; S sweeps leave an error <= rho^{S+1} ||x||_inf <= 1e-17.
+int setup_pinv(swr_handle *h) {
+  const int N = h->N, NT = h->NT;
+  if (N < 2) return SWR_OK;
+  std::vector<double2> l0((size_t)N * 4);
+  CK(cudaMemcpy2DAsync(l0.data(), sizeof(double2), h->X0, (size_t)NT * sizeof(double2), sizeof(double2),
+                       (size_t)N * 4, cudaMemcpyDeviceToHost, h->st));
+  CK(cudaStreamSynchronize(h->st));
+  auto X = [&](int j, int c) { return c2(l0[(size_t)(j - 1) * 4 + c]); };   // X^{j,c+1}_0
+  double rho = 0.0;
+  for (int i = 1; i <= N - 1; i++) {
+    const cplx p = X(i + 1, 0), q = X(i, 3), det = 1.0 - p * q;
+    if (std::abs(det) == 0.0) { g_detail = "exact P^{-1}: singular lag-0 interface block"; return SWR_ERR_UNSUPPORTED; }
+    const cplx d00 = 1.0 / det, d01 = p / det, d10 = q / det, d11 = 1.0 / det;
+    const double ca = (i + 1 <= N - 1) ? std::abs(X(i + 1, 1)) : 0.0, cb = (i >= 2) ? std::abs(X(i, 2)) : 0.0;
+    rho = std::max(rho, std::max(std::abs(d00) * ca + std::abs(d01) * cb, std::abs(d10) * ca + std::abs(d11) * cb));
+  }
+  int S = 0;
+  if (rho > 0.0) {
+    if (rho >= 0.5) { g_detail = "exact P^{-1}: lag-0 interface coupling too strong (rho >= 0.5)"; return SWR_ERR_UNSUPPORTED; }
+    S = std::max(0, (int)std::ceil(std::log(1e-17) / std::log(rho)) - 1);
+  }
+  h->pinv_sweeps = S;
+  h->pinv_rho = rho;
+  return SWR_OK;
+}
+
 int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
+  if (h->pinv_exact) {
+    int nl = 0;
+    CKS(record_pair(h, false, true));
+    CK(swr::launch_pinv_causal(h->X0, y, x, h->pinvF, h->N, h->NT, h->pinv_sweeps, h->st, &nl));
+    CKS(record_pair(h, false, false));
+    h->n_launches += nl;
+    return SWR_OK;
+  }
   CKS(fill_zero(h, x, h->ng));
   Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
   OpScaled A0s = [h](const double2 *a, const double2 *sp, double2 *vc, double2 *b) {
@@ -941,7 +982,7 @@ int alloc_krylov(Krylov &K, size_t mm, size_t ng) {
 }
 
 void free_all(swr_handle *h) {
-  void *ptrs[] = {h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
+  void *ptrs[] = {h->pinvF, h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev, h->counter,
@@ -1062,6 +1103,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->gs_passes = cfg->gs_passes == 2 ? 2 : 1;
   h->krylov = cfg->krylov;
   h->pade_m = cfg->pade_m;
+  h->pinv_exact = cfg->pinv_exact ? 1 : 0;
   if (const char *e = getenv("SWR_CGS_ALT")) h->cgs_alt = atoi(e) != 0;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
@@ -1142,6 +1184,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       return fail(s);
     if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, ng))))
       return fail(s);
+    if (precond && h->pinv_exact && (s = dalloc(&h->pinvF, (size_t)(2 * h->N - 2) * swr::PINV_B))) return fail(s);
     if (cfg->g0 && (s = dalloc(&h->g0, ng))) return fail(s);
     const char *tmode = getenv("SWR_TOEPLITZ");
     h->log4 = (tmode && strcmp(tmode, "direct") == 0) ? 0 : swr::fft_log4_for(h->NT);
@@ -1226,6 +1269,7 @@ int swr_build_interface_operator(swr_handle *h) {
       CKS(build_probes(h, true, h->X0, nullptr));  // L0: 2 RHS per subdomain
       CKS(transform_columns(h, true));
       h->have_L0 = true;
+      if (h->pinv_exact) CKS(setup_pinv(h));
       if (h->potential != SWR_POT_CUBIC) {
         CKS(sweep_R(h, nullptr, true, false, h->d, nullptr));  // d = R(0; u0)
         h->have_d = true;

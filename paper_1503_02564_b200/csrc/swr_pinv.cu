@@ -1,0 +1,153 @@
+// Exact P^{-1} = (I - L0)^{-1} by causal forward substitution in time
+// (P = I - L0 of P:1041-1059, L0 lower block triangular in
+// time with Toeplitz blocks, Props. 3-4).
+//
+// Row n of (I - L0) x = y:  x[n] - L0_0 x[n] = y[n] + sum_{k>=1} L0_k x[n-k].
+// The unknowns of step n pair up by interface i = 1..N-1: a = r_i (slot
+// 2i-2, emitted by subdomain i+1 through its left end) and b = l_{i+1}
+// (slot 2i-1, emitted by subdomain i through its right end).  The lag-0
+// matrix is the 2x2 block D_i = [[1, -X^{i+1,1}_0], [-X^{i,4}_0, 1]] per
+// interface plus the cross couplings a_i <- X^{i+1,2}_0 a_{i+1} and
+// b_i <- X^{i,3}_0 b_{i-1}; the host bounds rho = ||D^{-1} C||_inf and the
+// kernel runs exactly the block-Jacobi sweeps that push rho^{S+1} below
+// 1e-17 (reading A27) -- the lag-0 solve is exact to rounding.
+//
+// Time is cut into blocks of PINV_B steps: k_pinv_far adds the history of
+// all earlier blocks (a Toeplitz block times a vector, every SM, one warp
+// per (slot, step)); k_pinv_near walks the block's steps in one CTA (history
+// inside the block, lag-0 solve, sweeps).
+#include "swr_common.cuh"
+#include "swr_kernels.h"
+
+namespace swr {
+
+namespace {
+// sources of the history of slot s (0-based): slot s receives
+// c1 * x[src1] + c2 * x[src2] (c2 absent at the ends of the chain)
+__device__ __forceinline__ void pinv_sources(int s, int N, int NT, const double2 *X0, const double2 *x,
+                                             const double2 *&c1, const double2 *&x1, const double2 *&c2,
+                                             const double2 *&x2) {
+  const int i = s / 2 + 1;
+  if ((s & 1) == 0) {  // a = r_i = out_left of subdomain j = i + 1: X^{j,1} l_j + X^{j,2} r_j
+    const double2 *Xj = X0 + (size_t)i * 4 * NT;
+    c1 = Xj;
+    x1 = x + (size_t)(s + 1) * NT;
+    const bool has2 = i + 1 <= N - 1;
+    c2 = has2 ? Xj + NT : nullptr;
+    x2 = has2 ? x + (size_t)(s + 2) * NT : nullptr;
+  } else {             // b = l_{i+1} = out_right of subdomain j = i: X^{j,3} l_j + X^{j,4} r_j
+    const double2 *Xj = X0 + (size_t)(i - 1) * 4 * NT;
+    c1 = Xj + 3 * NT;
+    x1 = x + (size_t)(s - 1) * NT;
+    const bool has2 = i >= 2;
+    c2 = has2 ? Xj + 2 * NT : nullptr;
+    x2 = has2 ? x + (size_t)(s - 2) * NT : nullptr;
+  }
+}
+}  // namespace
+
+// F[s][n - n0] = sum_{t < n0} c1[n - t] x1[t] + c2[n - t] x2[t], n0 <= n < n0 + B
+__global__ void __launch_bounds__(256) k_pinv_far(const double2 *__restrict__ X0, const double2 *__restrict__ x,
+                                                  double2 *__restrict__ F, int N, int NT, int n0, int B) {
+  pdl_wait();
+  pdl_trigger();
+  const int warp = (int)((blockIdx.x * (size_t)blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  const int ns = 2 * N - 2;
+  if (warp >= ns * B) return;
+  const int s = warp / B, n = n0 + warp % B;
+  if (n >= NT) return;
+  const double2 *c1, *x1, *c2, *x2;
+  pinv_sources(s, N, NT, X0, x, c1, x1, c2, x2);
+  double2 acc = cz();
+  for (int t = lane; t < n0; t += 32) {
+    acc = cfma(__ldg(c1 + n - t), x1[t], acc);
+    if (c2) acc = cfma(__ldg(c2 + n - t), x2[t], acc);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_down2(acc, o));
+  if (lane == 0) F[(size_t)s * B + (n - n0)] = acc;
+}
+
+// Steps n0 .. n0+B-1 in one CTA.  smem: h[2][ni], xa/xb ping-pong [2][2][ni].
+__global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ X0, const double2 *__restrict__ y,
+                                                    const double2 *__restrict__ F, double2 *x, int N, int NT,
+                                                    int n0, int B, int sweeps, int has_far) {
+  pdl_wait();
+  pdl_trigger();
+  extern __shared__ double2 sm[];
+  const int ni = N - 1;
+  double2 *hs = sm, *xs = sm + 2 * ni;   // hs[2*i0 + w]; xs[buf][2*i0 + w]
+  const int n_end = min(n0 + B, NT);
+  for (int n = n0; n < n_end; n++) {
+    for (int i0 = threadIdx.x; i0 < ni; i0 += blockDim.x) {
+      double2 hv[2];
+#pragma unroll
+      for (int w = 0; w < 2; w++) {
+        const int s = 2 * i0 + w;
+        const double2 *c1, *x1, *c2, *x2;
+        pinv_sources(s, N, NT, X0, x, c1, x1, c2, x2);
+        double2 acc = y[(size_t)s * NT + n];
+        if (has_far) acc = cadd(acc, F[(size_t)s * B + (n - n0)]);
+        for (int t = n0; t < n; t++) {   // x of this block: written by this CTA (plain loads)
+          acc = cfma(__ldg(c1 + n - t), x1[t], acc);
+          if (c2) acc = cfma(__ldg(c2 + n - t), x2[t], acc);
+        }
+        hv[w] = acc;
+        hs[s] = acc;
+      }
+      // x^(0) = D_i^{-1} h, D_i = [[1, -p], [-q, 1]], p = X^{i+1,1}_0, q = X^{i,4}_0
+      const double2 p = __ldg(X0 + (size_t)(i0 + 1) * 4 * NT), q = __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
+      const double2 rd = crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
+      xs[2 * i0] = cmul(cfma(p, hv[1], hv[0]), rd);
+      xs[2 * i0 + 1] = cmul(cfma(q, hv[0], hv[1]), rd);
+    }
+    __syncthreads();
+    int cur = 0;
+    for (int sw = 0; sw < sweeps; sw++) {
+      const double2 *xo = xs + cur * 2 * ni;
+      double2 *xn = xs + (cur ^ 1) * 2 * ni;
+      for (int i0 = threadIdx.x; i0 < ni; i0 += blockDim.x) {
+        double2 ha = hs[2 * i0], hb = hs[2 * i0 + 1];
+        if (i0 + 1 < ni) ha = cfma(__ldg(X0 + ((size_t)(i0 + 1) * 4 + 1) * NT), xo[2 * (i0 + 1)], ha);  // X^{i+1,2}_0 a_{i+1}
+        if (i0 >= 1) hb = cfma(__ldg(X0 + ((size_t)i0 * 4 + 2) * NT), xo[2 * (i0 - 1) + 1], hb);        // X^{i,3}_0 b_{i-1}
+        const double2 p = __ldg(X0 + (size_t)(i0 + 1) * 4 * NT), q = __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
+        const double2 rd = crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
+        xn[2 * i0] = cmul(cfma(p, hb, ha), rd);
+        xn[2 * i0 + 1] = cmul(cfma(q, ha, hb), rd);
+      }
+      __syncthreads();
+      cur ^= 1;
+    }
+    const double2 *xf = xs + cur * 2 * ni;
+    for (int s = threadIdx.x; s < 2 * ni; s += blockDim.x) x[(size_t)s * NT + n] = xf[s];
+    __syncthreads();
+  }
+}
+
+cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, double2 *F, int N, int NT,
+                               int sweeps, cudaStream_t st, int *n_launches) {
+  const int ni = N - 1, ns = 2 * N - 2;
+  if (ni < 1) return cudaSuccess;
+  const size_t smem = (size_t)6 * ni * sizeof(double2);
+  if (smem > 48 * 1024) {
+    cudaError_t e = cudaFuncSetAttribute(k_pinv_near, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  const int thr = std::min(1024, (ni + 31) / 32 * 32);
+  for (int n0 = 0; n0 < NT; n0 += PINV_B) {
+    if (n0 > 0) {
+      const int warps = ns * PINV_B;
+      cudaError_t e = launch_pdl(k_pinv_far, dim3((warps + 7) / 8), dim3(256), 0, st, X0, (const double2 *)x, F, N,
+                                 NT, n0, (int)PINV_B);
+      if (e != cudaSuccess) return e;
+      ++*n_launches;
+    }
+    cudaError_t e = launch_pdl(k_pinv_near, dim3(1), dim3(thr), smem, st, X0, y, (const double2 *)F, x, N, NT, n0,
+                               (int)PINV_B, sweeps, n0 > 0 ? 1 : 0);
+    if (e != cudaSuccess) return e;
+    ++*n_launches;
+  }
+  return cudaSuccess;
+}
+
+}  // namespace swr

@@ -35,7 +35,7 @@ class Config(C.Structure):
         ("restart", C.c_int32), ("maxit", C.c_int32), ("tol_inner", C.c_double), ("maxit_inner", C.c_int32),
         ("tol_fp", C.c_double), ("maxit_fp", C.c_int32), ("g0", C.c_void_p),
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
-        ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("gs_passes", C.c_int32), ("krylov", C.c_int32), ("pade_m", C.c_int32),
+        ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("gs_passes", C.c_int32), ("krylov", C.c_int32), ("pade_m", C.c_int32), ("pinv_exact", C.c_int32),
     ]
 
 
@@ -162,6 +162,7 @@ class SWR:
         c.gs_passes = getattr(p, "gs_passes", 1)
         c.krylov = getattr(p, "krylov", 0)
         c.pade_m = getattr(p, "pade_m", 0)
+        c.pinv_exact = getattr(p, "pinv_exact", 0)
         self.cfg = c
         h = C.c_void_p()
         with torch.cuda.device(self.dev):

@@ -174,6 +174,27 @@ def test_higher_order_tc_parity(oracle_mod, gpu, name, tc, march, monkeypatch):
     assert rel(X_g.cpu().numpy(), o.build_L(), 1.0) <= 1e-12
 
 
+PINV_CASES = [("vtx-gmres", 5, si.POT_VTX, si.KRY_GMRES), ("vtx-bicgstab", 5, si.POT_VTX, si.KRY_BICGSTAB),
+              ("nl-fp", 5, si.POT_CUBIC, si.KRY_FIXED_POINT), ("vtx-gmres-N40", 40, si.POT_VTX, si.KRY_GMRES)]
+
+
+@pytest.mark.parametrize("name,N,pot,kry", PINV_CASES)
+def test_pinv_exact_parity(oracle_mod, gpu, name, N, pot, kry):
+    """Exact causal P^{-1} (reading A27) in the preconditioned
+    algorithms: the oracle's dense lag-0 LU vs the GPU's block-Jacobi sweeps
+    (N = 40 has five-cell subdomains, so several sweeps run): equal outer
+    iterations, no inner iterations, u(T) within 1e-10."""
+    p = si.config("C1", transmission=si.TC_S02, potential=pot, N=N, algorithm=si.ALG_PRECOND, krylov=kry,
+                  pinv_exact=1, u0_kind="soliton" if pot == si.POT_CUBIC else "gaussian")
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert rg["inner_iterations"] == 0 == ro["inner_iterations"]
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)
