@@ -1152,8 +1152,11 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   if (h->potential == SWR_POT_VTX_SEPARABLE) {
     const size_t nt = (size_t)h->n_terms;
     if ((s = dalloc(&h->tau, nt * (NTt + 1))) || (s = dalloc(&h->xi, nt * nx1)) ||
-        (s = dalloc(&h->qtd, NTt * (size_t)h->N * h->Nj)) || (s = dalloc(&h->ertd, NTt * (size_t)h->N * h->Nj)))
+        (s = dalloc(&h->qtd, NTt * (size_t)h->N * h->Nj)) || (s = dalloc(&h->ertd, NTt * (size_t)h->N * h->Nj + 2)))
       return fail(s);
+    // the march's bulk copies of er round up to 16 B: the last one reads one pad element
+    if (cudaMemsetAsync(h->ertd + NTt * (size_t)h->N * h->Nj, 0, 2 * sizeof(double), h->st) != cudaSuccess)
+      return fail(SWR_ERR_CUDA);
     if ((s = copy_in_r(h->tau, cfg->tau, nt * (NTt + 1), cfg->inputs_on_device, h->st)) ||
         (s = copy_in_r(h->xi, cfg->xi, nt * nx1, cfg->inputs_on_device, h->st)))
       return fail(s);

@@ -495,9 +495,21 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     imp[r][1] = G[r].flags & SYS_RIN_IMPULSE;
   }
 
+  // TDM: the factors of step n+1 arrive by bulk copy (TMA) into the scan-table
+  // region (unused on this path) while step n runs: pmb, pq[rows_cta], pe[rows_cta + 2]
+  unsigned long long *pmb = reinterpret_cast<unsigned long long *>(tabbase);
+  double2 *pq = tabbase + 1;
+  double *pe = reinterpret_cast<double *>(pq + P * M);   // [P M + 4]; row i at pe[emis + i]
+  const int fbase = crank * P * M;
+  const int fcnt = TDM ? max(0, min(P * M, Nj - fbase)) : 0;
   if (t == 0) {
     for (int i = 0; i < 4; i++) mbar_init(mbar + i, 1);
+    if (TDM) mbar_init(pmb, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (TDM) {
+    for (int i = fcnt + t; i < P * M; i += P) pq[i] = cz();
+    for (int i = t; i < P * M + 4; i += P) pe[i] = 0.0;
   }
   for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
   if (!TDM && p.tc_hi) {
@@ -546,6 +558,53 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     sAb[t] = Ab;
   };
   load_factor(G[0].q, G[0].er);
+  // TDM prefetch of step nn (thread 0): pq/pe by bulk copy, the previous CTA's
+  // last row (qprev / er_prev of thread 0) by plain loads into registers
+  double2 qprev_nx = cz();
+  double erprev_nx = 0.0;
+  auto prefetch = [&](int nn) {
+    if (t != 0) return;
+    const size_t off = (size_t)(nn - 1) * p.td_stride + fbase;
+    if (fcnt > 0) {
+      // er rows are 8 B: start one row early when the source is not 16-B aligned
+      const double *es = G[0].er + off;
+      const unsigned mis = (unsigned)(((uintptr_t)es >> 3) & 1);
+      const unsigned bq = (unsigned)fcnt * 16u, be = ((unsigned)(fcnt + mis) * 8u + 15u) & ~15u;
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_expect_tx(pmb, bq + be);
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(pq)), "l"(G[0].q + off), "r"(bq), "r"(smem_u32(pmb)) : "memory");
+      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                   ::"r"(smem_u32(pe)), "l"(es - mis), "r"(be), "r"(smem_u32(pmb)) : "memory");
+    }
+    if (fbase > 0 && fbase - 1 < Nj) {
+      qprev_nx = __ldg(G[0].q + off - 1);
+      erprev_nx = __ldg(G[0].er + off - 1);
+    }
+  };
+  auto load_factor_smem = [&](int nn) {
+    const double *pes = pe + (((uintptr_t)(G[0].er + (size_t)(nn - 1) * p.td_stride + fbase) >> 3) & 1);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      q[i] = pq[t * M + i];
+      er[i] = pes[t * M + i];
+    }
+    if (t > 0) {
+      er_prev = pes[t * M - 1];
+      qprev = pq[t * M - 1];
+    } else {
+      er_prev = erprev_nx;
+      qprev = qprev_nx;
+    }
+    double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      Af = cmul(Af, negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim));
+      Ab = cmul(Ab, negqe(q[i], er[i], eim));
+    }
+    sAf[t] = Af;
+    sAb[t] = Ab;
+  };
 #pragma unroll
   for (int r = 0; r < K; r++) {
     const double2 *u0p = G[r].u0;
@@ -609,6 +668,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     hlast[r * P + t] = u[r][M - 1];
   }
   csync(CS, true);
+  if (TDM && NT >= 2) prefetch(2);
   double2 uL[K], uR[K];
 #pragma unroll
   for (int r = 0; r < K; r++) {
@@ -629,8 +689,12 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     SWR_TRACE(0);
-    if (TDM && n > 1)   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
-      load_factor(G[0].q + (size_t)(n - 1) * p.td_stride, G[0].er + (size_t)(n - 1) * p.td_stride);
+    if (TDM && n > 1) {   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
+      if (fcnt > 0) mbar_wait(pmb, (uint32_t)((n - 2) & 1));
+      load_factor_smem(n);
+      __syncthreads();                 // every thread holds its rows: the buffer is free
+      if (n < NT) prefetch(n + 1);
+    }
     // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + P_n),
     // P_n = sum_{s<=n-2} beta_{n-s} v_s spread over the CTA during step n-1
     // (hred); the owner of the boundary row adds the newest term below.
