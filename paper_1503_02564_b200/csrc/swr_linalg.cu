@@ -797,6 +797,98 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
   if (threadIdx.x == 0) *counter = 0u;
 }
 
+// The CGS update pass without dots (CGS_AXPY | CGS_NORM [| CGS_SCALE]):
+// w -= V h and <w, w>.  No dots means no per-vector sums, so the entries
+// split over warps (each warp streams all nv basis vectors for its 32 KE
+// entries, four vectors per unrolled step) and no shared-memory exchange or
+// barrier sits in the loop.  Norm partials: warp tree, CTA fixed order, the
+// last CTA sums the CTAs in a fixed order (deterministic).
+template <int KE>
+__global__ void __launch_bounds__(256, 2) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
+                                                     const double2 *__restrict__ hsrc, double2 *__restrict__ w,
+                                                     int mode, double2 *__restrict__ partial,
+                                                     double2 *__restrict__ out, unsigned *counter, size_t ntot,
+                                                     double2 *__restrict__ out_host) {
+  pdl_wait();
+  pdl_trigger();
+  __shared__ double2 sh[32];
+  __shared__ double red[8];
+  __shared__ bool last;
+  for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
+  __syncthreads();
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  constexpr int CH = 32 * KE;
+  const size_t nch = (ntot + CH - 1) / CH, nwarps = (size_t)gridDim.x * nwp;
+  const bool rev = mode & CGS_REV;
+  double nacc = 0.0;
+  for (size_t ci = (size_t)blockIdx.x * nwp + wp; ci < nch; ci += nwarps) {
+    const size_t c = rev ? nch - 1 - ci : ci;
+    const size_t base = c * CH + lane;
+    double2 we[KE], p[KE];
+#pragma unroll
+    for (int k = 0; k < KE; k++) {
+      const size_t e = base + 32 * k;
+      we[k] = e < ntot ? w[e] : cz();
+      p[k] = cz();
+    }
+    int v = 0;
+    for (; v + 4 <= nv; v += 4) {
+      double2 x[4][KE];
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int k = 0; k < KE; k++) {
+          const size_t e = base + 32 * k;
+          x[j][k] = e < ntot ? V[(size_t)(v + j) * ldv + e] : cz();
+        }
+#pragma unroll
+      for (int j = 0; j < 4; j++)
+#pragma unroll
+        for (int k = 0; k < KE; k++) p[k] = cfma(sh[v + j], x[j][k], p[k]);
+    }
+    for (; v < nv; v++) {
+#pragma unroll
+      for (int k = 0; k < KE; k++) {
+        const size_t e = base + 32 * k;
+        p[k] = cfma(sh[v], e < ntot ? V[(size_t)v * ldv + e] : cz(), p[k]);
+      }
+    }
+#pragma unroll
+    for (int k = 0; k < KE; k++) {
+      const size_t e = base + 32 * k;
+      if (e < ntot) {
+        const double2 r = csub(we[k], p[k]);
+        w[e] = r;
+        nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+  if (lane == 0) red[wp] = nacc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double sacc = 0.0;
+    for (int q = 0; q < nwp; q++) sacc += red[q];
+    partial[blockIdx.x] = make_double2(sacc, 0.0);
+    __threadfence();
+    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  }
+  __syncthreads();
+  if (!last || wp != 0) return;
+  __threadfence();
+  double sum = 0.0;
+  for (int q = lane; q < (int)gridDim.x; q += 32) sum += __ldcg(partial + q).x;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
+  if (lane == 0) {
+    out[0] = make_double2(sum, 0.0);
+    if (out_host) out_host[0] = out[0];
+    if (mode & CGS_SCALE) out[1] = make_double2(1.0 / sqrt(sum), 0.0);
+    *counter = 0u;
+  }
+}
+
 // y = s x, s read from the device (the normalisation of a new basis vector)
 __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__restrict__ sp, double2 *__restrict__ y,
                             size_t n) {
@@ -1002,6 +1094,14 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
     if (nv <= 8) return launch_cgs_tma_t<8>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
     if (nv <= 16) return launch_cgs_tma_t<16>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
     return launch_cgs_tma_t<32>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
+  }
+  // update pass without dots: entry-split streaming form (SWR_CGS_AXPY=0 disables)
+  static const bool axpy_split = !(getenv("SWR_CGS_AXPY") && atoi(getenv("SWR_CGS_AXPY")) == 0);
+  if (axpy_split && (mode & CGS_AXPY) && !(mode & CGS_DOTS) && (mode & CGS_NORM) && nv >= 1) {
+    const size_t nwarp_needed = (ntot + 32 * 4 - 1) / (32 * 4);
+    const unsigned g = (unsigned)std::min<size_t>((nwarp_needed + 7) / 8, 148 * 2);
+    return launch_pdl(k_cgs_axpy<4>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter,
+                      ntot, out_host);
   }
   // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
   // grid only depends on the sizes, so the reduction order is fixed

@@ -1418,7 +1418,10 @@ MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi) {
   const int pmax_env = pm ? atoi(pm) : 0;
   const char *mm = getenv("SWR_MARCH_M");   // experiments: force M rows per thread
   const int m_env = mm ? atoi(mm) : 0;
+  const char *ce = getenv("SWR_MARCH_CS");  // experiments: force the cluster size
+  const int cs_env = ce ? atoi(ce) : 0;
   for (int CS = 1; CS <= 16; CS++) {
+    if (cs_env && CS != cs_env) continue;
     for (const Inst &in : kInst) {
       if (in.K != K) continue;
       if (pmax_env && in.PMAX != pmax_env) continue;
