@@ -803,8 +803,8 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
 // entries, four vectors per unrolled step) and no shared-memory exchange or
 // barrier sits in the loop.  Norm partials: warp tree, CTA fixed order, the
 // last CTA sums the CTAs in a fixed order (deterministic).
-template <int KE>
-__global__ void __launch_bounds__(256, 2) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
+template <int KE, int MINB, int VU = 4>
+__global__ void __launch_bounds__(256, MINB) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
                                                      const double2 *__restrict__ hsrc, double2 *__restrict__ w,
                                                      int mode, double2 *__restrict__ partial,
                                                      double2 *__restrict__ out, unsigned *counter, size_t ntot,
@@ -818,8 +818,11 @@ __global__ void __launch_bounds__(256, 2) k_cgs_axpy(const double2 *__restrict__
   __syncthreads();
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
   constexpr int CH = 32 * KE;
+  // the whole grid sweeps one front of chunks through memory (reversed with
+  // CGS_REV), so consecutive passes meet the tail of the previous one in L2
   const size_t nch = (ntot + CH - 1) / CH, nwarps = (size_t)gridDim.x * nwp;
   const bool rev = mode & CGS_REV;
+  const size_t hi = ntot;
   double nacc = 0.0;
   for (size_t ci = (size_t)blockIdx.x * nwp + wp; ci < nch; ci += nwarps) {
     const size_t c = rev ? nch - 1 - ci : ci;
@@ -828,21 +831,21 @@ __global__ void __launch_bounds__(256, 2) k_cgs_axpy(const double2 *__restrict__
 #pragma unroll
     for (int k = 0; k < KE; k++) {
       const size_t e = base + 32 * k;
-      we[k] = e < ntot ? w[e] : cz();
+      we[k] = e < hi ? w[e] : cz();
       p[k] = cz();
     }
     int v = 0;
-    for (; v + 4 <= nv; v += 4) {
-      double2 x[4][KE];
+    for (; v + VU <= nv; v += VU) {
+      double2 x[VU][KE];
 #pragma unroll
-      for (int j = 0; j < 4; j++)
+      for (int j = 0; j < VU; j++)
 #pragma unroll
         for (int k = 0; k < KE; k++) {
           const size_t e = base + 32 * k;
-          x[j][k] = e < ntot ? V[(size_t)(v + j) * ldv + e] : cz();
+          x[j][k] = e < hi ? V[(size_t)(v + j) * ldv + e] : cz();
         }
 #pragma unroll
-      for (int j = 0; j < 4; j++)
+      for (int j = 0; j < VU; j++)
 #pragma unroll
         for (int k = 0; k < KE; k++) p[k] = cfma(sh[v + j], x[j][k], p[k]);
     }
@@ -850,13 +853,13 @@ __global__ void __launch_bounds__(256, 2) k_cgs_axpy(const double2 *__restrict__
 #pragma unroll
       for (int k = 0; k < KE; k++) {
         const size_t e = base + 32 * k;
-        p[k] = cfma(sh[v], e < ntot ? V[(size_t)v * ldv + e] : cz(), p[k]);
+        p[k] = cfma(sh[v], e < hi ? V[(size_t)v * ldv + e] : cz(), p[k]);
       }
     }
 #pragma unroll
     for (int k = 0; k < KE; k++) {
       const size_t e = base + 32 * k;
-      if (e < ntot) {
+      if (e < hi) {
         const double2 r = csub(we[k], p[k]);
         w[e] = r;
         nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
@@ -1098,9 +1101,11 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
   // update pass without dots: entry-split streaming form (SWR_CGS_AXPY=0 disables)
   static const bool axpy_split = !(getenv("SWR_CGS_AXPY") && atoi(getenv("SWR_CGS_AXPY")) == 0);
   if (axpy_split && (mode & CGS_AXPY) && !(mode & CGS_DOTS) && (mode & CGS_NORM) && nv >= 1) {
+    // 4 entries x 4 vectors per unrolled step, 2 CTAs of 256 per SM (measured
+    // best of KE 1/2/4, 4 or 8 vectors per step, 1-3 CTAs per SM)
     const size_t nwarp_needed = (ntot + 32 * 4 - 1) / (32 * 4);
     const unsigned g = (unsigned)std::min<size_t>((nwarp_needed + 7) / 8, 148 * 2);
-    return launch_pdl(k_cgs_axpy<4>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter,
+    return launch_pdl(k_cgs_axpy<4, 2>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter,
                       ntot, out_host);
   }
   // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
