@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libswr.so")
-SOURCES = ["swr_march.cu", "swr_march_stream.cu", "swr_linalg.cu", "swr_pinv.cu", "swr_api.cu"]
+SOURCES = ["swr_march.cu", "swr_march_stream.cu", "swr_linalg.cu", "swr_pinv.cu", "swr_fft_halves.cu", "swr_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]

@@ -162,6 +162,7 @@ struct swr_handle {
   int log4 = 0;
   bool fft_fused = true;
   bool fft_reg = false;   // register four-step FFT kernel (NF = 1024)
+  bool fft_halves = false; // two 512-point transforms per warp pair (SWR_FFT_HALVES=1; measured slower)
   // V(t,x): per-step pivots [N_T][N][N_j]; f(u): fixed-point stats
   double *tau = nullptr, *xi = nullptr;
   double2 *qtd = nullptr;
@@ -729,7 +730,11 @@ int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
   if (h->N < 2) return SWR_OK;
   CKS(record_pair(h, false, true));
   if (h->log4 && h->fft_reg) {
-    CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
+    if (h->fft_halves)
+      CK(swr::launch_fft_conv_h(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, nullptr, nullptr,
+                                swr::l2_persist_bytes()));
+    else
+      CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
     h->n_launches++;
   } else if (h->log4 && h->fft_fused) {
     CK(swr::launch_fft_conv(h->log4, zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
@@ -755,7 +760,11 @@ int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
 // Fused GMRES operator (register FFT path only): y = (I - L)(s x), vcopy = s x.
 int apply_I_minus_L_scaled(swr_handle *h, bool zero, const double2 *x, const double2 *sp, double2 *vcopy, double2 *y) {
   CKS(record_pair(h, false, true));
-  CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy));
+  if (h->fft_halves)
+    CK(swr::launch_fft_conv_h(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy,
+                              swr::l2_persist_bytes()));
+  else
+    CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy));
   h->n_launches++;
   CKS(record_pair(h, false, false));
   return SWR_OK;
@@ -1105,6 +1114,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->pade_m = cfg->pade_m;
   h->pinv_exact = cfg->pinv_exact ? 1 : 0;
   if (const char *e = getenv("SWR_CGS_ALT")) h->cgs_alt = atoi(e) != 0;
+  if (const char *e = getenv("SWR_FFT_HALVES")) h->fft_halves = atoi(e) != 0;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;

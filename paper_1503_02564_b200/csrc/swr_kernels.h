@@ -51,6 +51,10 @@ __global__ void k_fill(double2 *x, double2 v, size_t n);
 enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8, CGS_REV = 16 };
 cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
                                 cudaStream_t st, const double2 *xs = nullptr, double2 *xcopy = nullptr);
+// y = (I - L) x with two warps per 1024-point transform (swr_fft_halves.cu)
+cudaError_t launch_fft_conv_h(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
+                              cudaStream_t st, const double2 *xs, double2 *xcopy, size_t l2_window);
+size_t l2_persist_bytes();
 // exact P^{-1} by causal forward substitution (swr_pinv.cu), time blocks of PINV_B steps
 constexpr int PINV_B = 16;
 cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, double2 *F, int N, int NT,

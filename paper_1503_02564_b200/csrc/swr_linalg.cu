@@ -475,7 +475,7 @@ __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restric
 
 // Bytes of L2 set aside for persisting accesses on the current device (0: none;
 // SWR_L2_PERSIST=0 disables the window).
-static size_t l2_persist_bytes() {
+size_t l2_persist_bytes() {
   static size_t v = [] {
     const char *e = getenv("SWR_L2_PERSIST");
     if (e && strcmp(e, "0") == 0) return (size_t)0;

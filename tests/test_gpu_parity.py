@@ -311,16 +311,21 @@ def test_cgs_kernel_forms(oracle_mod, gpu, cgs, monkeypatch):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["direct", "fft", "fft2", "fftsm"])
+@pytest.mark.parametrize("mode", ["direct", "fft", "fft2w", "fft2", "fftsm"])
 def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
     """All forms of y = (I - L) x (direct causal convolution; FFT convolution:
-    register four-step for NF = 1024 (default), fused or two-kernel radix-4
-    Stockham) against the oracle's direct convolution."""
+    for NF = 1024 the one-warp register four-step kernel (default) or two
+    512-point transforms per warp pair, fused or two-kernel radix-4 Stockham)
+    against the oracle's direct convolution."""
     import torch
     if mode in ("direct", "fft2", "fftsm"):
         monkeypatch.setenv("SWR_TOEPLITZ", mode)
     else:
         monkeypatch.delenv("SWR_TOEPLITZ", raising=False)
+    if mode == "fft2w":
+        monkeypatch.setenv("SWR_FFT_HALVES", "1")
+    else:
+        monkeypatch.delenv("SWR_FFT_HALVES", raising=False)
     for p in (si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX),
               si.Problem(dx=1e-3, dt=1e-3, N=20, potential=si.POT_VX)):   # N_T = 100 and 500
         o, g_ = _pair(oracle_mod, gpu, p)
