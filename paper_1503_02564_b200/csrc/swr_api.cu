@@ -137,6 +137,8 @@ struct swr_handle {
   double2 *pinvF = nullptr;   // [2N-2][PINV_B] far-history scratch
   bool cgs_alt = true; // alternate CGS traversal direction (SWR_CGS_ALT=0 disables)
   int cgs_dir = 0;
+  size_t vwin_bytes = 0;   // persisting L2 window over the first outer-Krylov basis vectors (SWR_V_PERSIST)
+  float vwin_ratio = 1.0f;
   int Nx, NT, Nj, m;
   size_t ng;
   int rank, world, device;
@@ -588,7 +590,10 @@ int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w
     h->cgs_dir ^= 1;
     if (h->cgs_dir) mode |= swr::CGS_REV;
   }
-  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st, out_host));
+  // the first basis vectors stay in L2 (persisting window; every pass reads them)
+  const bool win = V && V == h->kout.V && h->vwin_bytes > 0;
+  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st, out_host,
+                     win ? h->vwin_bytes : 0, h->vwin_ratio));
   h->n_launches++;
   return SWR_OK;
 }
@@ -1217,9 +1222,23 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
         size_t cur = 0;
         cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
         cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        const size_t want = std::min((size_t)maxp, (size_t)h->N * 4 * NF * sizeof(double2));
+        const size_t fxb = (size_t)h->N * 4 * NF * sizeof(double2);
+        // the first 4 outer basis vectors also persist (read by every CGS pass;
+        // measured: 0 / 3 / 4 / 5 / 6 / 8 vectors -> C5 solve 94.2 / 93.0 / 92.6 /
+        // 93.6 / 96.4 / 96.9 ms: more set-aside starves the streamed vectors)
+        const char *ve = getenv("SWR_V_PERSIST");
+        const int nvp = ve ? atoi(ve) : 4;
+        const size_t vb = (size_t)std::max(0, nvp) * ng * sizeof(double2);
+        const size_t want = std::min((size_t)maxp, fxb + vb);
         if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
         cudaGetLastError();
+        if (vb > 0 && (size_t)maxp > fxb) {
+          h->vwin_bytes = vb;
+          h->vwin_ratio = (float)std::min(1.0, (double)((size_t)maxp - fxb) / (double)vb);
+        }
+        if (getenv("SWR_L2_VERBOSE"))
+          fprintf(stderr, "L2 persisting: max %d B, FX %zu B, V window %zu B ratio %.3f\n", maxp, fxb, h->vwin_bytes,
+                  h->vwin_ratio);
       }
       swr::k_twiddles<<<(unsigned)((NF + 255) / 256), 256, 0, h->st>>>(h->tw, (int)NF);
       if (cudaGetLastError() != cudaSuccess) return fail(SWR_ERR_CUDA);

@@ -23,6 +23,30 @@ inline cudaError_t launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, siz
   return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
 }
 
+// launch_pdl plus an L2 access-policy window (persisting hits on
+// [wptr, wptr + wbytes), hit ratio wratio); wbytes = 0: no window
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl_win(const void *wptr, size_t wbytes, float wratio, void (*kern)(KArgs...), dim3 grid,
+                                  dim3 block, size_t smem, cudaStream_t st, Args &&...args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[1].val.accessPolicyWindow.base_ptr = const_cast<void *>(wptr);
+  at[1].val.accessPolicyWindow.num_bytes = wbytes;
+  at[1].val.accessPolicyWindow.hitRatio = wratio;
+  at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = wbytes ? 2 : 1;
+  return cudaLaunchKernelEx(&cfg, kern, std::forward<Args>(args)...);
+}
+
 struct FactorJob {
   const double *W;   // nodal W on the subdomain [N_j] (NULL = 0)
   int32_t has_left, has_right;
@@ -61,7 +85,7 @@ cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, 
                                int sweeps, cudaStream_t st, int *n_launches);
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
-                       double2 *out_host = nullptr);
+                       double2 *out_host = nullptr, size_t vwin = 0, float vratio = 1.0f);
 __global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);
 
 int fft_log4_for(int NT);

@@ -1087,7 +1087,8 @@ static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const 
 
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
                        double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
-                       double2 *out_host) {
+                       double2 *out_host, size_t vwin, float vratio) {
+  if (!V) vwin = 0;
   const size_t ntot = (size_t)(2 * N - 2) * NT;
   if (nv > 32) return cudaErrorInvalidValue;
   // default: register form below; SWR_CGS=tma selects the bulk-copy pipeline
@@ -1105,15 +1106,15 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
     // best of KE 1/2/4, 4 or 8 vectors per step, 1-3 CTAs per SM)
     const size_t nwarp_needed = (ntot + 32 * 4 - 1) / (32 * 4);
     const unsigned g = (unsigned)std::min<size_t>((nwarp_needed + 7) / 8, 148 * 2);
-    return launch_pdl(k_cgs_axpy<4, 2>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter,
-                      ntot, out_host);
+    return launch_pdl_win(V, vwin, vratio, k_cgs_axpy<4, 2>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode,
+                          partial, out, counter, ntot, out_host);
   }
   // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
   // grid only depends on the sizes, so the reduction order is fixed
   auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
-  if (nv <= 8) return launch_pdl(k_cgs<2, 8>, dim3(grid(256)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
-  if (nv <= 16) return launch_pdl(k_cgs<4, 4>, dim3(grid(128)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
-  return launch_pdl(k_cgs<8, 2>, dim3(grid(64)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  if (nv <= 8) return launch_pdl_win(V, vwin, vratio, k_cgs<2, 8>, dim3(grid(256)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  if (nv <= 16) return launch_pdl_win(V, vwin, vratio, k_cgs<4, 4>, dim3(grid(128)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  return launch_pdl_win(V, vwin, vratio, k_cgs<8, 2>, dim3(grid(64)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
 }
 
 // ---------------------------------------------------------------------------
