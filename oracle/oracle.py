@@ -54,10 +54,32 @@ class _Report(C.Structure):
 _lib = None
 
 
+_variants = {}
+
+
+def lib_fma():
+    """The same oracle source built with FMA contraction (-ffp-contract=fast):
+    only its rounding differs, so the spread between the two builds measures
+    how much a problem amplifies rounding (the parity floor of the full-size
+    sampled tests)."""
+    if "fma" not in _variants:
+        so = os.path.join(_HERE, "liboracle_fma.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
+            flags = [f for f in CFLAGS if f != "-ffp-contract=off"] + ["-ffp-contract=fast", "-mfma"]
+            subprocess.check_call(["gcc", *flags, "-o", so, _SRC, "-lm"])
+        _variants["fma"] = _bind(C.CDLL(so))
+    return _variants["fma"]
+
+
 def lib():
     global _lib
     if _lib is None:
-        _lib = C.CDLL(build())
+        _lib = _bind(C.CDLL(build()))
+    return _lib
+
+
+def _bind(_lib):
+    if True:
         P = C.POINTER(_Problem)
         vp, i32 = C.c_void_p, C.c_int32
         _lib.or_coeffs.argtypes = [i32, vp, vp, vp]
@@ -104,7 +126,7 @@ def _f64(a):
 class Oracle:
     """The oracle bound to one problem (swr_inputs.Problem + input arrays)."""
 
-    def __init__(self, p, arrays: dict):
+    def __init__(self, p, arrays: dict, library=None):
         self.p = p
         self.keep = {k: (_c128(v) if k in ("u0", "g0") else _f64(v)) for k, v in arrays.items()}
         s = _Problem()
@@ -126,7 +148,7 @@ class Oracle:
         s.pade_m = getattr(p, "pade_m", 0)
         s.pinv_exact = getattr(p, "pinv_exact", 0)
         self.s = s
-        self.L = lib()
+        self.L = library if library is not None else lib()
         self.Nx, self.NT, self.Nj = p.Nx, p.NT, p.Nj
         self.ng = (2 * p.N - 2) * p.NT
 
