@@ -26,6 +26,8 @@
 // same barriers.
 #include "swr_common.cuh"
 #include "swr_kernels.h"
+#include <cstdio>
+#include <cstdlib>
 #include <cooperative_groups.h>
 #include <cstdlib>
 
@@ -1123,8 +1125,8 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 // reduced over the cluster so the decision is uniform).  (A_NL - B) is the
 // V = 0 matrix: constant pivots, Re E_k = 1/h.
 // ---------------------------------------------------------------------------
-template <int M, int PMAX>
-__global__ void __launch_bounds__(PMAX, 1) k_march_nl(const MarchParams p) {
+template <int M, int PMAX, int MINB = 1>
+__global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
   extern __shared__ double2 sm[];
   const int P = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = P >> 5;
   const int CS = p.CS;
@@ -1443,8 +1445,12 @@ MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi) {
 MarchShape choose_march_shape_nl(int Nj) {
   MarchShape best{0, 0, 0, 1};
   double best_cost = 1e300;
+  const int m_env = getenv("SWR_NL_M") ? atoi(getenv("SWR_NL_M")) : 0;     // experiments
+  const int cs_env = getenv("SWR_NL_CS") ? atoi(getenv("SWR_NL_CS")) : 0;
   for (int CS = 1; CS <= 16; CS++) {
+    if (cs_env && CS != cs_env) continue;
     for (int M : {1, 2, 4, 8}) {
+      if (m_env && M != m_env) continue;
       const int PMAX = M <= 2 ? 512 : 256;
       long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
       int P = (int)((per + 31) / 32 * 32);
@@ -1464,9 +1470,9 @@ size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
   return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
 }
 
-template <int M, int PMAX>
+template <int M, int PMAX, int MINB = 1>
 static cudaError_t launch_nl_m(const MarchParams &p, const MarchShape &s, size_t smem, cudaStream_t st) {
-  auto kern = k_march_nl<M, PMAX>;
+  auto kern = k_march_nl<M, PMAX, MINB>;
   cudaError_t e = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   if (s.CS > 8) {
@@ -1488,6 +1494,14 @@ static cudaError_t launch_nl_m(const MarchParams &p, const MarchShape &s, size_t
     attr[0].val.clusterDim.z = 1;
     cfg.numAttrs = 1;
   }
+  if (getenv("SWR_MARCH_VERBOSE")) {
+    int ncl = 0;
+    cudaOccupancyMaxActiveClusters(&ncl, (void *)kern, &cfg);
+    cudaFuncAttributes fa;
+    cudaFuncGetAttributes(&fa, kern);
+    fprintf(stderr, "k_march_nl M=%d P=%d CS=%d systems=%d regs=%d smem=%zu: %d clusters resident\n", M, s.P, s.CS,
+            p.nsys, fa.numRegs, smem, ncl);
+  }
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
@@ -1499,7 +1513,11 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
     case 1: return launch_nl_m<1, 512>(p, s, smem, st);
     case 2: return launch_nl_m<2, 512>(p, s, smem, st);
     case 4: return launch_nl_m<4, 256>(p, s, smem, st);
-    case 8: return launch_nl_m<8, 256>(p, s, smem, st);
+    case 8:
+      // two CTAs per SM when the CTA has <= 192 threads (register cap 170):
+      // twice the resident clusters, fewer waves of systems (C4: 3 -> 2)
+      if (s.P <= 192 && !getenv("SWR_NL_ONE")) return launch_nl_m<8, 192, 2>(p, s, smem, st);
+      return launch_nl_m<8, 256>(p, s, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }
