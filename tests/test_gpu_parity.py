@@ -195,6 +195,20 @@ def test_pinv_exact_parity(oracle_mod, gpu, name, N, pot, kry):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
+@pytest.mark.parametrize("N,tc", [(2, si.TC_ROBIN), (2, si.TC_S02), (4, si.TC_ROBIN)])
+def test_pinv_exact_small_chains(oracle_mod, gpu, N, tc):
+    """Exact P^{-1} at the ends of its range: one interface (N = 2, no cross
+    couplings, no sweeps) and Robin (the 2x2 lag-0 blocks are far from the
+    identity), against the oracle's dense lag-0 LU."""
+    p = si.config("C1", transmission=tc, potential=si.POT_VTX, N=N, algorithm=si.ALG_PRECOND, pinv_exact=1,
+                  robin_p=5.0)
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0 and rg["iterations"] == ro["iterations"]
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)
