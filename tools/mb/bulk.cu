@@ -8,6 +8,7 @@ __global__ void kb(const char *base, size_t stride_step, size_t stride_cta, unsi
   unsigned long long *mb = (unsigned long long *)sm;
   char *buf = sm + 16;
   if (threadIdx.x == 0) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su(sm + 16 + ch + 16)), "r"(1));
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(su(mb)), "r"(1));
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -17,7 +18,38 @@ __global__ void kb(const char *base, size_t stride_step, size_t stride_cta, unsi
   for (int s = 0; s < steps; s++) {
     const char *src = base + (size_t)s * stride_step + (size_t)blockIdx.x * stride_cta;
     long long t0 = clock64();
-    if (mode == 0) {
+    if (mode >= 2) {
+      // copy issued, then ~12K cycles of other work, then the wait: is the copy
+      // (alone: ~1.8K cycles) slowed by smem traffic (2) or mbarrier polling (3)?
+      if (threadIdx.x == 0) {
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(mb)), "r"(ch) : "memory");
+        asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
+                     ::"r"(su(buf)), "l"(src), "r"(ch), "r"(su(mb)) : "memory");
+      }
+      double2 *sb = (double2 *)(buf + ch + 64);
+      unsigned long long *dmb = (unsigned long long *)(buf + ch + 16);   // never completes
+      const long long tw0 = clock64();
+      double acc = 0;
+      int k = 0;
+      while (clock64() - tw0 < 12000) {
+        if (mode == 2) {
+          double2 v = sb[(threadIdx.x * 7 + k) & 1023];
+          acc += v.x;
+          sb[(threadIdx.x * 13 + k) & 1023] = make_double2(acc, v.y);
+          k++;
+        } else {
+          uint32_t done;
+          asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                       : "=r"(done) : "r"(su(dmb)), "r"(1) : "memory");
+          k += done;
+        }
+      }
+      sink += acc + k;
+      uint32_t done = 0;
+      while (!done)
+        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
+                     : "=r"(done) : "r"(su(mb)), "r"(s & 1) : "memory");
+    } else if (mode == 0) {
       if (threadIdx.x == 0) {
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(su(mb)), "r"(ch) : "memory");
         asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
@@ -47,22 +79,31 @@ int main() {
   cudaMemset(a, 0, big);
   long long *o; cudaMalloc(&o, 1024 * 8);
   unsigned ch = 45056;
-  cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 100000);
+  cudaFuncSetAttribute(kb, cudaFuncAttributeMaxDynamicSharedMemorySize, 120000);
   struct { const char *name; size_t ss, sc; } cfg[] = {
     {"C3 layout (step 67MB, cta 672KB)", 67200000ull, 672016ull * 1},
     {"small span (step 64KB, cta 672KB)", 65536ull, 672016ull},
     {"per-cta contiguous (step 45KB, cta 22.5MB)", 45056ull, 22528000ull},
   };
-  for (int mode = 0; mode < 2; mode++)
+  cudaFuncSetAttribute(kb, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  for (int cs : {1, 15})
+  for (int mode = 0; mode < 4; mode++)
   for (auto &c : cfg) {
     for (int rep = 0; rep < 2; rep++) {
-      kb<<<120, 256, 100000>>>(a, c.ss, c.sc, ch, 500, o, mode);
-      cudaError_t e = cudaDeviceSynchronize();
+      cudaLaunchConfig_t lc = {};
+      lc.gridDim = dim3(120); lc.blockDim = dim3(256); lc.dynamicSmemBytes = 120000;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = cs; at[0].val.clusterDim.y = 1; at[0].val.clusterDim.z = 1;
+      lc.attrs = at; lc.numAttrs = 1;
+      cudaError_t e = cudaLaunchKernelEx(&lc, kb, (const char *)a, c.ss, c.sc, ch, 500, o, mode);
+      if (!e) e = cudaDeviceSynchronize();
       if (e) { printf("err %s\n", cudaGetErrorString(e)); return 1; }
     }
+    printf("cluster %2d ", cs);
     long long h[120]; cudaMemcpy(h, o, sizeof h, cudaMemcpyDeviceToHost);
     double m = 0; for (int i = 0; i < 120; i++) m += h[i]; m /= 120;
-    printf("%s %-45s mean cycles per 45KB copy: %.0f (%.1f B/cyc/SM)\n", mode ? "LDG " : "BULK", c.name, m, ch / m);
+    printf("%s %-45s mean cycles per 45KB copy: %.0f (%.1f B/cyc/SM)\n", mode == 0 ? "BULK" : mode == 1 ? "LDG " : mode == 2 ? "B+SM" : "B+MB", c.name, m, ch / m);
   }
   return 0;
 }
