@@ -74,7 +74,7 @@ enum swr_potential {
 /* Transmission operators (discrete P:218-267): Robin -ip;
  * potential strategy S0^2, S0^3, S0^4; gauge strategy S1^2, S1^4; Pade
  * strategy S2^{2,m}, S2^{4,m} with m = pade_m poles (coefficients: reading
- * A26).  Operators other than Robin / S0^2 need a time-independent potential
+ * A26, the rotated-branch-cut Pade approximant, theta = pi/4).  Operators other than Robin / S0^2 need a time-independent potential
  * (V = 0 or V(x)) and the NEW or CLASSICAL algorithm (readings A23-A26). */
 enum swr_transmission {
   SWR_TC_ROBIN = 0, SWR_TC_S0_2 = 1, SWR_TC_S0_3 = 2, SWR_TC_S0_4 = 3, SWR_TC_S1_2 = 4, SWR_TC_S1_4 = 5,

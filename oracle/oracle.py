@@ -242,7 +242,7 @@ def fem(nn, h, W=None):
 
 
 def pade_coeffs(m):
-    a, d = np.zeros(m + 1), np.zeros(m + 1)
+    a, d = np.zeros(m + 1, np.complex128), np.zeros(m + 1, np.complex128)
     lib().or_pade_coeffs(m, _ptr(a), _ptr(d))
     return a, d
 

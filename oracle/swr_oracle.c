@@ -173,34 +173,46 @@ static ocplx or_c0(const or_problem *P) {
 /* ------------------------------------------------------------------ */
 /* Pade strategy S2^{2,m}, S2^{4,m} (P:173-177 continuous, P:241-267     */
 /* discrete).  sqrt(z) ~ sum_{s=0}^m a_s - sum_{s=1}^m a_s d_s/(z + d_s). */
-/* The paper does not give a_s^m, d_s^m (reading A26): the rational       */
-/* approximation of the cited ABC literature, a_0 = 0,                    */
-/* a_s = 1/(m cos^2 th_s), d_s = tan^2 th_s, th_s = (2s-1) pi/(4m).       */
+/* The paper does not give a_s^m, d_s^m (reading A26): the rotated-branch- */
+/* cut Pade approximation of the cited ABC literature with theta = pi/4:  */
+/* sqrt z = e^{i th/2} sqrt(e^{-i th} z), sqrt(1 + x) by the diagonal      */
+/* Pade approximant 1 + sum_s b_s x/(1 + c_s x), b_s = 2/(2m+1) sin^2 u_s, */
+/* c_s = cos^2 u_s, u_s = s pi/(2m+1); in the form above                  */
+/*   d_s = e^{i th} (1 - c_s)/c_s,  a_s = e^{i th/2} b_s/(c_s (1 - c_s)),  */
+/*   a_0 = e^{i th/2} (1 + sum_s b_s/c_s) - sum_{s>=1} a_s  (complex).     */
+/* Chosen because it reproduces the fixed-point counts of the paper's     */
+/* Table 6 (187/76/39 vs 191/76/39 for m = 20/50/100), which */
+/* the unrotated forms miss by a factor ~3.7 (A26).             */
 /* In S2^2 the paper writes d_k^m in one denominator; read as d_s^m.      */
 /* ------------------------------------------------------------------ */
 static int or_is_pade(const or_problem *P) {
   return P->transmission == OR_TC_S22 || P->transmission == OR_TC_S24;
 }
 
-void or_pade_coeffs(int32_t m, double *a, double *d) {
-  a[0] = 0.0;
+void or_pade_coeffs(int32_t m, ocplx *a, ocplx *d) {
+  const double pi = acos(-1.0), th = pi / 4.0;
+  const ocplx eh = cexp(I_ * (th / 2.0)), ef = cexp(I_ * th);
+  ocplx sumb = 0.0, suma = 0.0;
   d[0] = 0.0;
   for (int32_t s = 1; s <= m; s++) {
-    const double th = (2.0 * s - 1.0) * acos(-1.0) / (4.0 * m);
-    const double c = cos(th);
-    a[s] = 1.0 / (m * c * c);
-    d[s] = tan(th) * tan(th);
+    const double u = s * pi / (2.0 * m + 1.0);
+    const double cs = cos(u) * cos(u), bs = 2.0 / (2.0 * m + 1.0) * sin(u) * sin(u);
+    d[s] = ef * ((1.0 - cs) / cs);
+    a[s] = eh * (bs / (cs * (1.0 - cs)));
+    sumb += bs / cs;
+    suma += a[s];
   }
+  a[0] = eh * (1.0 + sumb) - suma;
 }
 
 /* State of the auxiliary functions phi^s_{j,n-1} (s = 1..m) and psi_{j,n-1}
  * of one boundary point, both zero at n = 0. */
-typedef struct { int32_t m; double *a, *d; ocplx *phi; ocplx psi; } pade_state;
+typedef struct { int32_t m; ocplx *a, *d; ocplx *phi; ocplx psi; } pade_state;
 
 static int32_t pade_init(const or_problem *P, pade_state *S) {
   S->m = P->pade_m;
-  S->a = (double *)calloc((size_t)S->m + 1, sizeof(double));
-  S->d = (double *)calloc((size_t)S->m + 1, sizeof(double));
+  S->a = (ocplx *)calloc((size_t)S->m + 1, sizeof(ocplx));
+  S->d = (ocplx *)calloc((size_t)S->m + 1, sizeof(ocplx));
   S->phi = (ocplx *)calloc((size_t)S->m + 1, sizeof(ocplx));
   S->psi = 0.0;
   if (!S->a || !S->d || !S->phi) return OR_OOM;

@@ -75,8 +75,9 @@ typedef struct {
 void or_coeffs(int32_t n, double *alpha, double *beta, double *gamma);
 
 /* Mesh / partition sizes. */
-/* Pade coefficients a_s^m, d_s^m, s = 0..m (reading A26, a_0 = d_0 = 0). */
-void or_pade_coeffs(int32_t m, double *a, double *d);
+/* Pade coefficients a_s^m, d_s^m, s = 0..m (reading A26: rotated branch cut,
+ * theta = pi/4; complex; d_0 = 0). */
+void or_pade_coeffs(int32_t m, ocplx *a, ocplx *d);
 /* S v_n (n = 1..nsteps) of the configured transmission operator at one
  * boundary point with interface data W, dnW, applied to v_0..v_nsteps. */
 int32_t or_tc_apply(const or_problem *P, double W, double dnW, int32_t nsteps, const ocplx *v, ocplx *Sv);

@@ -409,13 +409,25 @@ int setup_tc(swr_handle *h) {
   const cplx cc2 = c2(h->c2v), e3 = cplx(1.0, 1.0) / std::sqrt(2.0) * std::sqrt(h->dt / 2.0);
   const int tc = h->transmission;
   const bool pade = tc == SWR_TC_S2_2 || tc == SWR_TC_S2_4;
-  // Pade poles (reading A26): a_s = 1/(m cos^2 th_s), d_s = tan^2 th_s, th_s = (2s-1) pi/(4m), a_0 = 0
+  // Pade poles (reading A26): the diagonal Pade approximant of sqrt(1 + x)
+  // (b_s = 2/(2m+1) sin^2 u_s, c_s = cos^2 u_s, u_s = s pi/(2m+1)) with the
+  // branch cut rotated by theta = pi/4, sqrt z = e^{i th/2} sqrt(e^{-i th} z),
+  // written as sum_{s>=0} a_s - sum_{s>=1} a_s d_s/(z + d_s) (complex a_s, d_s)
   const int pm = h->pade_m;
-  std::vector<double> pa(pade ? pm + 1 : 0, 0.0), pd(pade ? pm + 1 : 0, 0.0);
-  for (int s = 1; pade && s <= pm; s++) {
-    const double th = (2.0 * s - 1.0) * M_PI / (4.0 * pm), c = std::cos(th), t = std::tan(th);
-    pa[s] = 1.0 / (pm * c * c);
-    pd[s] = t * t;
+  std::vector<cplx> pa(pade ? pm + 1 : 0, cplx(0.0)), pd(pade ? pm + 1 : 0, cplx(0.0));
+  if (pade) {
+    const double tht = M_PI / 4.0;
+    const cplx eh = std::exp(cplx(0.0, tht / 2.0)), ef = std::exp(cplx(0.0, tht));
+    cplx sb(0.0), sa(0.0);
+    for (int s = 1; s <= pm; s++) {
+      const double u = s * M_PI / (2.0 * pm + 1.0), cs = std::cos(u) * std::cos(u);
+      const double bs = 2.0 / (2.0 * pm + 1.0) * std::sin(u) * std::sin(u);
+      pd[s] = ef * ((1.0 - cs) / cs);
+      pa[s] = eh * (bs / (cs * (1.0 - cs)));
+      sb += bs / cs;
+      sa += pa[s];
+    }
+    pa[0] = eh * (1.0 + sb) - sa;
   }
   const bool gauge = tc == SWR_TC_S1_2 || tc == SWR_TC_S1_4, order4 = tc == SWR_TC_S0_4 || tc == SWR_TC_S1_4;
   std::vector<double2> K((size_t)N * 2 * (NT + 1));
@@ -439,7 +451,7 @@ int setup_tc(swr_handle *h) {
         // i.e. the odd part 2 dlt rho_0^{n-t} with dlt = (dnW/4)(2i/dt)/(D_0^2 rho_0).
         const cplx s2(0.0, 2.0 / h->dt);
         cplx k0(0.0, 0.0);
-        for (int s = 1; s <= pm; s++) k0 += cplx(0.0, -1.0) * pa[s];
+        for (int s = 0; s <= pm; s++) k0 += cplx(0.0, -1.0) * pa[s];
         for (int m = 1; m <= NT; m++) k[m] = make_double2(0, 0);
         std::vector<cplx> acc(NT + 1, cplx(0.0, 0.0));
         for (int s = 1; s <= pm; s++) {

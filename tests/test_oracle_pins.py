@@ -457,18 +457,26 @@ PADE_TC = [si.TC_S22, si.TC_S24]
 @pytest.mark.parametrize("m", [1, 5, 20, 100])
 def test_pade_coefficients_approximate_sqrt(oracle_mod, m):
     """Reading A26: sqrt(z) ~ R_m(z) = sum_s a_s - sum_s a_s d_s/(z + d_s)
-    (the form of P:243-247).  R_m(1) = 1 exactly for every m, and R_m
-    converges to numpy's sqrt on the right half plane as m grows."""
+    (the form of P:243-247) with the branch cut rotated by pi/4.  R_m is
+    exact at the rotation point, R_m(e^{i pi/4}) = e^{i pi/8}, for every m,
+    its poles -d_s lie on the rotated cut, and R_m converges to numpy's sqrt
+    away from that cut (including z = 2i/dt, where the discrete operator
+    evaluates it) as m grows."""
     a, d = oracle_mod.pade_coeffs(m)
-    assert a[0] == 0.0 and np.all(a[1:] > 0) and np.all(np.diff(d[1:]) > 0)
+    assert d[0] == 0.0
+    assert np.allclose(np.angle(d[1:]), np.pi / 4) and np.all(np.diff(np.abs(d[1:])) > 0)
 
     def R(z):
         return a.sum() - np.sum(a[1:] * d[1:] / (z + d[1:]))
 
-    assert abs(R(1.0) - 1.0) <= 1e-14
+    assert abs(R(np.exp(1j * np.pi / 4)) - np.exp(1j * np.pi / 8)) <= 1e-13
     z = np.array([0.3, 2.0, 1 + 3j, 5j, 0.5 - 2j])
     err = max(abs(R(zz) - np.sqrt(zz)) / abs(np.sqrt(zz)) for zz in z)
-    assert err <= {1: 1.0, 5: 2e-2, 20: 1e-6, 100: 1e-13}[m], err
+    assert err <= {1: 1.0, 5: 1e-2, 20: 1e-8, 100: 1e-12}[m], err
+    # far out on the imaginary axis (z = 2i/dt at dt = 1e-3) the error still
+    # falls with m: 0.94 / 0.78 / 0.32 / 4.9e-4 for m = 1 / 5 / 20 / 100
+    e2 = abs(R(2000j) - np.sqrt(2000j)) / abs(np.sqrt(2000j))
+    assert e2 <= {1: 1.0, 5: 0.9, 20: 0.4, 100: 1e-3}[m], e2
 
 
 @pytest.mark.parametrize("tc", PADE_TC)
@@ -502,7 +510,7 @@ def test_pade_tends_to_s02_without_potential(oracle_mod):
     """With W = 0, S2^{2,m} -> S0^2 = -i sqrt(z_d) (the beta
     convolution) as m grows, wherever the Pade approximant of sqrt converges
     on the symbol's range (dt = 1 keeps z_d = O(1)); m = 100 agrees to
-    rounding on a random trace sequence, m = 20 does not."""
+    rounding on a random trace sequence, m = 20 only approximately."""
     base = si.config("C1", T=40.0, dt=1.0)
     rng = np.random.default_rng(1)
     v = rng.standard_normal(41) + 1j * rng.standard_normal(41)
@@ -512,7 +520,7 @@ def test_pade_tends_to_s02_without_potential(oracle_mod):
     for m in (20, 100):
         q = dataclasses.replace(base, transmission=si.TC_S22, pade_m=m)
         err[m] = np.abs(oracle_mod.Oracle(q, si.inputs(q)).tc_apply(v) - ref).max() / np.abs(ref).max()
-    assert err[100] <= 1e-12 and err[20] >= 1e-2, err
+    assert err[100] <= 1e-12 < err[20], err
 
 
 @pytest.mark.parametrize("tc", PADE_TC)
