@@ -540,6 +540,23 @@ def test_pade_tc_converges_to_monodomain(oracle_mod, tc):
     assert its[0] > its[1] > its[2], its
 
 
+def test_paper_table6_fixed_point_counts(oracle_mod):
+    """Pin to the paper's printed numbers (tests/golden/table6_fixed_point.txt,
+    Table 6): the fixed-point iteration counts of the new
+    algorithm for the Pade operators (reading A26) and Robin p = 44 on the
+    paper's problem (N = 2, V = -x^2, random g0), on a 10x coarser grid where
+    these counts are unchanged.  Pins the Pade coefficients and recursions,
+    the Robin rows, the interface operator and the fixed point together."""
+    here = os.path.join(os.path.dirname(__file__), "golden", "table6_fixed_point.txt")
+    rows = [l.split() for l in open(here) if l.strip() and not l.startswith("#")]
+    tcs = {"S22": si.TC_S22, "S24": si.TC_S24, "ROBIN": si.TC_ROBIN}
+    for name, m, pr, n_iter in rows:
+        p = si.config("C2", N=2, dx=1e-3, g0_random=True, krylov=si.KRY_FIXED_POINT, transmission=tcs[name],
+                      pade_m=int(m), robin_p=float(pr) if float(pr) > 0 else 5.0)
+        r = oracle_mod.Oracle(p, si.inputs(p)).solve()
+        assert r["status"] == 0 and r["iterations"] == int(n_iter), (name, m, pr, r["iterations"], n_iter)
+
+
 def test_gauge_tc_is_transparent_for_constant_potential(oracle_mod):
     """For a constant potential V0 the solution is e^{i V0 t} times a free one
     and the gauge operator S1^2 = e^{-i pi/4} e^{i calV} d_t^{1/2} e^{-i calV}
