@@ -209,6 +209,30 @@ def test_pinv_exact_small_chains(oracle_mod, gpu, N, tc):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
+PAPER_COUNT_CASES = [
+    # Table 5 (dx = 1e-4): classical fixed point, V = 5tx, N = 100 -> N_nopc = 71
+    ("table5-classical-N100", dict(name="C3", N=100, dx=1e-4, algorithm=si.ALG_CLASSICAL,
+                                   krylov=si.KRY_FIXED_POINT), 71),
+    # the NL table: preconditioned fixed point, |u|^2, N = 100 -> N_pc = 22 (C4 grid)
+    ("nl-precond-N100", dict(name="C4", maxit=2000), 22),
+    # Table 7: new algorithm, Robin p = 45, fixed point, N = 500, random g0 -> 1690
+    ("table7-robin45-N500", dict(name="C5", transmission=si.TC_ROBIN, robin_p=45.0, krylov=si.KRY_FIXED_POINT,
+                                 g0_random=True, maxit=2000), 1690),
+]
+
+
+@pytest.mark.parametrize("name,kw,count", PAPER_COUNT_CASES, ids=[c[0] for c in PAPER_COUNT_CASES])
+def test_paper_iteration_counts(gpu, name, kw, count):
+    """The GPU path reproduces iteration counts printed in the paper on the
+    paper's own experiments at full size (profiles/r01/table*.txt)."""
+    kw = dict(kw)
+    p = si.config(kw.pop("name"), **kw)
+    s = gpu.SWR(p, si.inputs(p))
+    s.build()
+    st, uT, r = s.solve()
+    assert st == 0 and r["iterations"] == count, (r["iterations"], count)
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)
