@@ -1449,8 +1449,9 @@ MarchShape choose_march_shape_nl(int Nj) {
   const int cs_env = getenv("SWR_NL_CS") ? atoi(getenv("SWR_NL_CS")) : 0;
   for (int CS = 1; CS <= 16; CS++) {
     if (cs_env && CS != cs_env) continue;
-    for (int M : {1, 2, 4, 8}) {
+    for (int M : {1, 2, 4, 8, 11}) {
       if (m_env && M != m_env) continue;
+      if (M == 11 && !m_env) continue;   // only when nothing smaller fits (below)
       const int PMAX = M <= 2 ? 512 : 256;
       long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
       int P = (int)((per + 31) / 32 * 32);
@@ -1459,6 +1460,14 @@ MarchShape choose_march_shape_nl(int Nj) {
       double padded = (double)CS * P * M;
       double cost = padded * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
       if (cost < best_cost) { best_cost = cost; best = {M, P, CS, 1}; }
+    }
+  }
+  if (best.M == 0 && !m_env) {   // N_j beyond 16 x 256 x 8 rows: 11 rows per thread
+    for (int CS = 1; CS <= 16 && best.M == 0; CS++) {
+      if (cs_env && CS != cs_env) continue;
+      const long per = ((long)Nj + (long)CS * 11 - 1) / ((long)CS * 11);
+      const int P = (int)((per + 31) / 32 * 32);
+      if (P <= 256) best = {11, P < 32 ? 32 : P, CS, 1};
     }
   }
   return best;
@@ -1518,6 +1527,8 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
       // twice the resident clusters, fewer waves of systems (C4: 3 -> 2)
       if (s.P <= 192 && !getenv("SWR_NL_ONE")) return launch_nl_m<8, 192, 2>(p, s, smem, st);
       return launch_nl_m<8, 256>(p, s, smem, st);
+    case 11:   // the largest subdomains (up to 16 x 256 x 11 = 45,056 rows)
+      return launch_nl_m<11, 256>(p, s, smem, st);
     default: return cudaErrorInvalidValue;
   }
 }

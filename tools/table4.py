@@ -26,7 +26,7 @@ for (pname, dxp), rows in PAPER.items():
         out = []
         for alg in (si.ALG_CLASSICAL, si.ALG_PRECOND):
             kry = si.KRY_GMRES if (alg == si.ALG_PRECOND and pot == si.POT_VTX) else si.KRY_FIXED_POINT
-            if pot == si.POT_CUBIC and 42.0 / (dxp * N) + 1 > 32768:   # no resident NL march beyond 32,768 rows
+            if pot == si.POT_CUBIC and 42.0 / (dxp * N) + 1 > 45056:   # no resident NL march beyond 45,056 rows
                 out.append(("n/a", 0.0))
                 continue
             p = si.config("C3", N=N, dx=dxp, potential=pot, algorithm=alg, krylov=kry, maxit=2000,
