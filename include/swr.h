@@ -107,7 +107,8 @@ typedef struct {
   int32_t inputs_on_device;   /* 1: u0, V_x, tau, xi, g0 are device pointers */
   int32_t algorithm;          /* swr_algorithm */
   double tol;                 /* outer tolerance (paper: 1e-10) */
-  int32_t restart, maxit;     /* GMRES(m): 30, 2000 */
+  int32_t restart, maxit;     /* GMRES(m): 30, 2000; restart <= 31 (the fused Gram-Schmidt
+                                 kernels hold up to 32 basis vectors), else SWR_ERR_INVALID_ARG */
   double tol_inner;           /* P^{-1} inner GMRES relative tol: 1e-12 */
   int32_t maxit_inner;        /* 2000 */
   double tol_fp;              /* NL inner fixed point relative max-norm: 1e-12 */

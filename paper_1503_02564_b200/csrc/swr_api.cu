@@ -1107,6 +1107,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     return SWR_ERR_INVALID_ARG;
   }
   if (cfg->krylov < 0 || cfg->krylov > 2 || cfg->algorithm < 0 || cfg->algorithm > 2) return SWR_ERR_INVALID_ARG;
+  if (cfg->restart > 31) { g_detail = "GMRES restart must be <= 31"; return SWR_ERR_INVALID_ARG; }
   if (cfg->algorithm == SWR_ALG_CLASSICAL && cfg->potential == SWR_POT_CUBIC && cfg->krylov != SWR_KRY_FIXED_POINT) {
     g_detail = "the classical Krylov algorithm needs an affine R (linear potential, P:734)";
     return SWR_ERR_INVALID_ARG;

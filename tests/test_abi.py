@@ -68,6 +68,9 @@ def test_setup_rejects_bad_config_without_gpu_work():
     assert L.swr_setup(C.byref(c), C.byref(h)) == 1
     c.transmission = 8                  # no such operator
     assert L.swr_setup(C.byref(c), C.byref(h)) == 1
+    c.transmission = si.TC_S02
+    c.restart = 32                      # beyond the fused Gram-Schmidt kernels
+    assert L.swr_setup(C.byref(c), C.byref(h)) == 1
     assert not h.value
     del np
 
