@@ -58,7 +58,8 @@ enum swr_status {
   SWR_ERR_ZERO_PIVOT = 3,         /* |pivot| < 1e-300: A - B singular (Prop. 1 hypothesis) */
   SWR_ERR_BREAKDOWN = 4,
   SWR_ERR_INNER_NOT_CONVERGED = 5,/* P^{-1} GMRES or NL fixed point hit its cap */
-  SWR_ERR_UNSUPPORTED = 6,        /* e.g. NEW with V(t,x) or f(u) */
+  SWR_ERR_UNSUPPORTED = 6,        /* e.g. NEW with V(t,x) or f(u); f(u) = |u|^2 with
+                                     N_j > 45,056 rows (the nonlinear march is resident only) */
   SWR_ERR_CUDA = 7,
   SWR_ERR_NCCL = 8,
   SWR_ERR_OOM = 9
