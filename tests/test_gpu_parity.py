@@ -233,6 +233,24 @@ def test_paper_iteration_counts(gpu, name, kw, count):
     assert st == 0 and r["iterations"] == count, (r["iterations"], count)
 
 
+@pytest.mark.parametrize("M", [8, 11])
+def test_nl_march_shapes(oracle_mod, gpu, M, monkeypatch):
+    """The NL march with 8 rows per thread and with the 11-row fallback used
+    beyond 16 x 256 x 8 rows (both forced on a problem the oracle solves; the
+    two-CTA-per-SM 192-thread variant runs in the C4 tests): the preconditioned fixed point for
+    |u|^2 with equal outer counts, equal NL fixed-point maxima, u(T) within
+    1e-10."""
+    monkeypatch.setenv("SWR_NL_M", str(M))
+    p = si.Problem(dx=2e-3, dt=5e-3, N=4, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT,
+                   u0_kind="soliton", pinv_exact=1)
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"] and rg["fp_max"] == ro["fp_max"], (rg, ro["iterations"])
+    assert rel(uT, ro["uT"]) <= 1e-10
+
+
 def test_random_g0_and_n1(oracle_mod, gpu):
     p = si.config("C1", transmission=si.TC_S02, potential=si.POT_VX, N=5, g0_random=True)
     o, g_ = _pair(oracle_mod, gpu, p)
