@@ -564,8 +564,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   // last row (qprev / er_prev of thread 0) by plain loads into registers
   double2 qprev_nx = cz();
   double erprev_nx = 0.0;
+  long long tpf = 0;   // trace builds: issue time of the last prefetch (copy latency, slot 28)
   auto prefetch = [&](int nn) {
     if (t != 0) return;
+    if (SWR_MARCH_TRACE) tpf = clock64();
     const size_t off = (size_t)(nn - 1) * p.td_stride + fbase;
     if (fcnt > 0) {
       // er rows are 8 B: start one row early when the source is not 16-B aligned
@@ -693,6 +695,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     SWR_TRACE(0);
     if (TDM && n > 1) {   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
       if (fcnt > 0) mbar_wait(pmb, (uint32_t)((n - 2) & 1));
+      if (SWR_TRACE_ON) p.trace[blockIdx.x * 32 + 28] = p.trace[blockIdx.x * 32] + (clock64() - tpf);
       load_factor_smem(n);
       __syncthreads();                 // every thread holds its rows: the buffer is free
       if (n < NT) prefetch(n + 1);
