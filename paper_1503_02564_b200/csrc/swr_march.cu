@@ -566,10 +566,10 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   double erprev_nx = 0.0;
   long long tpf = 0;   // trace builds: issue time of the last prefetch (copy latency, slot 28)
   auto prefetch = [&](int nn) {
-    if (t != 0) return;
-    if (SWR_MARCH_TRACE) tpf = clock64();
+    if (SWR_MARCH_TRACE && t == 0) tpf = clock64();
     const size_t off = (size_t)(nn - 1) * p.td_stride + fbase;
-    if (fcnt > 0) {
+    // issued by the last warp (warp 0 pushes the scan totals by st.async)
+    if (t == P - 32 && fcnt > 0) {
       // er rows are 8 B: start one row early when the source is not 16-B aligned
       const double *es = G[0].er + off;
       const unsigned mis = (unsigned)(((uintptr_t)es >> 3) & 1);
@@ -581,7 +581,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
                    ::"r"(smem_u32(pe)), "l"(es - mis), "r"(be), "r"(smem_u32(pmb)) : "memory");
     }
-    if (fbase > 0 && fbase - 1 < Nj) {
+    if (t == 0 && fbase > 0 && fbase - 1 < Nj) {
       qprev_nx = __ldg(G[0].q + off - 1);
       erprev_nx = __ldg(G[0].er + off - 1);
     }
