@@ -190,16 +190,22 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
     };
     // ---- forward: z_k = c_k z_{k-1} + q_k (i kappa s_k), c_k = -q_k E_{k-1} ----
+    // rows of this CTA through L1 (written by this SM); the halo rows of the
+    // neighbouring CTAs from L2 (written by other SMs in the previous step)
+    auto ldu = [&](int k) -> double2 { return (k >= rc0 && k < rc1) ? u[k] : __ldcg(u + k); };
+    // The two halo values u_{n-1}(rt0 - 1), u_{n-1}(rt1) are read once, before
+    // pass 1: once this CTA publishes its forward total, CTA c+1 may finish
+    // step n and overwrite its first row with u_n while pass 2 here still needs
+    // u_{n-1} (the neighbours' rows are final for step n-1 at this point).
+    const double2 halo_m = rt0 > 0 && rt0 < rt1 ? ldu(rt0 - 1) : cz();
+    const double2 halo_p = rt1 < Nj && rt0 < rt1 ? ldu(rt1) : cz();
     auto fwd_pass = [&](double2 zin, bool store, double2 &Aout) -> double2 {
       double2 zz = zin, A = make_double2(1.0, 0.0);
-      // rows of this CTA through L1 (written by this SM); the halo rows of the
-      // neighbouring CTAs from L2 (written by other SMs in the previous step)
-      auto ldu = [&](int k) -> double2 { return (k >= rc0 && k < rc1) ? u[k] : __ldcg(u + k); };
-      double2 um = rt0 > 0 ? ldu(rt0 - 1) : cz(), uk = rt0 < rt1 ? ldu(rt0) : cz();
+      double2 um = halo_m, uk = rt0 < rt1 ? ldu(rt0) : cz();
       double erp = rt0 > 0 ? er[rt0 - 1] : 0.0;
 #pragma unroll 4
       for (int k = rt0; k < rt1; k++) {
-        const double2 up = k + 1 < Nj ? ldu(k + 1) : cz();
+        const double2 up = k + 1 < Nj ? (k + 1 == rt1 ? halo_p : ldu(k + 1)) : cz();
         const double2 qk = __ldg(q + k);
         const double2 ck = negqe_s(qk, erp, eim);
         const double2 rr = cimul(kappa, sval(k, um, uk, up));
