@@ -23,7 +23,8 @@ def build(force: bool = False) -> str:
     """Compile the oracle (plain gcc, no FMA contraction)."""
     if force or not os.path.exists(_SO) or os.path.getmtime(_SO) < max(
             os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "swr_oracle.h"))):
-        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO, _SRC, "-lm"])
+        subprocess.check_call(["gcc", *CFLAGS, "-o", _SO + ".tmp", _SRC, "-lm", "-lpthread"])
+        os.replace(_SO + ".tmp", _SO)
     return _SO
 
 
@@ -57,18 +58,30 @@ _lib = None
 _variants = {}
 
 
+def _variant(tag, flags):
+    if tag not in _variants:
+        so = os.path.join(_HERE, f"liboracle_{tag}.so")
+        if not os.path.exists(so) or os.path.getmtime(so) < max(
+                os.path.getmtime(_SRC), os.path.getmtime(os.path.join(_HERE, "swr_oracle.h"))):
+            subprocess.check_call(["gcc", *flags, "-o", so + ".tmp", _SRC, "-lm", "-lpthread"])
+            os.replace(so + ".tmp", so)
+        _variants[tag] = _bind(C.CDLL(so))
+    return _variants[tag]
+
+
 def lib_fma():
     """The same oracle source built with FMA contraction (-ffp-contract=fast):
     only its rounding differs, so the spread between the two builds measures
     how much a problem amplifies rounding (the parity floor of the full-size
     sampled tests)."""
-    if "fma" not in _variants:
-        so = os.path.join(_HERE, "liboracle_fma.so")
-        if not os.path.exists(so) or os.path.getmtime(so) < os.path.getmtime(_SRC):
-            flags = [f for f in CFLAGS if f != "-ffp-contract=off"] + ["-ffp-contract=fast", "-mfma"]
-            subprocess.check_call(["gcc", *flags, "-o", so, _SRC, "-lm"])
-        _variants["fma"] = _bind(C.CDLL(so))
-    return _variants["fma"]
+    return _variant("fma", [f for f in CFLAGS if f != "-ffp-contract=off"] + ["-ffp-contract=fast", "-mfma"])
+
+
+def lib_mutant(k: int):
+    """The oracle with deliberate error k planted (-DOR_MUTANT=k, see the
+    mutation hooks in swr_oracle.c): tests/test_oracle_mutants.py shows that
+    the pins catch each one.  Never used for parity."""
+    return _variant(f"mut{k}", CFLAGS + [f"-DOR_MUTANT={int(k)}"])
 
 
 def lib():
@@ -102,9 +115,12 @@ def _bind(_lib):
         _lib.or_pade_coeffs.restype = None
         _lib.or_tc_apply.argtypes = [P, C.c_double, C.c_double, i32, vp, vp]
         _lib.or_pinv_causal.argtypes = [P, vp, vp, vp]
+        _lib.or_set_threads.argtypes = [i32]
+        _lib.or_set_threads.restype = None
+        _lib.or_get_threads.argtypes = []
         for f in ("or_sizes", "or_thomas", "or_subdomain_matrix", "or_march", "or_apply_R",
                   "or_build_L", "or_gmres_dense", "or_bicgstab_dense", "or_solve", "or_monodomain",
-                  "or_tc_apply", "or_pinv_causal"):
+                  "or_tc_apply", "or_pinv_causal", "or_get_threads"):
             getattr(_lib, f).restype = i32
         _lib.or_coeffs.restype = None
         _lib.or_fem.restype = None
@@ -226,6 +242,12 @@ class Oracle:
         fp = np.zeros(1, np.int32)
         st = self.L.or_monodomain(C.byref(self.s), _ptr(uT), _ptr(fp))
         return st, uT, int(fp[0])
+
+
+def set_threads(n: int, library=None):
+    """Threads of the oracle's subdomain-parallel loops (bitwise equal results
+    for any count; default 1)."""
+    (library or lib()).or_set_threads(int(n))
 
 
 def coeffs(n):

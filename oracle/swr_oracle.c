@@ -1,11 +1,15 @@
 /*
  * oracle/swr_oracle.c — TEST INFRASTRUCTURE ONLY (parity oracle).
  *
- * Plain, slow, single-threaded C implementation of the SWR method of
+ * Plain, slow C implementation of the SWR method of
  * Besse & Xing, arXiv:1503.02564.  Every function follows the paper's
  * formulas in the paper's order; "P:n" cites PAPER.md line n, "A<k>" cites
  * a reading listed in DESIGN.md.  Built with
  * -O2 -ffp-contract=off -fcx-limited-range (plain IEEE products, no FMA).
+ * Single-threaded by default; or_set_threads(P) runs independent subdomains
+ * (and element ranges of vector updates) on P threads with every reduction
+ * kept in its sequential order, so the results are bitwise those of one
+ * thread ("Oracle timing": T_oracle,1 and T_oracle,P).
  *
  * Only tests/, __graft_entry__.smoke() and bench.py (cpu_baseline and
  * --impl reference) may load this library.  The CUDA product path never
@@ -17,6 +21,60 @@
  */
 #include "swr_oracle.h"
 #include <math.h>
+#include <pthread.h>
+
+/* Mutation hooks for tests/test_oracle_mutants.py only: a build with
+ * -DOR_MUTANT=k plants one deliberate error (a wrong sign, time level or
+ * coefficient) so the test can show that a pin of tests/test_oracle_pins.py
+ * catches it.  The default build (OR_MUTANT = 0) contains none of them. */
+#ifndef OR_MUTANT
+#define OR_MUTANT 0
+#endif
+#define MUT(k) (OR_MUTANT == (k))
+
+/* ------------------------------------------------------------------ */
+/* Parallel loops.  par_for(n, fn, ctx) calls fn(ctx, i) for i = 0..n-1 */
+/* on up to or_threads threads (dynamic schedule).  Callers only use it */
+/* where every item writes disjoint outputs and sums keep their order. */
+/* ------------------------------------------------------------------ */
+static int32_t or_threads = 1;
+void or_set_threads(int32_t n) { or_threads = n < 1 ? 1 : (n > 256 ? 256 : n); }
+int32_t or_get_threads(void) { return or_threads; }
+
+typedef void (*or_item_fn)(void *ctx, int64_t item);
+typedef struct { or_item_fn fn; void *ctx; int64_t n, next; } par_job;
+
+static void *par_worker(void *arg) {
+  par_job *J = (par_job *)arg;
+  for (;;) {
+    const int64_t i = __atomic_fetch_add(&J->next, 1, __ATOMIC_RELAXED);
+    if (i >= J->n) break;
+    J->fn(J->ctx, i);
+  }
+  return NULL;
+}
+
+static void par_for(int64_t n, or_item_fn fn, void *ctx) {
+  int64_t T = or_threads < n ? or_threads : n;
+  par_job J = {fn, ctx, n, 0};
+  if (T <= 1) {
+    for (int64_t i = 0; i < n; i++) fn(ctx, i);
+    return;
+  }
+  pthread_t th[256];
+  int64_t started = 0;
+  for (int64_t t = 1; t < T; t++)
+    if (pthread_create(&th[started], NULL, par_worker, &J) == 0) started++;
+  par_worker(&J);
+  for (int64_t t = 0; t < started; t++) pthread_join(th[t], NULL);
+}
+
+/* element ranges of a length-n vector loop */
+#define PAR_CHUNK 8192
+static int64_t n_chunks(size_t n) { return (int64_t)((n + PAR_CHUNK - 1) / PAR_CHUNK); }
+#define CHUNK_RANGE(c, n, lo, hi)                 \
+  const size_t lo = (size_t)(c) * PAR_CHUNK;       \
+  const size_t hi = lo + PAR_CHUNK < (n) ? lo + PAR_CHUNK : (n)
 #include <stdlib.h>
 #include <string.h>
 
@@ -143,21 +201,23 @@ static ocplx or_tcK(const or_problem *P, const tc_side *t, int32_t n, int32_t s,
                     const double *beta, const double *gamma) {
   const double dt = P->dt;
   const ocplx c2 = or_c2(P);                                  /* e^{-i pi/4} sqrt(2/dt) */
-  const ocplx e3 = (1.0 + I_) / sqrt(2.0) * sqrt(dt / 2.0);   /* e^{i pi/4} sqrt(dt/2) */
+  const ocplx e3 = (1.0 + I_) / sqrt(2.0) * sqrt(MUT(7) ? dt : dt / 2.0);   /* e^{i pi/4} sqrt(dt/2) */
+  const double sa = MUT(3) ? -1.0 : 1.0, sg4 = MUT(4) ? -1.0 : 1.0;
   const int32_t d = n - s;
   switch (P->transmission) {
     case OR_TC_ROBIN: return d == 0 ? -I_ * P->robin_p : 0.0;
     case OR_TC_S02: return c2 * beta[d];
-    case OR_TC_S03: return c2 * beta[d] - e3 * (t->W / 2.0) * alpha[d];
-    case OR_TC_S04: return c2 * beta[d] - e3 * (t->W / 2.0) * alpha[d] - I_ * (t->dnW / 4.0) * (dt / 2.0) * gamma[d];
+    case OR_TC_S03: return c2 * beta[d] - sa * e3 * (t->W / 2.0) * alpha[d];
+    case OR_TC_S04:
+      return c2 * beta[d] - sa * e3 * (t->W / 2.0) * alpha[d] - sg4 * I_ * (t->dnW / 4.0) * (dt / 2.0) * gamma[d];
     case OR_TC_S12:
     case OR_TC_S14: {
       const double ph = or_calW(t, n, dt) - or_calW(t, s, dt);
-      const ocplx e = cexp(I_ * ph);
+      const ocplx e = cexp((MUT(5) ? -I_ : I_) * ph);
       ocplx k = c2 * e * beta[d];
       if (P->transmission == OR_TC_S14) {
         const double sg = t->dnW > 0 ? 1.0 : (t->dnW < 0 ? -1.0 : 0.0), r = sqrt(fabs(t->dnW)) / 2.0;
-        k -= I_ * sg * r * e * (dt / 2.0) * gamma[d] * r;
+        k -= (MUT(6) ? -I_ : I_) * sg * r * e * (dt / 2.0) * gamma[d] * r;
       }
       return k;
     }
@@ -321,7 +381,7 @@ static void or_local_W(const or_problem *P, int32_t j, int32_t n, int32_t fz,
     for (int32_t t = 0; t < P->n_terms; t++) {
       const double *tau = P->tau + (size_t)t * (NT + 1);
       const double *xi = P->xi + (size_t)t * (Nx + 1);
-      double tb = 0.5 * (tau[n] + tau[n - 1]);
+      double tb = MUT(2) ? tau[n] : 0.5 * (tau[n] + tau[n - 1]);
       for (int32_t k = 0; k < Nj; k++) W[k] += tb * xi[g0 + k];
     }
   }
@@ -450,8 +510,9 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
     if (hist) {
       if (P->transmission == OR_TC_S02) {   /* c2 factored out */
         for (int32_t s = 0; s < n; s++) {
-          Ha += beta[n - s] * va[s];
-          Hb += beta[n - s] * vb[s];
+          const int32_t ds = MUT(8) ? n - s - 1 : n - s;
+          Ha += beta[ds] * va[s];
+          Hb += beta[ds] * vb[s];
         }
         Ha = or_c2(P) * Ha;
         Hb = or_c2(P) * Hb;
@@ -485,7 +546,7 @@ int32_t or_march(const or_problem *P, int32_t j, const ocplx *lin, const ocplx *
           ocplx bf = Wd[k] * v[k];
           if (k > 0) bf += Wo[k - 1] * v[k - 1];
           if (k + 1 < Nj) bf += Wo[k] * v[k + 1];
-          rhs2[k] = rhs[k] - bf;
+          rhs2[k] = MUT(1) ? rhs[k] + bf : rhs[k] - bf;
         }
         st = or_thomas(Nj, lo, di, up, rhs2, rhs2);
         if (st) goto done;
@@ -536,6 +597,52 @@ done:
 static int32_t slot_l(int32_t j) { return 2 * j - 3; }
 static int32_t slot_r(int32_t j) { return 2 * j - 2; }
 
+/* One march of every subdomain j = 1..N with the incoming fluxes of g
+ * (NULL = 0); the outputs land in the neighbours' slots of Rg (NULL: none)
+ * and the local u(T) in uloc + (j-1) N_j (NULL: none).  The subdomains are
+ * independent (each writes its own two slots), so they run in parallel. */
+typedef struct {
+  const or_problem *P;
+  const ocplx *g;
+  int32_t use_u0, fz, NT, Nj;
+  ocplx *Rg, *uloc;
+  int32_t *st, *fp;
+} sweep_ctx;
+
+static void sweep_item(void *c, int64_t i) {
+  sweep_ctx *S = (sweep_ctx *)c;
+  const int32_t j = (int32_t)i + 1, N = S->P->N, NT = S->NT;
+  const ocplx *lin = (j >= 2 && S->g) ? S->g + (size_t)slot_l(j) * NT : NULL;
+  const ocplx *rin = (j <= N - 1 && S->g) ? S->g + (size_t)slot_r(j) * NT : NULL;
+  ocplx *ol = (j >= 2 && S->Rg) ? S->Rg + (size_t)slot_r(j - 1) * NT : NULL;
+  ocplx *orr = (j <= N - 1 && S->Rg) ? S->Rg + (size_t)slot_l(j + 1) * NT : NULL;
+  ocplx *ut = S->uloc ? S->uloc + (size_t)i * S->Nj : NULL;
+  S->fp[i] = 0;
+  S->st[i] = or_march(S->P, j, lin, rin, S->use_u0, S->fz, ol, orr, ut, &S->fp[i]);
+}
+
+/* status: the first hard error in subdomain order, else INNER_NOT_CONVERGED
+ * if any subdomain's NL fixed point hit its cap, else OK */
+static int32_t sweep_all(const or_problem *P, const ocplx *g, int32_t use_u0, int32_t fz, ocplx *Rg, ocplx *uloc,
+                         int32_t *fp_max) {
+  int32_t Nx, NT, Nj;
+  if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
+  const int32_t N = P->N;
+  int32_t *stv = (int32_t *)calloc((size_t)N, sizeof(int32_t)), *fpv = (int32_t *)calloc((size_t)N, sizeof(int32_t));
+  if (!stv || !fpv) { free(stv); free(fpv); return OR_OOM; }
+  sweep_ctx S = {P, g, use_u0, fz, NT, Nj, Rg, uloc, stv, fpv};
+  par_for(N, sweep_item, &S);
+  int32_t st = OR_OK;
+  for (int32_t i = 0; i < N; i++) {
+    if (stv[i] == OR_INNER_NOT_CONVERGED) { if (st == OR_OK) st = stv[i]; }
+    else if (stv[i]) { st = stv[i]; break; }
+  }
+  for (int32_t i = 0; i < N && fp_max; i++)
+    if (fpv[i] > *fp_max) *fp_max = fpv[i];
+  free(stv); free(fpv);
+  return st;
+}
+
 /* g -> R(g): every subdomain marches with its incoming fluxes from g and
  * its outputs land in the neighbours' slots (eq. 13). */
 int32_t or_apply_R(const or_problem *P, const ocplx *g, int32_t use_u0, int32_t fz,
@@ -545,37 +652,38 @@ int32_t or_apply_R(const or_problem *P, const ocplx *g, int32_t use_u0, int32_t 
   int32_t N = P->N;
   size_t ng = (size_t)(2 * N - 2) * NT;
   for (size_t i = 0; i < ng; i++) Rg[i] = 0.0;
-  int32_t st = OR_OK;
-  for (int32_t j = 1; j <= N; j++) {
-    const ocplx *lin = (j >= 2 && g) ? g + (size_t)slot_l(j) * NT : NULL;
-    const ocplx *rin = (j <= N - 1 && g) ? g + (size_t)slot_r(j) * NT : NULL;
-    ocplx *ol = (j >= 2) ? Rg + (size_t)slot_r(j - 1) * NT : NULL;
-    ocplx *orr = (j <= N - 1) ? Rg + (size_t)slot_l(j + 1) * NT : NULL;
-    int32_t s = or_march(P, j, lin, rin, use_u0, fz, ol, orr, NULL, fp_max);
-    if (s == OR_INNER_NOT_CONVERGED) st = s;
-    else if (s) return s;
-  }
-  return st;
+  return sweep_all(P, g, use_u0, fz, Rg, NULL, fp_max);
 }
 
 /* Probing with u0 = 0 (reading A14): a unit impulse at n = 1 on
  * l_j gives the first columns of X^{j,1} (out_left) and X^{j,3}
  * (out_right); on r_j it gives X^{j,2} and X^{j,4}. */
+typedef struct { const or_problem *P; int32_t fz, NT; ocplx *X; const ocplx *e; int32_t *st; } probe_ctx;
+
+static void probe_item(void *c, int64_t i) {
+  probe_ctx *Q = (probe_ctx *)c;
+  const int32_t j = (int32_t)i + 1, N = Q->P->N, NT = Q->NT;
+  ocplx *X1 = Q->X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+  int32_t st = OR_OK;
+  if (j >= 2) st = or_march(Q->P, j, Q->e, NULL, 0, Q->fz, X1, (j <= N - 1) ? X3 : NULL, NULL, NULL);
+  if (!st && j <= N - 1) st = or_march(Q->P, j, NULL, Q->e, 0, Q->fz, (j >= 2) ? X2 : NULL, X4, NULL, NULL);
+  Q->st[i] = st;
+}
+
 int32_t or_build_L(const or_problem *P, int32_t fz, ocplx *X) {
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
   int32_t N = P->N;
   memset(X, 0, sizeof(ocplx) * (size_t)N * 4 * NT);
   ocplx *e = (ocplx *)calloc((size_t)NT, sizeof(ocplx));
-  if (!e) return OR_OOM;
+  int32_t *stv = (int32_t *)calloc((size_t)N, sizeof(int32_t));
+  if (!e || !stv) { free(e); free(stv); return OR_OOM; }
   e[0] = 1.0;
+  probe_ctx Q = {P, fz, NT, X, e, stv};
+  par_for(N, probe_item, &Q);   /* the probes of different subdomains are independent */
   int32_t st = OR_OK;
-  for (int32_t j = 1; j <= N && !st; j++) {
-    ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
-    if (j >= 2) st = or_march(P, j, e, NULL, 0, fz, X1, (j <= N - 1) ? X3 : NULL, NULL, NULL);
-    if (!st && j <= N - 1) st = or_march(P, j, NULL, e, 0, fz, (j >= 2) ? X2 : NULL, X4, NULL, NULL);
-  }
-  free(e);
+  for (int32_t i = 0; i < N && !st; i++) st = stv[i];
+  free(e); free(stv);
   return st;
 }
 
@@ -590,25 +698,35 @@ static void conv_add(int32_t NT, const ocplx *x, const ocplx *y, ocplx *out) {
   }
 }
 
-/* Lg with the block pattern of eq. (15)/(16). */
+/* Lg with the block pattern of eq. (15)/(16).  Subdomain j
+ * produces exactly the two output slots r_{j-1} and l_{j+1}, so the
+ * subdomains run in parallel. */
+typedef struct { int32_t N, NT; const ocplx *X, *g; ocplx *Lg; } applyL_ctx;
+
+static void applyL_item(void *c, int64_t i) {
+  const applyL_ctx *A = (const applyL_ctx *)c;
+  const int32_t j = (int32_t)i + 1, N = A->N, NT = A->NT;
+  const ocplx *X = A->X, *g = A->g;
+  const ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
+  if (j >= 2) { /* r_{j-1}^{k+1} = X^{j,1} l_j + X^{j,2} r_j */
+    ocplx *out = A->Lg + (size_t)slot_r(j - 1) * NT;
+    conv_add(NT, X1, g + (size_t)slot_l(j) * NT, out);
+    if (j <= N - 1) conv_add(NT, X2, g + (size_t)slot_r(j) * NT, out);
+  }
+  if (j <= N - 1) { /* l_{j+1}^{k+1} = X^{j,3} l_j + X^{j,4} r_j */
+    ocplx *out = A->Lg + (size_t)slot_l(j + 1) * NT;
+    if (j >= 2) conv_add(NT, X3, g + (size_t)slot_l(j) * NT, out);
+    conv_add(NT, X4, g + (size_t)slot_r(j) * NT, out);
+  }
+}
+
 void or_apply_L(const or_problem *P, const ocplx *X, const ocplx *g, ocplx *Lg) {
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return;
   int32_t N = P->N;
   memset(Lg, 0, sizeof(ocplx) * (size_t)(2 * N - 2) * NT);
-  for (int32_t j = 1; j <= N; j++) {
-    const ocplx *X1 = X + ((size_t)(j - 1) * 4 + 0) * NT, *X2 = X1 + NT, *X3 = X2 + NT, *X4 = X3 + NT;
-    if (j >= 2) { /* r_{j-1}^{k+1} = X^{j,1} l_j + X^{j,2} r_j */
-      ocplx *out = Lg + (size_t)slot_r(j - 1) * NT;
-      conv_add(NT, X1, g + (size_t)slot_l(j) * NT, out);
-      if (j <= N - 1) conv_add(NT, X2, g + (size_t)slot_r(j) * NT, out);
-    }
-    if (j <= N - 1) { /* l_{j+1}^{k+1} = X^{j,3} l_j + X^{j,4} r_j */
-      ocplx *out = Lg + (size_t)slot_l(j + 1) * NT;
-      if (j >= 2) conv_add(NT, X3, g + (size_t)slot_l(j) * NT, out);
-      conv_add(NT, X4, g + (size_t)slot_r(j) * NT, out);
-    }
-  }
+  applyL_ctx A = {N, NT, X, g, Lg};
+  par_for(N, applyL_item, &A);
 }
 
 /* Exact P^{-1} = (I - L0)^{-1} (P:1041-1059 define P as
@@ -695,18 +813,29 @@ int32_t or_pinv_causal(const or_problem *P, const ocplx *X, const ocplx *y, ocpl
 /* Order-fixed inner product <x, y> = sum conj(x) y: one partial per
  * subdomain over the slots it owns (l_j, r_j), partials summed in
  * subdomain order. */
+typedef struct { int32_t N, NT; const ocplx *x, *y; ocplx *part; } dot_ctx;
+
+static void dot_item(void *c, int64_t i) {
+  const dot_ctx *D = (const dot_ctx *)c;
+  const int32_t j = (int32_t)i + 1, N = D->N, NT = D->NT;
+  ocplx part = 0.0;
+  int32_t s_lo = (j >= 2) ? slot_l(j) : slot_r(j);
+  int32_t s_hi = (j <= N - 1) ? slot_r(j) : slot_l(j);
+  for (size_t q = (size_t)s_lo * NT; q < (size_t)(s_hi + 1) * NT; q++) part += conj(D->x[q]) * D->y[q];
+  D->part[i] = part;
+}
+
 ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y) {
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return 0.0;
   int32_t N = P->N;
   ocplx total = 0.0;
-  for (int32_t j = 1; j <= N; j++) {
-    ocplx part = 0.0;
-    int32_t s_lo = (j >= 2) ? slot_l(j) : slot_r(j);
-    int32_t s_hi = (j <= N - 1) ? slot_r(j) : slot_l(j);
-    for (size_t i = (size_t)s_lo * NT; i < (size_t)(s_hi + 1) * NT; i++) part += conj(x[i]) * y[i];
-    total += part;
-  }
+  ocplx *part = (ocplx *)malloc(sizeof(ocplx) * (size_t)N);
+  if (!part) return NAN;
+  dot_ctx D = {N, NT, x, y, part};
+  par_for(N, dot_item, &D);          /* partials in parallel ... */
+  for (int32_t i = 0; i < N; i++) total += part[i];   /* ... summed in subdomain order */
+  free(part);
   return total;
 }
 
@@ -715,6 +844,54 @@ ocplx or_dot(const or_problem *P, const ocplx *x, const ocplx *y) {
 /* complex Givens rotations; stop when the residual estimate           */
 /* |gamma_{k+1}| <= tol ||b||_2 (A5); true residual at each restart.    */
 /* ------------------------------------------------------------------ */
+/* Element-range loops of the Krylov drivers.  Each element's arithmetic is
+ * the sequential one (the basis index runs in order inside an element), so
+ * the threads only split the index range. */
+typedef struct { size_t n, ldv; ocplx *out; const ocplx *a, *b, *V, *coef; double s; int32_t nv; } vec_ctx;
+
+static void vsub_item(void *c, int64_t k) {
+  const vec_ctx *v = (const vec_ctx *)c;
+  CHUNK_RANGE(k, v->n, lo, hi);
+  for (size_t i = lo; i < hi; i++) v->out[i] = v->a[i] - v->b[i];
+}
+static void vdiv_item(void *c, int64_t k) {
+  const vec_ctx *v = (const vec_ctx *)c;
+  CHUNK_RANGE(k, v->n, lo, hi);
+  for (size_t i = lo; i < hi; i++) v->out[i] = v->a[i] / v->s;
+}
+static void vmsub_item(void *c, int64_t k) {   /* out -= sum_q coef_q V_q, q in order */
+  const vec_ctx *v = (const vec_ctx *)c;
+  CHUNK_RANGE(k, v->n, lo, hi);
+  for (int32_t q = 0; q < v->nv; q++) {
+    const ocplx *vq = v->V + (size_t)q * v->ldv;
+    for (size_t i = lo; i < hi; i++) v->out[i] -= v->coef[q] * vq[i];
+  }
+}
+static void vmadd_item(void *c, int64_t k) {   /* out += sum_q coef_q V_q, q in order */
+  const vec_ctx *v = (const vec_ctx *)c;
+  CHUNK_RANGE(k, v->n, lo, hi);
+  for (int32_t q = 0; q < v->nv; q++) {
+    const ocplx *vq = v->V + (size_t)q * v->ldv;
+    for (size_t i = lo; i < hi; i++) v->out[i] += v->coef[q] * vq[i];
+  }
+}
+static void vec_sub(size_t n, ocplx *out, const ocplx *a, const ocplx *b) {
+  vec_ctx v = {n, 0, out, a, b, NULL, NULL, 0.0, 0};
+  par_for(n_chunks(n), vsub_item, &v);
+}
+static void vec_div(size_t n, ocplx *out, const ocplx *a, double s) {
+  vec_ctx v = {n, 0, out, a, NULL, NULL, NULL, s, 0};
+  par_for(n_chunks(n), vdiv_item, &v);
+}
+static void vec_msub(size_t n, ocplx *out, const ocplx *V, size_t ldv, const ocplx *coef, int32_t nv) {
+  vec_ctx v = {n, ldv, out, NULL, NULL, V, coef, 0.0, nv};
+  par_for(n_chunks(n), vmsub_item, &v);
+}
+static void vec_madd(size_t n, ocplx *out, const ocplx *V, size_t ldv, const ocplx *coef, int32_t nv) {
+  vec_ctx v = {n, ldv, out, NULL, NULL, V, coef, 0.0, nv};
+  par_for(n_chunks(n), vmadd_item, &v);
+}
+
 typedef int32_t (*or_opfn)(void *ctx, const ocplx *x, ocplx *y);
 typedef ocplx (*or_dotfn)(const void *ctx, const ocplx *x, const ocplx *y);
 
@@ -747,11 +924,11 @@ static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const v
   while (!done) {
     st = A(actx, x, w);
     if (st && st != OR_INNER_NOT_CONVERGED) goto out;
-    for (size_t i = 0; i < n; i++) V[i] = b[i] - w[i];
+    vec_sub(n, V, b, w);
     double beta = vnorm(dot, dctx, V);
     if (beta <= tol * bnorm) { *converged = 1; break; }
     if (total >= maxit) break;
-    for (size_t i = 0; i < n; i++) V[i] = V[i] / beta;
+    vec_div(n, V, V, beta);
     for (int32_t i = 0; i <= m; i++) gam[i] = 0.0;
     gam[0] = beta;
     int32_t k, kend = 0;
@@ -765,15 +942,12 @@ static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const v
       for (int32_t i = 0; i <= k; i++) Hm(i, k) = 0.0;
       for (int pass = 0; pass < npass; pass++) {    /* classical Gram-Schmidt, npass times */
         for (int32_t i = 0; i <= k; i++) hc[i] = dot(dctx, V + (size_t)i * n, w);
-        for (int32_t i = 0; i <= k; i++) {
-          const ocplx *vi = V + (size_t)i * n;
-          for (size_t q = 0; q < n; q++) w[q] -= hc[i] * vi[q];
-          Hm(i, k) += hc[i];
-        }
+        vec_msub(n, w, V, n, hc, k + 1);           /* w -= sum_i hc_i v_i */
+        for (int32_t i = 0; i <= k; i++) Hm(i, k) += hc[i];
       }
       double hk1 = vnorm(dot, dctx, w);
       int32_t breakdown = (hk1 <= 1e-14 * wn0);
-      if (!breakdown) for (size_t q = 0; q < n; q++) vk1[q] = w[q] / hk1;
+      if (!breakdown) vec_div(n, vk1, w, hk1);
       for (int32_t i = 0; i < k; i++) {             /* previous rotations */
         ocplx t = cs[i] * Hm(i, k) + sn[i] * Hm(i + 1, k);
         Hm(i + 1, k) = -conj(sn[i]) * Hm(i, k) + cs[i] * Hm(i + 1, k);
@@ -802,10 +976,7 @@ static int32_t gmres_core(size_t n, or_opfn A, void *actx, or_dotfn dot, const v
       for (int32_t q = i + 1; q < kend; q++) acc -= Hm(i, q) * y[q];
       y[i] = acc / Hm(i, i);
     }
-    for (int32_t i = 0; i < kend; i++) {
-      const ocplx *vi = V + (size_t)i * n;
-      for (size_t q = 0; q < n; q++) x[q] += y[i] * vi[q];
-    }
+    vec_madd(n, x, V, n, y, kend);                 /* x += sum_i y_i v_i */
   }
 #undef Hm
   *iters = total;
@@ -947,7 +1118,7 @@ static ocplx drv_dot(const void *c, const ocplx *x, const ocplx *y) { return or_
 static int32_t op_I_minus_L(void *c, const ocplx *x, ocplx *y) {
   drv_ctx *d = (drv_ctx *)c;
   or_apply_L(d->P, d->X, x, y);
-  for (size_t i = 0; i < d->ng; i++) y[i] = x[i] - y[i];
+  vec_sub(d->ng, y, x, y);
   return OR_OK;
 }
 
@@ -979,7 +1150,7 @@ static int32_t op_I_minus_L_mf(void *c, const ocplx *x, ocplx *y) {
   drv_ctx *d = (drv_ctx *)c;
   int32_t st = or_apply_R(d->P, x, 0, 0, d->tmp, &d->fp_max);
   if (st) return st;
-  for (size_t i = 0; i < d->ng; i++) y[i] = x[i] - d->tmp[i];
+  vec_sub(d->ng, y, x, d->tmp);
   return OR_OK;
 }
 
@@ -989,7 +1160,7 @@ static int32_t op_precond(void *c, const ocplx *x, ocplx *y) {
   drv_ctx *d = (drv_ctx *)c;
   int32_t st = or_apply_R(d->P, x, 0, 0, d->tmp, &d->fp_max);
   if (st) return st;
-  for (size_t i = 0; i < d->ng; i++) d->tmp[i] = x[i] - d->tmp[i];
+  vec_sub(d->ng, d->tmp, x, d->tmp);
   return apply_Pinv(d, d->tmp, y);
 }
 
@@ -999,18 +1170,16 @@ static int32_t final_march(const or_problem *P, const ocplx *g, ocplx *uT, int32
   int32_t Nx, NT, Nj;
   if (or_sizes(P, &Nx, &NT, &Nj)) return OR_ERR_ARG;
   int32_t N = P->N, m = Nx / N;
-  ocplx *loc = (ocplx *)calloc((size_t)Nj, sizeof(ocplx));
+  ocplx *loc = (ocplx *)calloc((size_t)Nj * N, sizeof(ocplx));
   ocplx *sum = (ocplx *)calloc((size_t)Nx + 1, sizeof(ocplx));
   int *cnt = (int *)calloc((size_t)Nx + 1, sizeof(int));
   int32_t st = OR_OK;
   if (!loc || !sum || !cnt) { st = OR_OOM; goto out; }
+  st = sweep_all(P, g, 1, 0, NULL, loc, fp_max);
+  if (st && st != OR_INNER_NOT_CONVERGED) goto out;
   for (int32_t j = 1; j <= N; j++) {
-    const ocplx *lin = (j >= 2 && g) ? g + (size_t)slot_l(j) * NT : NULL;
-    const ocplx *rin = (j <= N - 1 && g) ? g + (size_t)slot_r(j) * NT : NULL;
-    int32_t s = or_march(P, j, lin, rin, 1, 0, NULL, NULL, loc, fp_max);
-    if (s && s != OR_INNER_NOT_CONVERGED) { st = s; goto out; }
-    if (s) st = s;
-    for (int32_t k = 0; k < Nj; k++) { sum[(size_t)(j - 1) * m + k] += loc[k]; cnt[(size_t)(j - 1) * m + k]++; }
+    const ocplx *lj = loc + (size_t)(j - 1) * Nj;
+    for (int32_t k = 0; k < Nj; k++) { sum[(size_t)(j - 1) * m + k] += lj[k]; cnt[(size_t)(j - 1) * m + k]++; }
   }
   for (int32_t i = 0; i <= Nx; i++) uT[i] = sum[i] / (double)cnt[i];
 out:

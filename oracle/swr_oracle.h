@@ -143,6 +143,14 @@ int32_t or_gmres_dense(int32_t n, int32_t gs_passes, const ocplx *A, const ocplx
 int32_t or_solve(const or_problem *P, ocplx *uT, or_report *rep,
                  ocplx *g_out /* [(2N-2)N_T] or NULL */);
 
+/* Worker threads of the subdomain-parallel loops (marches of independent
+ * subdomains, per-subdomain Toeplitz blocks and dot-product partials,
+ * element ranges of the Krylov vector updates).  Every parallel item writes
+ * its own outputs and reductions keep their sequential order, so results are
+ * bitwise independent of the count.  Default 1. */
+void or_set_threads(int32_t n);
+int32_t or_get_threads(void);
+
 /* Single-domain reference solve (N = 1, Neumann both ends). */
 int32_t or_monodomain(const or_problem *P, ocplx *uT, int32_t *fp_max);
 
