@@ -38,8 +38,8 @@ UNIT = "cell-steps/s"
 PAPER_T_NEW_GMRES_N500_S = 6.86      # 500 Sandy Bridge cores
 FLOP_PER_CELL_STEP = 36.0            # algorithmic flops of one CN cell-step
 BYTES_PER_CELL_STEP = 32.0           # u_{n-1} read + u_n write, complex fp64
-FP64_PEAK_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 DFMA/clk at 1965 MHz
-TOEPLITZ_FLOP = 8.0                  # per complex multiply-add of the causal convolution
+FP64_DERIVED_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 DFMA/clk at 1965 MHz
+FP64_PROBE = os.path.join(ROOT, "profiles", "r02", "probe_fp64_b200.txt")
 
 
 def load_peaks():
@@ -47,6 +47,17 @@ def load_peaks():
         return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except Exception:
         return {}
+
+
+def fp64_peak():
+    """Measured DFMA throughput on this pool's B200 (tools/probe_fp64.cu,
+    committed output), else the derived unit-count figure."""
+    try:
+        vals = [float(l.split(":")[1].split()[0]) for l in open(FP64_PROBE) if l.startswith("dfma tput")]
+        return max(vals), "measured: tools/probe_fp64.cu DFMA throughput on a B200 of this pool " \
+                          "(profiles/r02/probe_fp64_b200.txt)"
+    except Exception:
+        return FP64_DERIVED_TFLOPS, "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz"
 
 
 class ClockSampler:
@@ -104,62 +115,49 @@ def dist_env():
     return int(os.environ.get("RANK", 0)), int(os.environ.get("WORLD_SIZE", 1)), int(os.environ.get("LOCAL_RANK", 0))
 
 
-def oracle_cpu_sample(p, arrays, seconds: float, max_subdomains: int | None = None):
-    """The oracle as it stands (single-threaded C): marches of whole C5
-    subdomains with the d right-hand side until ~seconds of CPU work."""
+def oracle_time_to_solution(p, arrays, threads: int):
+    """The oracle as it stands on `threads` host threads (subdomain-parallel
+    loops, bitwise equal to one thread): the whole time-to-solution of the
+    workload -- build of d and L, every GMRES iteration, the final sweep."""
     from oracle import oracle
-    o = oracle.Oracle(p, arrays)
-    t0 = time.perf_counter()
-    cells = 0
-    nsub = 0
-    order = list(range(1, p.N + 1))
-    rng = np.random.default_rng(0)
-    rng.shuffle(order)
-    for j in order:
-        o.march(j, None, None, use_u0=True)
-        cells += p.Nj * p.NT
-        nsub += 1
-        if time.perf_counter() - t0 >= seconds or (max_subdomains and nsub >= max_subdomains):
-            break
-    dt = time.perf_counter() - t0
-    return cells / dt, dt, nsub, cells
+    oracle.set_threads(threads)
+    try:
+        t0 = time.perf_counter()
+        r = oracle.Oracle(p, arrays).solve()
+        dt = time.perf_counter() - t0
+    finally:
+        oracle.set_threads(1)
+    return dt, r
 
 
 def run_reference(args, p, arrays):
-    """--impl reference: the CPU oracle on the host cores (rank 0 only)."""
+    """--impl reference: the CPU oracle on the host cores (rank 0 only).  One
+    step = one sweep R(0; u0) of the workload (every subdomain marches once:
+    N N_j N_T cell-steps), the oracle's subdomain-parallel march on all
+    cores; the same unit the GPU's cell-steps/s counts."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    per_step = max(1, args.ref_subdomains)
     from oracle import oracle
+    P = os.cpu_count() or 1
+    oracle.set_threads(P)
     o = oracle.Oracle(p, arrays)
-    order = list(range(1, p.N + 1))
     times, cells = [], 0
-
-    def step(k):
-        nonlocal cells
-        c = 0
-        for i in range(per_step):
-            j = order[(k * per_step + i) % p.N]
-            o.march(j, None, None, use_u0=True)
-            c += p.Nj * p.NT
-        return c
-
-    for k in range(args.warmup):
-        step(k)
-    for k in range(args.steps):
+    for k in range(args.warmup + args.steps):
         t0 = time.perf_counter()
-        cells += step(args.warmup + k)
-        times.append(time.perf_counter() - t0)
+        o.apply_R(None, use_u0=True)
+        if k >= args.warmup:
+            times.append(time.perf_counter() - t0)
+            cells += p.N * p.Nj * p.NT
     total = sum(times)
     value = cells / total
-    sample = (f"oracle or_march of {per_step} full C5 subdomains per step (N_j={p.Nj}, N_T={p.NT}, d RHS), "
-              f"single-threaded C, GMRES not sampled")
+    sample = (f"oracle or_apply_R(0; u0) of the whole {p.name} workload per step ({p.N} subdomain marches, "
+              f"N_j={p.Nj}, N_T={p.NT}) on {P} threads (subdomain-parallel, bitwise equal to one thread)")
     line = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * total / args.steps,
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": workload_config(p),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": P, "kind": "oracle", "sample": sample},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -187,10 +185,9 @@ def main():
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="C5")
-    ap.add_argument("--cpu-seconds", type=float, default=12.0)
-    ap.add_argument("--ref-subdomains", type=int, default=4)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-extra", action="store_true", help="skip the C3 / C4 time-to-solution keys")
     args = ap.parse_args()
 
     p = si.config(args.config)
@@ -261,20 +258,21 @@ def main():
     value = cells / (ms / 1e3)
     t_march = statistics.mean(r["t_march_ms"] for r in reps)
     t_intf = statistics.mean(r["t_interface_ms"] for r in reps)
+    t_comm = statistics.mean(r["t_comm_ms"] for r in reps)
     n_march = reps[0]["n_marches"]
     launches = sum(r["n_kernel_launches"] for r in reps)
     iters = reps[-1]["iterations"]
     cells_rank = statistics.mean(r["cell_steps"] for r in reps)
     peaks = load_peaks()
     hbm = peaks.get("hbm_gbs", 6538.6)
+    fp64, fp64_src = fp64_peak()
 
-    # roofline of the dominant kernel class (the march): FP64-ALU bound
-    # (state register-resident for the whole window)
+    # roofline of the dominant kernel class (the march): FP64-ALU / latency
+    # bound (state register-resident for the whole window)
     march_flops = FLOP_PER_CELL_STEP * cells_rank
     achieved = march_flops / (t_march / 1e3) / 1e12
-    roof = {"bound": "alu", "kernel": "k_march_resident", "achieved": achieved, "peak": FP64_PEAK_TFLOPS,
-            "unit": "TFLOP/s", "frac": achieved / FP64_PEAK_TFLOPS, "traffic": None,
-            "peak_source": "derived: 148 SMs x 64 FP64 FMA/clk x 2 x 1965 MHz (B200_PROFILING.md unit counts)",
+    roof = {"bound": "alu", "kernel": "k_march_resident", "achieved": achieved, "peak": fp64,
+            "unit": "TFLOP/s", "frac": achieved / fp64, "traffic": None, "peak_source": fp64_src,
             "algorithmic": f"{FLOP_PER_CELL_STEP:g} flop/cell-step x {cells_rank:.4g} cell-steps over {n_march} launches",
             "avg_launch_ms": t_march / max(n_march, 1)}
     prof = os.path.join(ROOT, "profiles", "march_traffic.json")
@@ -290,11 +288,17 @@ def main():
             "vs_baseline": value / (cells / PAPER_T_NEW_GMRES_N500_S) if args.config == "C5" else None,
             "dtype": "f64", "data": "synthetic", "config": workload_config(p),
             "time_to_solution_ms": ms, "gmres_iterations": iters,
-            "hbm_roofline_frac": hbm_equiv / hbm,
-            "breakdown_ms": {"march": t_march, "toeplitz": t_intf, "krylov_vector_and_host": ms - t_march - t_intf},
+            # the BASELINE metric's "% of HBM roofline": the bandwidth a streaming march
+            # would need (32 B per cell-step) over the measured HBM peak; the resident
+            # march moves ~1/1000 of that through DRAM (profiles/march_traffic.json)
+            "streaming_equiv_bw_frac": hbm_equiv / hbm,
+            "breakdown_ms": {"march": t_march, "toeplitz": t_intf, "comm": t_comm,
+                             "krylov_vector_and_host": ms - t_march - t_intf - t_comm,
+                             "setup_once": reps[-1]["t_setup_ms"]},
             "roofline": roof, "gpu_launches": launches, "clocks": clocks, "wall_s_timed": wall}
-    line["config"]["parallelism"] = (f"subdomains sharded over {world} GPUs (marches), interface Krylov solve "
-                                     f"replicated, NCCL allreduce assembly" if world > 1 else "1 GPU")
+    line["config"]["parallelism"] = (f"subdomains and their interface slots sharded over {world} GPUs (owner "
+                                     f"computes); cut traces by ncclSend/Recv, per-subdomain Gram-Schmidt partials "
+                                     f"by ncclAllReduce" if world > 1 else "1 GPU")
     # the interface operator (I - L)x: FFT convolution (N_T <= 512), HBM-bound;
     # algorithmic bytes per apply = x + the transformed first columns + y
     nf = 1 << (2 * next(l for l in range(2, 6) if (1 << (2 * l)) >= 2 * p.NT - 1))
@@ -330,11 +334,45 @@ def main():
                        "d2h_bytes_per_step": out_h.numel() * 16, "ms_per_step": em,
                        "path": "swr_update_inputs(host u0, V_x) + swr_build_interface_operator + swr_solve(host u_T)"}
 
+    # the other BASELINE configs' time-to-solution:
+    # C3 V(t,x) preconditioned GMRES, C4 |u|^2 preconditioned fixed point
+    if not args.no_extra and world == 1:
+        extra = {}
+        for name in ("C3", "C4"):
+            q = si.config(name)
+            sq = SWR(q, si.inputs(q), device=local, stream=stream)
+            with torch.cuda.stream(stream):
+                sq.build()
+                sq.solve(out=uT_dev if q.Nx == p.Nx else None)
+                torch.cuda.synchronize(dev)
+                e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                flush.fill_(1.0)
+                e0.record(stream)
+                sq.build()
+                stq, _, rq = sq.solve(out=uT_dev if q.Nx == p.Nx else None)
+                e1.record(stream)
+                e1.synchronize()
+            tq = e0.elapsed_time(e1)
+            extra[name] = {"workload": workload_config(q)["workload"], "status": stq,
+                           "time_to_solution_ms": tq, "value": rq["cell_steps"] / (tq / 1e3), "unit": UNIT,
+                           "outer_iterations": rq["iterations"], "inner_iterations": rq["inner_iterations"],
+                           "fp_max": rq["fp_max"], "march_ms": rq["t_march_ms"],
+                           "march_frac_of_step": rq["t_march_ms"] / tq,
+                           "march_fp64_frac": FLOP_PER_CELL_STEP * rq["cell_steps"] / (rq["t_march_ms"] / 1e3)
+                                              / 1e12 / fp64,
+                           "march_streaming_equiv_bw_frac": BYTES_PER_CELL_STEP * rq["cell_steps"]
+                                                            / (rq["t_march_ms"] / 1e3) / 1e9 / hbm}
+            sq.close()
+        line["other_configs"] = extra
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        v, dt, nsub, c = oracle_cpu_sample(p, arrays, args.cpu_seconds)
-        line["cpu_baseline"] = {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                                "sample": f"oracle or_march of {nsub} whole C5 subdomains ({c:.3g} cell-steps, d RHS, "
-                                          f"{dt:.1f} s single-threaded); GMRES not sampled"}
+        P = os.cpu_count() or 1
+        dt, ro = oracle_time_to_solution(p, arrays, P)
+        line["cpu_baseline"] = {"value": cells / dt, "unit": UNIT, "cores": P, "kind": "oracle",
+                                "seconds": dt, "iterations": ro["iterations"],
+                                "sample": f"the whole {p.name} time-to-solution (build of d and L, "
+                                          f"{ro['iterations']} GMRES iterations, final sweep) by the oracle on "
+                                          f"{P} host threads; single-thread T_oracle,1 in "
+                                          f"profiles/r02/oracle_c5_single_thread.txt"}
     if rank == 0:
         print(json.dumps(line), flush=True)
     if world > 1:

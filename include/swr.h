@@ -129,6 +129,15 @@ typedef struct {
                                  (P:1059); 1 = exact causal forward substitution in time (reading
                                  A27); fails with SWR_ERR_UNSUPPORTED when the lag-0 interface
                                  coupling is too strong for the bounded sweep count */
+  /* Kernel forms (same arithmetic, different rounding order only; 0 = automatic): */
+  int32_t march_form;         /* 0: the resident cluster march when a subdomain fits one thread-block
+                                 cluster (N_j up to ~45K rows), the streaming march otherwise;
+                                 1: always the streaming march */
+  int32_t toeplitz_form;      /* (I - L) x: 0: FFT convolution (register four-step kernel for
+                                 257 <= N_T <= 512, shared-memory radix-4 for N_T <= 256), the direct
+                                 causal convolution for N_T > 512; 1: direct; 2: shared-memory FFT */
+  int32_t nl_rows_per_thread; /* f(u) march: 0: automatic; 8 or 11 forces the rows per thread (the
+                                 11-row shape serves 16 x 256 x 8 < N_j <= 45,056) */
 } swr_config;
 
 typedef struct {
@@ -144,7 +153,9 @@ typedef struct {
   double t_interface_ms;      /* Toeplitz apply + Krylov vector kernels */
   double cell_steps;          /* sum over marches of (sum_j N_j) * N_T * RHS (this rank) */
   int32_t n_marches;          /* march-kernel launches */
-  int32_t n_kernel_launches;  /* all kernels of this library launched */
+  int32_t n_kernel_launches;  /* all kernels of this library launched (and collectives) */
+  double t_setup_ms;          /* swr_setup, host wall time (allocation, copies, factorisation) */
+  double t_comm_ms;           /* collectives of build + solve (cut traces, partial sums), device time */
 } swr_report;
 
 /* Validate the configuration, copy the inputs to the GPU, assemble and
@@ -176,7 +187,8 @@ const char *swr_error_string(int status);
 const char *swr_last_error_detail(void);
 
 /* ---- Lower-level entry points (parity tests, benchmarks). -------------
- * Device pointers (this rank's GPU), n_g = (2N-2) N_T complex, world = 1. */
+ * Device pointers (this rank's GPU), n_g = (2N-2) N_T complex, world = 1
+ * only (SWR_ERR_INVALID_ARG otherwise). */
 
 /* Rg = R(g; u0 if use_u0 else 0) with the true potential, or with V = 0 if
  * force_zero_potential (eq. 13): one march of every subdomain and the
@@ -193,26 +205,40 @@ int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y
  * = first column of X^{j,p}; which = 0: L, 1: L0). NULL skips. */
 int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X);
 
-/* Copy out the interface vector g of the last swr_solve [2*n_g]. */
+/* Copy out this rank's slots of the interface vector g of the last swr_solve:
+ * [2 * (s_hi - s_lo + 1) * N_T] (swr_owned_slots; the whole g on one GPU). */
 int swr_get_g(swr_handle *h, double *g);
 
 /* Sizes: N_x, N_T, N_j, n_g. */
 int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_t *ng);
 
 /* ---- Multi-GPU (one process per GPU). ----------------------
- * Subdomains are sharded contiguously: rank r of W owns
- * j in [floor(rN/W)+1, floor((r+1)N/W)] (P:982-1011 ownership rule).  Each
- * rank marches only its subdomains; the outputs of eq. (8) that cross a rank
- * cut, the interface operator d, L (L0) and u(T) are summed over ranks with
- * ncclAllReduce (disjoint supports: exact), and the interface Krylov solve is
- * replicated on every rank (identical iteration counts to one GPU).
- * Pure host function, no GPU needed: */
+ * Owner computes (the block-column ownership of P:982-1011): rank r of W owns
+ * the subdomains j in [floor(rN/W)+1, floor((r+1)N/W)] and their interface
+ * slots [s_lo, s_hi] (swr_owned_slots, contiguous); its d, g and Krylov
+ * vectors hold those slots only, its first columns of L are those of its
+ * subdomains.  Per march sweep or (I - L) apply only the two cut traces cross
+ * a rank cut (ncclSend/ncclRecv of N_T complex with each neighbour rank); per
+ * Gram-Schmidt pass the per-subdomain partial sums are summed over ranks
+ * (ncclAllReduce of disjoint columns, exact) and reduced in the same fixed
+ * order as on one GPU, so any W reproduces the one-GPU iterates bitwise;
+ * u(T) is reduced onto rank 0 (ncclReduce).  L0 (PRECOND) is held whole by
+ * every rank (its interior blocks coincide), and the exact P^{-1}
+ * (pinv_exact = 1) runs replicated on the gathered vector.
+ * Pure host functions, no GPU needed: */
 int swr_partition(int32_t N, int32_t world, int32_t rank, int32_t *j_lo, int32_t *j_hi);
+int swr_owned_slots(int32_t N, int32_t world, int32_t rank, int32_t *s_lo, int32_t *s_hi);
 
 /* Writes a 128-byte ncclUniqueId (rank 0; broadcast it to the other ranks
  * and pass it as swr_config.nccl_unique_id).  SWR_ERR_NCCL if libnccl is
  * not loadable. */
 int swr_nccl_unique_id(void *out128);
+
+/* TEST INFRASTRUCTURE: an id (pass as swr_config.nccl_unique_id) that runs
+ * `world` logical ranks as host threads of this process on one GPU, with
+ * device copies standing in for NCCL (tests/test_multirank.py drives the
+ * multi-rank code path with it; never a performance configuration). */
+int swr_loopback_id(void *out128, int32_t world);
 
 #ifdef __cplusplus
 }

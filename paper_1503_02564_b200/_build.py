@@ -10,7 +10,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 SO = os.path.join(PKG, "libswr.so")
-SOURCES = ["swr_march.cu", "swr_march_stream.cu", "swr_linalg.cu", "swr_pinv.cu", "swr_fft_halves.cu", "swr_api.cu"]
+SOURCES = ["swr_march.cu", "swr_march_stream.cu", "swr_linalg.cu", "swr_pinv.cu", "swr_api.cu"]
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a",
          "-Xcompiler", "-fPIC", "-I", os.path.join(ROOT, "include"), "-I", CSRC]
@@ -65,6 +65,35 @@ def build(force: bool = False, verbose: bool = False) -> str:
     with open(STAMP, "w") as f:
         f.write(" ".join(_extra_flags()))
     return SO
+
+
+def build_variant(tag: str, defines: list, force: bool = False) -> str:
+    """A libswr build with extra nvcc defines at ROOT/build_variants/libswr_<tag>.so
+    (race-stress tests: -DSWR_RACE_STRESS=1; kernel-shape experiments).  Not
+    the product library; never loaded by the package unless passed explicitly."""
+    out = os.path.join(ROOT, "build_variants")
+    os.makedirs(out, exist_ok=True)
+    so = os.path.join(out, f"libswr_{tag}.so")
+    deps = [os.path.join(CSRC, f) for f in os.listdir(CSRC)] + [os.path.join(ROOT, "include", "swr.h")]
+    if not force and os.path.exists(so) and all(os.path.getmtime(d) <= os.path.getmtime(so) for d in deps):
+        return so
+
+    def comp(src):
+        obj = os.path.join(out, f"{tag}_{src.replace('.cu', '.o')}")
+        r = subprocess.run([NVCC, *FLAGS, *defines, "-Xptxas", "-O3", "-c", os.path.join(CSRC, src), "-o", obj],
+                           capture_output=True, text=True)
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed for {src}:\n{r.stderr}")
+        return obj
+
+    with ThreadPoolExecutor(len(SOURCES)) as ex:
+        objs = list(ex.map(comp, SOURCES))
+    subprocess.check_call([NVCC, "-shared", "-gencode", "arch=compute_100a,code=sm_100a", "-o", so + ".tmp", *objs,
+                           "-ldl"])
+    os.replace(so + ".tmp", so)
+    for o in objs:
+        os.remove(o)
+    return so
 
 
 if __name__ == "__main__":

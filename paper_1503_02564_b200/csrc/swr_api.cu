@@ -1,19 +1,34 @@
 // swr_api.cu — host orchestration behind include/swr.h: setup, interface
 // operator construction (Algorithm 3 of PAPER.md), GMRES(m) with
-// CGS2 on the interface problem, the preconditioned algorithms
-// and the final sweep.  All arithmetic of the method runs in
-// the kernels of swr_march.cu / swr_linalg.cu; the host only keeps the
-// (m+1) x m Hessenberg matrix and its Givens rotations.
+// classical Gram-Schmidt on the interface problem, the preconditioned
+// algorithms and the final sweep, one process (rank) per GPU.
+// All arithmetic of the method runs in the kernels of swr_march.cu /
+// swr_linalg.cu; the host only keeps the (m+1) x m Hessenberg matrix and its
+// Givens rotations.
+//
+// Multi-GPU (the block-column ownership of P:982-1011): a rank
+// owns a contiguous range of subdomains and their interface slots; its
+// Krylov vectors, d and g hold those slots only.  Per operator application
+// (a march sweep or the Toeplitz apply) only the two cut traces cross to the
+// neighbour ranks (send/recv of N_T complex each); per Gram-Schmidt pass the
+// per-subdomain partial sums are summed over ranks (disjoint columns) and
+// reduced in the same fixed order as on one GPU, so G GPUs reproduce the
+// one-GPU scalars bitwise.
 #include "swr.h"
 #include "swr_kernels.h"
 
 #include <algorithm>
+#include <chrono>
 #include <cmath>
 #include <complex>
+#include <condition_variable>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <functional>
+#include <map>
+#include <memory>
+#include <mutex>
 #include <string>
 #include <vector>
 #include <dlfcn.h>
@@ -54,6 +69,7 @@ typedef int (*fn_send)(const void *, size_t, int, int, ncclComm_t, cudaStream_t)
 typedef int (*fn_recv)(void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_allreduce)(const void *, void *, size_t, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_allgather)(const void *, void *, size_t, int, ncclComm_t, cudaStream_t);
+typedef int (*fn_reduce)(const void *, void *, size_t, int, int, int, ncclComm_t, cudaStream_t);
 typedef int (*fn_group)(void);
 typedef int (*fn_getid)(ncclUniqueId_t *);
 struct Nccl {
@@ -64,11 +80,12 @@ struct Nccl {
   fn_recv recv;
   fn_allreduce allReduce;
   fn_allgather allGather;
+  fn_reduce reduce;
   fn_group groupStart, groupEnd;
   fn_getid getUniqueId;
 };
 Nccl g_nccl;
-enum { nccl_float64 = 8, nccl_sum = 0, nccl_uint8 = 1 };
+enum { nccl_int32 = 2, nccl_float64 = 8, nccl_sum = 0, nccl_max = 2 };
 
 int load_nccl() {
   if (g_nccl.lib) return SWR_OK;
@@ -84,15 +101,170 @@ int load_nccl() {
   g_nccl.recv = (fn_recv)dlsym(g_nccl.lib, "ncclRecv");
   g_nccl.allReduce = (fn_allreduce)dlsym(g_nccl.lib, "ncclAllReduce");
   g_nccl.allGather = (fn_allgather)dlsym(g_nccl.lib, "ncclAllGather");
+  g_nccl.reduce = (fn_reduce)dlsym(g_nccl.lib, "ncclReduce");
   g_nccl.groupStart = (fn_group)dlsym(g_nccl.lib, "ncclGroupStart");
   g_nccl.groupEnd = (fn_group)dlsym(g_nccl.lib, "ncclGroupEnd");
   g_nccl.getUniqueId = (fn_getid)dlsym(g_nccl.lib, "ncclGetUniqueId");
-  if (!g_nccl.commInitRank || !g_nccl.send || !g_nccl.recv || !g_nccl.allReduce || !g_nccl.groupStart) {
+  if (!g_nccl.commInitRank || !g_nccl.send || !g_nccl.recv || !g_nccl.allReduce || !g_nccl.reduce ||
+      !g_nccl.groupStart) {
     g_detail = "libnccl is missing symbols";
     return SWR_ERR_NCCL;
   }
   return SWR_OK;
 }
+
+// ---- communicators ----------------------------------------------------------
+// The ranks of one handle exchange: sums of vectors with disjoint supports
+// (exact in any order), the cut traces with the two neighbour ranks, an
+// integer max, and the final reduction of u(T) to rank 0.  NcclComm is the
+// product path (one process per GPU, NVLink / NVSwitch); LoopbackComm runs G
+// logical ranks as G host threads of one process on one GPU with device copies
+// standing in for NCCL -- test infrastructure for the multi-rank code path
+// (swr_loopback_id), never selected otherwise.
+struct Comm {
+  virtual ~Comm() {}
+  virtual int allreduce_sum(const double *send, double *recv, size_t n, cudaStream_t st) = 0;
+  virtual int allreduce_max_i32(int *buf, size_t n, cudaStream_t st) = 0;
+  // sendL -> rank-1 (its recvR), sendR -> rank+1 (its recvL); nullptr where absent
+  virtual int exchange(const double2 *sendL, double2 *recvL, const double2 *sendR, double2 *recvR, size_t n,
+                       cudaStream_t st) = 0;
+  virtual int reduce_sum_root(double *buf, size_t n, cudaStream_t st) = 0;
+};
+
+struct NcclComm : Comm {
+  ncclComm_t comm = nullptr;
+  int rank = 0, world = 1;
+  ~NcclComm() override {
+    if (comm && g_nccl.commDestroy) g_nccl.commDestroy(comm);
+  }
+  int allreduce_sum(const double *send, double *recv, size_t n, cudaStream_t st) override {
+    if (g_nccl.allReduce(send, recv, n, nccl_float64, nccl_sum, comm, st) != 0) {
+      g_detail = "ncclAllReduce failed";
+      return SWR_ERR_NCCL;
+    }
+    return SWR_OK;
+  }
+  int allreduce_max_i32(int *buf, size_t n, cudaStream_t st) override {
+    if (g_nccl.allReduce(buf, buf, n, nccl_int32, nccl_max, comm, st) != 0) {
+      g_detail = "ncclAllReduce (max) failed";
+      return SWR_ERR_NCCL;
+    }
+    return SWR_OK;
+  }
+  int exchange(const double2 *sendL, double2 *recvL, const double2 *sendR, double2 *recvR, size_t n,
+               cudaStream_t st) override {
+    g_nccl.groupStart();
+    int e = 0;
+    if (sendL) e |= g_nccl.send(sendL, 2 * n, nccl_float64, rank - 1, comm, st);
+    if (recvL) e |= g_nccl.recv(recvL, 2 * n, nccl_float64, rank - 1, comm, st);
+    if (sendR) e |= g_nccl.send(sendR, 2 * n, nccl_float64, rank + 1, comm, st);
+    if (recvR) e |= g_nccl.recv(recvR, 2 * n, nccl_float64, rank + 1, comm, st);
+    e |= g_nccl.groupEnd();
+    if (e) { g_detail = "ncclSend/ncclRecv of the cut traces failed"; return SWR_ERR_NCCL; }
+    return SWR_OK;
+  }
+  int reduce_sum_root(double *buf, size_t n, cudaStream_t st) override {
+    if (g_nccl.reduce(buf, buf, n, nccl_float64, nccl_sum, 0, comm, st) != 0) {
+      g_detail = "ncclReduce failed";
+      return SWR_ERR_NCCL;
+    }
+    return SWR_OK;
+  }
+};
+
+// In-process group of G logical ranks (one host thread each, same device).
+struct LoopGroup {
+  int world = 0;
+  std::mutex mu;
+  std::condition_variable cv;
+  int arrived = 0;
+  unsigned long long gen = 0;
+  std::vector<const void *> a, b;   // published pointers of each rank
+  void barrier() {
+    std::unique_lock<std::mutex> lk(mu);
+    const unsigned long long g = gen;
+    if (++arrived == world) {
+      arrived = 0;
+      gen++;
+      cv.notify_all();
+    } else {
+      cv.wait(lk, [&] { return gen != g; });
+    }
+  }
+};
+std::mutex g_loop_mu;
+std::map<unsigned long long, std::shared_ptr<LoopGroup>> g_loop_groups;
+const char kLoopMagic[8] = {'S', 'W', 'R', 'L', 'O', 'O', 'P', 0};
+
+struct LoopbackComm : Comm {
+  std::shared_ptr<LoopGroup> grp;
+  int rank = 0, world = 1;
+  double *scratch = nullptr;
+  size_t scratch_n = 0;
+  ~LoopbackComm() override {
+    if (scratch) cudaFree(scratch);
+  }
+  int sync(cudaStream_t st) {
+    if (cudaStreamSynchronize(st) != cudaSuccess) { g_detail = "loopback: stream sync failed"; return SWR_ERR_CUDA; }
+    return SWR_OK;
+  }
+  int allreduce_sum(const double *send, double *recv, size_t n, cudaStream_t st) override {
+    if (n > scratch_n) {
+      if (scratch) cudaFree(scratch);
+      if (cudaMalloc((void **)&scratch, n * sizeof(double)) != cudaSuccess) return SWR_ERR_OOM;
+      scratch_n = n;
+    }
+    int s = sync(st);
+    if (s) return s;
+    grp->a[rank] = send;
+    grp->barrier();
+    // every rank sums all ranks' buffers in rank order into its own scratch
+    if (cudaMemcpyAsync(scratch, grp->a[0], n * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return SWR_ERR_CUDA;
+    for (int r = 1; r < world; r++)
+      swr::k_add_f64<<<(unsigned)std::min<size_t>((n + 255) / 256, 4096), 256, 0, st>>>(
+          scratch, (const double *)grp->a[r], n);
+    if ((s = sync(st))) return s;
+    grp->barrier();   // nobody reads the send buffers any more
+    if (cudaMemcpyAsync(recv, scratch, n * sizeof(double), cudaMemcpyDeviceToDevice, st) != cudaSuccess)
+      return SWR_ERR_CUDA;
+    return sync(st);
+  }
+  int allreduce_max_i32(int *buf, size_t n, cudaStream_t st) override {
+    std::vector<int> mine(n), acc(n);
+    if (cudaMemcpyAsync(mine.data(), buf, n * sizeof(int), cudaMemcpyDeviceToHost, st) != cudaSuccess)
+      return SWR_ERR_CUDA;
+    int s = sync(st);
+    if (s) return s;
+    grp->a[rank] = mine.data();
+    grp->barrier();
+    for (size_t i = 0; i < n; i++) {
+      int m = ((const int *)grp->a[0])[i];
+      for (int r = 1; r < world; r++) m = std::max(m, ((const int *)grp->a[r])[i]);
+      acc[i] = m;
+    }
+    grp->barrier();
+    if (cudaMemcpyAsync(buf, acc.data(), n * sizeof(int), cudaMemcpyHostToDevice, st) != cudaSuccess)
+      return SWR_ERR_CUDA;
+    return sync(st);
+  }
+  int exchange(const double2 *sendL, double2 *recvL, const double2 *sendR, double2 *recvR, size_t n,
+               cudaStream_t st) override {
+    int s = sync(st);
+    if (s) return s;
+    grp->a[rank] = sendL;
+    grp->b[rank] = sendR;
+    grp->barrier();
+    if (recvL && cudaMemcpyAsync(recvL, grp->b[rank - 1], n * sizeof(double2), cudaMemcpyDeviceToDevice, st))
+      return SWR_ERR_CUDA;
+    if (recvR && cudaMemcpyAsync(recvR, grp->a[rank + 1], n * sizeof(double2), cudaMemcpyDeviceToDevice, st))
+      return SWR_ERR_CUDA;
+    if ((s = sync(st))) return s;
+    grp->barrier();
+    return SWR_OK;
+  }
+  int reduce_sum_root(double *buf, size_t n, cudaStream_t st) override { return allreduce_sum(buf, buf, n, st); }
+};
 
 template <typename T>
 int dalloc(T **p, size_t n) {
@@ -135,15 +307,24 @@ struct swr_handle {
   int pinv_sweeps = 0; // block-Jacobi sweeps of its lag-0 solve
   double pinv_rho = 0.0;
   double2 *pinvF = nullptr;   // [2N-2][PINV_B] far-history scratch
-  bool cgs_alt = true; // alternate CGS traversal direction (SWR_CGS_ALT=0 disables)
-  int cgs_dir = 0;
-  size_t vwin_bytes = 0;   // persisting L2 window over the first outer-Krylov basis vectors (SWR_V_PERSIST)
+  double2 *pinv_y = nullptr, *pinv_x = nullptr;   // world > 1: full-length P^{-1} operands
+  int cgs_dir = 0;         // alternating traversal direction of the CGS passes (L2 reuse)
+  size_t vwin_bytes = 0;   // persisting L2 window over the first outer-Krylov basis vectors
   float vwin_ratio = 1.0f;
+  size_t l2_window = 0;    // persisting L2 set-aside this handle asked for
   int Nx, NT, Nj, m;
-  size_t ng;
+  size_t ng;               // full interface vector, (2N-2) N_T
+  size_t nloc;             // this rank's slots, (s_hi - s_lo + 1) N_T (= ng on one GPU)
   int rank, world, device;
   int j_lo, j_hi;                          // this rank's subdomains (1-based, inclusive)
-  ncclComm_t comm = nullptr;
+  int s_lo, s_hi;                          // and their slots
+  swr::SlotMap smap;
+  Comm *comm = nullptr;
+  double2 *haloL = nullptr, *haloR = nullptr;     // [N_T] outputs for the neighbour ranks
+  double2 *hrecvL = nullptr, *hrecvR = nullptr;   // [N_T] (I - L) contributions from them
+  double2 *part_send = nullptr, *part_recv = nullptr;   // [33][N] CGS unit partials (world > 1)
+  int march_form = 0, toeplitz_form = 0, nl_rows = 0;
+  double t_setup_ms = 0.0;
   cudaStream_t st;
   double2 c0, c2v;
   // higher-order transmission operators (tc_hi): per subdomain side
@@ -151,7 +332,7 @@ struct swr_handle {
   double2 *kap = nullptr;                 // device [N][2][N_T+1] even kernels
   std::vector<double2> tc_c0, tc_c0e, tc_dlt, tc_rho, tc_f0;   // [N][2]
   double kappa, eim;
-  MarchShape shape[4];                     // launch shape per K = 1..3 RHS per group
+  MarchShape shape;                        // launch shape of the resident march (one RHS per group)
   // device data
   double2 *u0 = nullptr;
   double *Vx = nullptr, *beta = nullptr;
@@ -160,18 +341,16 @@ struct swr_handle {
   double2 *d = nullptr, *X = nullptr, *X0 = nullptr, *g = nullptr, *g0 = nullptr;
   double2 *uloc = nullptr, *uT = nullptr;
   double2 *tmp = nullptr, *tmp2 = nullptr, *rhs = nullptr;
-  // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0, transformed inputs
-  int log4 = 0;
-  bool fft_fused = true;
+  // FFT form of the Toeplitz apply: twiddles, transformed columns of L and L0
+  int log4 = 0;           // NF = 4^log4 (0: the direct causal convolution)
   bool fft_reg = false;   // register four-step FFT kernel (NF = 1024)
-  bool fft_halves = false; // two 512-point transforms per warp pair (SWR_FFT_HALVES=1; measured slower)
   // V(t,x): per-step pivots [N_T][N][N_j]; f(u): fixed-point stats
   double *tau = nullptr, *xi = nullptr;
   double2 *qtd = nullptr;
   double *ertd = nullptr;
   int *fp_stat = nullptr;
   MarchShape shape_nl;
-  double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr, *Fx = nullptr;
+  double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr;
   double2 *partial = nullptr;
   // streaming march (subdomains too large for the resident kernel)
   bool stream_march = false;
@@ -191,17 +370,18 @@ struct swr_handle {
   bool inner_fail = false;
   double cell_steps = 0;
   int n_marches = 0, n_launches = 0;
-  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> march_ev, intf_ev;
-  size_t march_ev_used = 0, intf_ev_used = 0;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> march_ev, intf_ev, comm_ev;
+  size_t march_ev_used = 0, intf_ev_used = 0, comm_ev_used = 0;
   cudaEvent_t ev_b0, ev_b1, ev_s0, ev_s1;
   bool build_timed = false;
 };
 
 namespace {
 
-int record_pair(swr_handle *h, bool march, bool begin) {
-  auto &vec = march ? h->march_ev : h->intf_ev;
-  size_t &used = march ? h->march_ev_used : h->intf_ev_used;
+enum { EV_INTF = 0, EV_MARCH = 1, EV_COMM = 2 };
+int record_pair(swr_handle *h, int kind, bool begin) {
+  auto &vec = kind == EV_MARCH ? h->march_ev : (kind == EV_COMM ? h->comm_ev : h->intf_ev);
+  size_t &used = kind == EV_MARCH ? h->march_ev_used : (kind == EV_COMM ? h->comm_ev_used : h->intf_ev_used);
   if (begin) {
     if (used == vec.size()) {
       cudaEvent_t a, b;
@@ -217,9 +397,9 @@ int record_pair(swr_handle *h, bool march, bool begin) {
   return SWR_OK;
 }
 
-double sum_pairs(swr_handle *h, bool march) {
-  auto &vec = march ? h->march_ev : h->intf_ev;
-  size_t used = march ? h->march_ev_used : h->intf_ev_used;
+double sum_pairs(swr_handle *h, int kind) {
+  auto &vec = kind == EV_MARCH ? h->march_ev : (kind == EV_COMM ? h->comm_ev : h->intf_ev);
+  size_t used = kind == EV_MARCH ? h->march_ev_used : (kind == EV_COMM ? h->comm_ev_used : h->intf_ev_used);
   double s = 0;
   for (size_t i = 0; i < used; i++) {
     float ms = 0;
@@ -232,10 +412,10 @@ int slot_l(int j) { return 2 * j - 3; }
 int slot_r(int j) { return 2 * j - 2; }
 int zero_matrix_index(swr_handle *h, int j) { return j == 1 ? 0 : (j == h->N ? 2 : 1); }
 
-// ---- one batched march over groups of K systems sharing a matrix --------
+// ---- one batched march of many systems --------------------------------------
 enum { MARCH_CONST = 0, MARCH_TD = 1, MARCH_NL = 2 };
 
-int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal, int mode = MARCH_CONST) {
+int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mode = MARCH_CONST) {
   if (sys.empty()) return SWR_OK;
   CK(cudaMemcpyAsync(h->sys_dev, sys.data(), sys.size() * sizeof(MarchSys), cudaMemcpyHostToDevice, h->st));
   MarchParams p;
@@ -243,7 +423,7 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
   p.nsys = (int)sys.size();
   p.Nj = h->Nj;
   p.NT = h->NT;
-  p.CS = h->shape[K].CS;
+  p.CS = h->shape.CS;
   p.e_im = h->eim;
   p.kappa = h->kappa;
   p.c0 = h->c0;
@@ -262,28 +442,29 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
   p.maxit_fp = h->maxit_fp;
   p.fp_stat = h->fp_stat;
   if (mode == MARCH_NL) {
-    CKS(record_pair(h, true, true));
+    CKS(record_pair(h, EV_MARCH, true));
     CK(swr::launch_march_nl(p, h->shape_nl, h->st));
     CK(cudaGetLastError());
-    CKS(record_pair(h, true, false));
+    CKS(record_pair(h, EV_MARCH, false));
     h->n_marches++;
     h->n_launches++;
     h->cell_steps += (double)nreal * h->Nj * h->NT;
     return SWR_OK;
   }
-  if (getenv("SWR_TRACE")) {
-    // per-CTA phase trace of the first cluster (tools/march_trace.sh)
+#if SWR_MARCH_TRACE
+  if (getenv("SWR_TRACE") && !h->stream_march) {
+    // per-CTA phase trace of the first cluster (trace builds only: tools/march_trace.sh)
     static long long *tr = nullptr;
     const int ntr = 16 * 32;
     if (!tr) CK(cudaMalloc(&tr, ntr * sizeof(long long)));
     CK(cudaMemsetAsync(tr, 0, ntr * sizeof(long long), h->st));
     p.trace = tr;
-    CK(swr::launch_march(p, h->shape[K], h->st));
+    CK(swr::launch_march(p, h->shape, h->st));
     std::vector<long long> hv(ntr);
     CK(cudaMemcpyAsync(hv.data(), tr, ntr * sizeof(long long), cudaMemcpyDeviceToHost, h->st));
     CK(cudaStreamSynchronize(h->st));
-    const MarchShape &sh = h->shape[K];
-    fprintf(stderr, "march trace K=%d M=%d P=%d CS=%d (cycles from step start)\n", K, sh.M, sh.P, sh.CS);
+    const MarchShape &sh = h->shape;
+    fprintf(stderr, "march trace M=%d P=%d CS=%d (cycles from step start)\n", sh.M, sh.P, sh.CS);
     for (int c = 0; c < sh.CS; c++) {
       const long long *r = hv.data() + c * 32;
       fprintf(stderr, "  cta %d:", c);
@@ -293,35 +474,38 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int K, int nreal,
     }
     p.trace = nullptr;
   }
-  CKS(record_pair(h, true, true));
+#endif
+  CKS(record_pair(h, EV_MARCH, true));
   if (h->stream_march) {
-    // one system per group (K = 1), in batches of co-resident chains
-    if (K != 1) { g_detail = "streaming march takes K = 1"; return SWR_ERR_UNSUPPORTED; }
+    // in batches of co-resident chains
     if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
-    CK(swr::launch_march_stream(p, (int)sys.size(), h->sst_u, h->sst_z, h->sst_flags, h->sst_vals, h->st));
+    CK(swr::launch_march_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->sst_flags, h->sst_vals, h->st));
   } else {
-    CK(swr::launch_march(p, h->shape[K], h->st));
+    CK(swr::launch_march(p, h->shape, h->st));
   }
   CK(cudaGetLastError());
-  CKS(record_pair(h, true, false));
+  CKS(record_pair(h, EV_MARCH, false));
   h->n_marches++;
   h->n_launches++;
   h->cell_steps += (double)nreal * h->Nj * h->NT;
   return SWR_OK;
 }
 
-// system of subdomain j (1-based) with fluxes from g (may be NULL)
+// system of owned subdomain j (1-based) with fluxes from the local interface
+// vector g (may be NULL); its outputs go to the local slots of Rg, or to the
+// halo buffers when the neighbour rank owns the slot (eq. 8 across a cut)
 MarchSys make_sys(swr_handle *h, int j, const double2 *g, bool use_u0, bool zero_pot, double2 *Rg,
                   double2 *uloc) {
   MarchSys s;
   memset(&s, 0, sizeof s);
-  const int N = h->N, NT = h->NT;
+  const int N = h->N;
   if (j >= 2) s.flags |= swr::SYS_HAS_LEFT;
   if (j <= N - 1) s.flags |= swr::SYS_HAS_RIGHT;
-  if (g && j >= 2) s.lin = g + (size_t)slot_l(j) * NT;
-  if (g && j <= N - 1) s.rin = g + (size_t)slot_r(j) * NT;
-  if (Rg && j >= 2) s.out_left = Rg + (size_t)slot_r(j - 1) * NT;
-  if (Rg && j <= N - 1) s.out_right = Rg + (size_t)slot_l(j + 1) * NT;
+  if (g && j >= 2) s.lin = swr::slot_ptr(h->smap, g, slot_l(j));
+  if (g && j <= N - 1) s.rin = swr::slot_ptr(h->smap, g, slot_r(j));
+  bool remote;
+  if (Rg && j >= 2) s.out_left = swr::out_ptr(h->smap, Rg, slot_r(j - 1), remote);
+  if (Rg && j <= N - 1) s.out_right = swr::out_ptr(h->smap, Rg, slot_l(j + 1), remote);
   s.uT = uloc ? uloc + (size_t)(j - 1) * h->Nj : nullptr;
   s.u0 = use_u0 ? h->u0 + (size_t)(j - 1) * h->m : nullptr;
   if (zero_pot) {
@@ -354,28 +538,44 @@ int fill_zero(swr_handle *h, double2 *x, size_t n) {
   return SWR_OK;
 }
 
-// Sum over ranks of vectors each rank filled on its own subdomains' slots
-// (disjoint supports, zeros elsewhere: the sum is exact).
-int allreduce_sum(swr_handle *h, double2 *buf, size_t n) {
-  if (h->world <= 1 || n == 0) return SWR_OK;
-  if (g_nccl.allReduce(buf, buf, 2 * n, nccl_float64, nccl_sum, h->comm, h->st) != 0) {
-    g_detail = "ncclAllReduce failed";
-    return SWR_ERR_NCCL;
-  }
+// ---- collectives (world > 1), timed as communication ----------------------
+// The cut traces of eq. (8): what this rank's subdomains produced for the
+// neighbours' first / last slot (halo buffers) goes out, and the neighbours'
+// contributions arrive -- into recvL / recvR (first and last local slot).
+int exchange_cut(swr_handle *h, double2 *recvL, double2 *recvR) {
+  if (h->world <= 1) return SWR_OK;
+  CKS(record_pair(h, EV_COMM, true));
+  CKS(h->comm->exchange(h->rank > 0 ? h->haloL : nullptr, h->rank > 0 ? recvL : nullptr,
+                        h->rank < h->world - 1 ? h->haloR : nullptr, h->rank < h->world - 1 ? recvR : nullptr,
+                        (size_t)h->NT, h->st));
+  CKS(record_pair(h, EV_COMM, false));
   h->n_launches++;
   return SWR_OK;
 }
 
-// Rg = R(g; u0?) (eq. 13): every subdomain marches once.
+double2 *last_slot(swr_handle *h, double2 *v) { return v + (size_t)(h->s_hi - h->s_lo) * h->NT; }
+
+// Sum over ranks of n doubles (disjoint supports: exact in any order).
+int allreduce_sum(swr_handle *h, const double *send, double *recv, size_t n) {
+  if (h->world <= 1 || n == 0) return SWR_OK;
+  CKS(record_pair(h, EV_COMM, true));
+  CKS(h->comm->allreduce_sum(send, recv, n, h->st));
+  CKS(record_pair(h, EV_COMM, false));
+  h->n_launches++;
+  return SWR_OK;
+}
+
+// Rg = R(g; u0?) (eq. 13): every owned subdomain marches once; the outputs
+// that cross a rank cut are exchanged with the neighbour ranks.
 int sweep_R(swr_handle *h, const double2 *g, bool use_u0, bool zero_pot, double2 *Rg, double2 *uloc) {
   std::vector<MarchSys> sys;
   for (int j = h->j_lo; j <= h->j_hi; j++) sys.push_back(make_sys(h, j, g, use_u0, zero_pot, Rg, uloc));
-  if (Rg) CKS(fill_zero(h, Rg, h->ng));
+  if (Rg) CKS(fill_zero(h, Rg, h->nloc));
   int mode = MARCH_CONST;
   if (!zero_pot && h->potential == SWR_POT_VTX_SEPARABLE) mode = MARCH_TD;
   if (!zero_pot && h->potential == SWR_POT_CUBIC) mode = MARCH_NL;
-  CKS(run_march(h, sys, 1, (int)sys.size(), mode));
-  if (Rg) CKS(allreduce_sum(h, Rg, h->ng));   // exchange of eq. (8) across rank cuts
+  CKS(run_march(h, sys, (int)sys.size(), mode));
+  if (Rg) CKS(exchange_cut(h, Rg, last_slot(h, Rg)));
   return SWR_OK;
 }
 
@@ -589,31 +789,39 @@ typedef std::function<int(const double2 *, double2 *)> Op;
 // s = sp->x on the device (the new basis vector is normalised on load).
 typedef std::function<int(const double2 *x, const double2 *sp, double2 *vcopy, double2 *y)> OpScaled;
 
-// GMRES(m) with CGS2 and complex Givens rotations, the same algorithm as the
-// oracle (reading A5/A6): stop at |gamma_{k+1}| <= tol ||b||, true residual
-// at restarts, happy breakdown at h_{k+1,k} <= 1e-14 ||A v_k||.  Device work
-// per Arnoldi step: the operator, three fused CGS kernels (dots; axpy+dots;
-// axpy+norm) and the normalisation; one host round trip for the Givens
-// update.
+// One fused Gram-Schmidt pass (dots / axpy / norm, see launch_cgs) on this
+// rank's slots.  Every pass alternates its traversal direction (the first
+// units of a pass meet the last ones of the previous pass in L2).  World > 1:
+// the unit partials of all ranks are summed (disjoint columns, exact) and
+// reduced in the one-GPU order.
 int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w, int mode, double2 *out,
         double2 *out_host = nullptr) {
-  // alternate the traversal direction pass to pass (L2 reuse of V's tail)
-  if (h->cgs_alt) {
-    h->cgs_dir ^= 1;
-    if (h->cgs_dir) mode |= swr::CGS_REV;
-  }
+  h->cgs_dir ^= 1;
+  if (h->cgs_dir) mode |= swr::CGS_REV;
   // the first basis vectors stay in L2 (persisting window; every pass reads them)
   const bool win = V && V == h->kout.V && h->vwin_bytes > 0;
-  CK(swr::launch_cgs(V, h->ng, nv, hsrc, w, mode, h->partial, out, h->counter, h->N, h->NT, h->st, out_host,
-                     win ? h->vwin_bytes : 0, h->vwin_ratio));
+#ifndef SWR_CGS_SEPARATE_REDUCE
+#define SWR_CGS_SEPARATE_REDUCE 0   // 1: one GPU reduces the unit partials in a second kernel too
+#endif
+  const bool dist = h->world > 1 || SWR_CGS_SEPARATE_REDUCE;
+  CK(swr::launch_cgs(V, h->nloc, nv, hsrc, w, mode, h->smap, dist ? h->part_send : h->partial, dist ? nullptr : out,
+                     h->counter, h->st, out_host, win ? h->vwin_bytes : 0, h->vwin_ratio));
   h->n_launches++;
+  if (dist) {
+    const int nred = ((mode & swr::CGS_DOTS) ? nv : 0) + ((mode & swr::CGS_NORM) ? 1 : 0);
+    const int nu = swr::cgs_units_global(h->smap);
+    if (h->world > 1)
+      CKS(allreduce_sum(h, (const double *)h->part_send, (double *)h->part_recv, (size_t)2 * nred * nu));
+    CK(swr::launch_cgs_reduce(h->world > 1 ? h->part_recv : h->part_send, nu, nred, mode, out, out_host, h->st));
+    h->n_launches++;
+  }
   return SWR_OK;
 }
 
 int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int m, int maxit, Krylov &K,
           int *iters, std::vector<double> *hist, int *converged, bool speculate = true,
           const OpScaled *AS = nullptr) {
-  const size_t n = h->ng;
+  const size_t n = h->nloc;
   const size_t ldv = n;
   double2 *V = K.V, *w = K.w;
   *iters = 0;
@@ -741,56 +949,68 @@ int gmres(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, 
   return st;
 }
 
-// y = (I - L) x or (I - L0) x: FFT convolution (default when N_T <= 512)
-// or the direct causal-convolution kernel.
-int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
+// y = (I - L) x or (I - L0) x on this rank's slots: the FFT convolution
+// (N_T <= 512) or the direct causal convolution; xs (device, optional): the
+// input is xs->x times x and vcopy receives that scaled input (register FFT
+// only: the GMRES step normalises its new basis vector on load).  Across a
+// rank cut the neighbour computes -(L x) of our first / last slot and we add
+// our own (scaled) x after the exchange.
+int apply_toeplitz(swr_handle *h, bool zero, const double2 *x, const double2 *xs, double2 *vcopy, double2 *y) {
   if (h->N < 2) return SWR_OK;
-  CKS(record_pair(h, false, true));
+  CKS(record_pair(h, EV_INTF, true));
+  const double2 *F = zero ? h->FX0 : h->FX;
   if (h->log4 && h->fft_reg) {
-    if (h->fft_halves)
-      CK(swr::launch_fft_conv_h(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, nullptr, nullptr,
-                                swr::l2_persist_bytes()));
-    else
-      CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
-    h->n_launches++;
-  } else if (h->log4 && h->fft_fused) {
-    CK(swr::launch_fft_conv(h->log4, zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st));
-    h->n_launches++;
+    CK(swr::launch_fft_conv_reg(F, x, y, h->smap, h->tw, h->st, xs, vcopy));
+  } else if (xs) {
+    g_detail = "scaled Toeplitz apply needs the register FFT";
+    return SWR_ERR_UNSUPPORTED;
   } else if (h->log4) {
-    CK(swr::launch_fft_fwd(h->log4, x, h->NT, 2 * h->N - 2, h->NT, h->tw, h->Fx, h->st));
-    CK(swr::launch_fft_apply(h->log4, zero ? h->FX0 : h->FX, h->Fx, x, y, h->N, h->NT, h->tw, h->st));
-    h->n_launches += 2;
+    CK(swr::launch_fft_conv(h->log4, F, x, y, h->smap, h->tw, h->st));
   } else {
     const double2 *X = zero ? h->X0 : h->X;
     const int G = (h->NT + swr::TR - 1) / swr::TR;
     const int thr = (2 * ((G + 1) / 2) + 31) / 32 * 32;
     const size_t smem = (4 * ((size_t)h->NT + 3 * swr::TR) + 2 * ((size_t)h->NT + swr::TR)) * sizeof(double2);
     if (smem > 48 * 1024) CK(cudaFuncSetAttribute(swr::k_toeplitz_I_minus_L, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    swr::k_toeplitz_I_minus_L<<<h->N, thr, smem, h->st>>>(X, x, y, h->N, h->NT);
-    CK(cudaGetLastError());
-    h->n_launches++;
+    swr::k_toeplitz_I_minus_L<<<h->j_hi - h->j_lo + 1, thr, smem, h->st>>>(X, x, y, h->smap);
   }
-  CKS(record_pair(h, false, false));
+  CK(cudaGetLastError());
+  h->n_launches++;
+  CKS(record_pair(h, EV_INTF, false));
+  if (h->world > 1) {
+    CKS(exchange_cut(h, h->hrecvL, h->hrecvR));
+    const int NT = h->NT;
+    // (vcopy is complete: every owned slot is an input of an owned subdomain)
+    if (h->rank > 0) {
+      swr::k_halo_add<<<(NT + 127) / 128, 128, 0, h->st>>>(x, h->hrecvL, y, NT, xs);
+      h->n_launches++;
+    }
+    if (h->rank < h->world - 1) {
+      const size_t o = (size_t)(h->s_hi - h->s_lo) * NT;
+      swr::k_halo_add<<<(NT + 127) / 128, 128, 0, h->st>>>(x + o, h->hrecvR, y + o, NT, xs);
+      h->n_launches++;
+    }
+    CK(cudaGetLastError());
+  }
   return SWR_OK;
+}
+
+int apply_I_minus_L(swr_handle *h, bool zero, const double2 *x, double2 *y) {
+  return apply_toeplitz(h, zero, x, nullptr, nullptr, y);
 }
 
 // Fused GMRES operator (register FFT path only): y = (I - L)(s x), vcopy = s x.
 int apply_I_minus_L_scaled(swr_handle *h, bool zero, const double2 *x, const double2 *sp, double2 *vcopy, double2 *y) {
-  CKS(record_pair(h, false, true));
-  if (h->fft_halves)
-    CK(swr::launch_fft_conv_h(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy,
-                              swr::l2_persist_bytes()));
-  else
-    CK(swr::launch_fft_conv_reg(zero ? h->FX0 : h->FX, x, y, h->N, h->NT, h->tw, h->st, sp, vcopy));
-  h->n_launches++;
-  CKS(record_pair(h, false, false));
-  return SWR_OK;
+  return apply_toeplitz(h, zero, x, sp, vcopy, y);
 }
 
-// transforms of the first columns, once per build
+// transforms of this rank's first columns, once per build
 int transform_columns(swr_handle *h, bool zero) {
   if (!h->log4) return SWR_OK;
-  CK(swr::launch_fft_fwd(h->log4, zero ? h->X0 : h->X, h->NT, 4 * h->N, h->NT, h->tw, zero ? h->FX0 : h->FX, h->st));
+  const size_t o = (size_t)(h->j_lo - 1) * 4;
+  const size_t NF = (size_t)1 << (2 * h->log4);
+  CK(swr::launch_fft_fwd(h->log4, (zero ? h->X0 : h->X) + o * h->NT, h->NT, 4 * (h->j_hi - h->j_lo + 1), h->NT, h->tw,
+                         (zero ? h->FX0 : h->FX) + o * NF, h->st));
   h->n_launches++;
   return SWR_OK;
 }
@@ -801,7 +1021,7 @@ int transform_columns(swr_handle *h, bool zero) {
 // each half step (the method's own decisions: alpha, omega, the stops).
 int bicgstab(swr_handle *h, const Op &A, const double2 *b, double2 *x, double tol, int maxit, Krylov &K, int *iters,
              std::vector<double> *hist, int *converged) {
-  const size_t n = h->ng;
+  const size_t n = h->nloc;
   double2 *r = K.V, *rh = K.V + n, *p = K.V + 2 * n, *v = K.V + 3 * n, *sv = K.V + 4 * n, *t = K.V + 5 * n;
   double2 *dv = K.dots, *hp = K.hp;
   const dim3 g(grid_for(n)), bl(256);
@@ -912,14 +1132,30 @@ int setup_pinv(swr_handle *h) {
 
 int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   if (h->pinv_exact) {
+    // the forward substitution in time couples every interface at every step:
+    // on multi-GPU runs it is replicated on the whole vector (every rank holds
+    // L0), gathered by one sum of zero-padded slices, and each rank keeps its
+    // own slots
+    const size_t off = (size_t)h->s_lo * h->NT;
+    const double2 *yf = y;
+    double2 *xf = x;
+    if (h->world > 1) {
+      CKS(fill_zero(h, h->pinv_y, h->ng));
+      CK(cudaMemcpyAsync(h->pinv_y + off, y, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+      CKS(allreduce_sum(h, (const double *)h->pinv_y, (double *)h->pinv_y, 2 * h->ng));
+      yf = h->pinv_y;
+      xf = h->pinv_x;
+    }
     int nl = 0;
-    CKS(record_pair(h, false, true));
-    CK(swr::launch_pinv_causal(h->X0, y, x, h->pinvF, h->N, h->NT, h->pinv_sweeps, h->st, &nl));
-    CKS(record_pair(h, false, false));
+    CKS(record_pair(h, EV_INTF, true));
+    CK(swr::launch_pinv_causal(h->X0, yf, xf, h->pinvF, h->N, h->NT, h->pinv_sweeps, h->st, &nl));
+    CKS(record_pair(h, EV_INTF, false));
     h->n_launches += nl;
+    if (h->world > 1)
+      CK(cudaMemcpyAsync(x, h->pinv_x + off, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
     return SWR_OK;
   }
-  CKS(fill_zero(h, x, h->ng));
+  CKS(fill_zero(h, x, h->nloc));
   Op A0 = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, true, a, b); };
   OpScaled A0s = [h](const double2 *a, const double2 *sp, double2 *vc, double2 *b) {
     return apply_I_minus_L_scaled(h, true, a, sp, vc, b);
@@ -934,30 +1170,38 @@ int apply_Pinv(swr_handle *h, const double2 *y, double2 *x) {
   return s;
 }
 
-// the L / L0 first columns by impulse probing, with d = R(0; u0)
-// in the same launch: one group per subdomain, K = 3 (d, l_j probe, r_j
-// probe; the end subdomains pad with an all-zero RHS) or K = 2 without d.
+// The L / L0 first columns by impulse probing, with d = R(0; u0)
+// in the same launch (NEW): per owned subdomain the d system and the l_j / r_j
+// unit-impulse probes.  L0 (V = 0, PRECOND): the probes of an interior
+// subdomain do not depend on j (same matrix, u0 = 0; reading A14), so only
+// the three distinct subdomains j = 1, 2, N march and the interior columns
+// are copied -- bitwise what probing every subdomain gives -- and every rank
+// holds all of L0 (the exact P^{-1} needs it on multi-GPU runs).
 int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
   std::vector<MarchSys> sys;
   const int N = h->N, NT = h->NT;
-  const char *kenv = getenv("SWR_BUILD_K");
-  int K = kenv ? atoi(kenv) : 1;
-  if (K < 1 || K > 3 || h->shape[K].M == 0) K = 1;
   int nreal = 0;
   CKS(fill_zero(h, X, (size_t)N * 4 * NT));
-  if (dvec) CKS(fill_zero(h, dvec, h->ng));
-  for (int j = h->j_lo; j <= h->j_hi; j++) {
+  if (dvec) CKS(fill_zero(h, dvec, h->nloc));
+  std::vector<int> js;
+  if (zero) {
+    js.push_back(1);
+    if (N >= 3) js.push_back(2);
+    js.push_back(N);
+  } else {
+    for (int j = h->j_lo; j <= h->j_hi; j++) js.push_back(j);
+  }
+  for (int j : js) {
     double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
     const MarchSys blank = make_sys(h, j, nullptr, false, zero, nullptr, nullptr);
-    int kk = 0;
-    if (dvec) { sys.push_back(make_sys(h, j, nullptr, true, zero, dvec, nullptr)); kk++; }
+    if (dvec) { sys.push_back(make_sys(h, j, nullptr, true, zero, dvec, nullptr)); nreal++; }
     if (j >= 2) {  // l_{j,1} = 1 -> X^{j,1} (out_left), X^{j,3} (out_right)
       MarchSys s = blank;
       s.flags |= swr::SYS_LIN_IMPULSE;
       s.out_left = Xj + 0 * NT;
       s.out_right = (j <= N - 1) ? Xj + 2 * NT : nullptr;
       sys.push_back(s);
-      kk++;
+      nreal++;
     }
     if (j <= N - 1) {  // r_{j,1} = 1 -> X^{j,2}, X^{j,4}
       MarchSys s = blank;
@@ -965,24 +1209,34 @@ int build_probes(swr_handle *h, bool zero, double2 *X, double2 *dvec) {
       s.out_left = (j >= 2) ? Xj + 1 * NT : nullptr;
       s.out_right = Xj + 3 * NT;
       sys.push_back(s);
-      kk++;
+      nreal++;
     }
-    nreal += kk;
-    if (K > 1)
-      for (; kk % K; kk++) sys.push_back(blank);
   }
-  CKS(run_march(h, sys, K, nreal));
-  CKS(allreduce_sum(h, X, (size_t)N * 4 * NT));
-  if (dvec) CKS(allreduce_sum(h, dvec, h->ng));
+  CKS(run_march(h, sys, nreal));
+  if (zero && N >= 4) {   // interior columns j = 3..N-1 := those of j = 2
+    const size_t blk = (size_t)4 * NT;
+    swr::k_replicate<<<grid_for(blk * (N - 3)), 256, 0, h->st>>>(X + blk, X + 2 * blk, blk, (size_t)(N - 3));
+    CK(cudaGetLastError());
+    h->n_launches++;
+  }
+  if (dvec) CKS(exchange_cut(h, dvec, last_slot(h, dvec)));
   return SWR_OK;
 }
 
+// Final sweep and u(T) on the global mesh; multi-GPU: every rank fills its
+// nodes (half of each copy at a node shared with a neighbour rank) and the
+// sum over ranks lands on rank 0.
 int final_sweep(swr_handle *h, const double2 *g) {
   CKS(sweep_R(h, g, true, false, nullptr, h->uloc));
   swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->j_lo, h->j_hi, h->uT);
   CK(cudaGetLastError());
   h->n_launches++;
-  CKS(allreduce_sum(h, h->uT, (size_t)h->Nx + 1));
+  if (h->world > 1) {
+    CKS(record_pair(h, EV_COMM, true));
+    CKS(h->comm->reduce_sum_root((double *)h->uT, (size_t)2 * (h->Nx + 1), h->st));
+    CKS(record_pair(h, EV_COMM, false));
+    h->n_launches++;
+  }
   return SWR_OK;
 }
 
@@ -1007,12 +1261,40 @@ int alloc_krylov(Krylov &K, size_t mm, size_t ng) {
   return SWR_OK;
 }
 
+// Persisting-L2 set-aside (device-wide limit): raised by the first live
+// handle of a device, restored (and the persisting lines reset) when the
+// last one is freed, so it does not leak into other work of the process.
+struct L2State { int users = 0; size_t prev = 0; };
+std::mutex g_l2_mu;
+std::map<int, L2State> g_l2;
+
+void l2_acquire(int dev, size_t want) {
+  std::lock_guard<std::mutex> lk(g_l2_mu);
+  L2State &S = g_l2[dev];
+  if (S.users++ == 0) cudaDeviceGetLimit(&S.prev, cudaLimitPersistingL2CacheSize);
+  size_t cur = 0;
+  cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+  if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  cudaGetLastError();
+}
+
+void l2_release(int dev) {
+  std::lock_guard<std::mutex> lk(g_l2_mu);
+  L2State &S = g_l2[dev];
+  if (S.users > 0 && --S.users == 0) {
+    cudaCtxResetPersistingL2Cache();
+    cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, S.prev);
+    cudaGetLastError();
+  }
+}
+
 void free_all(swr_handle *h) {
   void *ptrs[] = {h->pinvF, h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
-                  h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0, h->Fx,
+                  h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev, h->counter,
-                  h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap};
+                  h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
+                  h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
@@ -1023,9 +1305,12 @@ void free_all(swr_handle *h) {
       if (K->ev[i]) cudaEventDestroy(K->ev[i]);
   }
   if (h->hpin) cudaFreeHost(h->hpin);
-  for (auto &e : h->march_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
-  if (h->comm && g_nccl.commDestroy) g_nccl.commDestroy(h->comm);
-  for (auto &e : h->intf_ev) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  for (auto *vec : {&h->march_ev, &h->intf_ev, &h->comm_ev})
+    for (auto &e : *vec) { cudaEventDestroy(e.first); cudaEventDestroy(e.second); }
+  delete h->comm;
+  h->comm = nullptr;
+  if (h->l2_window) l2_release(h->device);
+  h->l2_window = 0;
 }
 
 }  // namespace
@@ -1057,6 +1342,15 @@ int swr_partition(int32_t N, int32_t world, int32_t rank, int32_t *j_lo, int32_t
   return SWR_OK;
 }
 
+int swr_owned_slots(int32_t N, int32_t world, int32_t rank, int32_t *s_lo, int32_t *s_hi) {
+  int32_t jl, jh;
+  CKS(swr_partition(N, world, rank, &jl, &jh));
+  if (!s_lo || !s_hi || N < 2) return SWR_ERR_INVALID_ARG;
+  *s_lo = swr::slot_first(jl);
+  *s_hi = swr::slot_last(jh, N);
+  return SWR_OK;
+}
+
 int swr_nccl_unique_id(void *out) {
   if (!out) return SWR_ERR_INVALID_ARG;
   CKS(load_nccl());
@@ -1064,6 +1358,22 @@ int swr_nccl_unique_id(void *out) {
   ncclUniqueId_t id;
   if (g_nccl.getUniqueId(&id) != 0) { g_detail = "ncclGetUniqueId failed"; return SWR_ERR_NCCL; }
   memcpy(out, &id, sizeof id);
+  return SWR_OK;
+}
+
+int swr_loopback_id(void *out, int32_t world) {
+  if (!out || world < 1) return SWR_ERR_INVALID_ARG;
+  static unsigned long long next = 1;
+  std::lock_guard<std::mutex> lk(g_loop_mu);
+  const unsigned long long gid = next++;
+  auto grp = std::make_shared<LoopGroup>();
+  grp->world = world;
+  grp->a.assign(world, nullptr);
+  grp->b.assign(world, nullptr);
+  g_loop_groups[gid] = grp;
+  memset(out, 0, 128);
+  memcpy(out, kLoopMagic, 8);
+  memcpy((char *)out + 8, &gid, sizeof gid);
   return SWR_OK;
 }
 
@@ -1077,6 +1387,7 @@ int swr_sizes(const swr_handle *h, int32_t *Nx, int32_t *NT, int32_t *Nj, int64_
 }
 
 int swr_setup(const swr_config *cfg, swr_handle **out) {
+  const auto t_start = std::chrono::steady_clock::now();
   g_detail.clear();
   if (!out) return SWR_ERR_INVALID_ARG;
   *out = nullptr;
@@ -1117,6 +1428,11 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     g_detail = "V(t,x) needs n_terms >= 1, tau and xi";
     return SWR_ERR_INVALID_ARG;
   }
+  if (cfg->march_form < 0 || cfg->march_form > 1 || cfg->toeplitz_form < 0 || cfg->toeplitz_form > 2 ||
+      !(cfg->nl_rows_per_thread == 0 || cfg->nl_rows_per_thread == 8 || cfg->nl_rows_per_thread == 11)) {
+    g_detail = "march_form in {0,1}, toeplitz_form in {0,1,2}, nl_rows_per_thread in {0,8,11}";
+    return SWR_ERR_INVALID_ARG;
+  }
 
   int ndev = 0;
   if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) { g_detail = "no CUDA device"; return SWR_ERR_CUDA; }
@@ -1131,20 +1447,52 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->krylov = cfg->krylov;
   h->pade_m = cfg->pade_m;
   h->pinv_exact = cfg->pinv_exact ? 1 : 0;
-  if (const char *e = getenv("SWR_CGS_ALT")) h->cgs_alt = atoi(e) != 0;
-  if (const char *e = getenv("SWR_FFT_HALVES")) h->fft_halves = atoi(e) != 0;
+  h->march_form = cfg->march_form;
+  h->toeplitz_form = cfg->toeplitz_form;
+  h->nl_rows = cfg->nl_rows_per_thread;
   h->maxit_inner = cfg->maxit_inner > 0 ? cfg->maxit_inner : 2000; h->maxit_fp = cfg->maxit_fp > 0 ? cfg->maxit_fp : 50;
   h->n_terms = cfg->n_terms;
   h->Nx = (int)Nx; h->NT = (int)NT; h->m = (int)(Nx / cfg->N); h->Nj = h->m + 1;
   h->ng = (size_t)(2 * h->N - 2) * h->NT;
   h->rank = cfg->rank; h->world = cfg->world; h->device = cfg->device;
   swr_partition(h->N, h->world, h->rank, &h->j_lo, &h->j_hi);
+  h->s_lo = h->N >= 2 ? swr::slot_first(h->j_lo) : 0;
+  h->s_hi = h->N >= 2 ? swr::slot_last(h->j_hi, h->N) : -1;
+  h->nloc = h->N >= 2 ? (size_t)(h->s_hi - h->s_lo + 1) * h->NT : 0;
   h->st = (cudaStream_t)cfg->cuda_stream;
+  auto fail = [&](int s) { free_all(h); delete h; return s; };
   if (h->world > 1) {
-    if (load_nccl() != 0 || !cfg->nccl_unique_id) { delete h; g_detail = "NCCL unavailable or no unique id"; return SWR_ERR_NCCL; }
-    ncclUniqueId_t id;
-    memcpy(&id, cfg->nccl_unique_id, sizeof id);
-    if (g_nccl.commInitRank(&h->comm, h->world, id, h->rank) != 0) { delete h; g_detail = "ncclCommInitRank failed"; return SWR_ERR_NCCL; }
+    if (!cfg->nccl_unique_id) { delete h; g_detail = "world > 1 needs a communicator id"; return SWR_ERR_NCCL; }
+    if (memcmp(cfg->nccl_unique_id, kLoopMagic, 8) == 0) {
+      unsigned long long gid;
+      memcpy(&gid, (const char *)cfg->nccl_unique_id + 8, sizeof gid);
+      std::shared_ptr<LoopGroup> grp;
+      {
+        std::lock_guard<std::mutex> lk(g_loop_mu);
+        auto it = g_loop_groups.find(gid);
+        if (it != g_loop_groups.end()) grp = it->second;
+      }
+      if (!grp || grp->world != h->world) { delete h; g_detail = "unknown loopback group"; return SWR_ERR_NCCL; }
+      auto *lc = new LoopbackComm();
+      lc->grp = grp;
+      lc->rank = h->rank;
+      lc->world = h->world;
+      h->comm = lc;
+    } else {
+      if (load_nccl() != 0) { delete h; return SWR_ERR_NCCL; }
+      ncclUniqueId_t id;
+      memcpy(&id, cfg->nccl_unique_id, sizeof id);
+      auto *nc = new NcclComm();
+      nc->rank = h->rank;
+      nc->world = h->world;
+      if (g_nccl.commInitRank(&nc->comm, h->world, id, h->rank) != 0) {
+        delete nc;
+        delete h;
+        g_detail = "ncclCommInitRank failed";
+        return SWR_ERR_NCCL;
+      }
+      h->comm = nc;
+    }
   }
   // transmission constants: c2 = e^{-i pi/4} sqrt(2/dt) = (1-i)/sqrt(dt)
   const double sq = std::sqrt(h->dt);
@@ -1153,23 +1501,14 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   h->tc_hi = h->transmission >= SWR_TC_S0_3;
   h->kappa = (2.0 / h->dt) * (h->dx / 6.0);
   h->eim = (2.0 / h->dt) * (h->dx / 6.0);
-  for (int K = 1; K <= 3; K++) h->shape[K] = swr::choose_march_shape(h->Nj, K, h->NT, h->tc_hi);
-  h->shape[0] = h->shape[1];
-  bool shapes_ok = true;
-  if (h->shape[1].M == 0 || swr::march_smem_bytes(h->shape[1], h->NT, true, h->tc_hi) > 227 * 1024) shapes_ok = false;
-  for (int K = 2; K <= 3; K++)
-    if (h->shape[K].M == 0 || swr::march_smem_bytes(h->shape[K], h->NT, false, h->tc_hi) > 227 * 1024) h->shape[K].M = 0;
-  {
-    const char *me = getenv("SWR_MARCH");
-    if (!shapes_ok || (me && strcmp(me, "stream") == 0)) {
-      // too large for a resident cluster (or forced): stream the state through HBM
-      h->stream_march = true;
-      for (int K = 0; K <= 3; K++) h->shape[K] = {1, 256, 1, 1};
-    }
+  h->shape = swr::choose_march_shape(h->Nj, h->NT, h->tc_hi);
+  if (h->march_form == 1 || h->shape.M == 0 || swr::march_smem_bytes(h->shape, h->NT, true, h->tc_hi) > 227 * 1024) {
+    // too large for a resident cluster (or asked for): stream the state through HBM
+    h->stream_march = true;
+    h->shape = {1, 256, 1, 1};
   }
-  auto fail = [&](int s) { free_all(h); delete h; return s; };
   int s;
-  const size_t nx1 = (size_t)h->Nx + 1, ng = h->ng, NTt = h->NT;
+  const size_t nx1 = (size_t)h->Nx + 1, ng = h->ng, nloc = h->nloc, NTt = h->NT;
   const bool precond = h->algorithm == SWR_ALG_PRECOND;
   if ((s = dalloc(&h->u0, nx1)) || (s = dalloc(&h->beta, NTt + 1)) || (s = dalloc(&h->q, (size_t)h->N * h->Nj)) ||
       (s = dalloc(&h->er, (size_t)h->N * h->Nj)) || (s = dalloc(&h->uloc, (size_t)h->N * h->Nj)) ||
@@ -1199,7 +1538,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   }
   if ((s = dalloc(&h->fp_stat, 2))) return fail(s);
   if (cudaMemset(h->fp_stat, 0, 2 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_CUDA);
-  h->shape_nl = swr::choose_march_shape_nl(h->Nj);
+  h->shape_nl = swr::choose_march_shape_nl(h->Nj, h->nl_rows);
   if (h->potential == SWR_POT_CUBIC &&
       (h->shape_nl.M == 0 || swr::march_nl_smem_bytes(h->shape_nl, h->NT, true) > 227 * 1024)) {
     g_detail = "subdomain too large for the resident nonlinear march";
@@ -1208,54 +1547,58 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
   if (ng) {
     const size_t mm = std::max(h->restart + 1, 6);   // BiCGStab uses 6 of the basis slots
-    if ((s = dalloc(&h->d, ng)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, ng)) ||
-        (s = alloc_krylov(h->kout, mm, ng)) || (s = dalloc(&h->tmp, ng)) ||
-        (s = dalloc(&h->tmp2, ng)) || (s = dalloc(&h->rhs, ng)) || (s = dalloc(&h->partial, (mm + 2) * 148 * 4)) ||
-        false)
+    if ((s = dalloc(&h->d, nloc)) || (s = dalloc(&h->X, (size_t)h->N * 4 * NTt)) || (s = dalloc(&h->g, nloc)) ||
+        (s = alloc_krylov(h->kout, mm, nloc)) || (s = dalloc(&h->tmp, nloc)) || (s = dalloc(&h->tmp2, nloc)) ||
+        (s = dalloc(&h->rhs, nloc)) || (s = dalloc(&h->partial, (mm + 2) * (size_t)(2 * h->N))))
       return fail(s);
-    if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, ng))))
+    if (precond && ((s = dalloc(&h->X0, (size_t)h->N * 4 * NTt)) || (s = alloc_krylov(h->kin, mm, nloc))))
       return fail(s);
     if (precond && h->pinv_exact && (s = dalloc(&h->pinvF, (size_t)(2 * h->N - 2) * swr::PINV_B))) return fail(s);
-    if (cfg->g0 && (s = dalloc(&h->g0, ng))) return fail(s);
-    const char *tmode = getenv("SWR_TOEPLITZ");
-    h->log4 = (tmode && strcmp(tmode, "direct") == 0) ? 0 : swr::fft_log4_for(h->NT);
-    h->fft_fused = !(tmode && strcmp(tmode, "fft2") == 0);
-    // register FFT for NF = 1024 unless a Stockham form is requested
-    h->fft_reg = h->log4 == 5 && !(tmode && (strcmp(tmode, "fft2") == 0 || strcmp(tmode, "fftsm") == 0));
+    if (cfg->g0 && (s = dalloc(&h->g0, nloc))) return fail(s);
+    if (SWR_CGS_SEPARATE_REDUCE && h->world == 1 && (s = dalloc(&h->part_send, (mm + 2) * (size_t)(2 * h->N))))
+      return fail(s);
+    if (h->world > 1) {
+      if ((s = dalloc(&h->haloL, NTt)) || (s = dalloc(&h->haloR, NTt)) || (s = dalloc(&h->hrecvL, NTt)) ||
+          (s = dalloc(&h->hrecvR, NTt)) || (s = dalloc(&h->part_send, (mm + 2) * (size_t)(2 * h->N))) ||
+          (s = dalloc(&h->part_recv, (mm + 2) * (size_t)(2 * h->N))))
+        return fail(s);
+      if (precond && h->pinv_exact && ((s = dalloc(&h->pinv_y, ng)) || (s = dalloc(&h->pinv_x, ng)))) return fail(s);
+      // the other ranks' columns of the partials stay 0 (this rank writes its own only)
+      if (cudaMemset(h->part_send, 0, (mm + 2) * (size_t)(2 * h->N) * sizeof(double2)) != cudaSuccess)
+        return fail(SWR_ERR_CUDA);
+    }
+    h->smap = {h->N, h->NT, h->j_lo, h->j_hi, h->s_lo, h->s_hi, h->haloL, h->haloR};
+    // (I - L) apply: FFT convolution for N_T <= 512 (register form for NF =
+    // 1024), the direct causal convolution beyond or when asked for
+    h->log4 = h->toeplitz_form == 1 ? 0 : swr::fft_log4_for(h->NT);
+    h->fft_reg = h->log4 == 5 && h->toeplitz_form == 0;
     if (h->log4) {
       const size_t NF = (size_t)1 << (2 * h->log4);
       if ((s = dalloc(&h->tw, NF)) || (s = dalloc(&h->FX, (size_t)h->N * 4 * NF)) ||
-          (s = dalloc(&h->Fx, (size_t)(2 * h->N - 2) * NF)) || (precond && (s = dalloc(&h->FX0, (size_t)h->N * 4 * NF))))
+          (precond && (s = dalloc(&h->FX0, (size_t)h->N * 4 * NF))))
         return fail(s);
-      // set aside L2 for the transformed columns re-read by every (I - L) apply
-      // (device-wide limit, raised only; SWR_L2_PERSIST=0 leaves it alone)
-      const char *pe = getenv("SWR_L2_PERSIST");
-      if (!(pe && strcmp(pe, "0") == 0)) {
-        int maxp = 0;
-        size_t cur = 0;
-        cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
-        cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-        const size_t fxb = (size_t)h->N * 4 * NF * sizeof(double2);
-        // the first 4 outer basis vectors also persist (read by every CGS pass;
-        // measured: 0 / 3 / 4 / 5 / 6 / 8 vectors -> C5 solve 94.2 / 93.0 / 92.6 /
-        // 93.6 / 96.4 / 96.9 ms: more set-aside starves the streamed vectors)
-        const char *ve = getenv("SWR_V_PERSIST");
-        const int nvp = ve ? atoi(ve) : 4;
-        const size_t vb = (size_t)std::max(0, nvp) * ng * sizeof(double2);
-        const size_t want = std::min((size_t)maxp, fxb + vb);
-        if (want > cur) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-        cudaGetLastError();
-        if (vb > 0 && (size_t)maxp > fxb) {
-          h->vwin_bytes = vb;
-          h->vwin_ratio = (float)std::min(1.0, (double)((size_t)maxp - fxb) / (double)vb);
-        }
-        if (getenv("SWR_L2_VERBOSE"))
-          fprintf(stderr, "L2 persisting: max %d B, FX %zu B, V window %zu B ratio %.3f\n", maxp, fxb, h->vwin_bytes,
-                  h->vwin_ratio);
+      // set aside L2 for this rank's transformed columns, re-read by every (I - L)
+      // apply, and for the first 4 outer basis vectors, read by every CGS pass
+      // (measured: 0 / 3 / 4 / 5 / 6 / 8 vectors -> C5 solve 94.2 / 93.0 / 92.6 /
+      // 93.6 / 96.4 / 96.9 ms: more set-aside starves the streamed vectors)
+      int maxp = 0;
+      cudaDeviceGetAttribute(&maxp, cudaDevAttrMaxPersistingL2CacheSize, h->device);
+      const size_t fxb = (size_t)(h->j_hi - h->j_lo + 1) * 4 * NF * sizeof(double2);
+      const size_t vb = (size_t)4 * nloc * sizeof(double2);
+      h->l2_window = std::max<size_t>(1, std::min((size_t)maxp, fxb + vb));
+      l2_acquire(h->device, h->l2_window);
+      if ((size_t)maxp > fxb) {
+        h->vwin_bytes = vb;
+        h->vwin_ratio = (float)std::min(1.0, (double)((size_t)maxp - fxb) / (double)vb);
       }
+      if (getenv("SWR_VERBOSE"))
+        fprintf(stderr, "L2 persisting: max %d B, FX %zu B, V window %zu B ratio %.3f\n", maxp, fxb, h->vwin_bytes,
+                h->vwin_ratio);
       swr::k_twiddles<<<(unsigned)((NF + 255) / 256), 256, 0, h->st>>>(h->tw, (int)NF);
       if (cudaGetLastError() != cudaSuccess) return fail(SWR_ERR_CUDA);
     }
+  } else {
+    h->smap = {h->N, h->NT, h->j_lo, h->j_hi, 0, -1, nullptr, nullptr};
   }
   if (cudaMallocHost((void **)&h->hpin, sizeof(double2) * (3 * (h->restart + 1) + 16)) != cudaSuccess) return fail(SWR_ERR_OOM);
   if (h->counter && cudaMemset(h->counter, 0, sizeof(unsigned)) != cudaSuccess) return fail(SWR_ERR_CUDA);
@@ -1264,7 +1607,8 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   const bool od = cfg->inputs_on_device != 0;
   if ((s = copy_in(h->u0, cfg->u0, nx1, od, h->st))) return fail(s);
   if (h->Vx && (s = copy_in_r(h->Vx, cfg->V_x, nx1, od, h->st))) return fail(s);
-  if (h->g0 && (s = copy_in(h->g0, cfg->g0, ng, od, h->st))) return fail(s);
+  // g0: this rank's slots of the full initial interface vector
+  if (h->g0 && (s = copy_in(h->g0, cfg->g0 + 2 * (size_t)h->s_lo * h->NT, nloc, od, h->st))) return fail(s);
   // beta_s: alpha_0 = 1, alpha_{2k} = alpha_{2k-2}(2k-1)/(2k), alpha_{2k+1} = alpha_{2k}
   {
     std::vector<double> al(NTt + 1), be(NTt + 1);
@@ -1277,6 +1621,8 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       return fail(SWR_ERR_CUDA);
   }
   if ((s = factor_matrices(h))) return fail(s);
+  if (cudaStreamSynchronize(h->st) != cudaSuccess) return fail(SWR_ERR_CUDA);
+  h->t_setup_ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t_start).count();
   *out = h;
   return SWR_OK;
 }
@@ -1296,7 +1642,7 @@ int swr_update_inputs(swr_handle *h, const double *u0, const double *V_x, int32_
 
 int swr_build_interface_operator(swr_handle *h) {
   if (!h) return SWR_ERR_INVALID_ARG;
-  h->march_ev_used = h->intf_ev_used = 0;
+  h->march_ev_used = h->intf_ev_used = h->comm_ev_used = 0;
   h->n_marches = h->n_launches = 0;
   h->cell_steps = 0;
   CK(cudaEventRecord(h->ev_b0, h->st));
@@ -1311,7 +1657,7 @@ int swr_build_interface_operator(swr_handle *h) {
         h->have_d = true;
       }
     } else {
-      CKS(build_probes(h, true, h->X0, nullptr));  // L0: 2 RHS per subdomain
+      CKS(build_probes(h, true, h->X0, nullptr));  // L0: the probes of j = 1, 2, N
       CKS(transform_columns(h, true));
       h->have_L0 = true;
       if (h->pinv_exact) CKS(setup_pinv(h));
@@ -1329,7 +1675,7 @@ int swr_build_interface_operator(swr_handle *h) {
 int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep) {
   if (!h) return SWR_ERR_INVALID_ARG;
   if (!h->build_timed) {
-    h->march_ev_used = h->intf_ev_used = 0;
+    h->march_ev_used = h->intf_ev_used = h->comm_ev_used = 0;
     h->n_marches = h->n_launches = 0;
     h->cell_steps = 0;
   }
@@ -1342,8 +1688,8 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
   CK(cudaMemsetAsync(h->fp_stat, 0, 2 * sizeof(int), h->st));
   int st = SWR_OK;
   if (h->N > 1) {
-    if (h->g0) CK(cudaMemcpyAsync(h->g, h->g0, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
-    else CKS(fill_zero(h, h->g, h->ng));
+    if (h->g0) CK(cudaMemcpyAsync(h->g, h->g0, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+    else CKS(fill_zero(h, h->g, h->nloc));
     int it = 0, conv = 0;
     double2 *hp = h->hpin;
     // fixed point driver: g <- next(g), stop at ||g^{k+1} - g^k||_2 < tol (A5, A21);
@@ -1361,7 +1707,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
       }
       return SWR_OK;
     };
-    const dim3 gg(grid_for(h->ng)), bb(256);
+    const dim3 gg(grid_for(h->nloc)), bb(256);
     if (h->algorithm == SWR_ALG_NEW) {
       if (!h->have_L || !h->have_d) CKS(swr_build_interface_operator(h));
       Op A = [h](const double2 *a, double2 *b) { return apply_I_minus_L(h, false, a, b); };
@@ -1373,9 +1719,9 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         st = fixed_point([&]() -> int {
           CKS(apply_I_minus_L(h, false, h->g, h->tmp));
           CK(swr::launch_pdl(swr::k_lin2, gg, bb, 0, h->st, h->tmp2, make_double2(1, 0), (const double2 *)h->d,
-                             make_double2(-1, 0), (const double2 *)h->tmp, h->ng));
+                             make_double2(-1, 0), (const double2 *)h->tmp, h->nloc));
           CK(swr::launch_pdl(swr::k_axpby, gg, bb, 0, h->st, make_double2(1, 0), (const double2 *)h->tmp2,
-                             make_double2(1, 0), h->g, h->ng));
+                             make_double2(1, 0), h->g, h->nloc));
           h->n_launches += 2;
           return SWR_OK;
         });
@@ -1390,9 +1736,9 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         // Algorithm 1: g <- R(g) (with u0; R_nl for f(u))
         st = fixed_point([&]() -> int {
           CKS(sweep_R(h, h->g, true, false, h->tmp, nullptr));
-          swr::k_sub<<<gg, bb, 0, h->st>>>(h->tmp, h->g, h->tmp2, h->ng);
+          swr::k_sub<<<gg, bb, 0, h->st>>>(h->tmp, h->g, h->tmp2, h->nloc);
           CK(cudaGetLastError());
-          CK(cudaMemcpyAsync(h->g, h->tmp, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+          CK(cudaMemcpyAsync(h->g, h->tmp, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
           h->n_launches++;
           return SWR_OK;
         });
@@ -1401,7 +1747,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
         if (!h->have_d) CKS(swr_build_interface_operator(h));
         Op A = [h](const double2 *a, double2 *b) -> int {
           CKS(sweep_R(h, a, false, false, h->tmp, nullptr));
-          swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(a, h->tmp, b, h->ng);
+          swr::k_sub<<<grid_for(h->nloc), 256, 0, h->st>>>(a, h->tmp, b, h->nloc);
           CK(cudaGetLastError());
           h->n_launches++;
           return SWR_OK;
@@ -1416,14 +1762,14 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
       if (!h->have_L0) CKS(swr_build_interface_operator(h));
       st = fixed_point([&]() -> int {
         CKS(sweep_R(h, h->g, true, false, h->tmp, nullptr));
-        swr::k_sub<<<gg, bb, 0, h->st>>>(h->g, h->tmp, h->tmp2, h->ng);
+        swr::k_sub<<<gg, bb, 0, h->st>>>(h->g, h->tmp, h->tmp2, h->nloc);
         CK(cudaGetLastError());
         const int s2 = apply_Pinv(h, h->tmp2, h->tmp);
         if (s2 && s2 != SWR_ERR_INNER_NOT_CONVERGED) return s2;
-        swr::k_axpby<<<gg, bb, 0, h->st>>>(make_double2(-1.0, 0.0), h->tmp, make_double2(1.0, 0.0), h->g, h->ng);
+        swr::k_axpby<<<gg, bb, 0, h->st>>>(make_double2(-1.0, 0.0), h->tmp, make_double2(1.0, 0.0), h->g, h->nloc);
         CK(cudaGetLastError());
         // increment g^{k+1} - g^k = -P^{-1}(...): same norm as h->tmp
-        CK(cudaMemcpyAsync(h->tmp2, h->tmp, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+        CK(cudaMemcpyAsync(h->tmp2, h->tmp, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
         h->n_launches += 2;
         return s2;
       });
@@ -1432,7 +1778,7 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
       CKS(apply_Pinv(h, h->d, h->rhs));
       Op A = [h](const double2 *a, double2 *b) -> int {
         CKS(sweep_R(h, a, false, false, h->tmp, nullptr));
-        swr::k_sub<<<grid_for(h->ng), 256, 0, h->st>>>(a, h->tmp, h->tmp2, h->ng);
+        swr::k_sub<<<grid_for(h->nloc), 256, 0, h->st>>>(a, h->tmp, h->tmp2, h->nloc);
         CK(cudaGetLastError());
         return apply_Pinv(h, h->tmp2, b);
       };
@@ -1452,6 +1798,8 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
   if (u_T && h->rank == 0)
     CK(cudaMemcpyAsync(u_T, h->uT, ((size_t)h->Nx + 1) * sizeof(double2),
                        u_T_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyDeviceToHost, h->st));
+  // NL fixed-point statistics of all ranks' marches (max iterations, failure)
+  if (h->world > 1) CKS(h->comm->allreduce_max_i32(h->fp_stat, 2, h->st));
   CK(cudaStreamSynchronize(h->st));
   {
     int fs[2] = {0, 0};
@@ -1470,8 +1818,10 @@ int swr_solve(swr_handle *h, double *u_T, int32_t u_T_on_device, swr_report *rep
     float ms = 0;
     if (h->build_timed && cudaEventElapsedTime(&ms, h->ev_b0, h->ev_b1) == cudaSuccess) rep->t_build_ms = ms;
     if (cudaEventElapsedTime(&ms, h->ev_s0, h->ev_s1) == cudaSuccess) rep->t_solve_ms = ms;
-    rep->t_march_ms = sum_pairs(h, true);
-    rep->t_interface_ms = sum_pairs(h, false);
+    rep->t_march_ms = sum_pairs(h, EV_MARCH);
+    rep->t_interface_ms = sum_pairs(h, EV_INTF);
+    rep->t_comm_ms = sum_pairs(h, EV_COMM);
+    rep->t_setup_ms = h->t_setup_ms;
     rep->cell_steps = h->cell_steps;
     rep->n_marches = h->n_marches;
     rep->n_kernel_launches = h->n_launches;
@@ -1491,7 +1841,7 @@ void swr_free(swr_handle *h) {
 
 int swr_apply_R(swr_handle *h, const double *g, int32_t use_u0, int32_t force_zero_potential, double *Rg,
                 double *u_T) {
-  if (!h || h->N < 1) return SWR_ERR_INVALID_ARG;
+  if (!h || h->N < 1 || h->world > 1) return SWR_ERR_INVALID_ARG;
   if (force_zero_potential && !h->q0) return SWR_ERR_UNSUPPORTED;
   CKS(sweep_R(h, (const double2 *)g, use_u0 != 0, force_zero_potential != 0, (double2 *)Rg,
               u_T ? h->uloc : nullptr));
@@ -1499,14 +1849,13 @@ int swr_apply_R(swr_handle *h, const double *g, int32_t use_u0, int32_t force_ze
     swr::k_gather_uT<<<grid_for(h->Nx + 1), 256, 0, h->st>>>(h->uloc, h->N, h->m, h->Nj, h->j_lo, h->j_hi,
                                                              (double2 *)u_T);
     CK(cudaGetLastError());
-    CKS(allreduce_sum(h, (double2 *)u_T, (size_t)h->Nx + 1));
   }
   CK(cudaStreamSynchronize(h->st));
   return SWR_OK;
 }
 
 int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y) {
-  if (!h) return SWR_ERR_INVALID_ARG;
+  if (!h || h->world > 1) return SWR_ERR_INVALID_ARG;
   if ((which == 0 && !h->have_L) || (which == 1 && !h->have_L0)) return SWR_ERR_INVALID_ARG;
   CKS(apply_I_minus_L(h, which == 1, (const double2 *)x, (double2 *)y));
   CK(cudaStreamSynchronize(h->st));
@@ -1514,7 +1863,7 @@ int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y
 }
 
 int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X) {
-  if (!h) return SWR_ERR_INVALID_ARG;
+  if (!h || h->world > 1) return SWR_ERR_INVALID_ARG;
   if (d && h->have_d) CK(cudaMemcpyAsync(d, h->d, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
   const double2 *src = which ? h->X0 : h->X;
   if (X && src) CK(cudaMemcpyAsync(X, src, (size_t)h->N * 4 * h->NT * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
@@ -1524,7 +1873,7 @@ int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X) {
 
 int swr_get_g(swr_handle *h, double *g) {
   if (!h || !h->have_g) return SWR_ERR_INVALID_ARG;
-  CK(cudaMemcpyAsync(g, h->g, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemcpyAsync(g, h->g, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
   CK(cudaStreamSynchronize(h->st));
   return SWR_OK;
 }

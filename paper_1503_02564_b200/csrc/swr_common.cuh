@@ -42,8 +42,57 @@ __device__ __forceinline__ double2 shfl_down2(double2 v, int o) {
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 
+// Race-stress builds (-DSWR_RACE_STRESS=1, tests/test_race_stress.py; the
+// compute-sanitizer is closed on this pool): a pseudo-random delay of up to
+// ~2 us for a quarter of the (warp, step, site) points of the cluster / chain
+// kernels perturbs how their CTAs interleave; every result must stay bitwise
+// equal to the normal build, or an ordering between CTAs is missing.
+#ifndef SWR_RACE_STRESS
+#define SWR_RACE_STRESS 0
+#endif
+__device__ __forceinline__ void race_jitter(unsigned site, unsigned step) {
+#if SWR_RACE_STRESS
+  unsigned h = (blockIdx.x * 0x9E3779B1u) ^ ((threadIdx.x >> 5) * 0x85EBCA6Bu) ^ (step * 0xC2B2AE35u) ^
+               (site * 0x27D4EB2Fu);
+  h ^= h >> 15;
+  h *= 0x2C1B3C6Du;
+  h ^= h >> 12;
+  if ((h & 3u) == 0u) __nanosleep((h >> 20) & 2047u);
+#else
+  (void)site;
+  (void)step;
+#endif
+}
+
 __device__ __forceinline__ double2 shfl_xor2(double2 v, int o) {
   return make_double2(__shfl_xor_sync(0xffffffffu, v.x, o), __shfl_xor_sync(0xffffffffu, v.y, o));
+}
+
+// ---- interface-vector layout of one rank -------
+// Slots of g: l_j = 2j-3 (j >= 2), r_j = 2j-2 (j <= N-1).  A rank
+// owns subdomains [j_lo, j_hi] and their slots [s_lo, s_hi] = [slot_first(j_lo),
+// slot_last(j_hi)] (contiguous); its interface vectors hold those slots only
+// (slot s at local offset (s - s_lo) N_T).  Every owned slot is an input of an
+// owned subdomain; the two outputs of owned subdomains that land in a
+// neighbour's slot, r_{j_lo - 1} (= s_lo - 1) and l_{j_hi + 1} (= s_hi + 1), go to
+// the halo buffers and cross the rank cut (the "cut traces").
+struct SlotMap {
+  int32_t N, NT, j_lo, j_hi, s_lo, s_hi;
+  double2 *haloL, *haloR;   // [N_T] each, nullptr where there is no neighbour rank
+};
+__host__ __device__ __forceinline__ int slot_first(int j) { return j >= 2 ? 2 * j - 3 : 0; }
+__host__ __device__ __forceinline__ int slot_last(int j, int N) { return j <= N - 1 ? 2 * j - 2 : 2 * N - 3; }
+// slot s of the local vector v (nullptr if another rank owns it)
+template <typename T>
+__host__ __device__ __forceinline__ T *slot_ptr(const SlotMap &m, T *v, int s) {
+  return (s >= m.s_lo && s <= m.s_hi) ? v + (size_t)(s - m.s_lo) * m.NT : nullptr;
+}
+// where output slot o of an owned subdomain goes: the local slot, or the halo
+// buffer of the neighbour rank that owns it (remote = true)
+__host__ __device__ __forceinline__ double2 *out_ptr(const SlotMap &m, double2 *v, int o, bool &remote) {
+  remote = !(o >= m.s_lo && o <= m.s_hi);
+  if (!remote) return v + (size_t)(o - m.s_lo) * m.NT;
+  return o < m.s_lo ? m.haloL : m.haloR;
 }
 
 // ---- one whole-window march of one system (subdomain j, one RHS) ---------

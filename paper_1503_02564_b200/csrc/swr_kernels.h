@@ -58,7 +58,8 @@ struct FactorJob {
 
 __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, double dt, double2 c0, int *err);
 constexpr int TR = 8;  // outputs per thread of the Toeplitz kernel (N_T = 500: 32 threads per output slot)
-__global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, int N, int NT);
+__global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, const SlotMap m);
+__global__ void k_halo_add(const double2 *x, const double2 *h, double2 *y, int NT, const double2 *xs);
 __global__ void k_multi_axpy(const double2 *V, size_t ldv, int nvec, const double2 *h, double2 *w, size_t n);
 __global__ void k_axpby(double2 a, const double2 *x, double2 b, double2 *y, size_t n);
 __global__ void k_lin2(double2 *z, double2 a, const double2 *x, double2 b, const double2 *y, size_t n);
@@ -69,42 +70,44 @@ __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);
 __global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const double2 *y, double2 *x, size_t n);
 __global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, int j_lo, int j_hi, double2 *uT);
 __global__ void k_fill(double2 *x, double2 v, size_t n);
+__global__ void k_replicate(const double2 *src, double2 *dst, size_t blk, size_t count);
+__global__ void k_add_f64(double *y, const double *x, size_t n);
 
 // CGS_REV: walk the element chunks from the end (alternating directions
 // between consecutive passes keeps the last-read part of V hot in L2)
 enum : int { CGS_AXPY = 1, CGS_DOTS = 2, CGS_NORM = 4, CGS_SCALE = 8, CGS_REV = 16 };
-cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
+cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, const SlotMap &m, const double2 *tw,
                                 cudaStream_t st, const double2 *xs = nullptr, double2 *xcopy = nullptr);
-// y = (I - L) x with two warps per 1024-point transform (swr_fft_halves.cu)
-cudaError_t launch_fft_conv_h(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
-                              cudaStream_t st, const double2 *xs, double2 *xcopy, size_t l2_window);
 size_t l2_persist_bytes();
 // exact P^{-1} by causal forward substitution (swr_pinv.cu), time blocks of PINV_B steps
 constexpr int PINV_B = 16;
 cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, double2 *F, int N, int NT,
                                int sweeps, cudaStream_t st, int *n_launches);
+// out == nullptr: unit partials only (multi-GPU; reduced by launch_cgs_reduce
+// after the exchange); partial is [nred][N]
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
+                       const SlotMap &m, double2 *partial, double2 *out, unsigned *counter, cudaStream_t st,
                        double2 *out_host = nullptr, size_t vwin = 0, float vratio = 1.0f);
+int cgs_units_global(const SlotMap &m);   // columns of the partials (units of the fixed-order sums)
+cudaError_t launch_cgs_reduce(const double2 *partial, int nu, int nred, int mode, double2 *out, double2 *out_host,
+                              cudaStream_t st);
 __global__ void k_scale_dev(const double2 *x, const double2 *sp, double2 *y, size_t n);
 
 int fft_log4_for(int NT);
-cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
+cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, const SlotMap &m,
                             const double2 *tw, cudaStream_t st);
 __global__ void k_twiddles(double2 *tw, int NF);
 cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int count, int NT, const double2 *tw,
                            double2 *F, cudaStream_t st);
-cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, const double2 *x, double2 *y, int N,
-                             int NT, const double2 *tw, cudaStream_t st);
 
 struct MarchShape { int M, P, CS, K; };
-MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi = false);
+MarchShape choose_march_shape(int Nj, int NT, bool tc_hi = false);
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem, bool tc_hi = false);
 cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
 size_t march_stream_smem_bytes(int NT);
-cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, double2 *zst, int *flags, double2 *vals,
-                                cudaStream_t st);
-MarchShape choose_march_shape_nl(int Nj);
+cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst, int *flags,
+                                double2 *vals, cudaStream_t st);
+MarchShape choose_march_shape_nl(int Nj, int rows = 0);
 size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st);
 __global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, double h, double dt, double2 c0,

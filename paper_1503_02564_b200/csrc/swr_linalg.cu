@@ -131,24 +131,28 @@ __global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, do
 // Each thread accumulates TR consecutive outputs over blocks of TR input
 // samples (2TR-1 column values and TR inputs per block in registers) and
 // takes output groups g and G-1-g so the triangular work is balanced.
-// X is [N][4][NT] (subdomain-major), g slot-major.
+// X is [N][4][NT] (subdomain-major), x and y the rank's slots (SlotMap):
+// one CTA per owned subdomain j = j_lo + blockIdx.x; an output slot owned by
+// the neighbour rank receives -(L x) in the halo buffer (the owner adds x).
 // ---------------------------------------------------------------------------
 __global__ void k_toeplitz_I_minus_L(const double2 *__restrict__ X, const double2 *__restrict__ x,
-                                     double2 *__restrict__ y, int N, int NT) {
+                                     double2 *__restrict__ y, const SlotMap m) {
   extern __shared__ double2 ts[];
-  const int j = blockIdx.x + 1;
+  const int N = m.N, NT = m.NT;
+  const int j = m.j_lo + blockIdx.x;
   const int CL = NT + 3 * TR, IL = NT + TR;
   double2 *cbase = ts + 2 * TR;                       // 4 columns, stride CL, index range [-2TR, NT+TR)
   double2 *il = ts + 4 * CL, *ir = il + IL;           // inputs l_j, r_j, index range [0, NT+TR)
-  const int sl = (j >= 2) ? 2 * j - 3 : -1, sr = (j <= N - 1) ? 2 * j - 2 : -1;
+  const double2 *xl = (j >= 2) ? slot_ptr(m, x, 2 * j - 3) : nullptr;
+  const double2 *xr = (j <= N - 1) ? slot_ptr(m, x, 2 * j - 2) : nullptr;
   const double2 *Xj = X + (size_t)(j - 1) * 4 * NT;
   for (int n = threadIdx.x - 2 * TR; n < NT + TR; n += blockDim.x) {
     const bool in = n >= 0 && n < NT;
 #pragma unroll
     for (int pcol = 0; pcol < 4; pcol++) cbase[pcol * CL + n] = in ? Xj[(size_t)pcol * NT + n] : cz();
     if (n >= 0) {
-      il[n] = (in && sl >= 0) ? x[(size_t)sl * NT + n] : cz();
-      ir[n] = (in && sr >= 0) ? x[(size_t)sr * NT + n] : cz();
+      il[n] = (in && xl) ? xl[n] : cz();
+      ir[n] = (in && xr) ? xr[n] : cz();
     }
   }
   __syncthreads();
@@ -158,8 +162,9 @@ __global__ void k_toeplitz_I_minus_L(const double2 *__restrict__ X, const double
   const int o = half == 0 ? 2 * j - 4 : 2 * j - 1;    // r_{j-1} or l_{j+1}
   if ((half == 0 && j < 2) || (half == 1 && j > N - 1)) return;
   const double2 *c1 = cbase + (half == 0 ? 0 : 2) * CL, *c2 = c1 + CL;   // (X^{j,1},X^{j,2}) or (X^{j,3},X^{j,4})
-  const double2 *xo = x + (size_t)o * NT;
-  double2 *yo = y + (size_t)o * NT;
+  bool remote;
+  double2 *yo = out_ptr(m, y, o, remote);
+  const double2 *xo = remote ? nullptr : slot_ptr(m, x, o);
   for (int pass = 0; pass < 2; pass++) {
     const int g = pass == 0 ? t : G - 1 - t;
     if (pass == 1 && g == t) break;
@@ -191,7 +196,7 @@ __global__ void k_toeplitz_I_minus_L(const double2 *__restrict__ X, const double
     for (int r = 0; r < TR; r++) {
       const int n = n0 + r;
       if (n < NT) {
-        const double2 xv = xo[n];
+        const double2 xv = xo ? xo[n] : cz();
         yo[n] = make_double2(xv.x - acc[r].x, xv.y - acc[r].y);
       }
     }
@@ -202,8 +207,8 @@ __global__ void k_toeplitz_I_minus_L(const double2 *__restrict__ X, const double
 // FFT form of the same operator (the causal convolutions of Props. 3-4 as
 // zero-padded cyclic convolutions of length NF = 4^LOG4 >= 2 N_T - 1).
 // Radix-4 Stockham FFT in shared memory, one CTA per sequence, NF/4 threads.
-//   k_fft_fwd:   F[q] = FFT(pad(src[q]))           (inputs slots; columns at build)
-//   k_fft_apply: y_o  = x_o - IFFT(Fc_a .* Fx_a + Fc_b .* Fx_b)[0:N_T]
+//   k_fft_fwd:   F[q] = FFT(pad(src[q]))           (the first columns, at build)
+//   k_fft_conv:  y_o  = x_o - IFFT(Fc_a .* FFT(x_a) + Fc_b .* FFT(x_b))[0:N_T]
 // ---------------------------------------------------------------------------
 template <int LOG4>
 __device__ __forceinline__ void fft4_stockham(double2 *a, double2 *b, const double2 *__restrict__ tw, bool inverse) {
@@ -253,53 +258,28 @@ __global__ void k_fft_fwd(const double2 *__restrict__ src, size_t src_stride, in
   for (int i = threadIdx.x; i < NF; i += Q) f[i] = a[i];
 }
 
-// Fx: [2N-2][NF] transforms of the input slots; Fc: [N][4][NF] of the columns.
-template <int LOG4>
-__global__ void k_fft_apply(const double2 *__restrict__ Fc, const double2 *__restrict__ Fx,
-                            const double2 *__restrict__ x, double2 *__restrict__ y, int N, int NT,
-                            const double2 *__restrict__ tw) {
-  constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
-  __shared__ double2 a[NF], b[NF];
-  const int o = blockIdx.x;
-  int j, p1, p2, s1, s2;
-  if ((o & 1) == 0) { j = o / 2 + 2; p1 = 0; s1 = 2 * j - 3; p2 = 1; s2 = (j <= N - 1) ? 2 * j - 2 : -1; }
-  else { j = (o + 1) / 2; p1 = 2; s1 = (j >= 2) ? 2 * j - 3 : -1; p2 = 3; s2 = 2 * j - 2; }
-  const double2 *c1 = Fc + ((size_t)(j - 1) * 4 + p1) * NF, *c2 = Fc + ((size_t)(j - 1) * 4 + p2) * NF;
-  for (int i = threadIdx.x; i < NF; i += Q) {
-    double2 acc = cz();
-    if (s1 >= 0) acc = cmul(c1[i], Fx[(size_t)s1 * NF + i]);
-    if (s2 >= 0) acc = cfma(c2[i], Fx[(size_t)s2 * NF + i], acc);
-    a[i] = acc;
-  }
-  __syncthreads();
-  fft4_stockham<LOG4>(a, b, tw, true);
-  const double inv = 1.0 / NF;
-  const double2 *xo = x + (size_t)o * NT;
-  double2 *yo = y + (size_t)o * NT;
-  for (int n = threadIdx.x; n < NT; n += Q) {
-    const double2 xv = xo[n];
-    yo[n] = make_double2(fma(-inv, a[n].x, xv.x), fma(-inv, a[n].y, xv.y));
-  }
-}
-
-// Fused form: one CTA per output slot transforms its (<= 2) input slots
-// itself (no transformed-input round trip through HBM), multiplies by the
-// transformed columns, and inverse-transforms.
+// One CTA per output of an owned subdomain (blockIdx = 2 b + side, j = j_lo +
+// b; side 0: r_{j-1} from X^{j,1}, X^{j,2}; side 1: l_{j+1} from X^{j,3},
+// X^{j,4}) transforms the (<= 2) input slots l_j, r_j itself, multiplies by
+// the transformed columns and inverse-transforms; an output owned by the
+// neighbour rank receives -(L x) in the halo buffer.
 template <int LOG4>
 __global__ void k_fft_conv(const double2 *__restrict__ Fc, const double2 *__restrict__ x, double2 *__restrict__ y,
-                           int N, int NT, const double2 *__restrict__ tw) {
+                           const SlotMap m, const double2 *__restrict__ tw) {
   pdl_wait();
   pdl_trigger();
   constexpr int NF = 1 << (2 * LOG4), Q = NF / 4;
   extern __shared__ double2 fs[];
   double2 *a1 = fs, *a2 = fs + NF, *bb = fs + 2 * NF;   // two transforms + scratch
-  const int o = blockIdx.x;
-  int j, p1, p2, s1, s2;
-  if ((o & 1) == 0) { j = o / 2 + 2; p1 = 0; s1 = 2 * j - 3; p2 = 1; s2 = (j <= N - 1) ? 2 * j - 2 : -1; }
-  else { j = (o + 1) / 2; p1 = 2; s1 = (j >= 2) ? 2 * j - 3 : -1; p2 = 3; s2 = 2 * j - 2; }
+  const int N = m.N, NT = m.NT;
+  const int j = m.j_lo + (int)(blockIdx.x >> 1), side = blockIdx.x & 1;
+  if ((side == 0 && j < 2) || (side == 1 && j > N - 1)) return;
+  const int o = side == 0 ? 2 * j - 4 : 2 * j - 1, p1 = 2 * side, p2 = 2 * side + 1;
+  const double2 *x1 = j >= 2 ? slot_ptr(m, x, 2 * j - 3) : nullptr;       // l_j
+  const double2 *x2 = j <= N - 1 ? slot_ptr(m, x, 2 * j - 2) : nullptr;   // r_j
   for (int i = threadIdx.x; i < NF; i += Q) {
-    a1[i] = (s1 >= 0 && i < NT) ? x[(size_t)s1 * NT + i] : cz();
-    a2[i] = (s2 >= 0 && i < NT) ? x[(size_t)s2 * NT + i] : cz();
+    a1[i] = (x1 && i < NT) ? x1[i] : cz();
+    a2[i] = (x2 && i < NT) ? x2[i] : cz();
   }
   __syncthreads();
   fft4_stockham<LOG4>(a1, bb, tw, false);
@@ -307,17 +287,18 @@ __global__ void k_fft_conv(const double2 *__restrict__ Fc, const double2 *__rest
   const double2 *c1 = Fc + ((size_t)(j - 1) * 4 + p1) * NF, *c2 = Fc + ((size_t)(j - 1) * 4 + p2) * NF;
   for (int i = threadIdx.x; i < NF; i += Q) {
     double2 acc = cz();
-    if (s1 >= 0) acc = cmul(__ldg(c1 + i), a1[i]);
-    if (s2 >= 0) acc = cfma(__ldg(c2 + i), a2[i], acc);
+    if (x1) acc = cmul(__ldg(c1 + i), a1[i]);
+    if (x2) acc = cfma(__ldg(c2 + i), a2[i], acc);
     a1[i] = acc;
   }
   __syncthreads();
   fft4_stockham<LOG4>(a1, bb, tw, true);
   const double inv = 1.0 / NF;
-  const double2 *xo = x + (size_t)o * NT;
-  double2 *yo = y + (size_t)o * NT;
+  bool remote;
+  double2 *yo = out_ptr(m, y, o, remote);
+  const double2 *xo = remote ? nullptr : slot_ptr(m, x, o);
   for (int n = threadIdx.x; n < NT; n += Q) {
-    const double2 xv = xo[n];
+    const double2 xv = xo ? xo[n] : cz();
     yo[n] = make_double2(fma(-inv, a1[n].x, xv.x), fma(-inv, a1[n].y, xv.y));
   }
 }
@@ -413,25 +394,27 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const doub
 // (optional) receives s * x — the GMRES step normalises its new basis vector
 // here instead of in a separate pass.
 __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
-                                                     double2 *__restrict__ y, int N, int NT,
+                                                     double2 *__restrict__ y, const SlotMap m,
                                                      const double2 *__restrict__ tw, const double2 *__restrict__ xs,
                                                      double2 *__restrict__ xcopy) {
   pdl_wait();
   pdl_trigger();
   constexpr int NF = 1024;
   extern __shared__ double2 fsm[];
+  const int N = m.N, NT = m.NT;
   const int q = threadIdx.x >> 5, lane = threadIdx.x & 31;
   double2 *T = fsm + q * (32 * 33);        // per-warp transpose buffer, also the spectrum exchange
-  const int j = blockIdx.x + 1;
+  const int j = m.j_lo + blockIdx.x;       // owned subdomain
   const int sidx = q == 0 ? 2 * j - 3 : 2 * j - 2;
   const bool has_in = q == 0 ? j >= 2 : j <= N - 1;
+  const size_t ioff = has_in ? (size_t)(sidx - m.s_lo) * NT : 0;   // input slots are always owned
   const double sx = xs ? xs->x : 1.0;
   double2 v[32];
 #pragma unroll
   for (int n2 = 0; n2 < 32; n2++) {
     const int n = lane + 32 * n2;
-    v[n2] = (n2 < 16 && has_in && n < NT) ? cscale(sx, x[(size_t)sidx * NT + n]) : cz();
-    if (xcopy && n2 < 16 && has_in && n < NT) xcopy[(size_t)sidx * NT + n] = v[n2];
+    v[n2] = (n2 < 16 && has_in && n < NT) ? cscale(sx, x[ioff + n]) : cz();
+    if (xcopy && n2 < 16 && has_in && n < NT) xcopy[ioff + n] = v[n2];
   }
   fftr::fft1024<false, true>(v, T, tw, lane);
   // spectra of l_j (warp 0) and r_j (warp 1) in the own buffer (natural
@@ -461,24 +444,34 @@ __global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restric
   if (!has_out) return;
   fftr::fft1024<true, false>(v, T, tw, lane);
   const double inv = 1.0 / NF;
-  const double2 *xo = x + (size_t)o * NT;
-  double2 *yo = y + (size_t)o * NT;
+  bool remote;   // an output owned by the neighbour rank gets -(L s x) only (the owner adds s x)
+  double2 *yo = out_ptr(m, y, o, remote);
+  // the x loads stay unconditional (the compiler issues them ahead of the
+  // inverse transform); a remote output reads the first owned slot, times 0
+  const double2 *xo = remote ? x : slot_ptr(m, x, o);
+  const double so = remote ? 0.0 : sx;
 #pragma unroll
   for (int k1 = 0; k1 < 16; k1++) {
     const int n = lane + 32 * k1;
     if (n < NT) {
-      const double2 xv = cscale(sx, xo[n]), a = v[fftr::br5(k1)];
+      const double2 xv = cscale(so, xo[n]), a = v[fftr::br5(k1)];
       yo[n] = make_double2(fma(-inv, a.x, xv.x), fma(-inv, a.y, xv.y));
     }
   }
 }
 
-// Bytes of L2 set aside for persisting accesses on the current device (0: none;
-// SWR_L2_PERSIST=0 disables the window).
+// Owner side of a cut trace after the exchange: y_s = sx x_s + h (h = -(L x)_s
+// computed by the neighbour rank), sx = xs->x or 1.
+__global__ void k_halo_add(const double2 *__restrict__ x, const double2 *__restrict__ h, double2 *__restrict__ y,
+                           int NT, const double2 *__restrict__ xs) {
+  const double sx = xs ? xs->x : 1.0;
+  for (int n = blockIdx.x * blockDim.x + threadIdx.x; n < NT; n += gridDim.x * blockDim.x)
+    y[n] = cadd(cscale(sx, x[n]), h[n]);
+}
+
+// Bytes of L2 set aside for persisting accesses on the current device (0: none).
 size_t l2_persist_bytes() {
   static size_t v = [] {
-    const char *e = getenv("SWR_L2_PERSIST");
-    if (e && strcmp(e, "0") == 0) return (size_t)0;
     size_t lim = 0;
     if (cudaDeviceGetLimit(&lim, cudaLimitPersistingL2CacheSize) != cudaSuccess) return (size_t)0;
     return lim;
@@ -486,10 +479,11 @@ size_t l2_persist_bytes() {
   return v;
 }
 
-cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, int N, int NT, const double2 *tw,
+cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y, const SlotMap &m, const double2 *tw,
                                 cudaStream_t st, const double2 *xs, double2 *xcopy) {
+  const int N = m.N;
   if (N < 2) return cudaSuccess;
-  if (NT > 512) return cudaErrorInvalidValue;
+  if (m.NT > 512) return cudaErrorInvalidValue;
   const size_t smem = (2 * 32 * 33) * sizeof(double2);
   cudaError_t e = cudaFuncSetAttribute(k_fft_conv_reg, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -497,7 +491,7 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   // every apply: ask L2 to keep them (persisting window; the Krylov vectors
   // streamed between applies are normal accesses and do not evict them)
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(N);
+  cfg.gridDim = dim3(m.j_hi - m.j_lo + 1);
   cfg.blockDim = dim3(64);
   cfg.dynamicSmemBytes = smem;
   cfg.stream = st;
@@ -505,8 +499,8 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   at[0].val.programmaticStreamSerializationAllowed = 1;
   at[1].id = cudaLaunchAttributeAccessPolicyWindow;
-  at[1].val.accessPolicyWindow.base_ptr = const_cast<double2 *>(Fc);
-  at[1].val.accessPolicyWindow.num_bytes = (size_t)N * 4 * 1024 * sizeof(double2);
+  at[1].val.accessPolicyWindow.base_ptr = const_cast<double2 *>(Fc + (size_t)(m.j_lo - 1) * 4 * 1024);
+  at[1].val.accessPolicyWindow.num_bytes = (size_t)(m.j_hi - m.j_lo + 1) * 4 * 1024 * sizeof(double2);
   at[1].val.accessPolicyWindow.hitRatio = 1.0f;
   at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
   at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
@@ -515,22 +509,22 @@ cudaError_t launch_fft_conv_reg(const double2 *Fc, const double2 *x, double2 *y,
   if (cfg.numAttrs == 2 && at[1].val.accessPolicyWindow.num_bytes > l2_persist_bytes()) {
     at[1].val.accessPolicyWindow.hitRatio = (float)l2_persist_bytes() / (float)at[1].val.accessPolicyWindow.num_bytes;
   }
-  return cudaLaunchKernelEx(&cfg, k_fft_conv_reg, Fc, x, y, N, NT, tw, xs, xcopy);
+  return cudaLaunchKernelEx(&cfg, k_fft_conv_reg, Fc, x, y, m, tw, xs, xcopy);
 }
 
-cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, int N, int NT,
+cudaError_t launch_fft_conv(int log4, const double2 *Fc, const double2 *x, double2 *y, const SlotMap &m,
                             const double2 *tw, cudaStream_t st) {
-  if (N < 2) return cudaSuccess;
-  const int nslots = 2 * N - 2;
+  if (m.N < 2) return cudaSuccess;
+  const int nblk = 2 * (m.j_hi - m.j_lo + 1);
   const size_t smem = 3 * ((size_t)1 << (2 * log4)) * sizeof(double2);
   switch (log4) {
-    case 2: k_fft_conv<2><<<nslots, 4, smem, st>>>(Fc, x, y, N, NT, tw); break;
-    case 3: k_fft_conv<3><<<nslots, 16, smem, st>>>(Fc, x, y, N, NT, tw); break;
-    case 4: k_fft_conv<4><<<nslots, 64, smem, st>>>(Fc, x, y, N, NT, tw); break;
+    case 2: k_fft_conv<2><<<nblk, 4, smem, st>>>(Fc, x, y, m, tw); break;
+    case 3: k_fft_conv<3><<<nblk, 16, smem, st>>>(Fc, x, y, m, tw); break;
+    case 4: k_fft_conv<4><<<nblk, 64, smem, st>>>(Fc, x, y, m, tw); break;
     case 5: {
       cudaError_t e = cudaFuncSetAttribute(k_fft_conv<5>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
       if (e != cudaSuccess) return e;
-      k_fft_conv<5><<<nslots, 256, smem, st>>>(Fc, x, y, N, NT, tw);
+      k_fft_conv<5><<<nblk, 256, smem, st>>>(Fc, x, y, m, tw);
       break;
     }
     default: return cudaErrorInvalidValue;
@@ -561,20 +555,6 @@ cudaError_t launch_fft_fwd(int log4, const double2 *src, size_t stride, int coun
     case 3: k_fft_fwd<3><<<count, 16, 0, st>>>(src, stride, NT, tw, F); break;
     case 4: k_fft_fwd<4><<<count, 64, 0, st>>>(src, stride, NT, tw, F); break;
     case 5: k_fft_fwd<5><<<count, 256, 0, st>>>(src, stride, NT, tw, F); break;
-    default: return cudaErrorInvalidValue;
-  }
-  return cudaGetLastError();
-}
-
-cudaError_t launch_fft_apply(int log4, const double2 *Fc, const double2 *Fx, const double2 *x, double2 *y, int N,
-                             int NT, const double2 *tw, cudaStream_t st) {
-  if (N < 2) return cudaSuccess;
-  const int nslots = 2 * N - 2;
-  switch (log4) {
-    case 2: k_fft_apply<2><<<nslots, 4, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
-    case 3: k_fft_apply<3><<<nslots, 16, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
-    case 4: k_fft_apply<4><<<nslots, 64, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
-    case 5: k_fft_apply<5><<<nslots, 256, 0, st>>>(Fc, Fx, x, y, N, NT, tw); break;
     default: return cudaErrorInvalidValue;
   }
   return cudaGetLastError();
@@ -671,121 +651,69 @@ __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nv
 }
 
 // ---------------------------------------------------------------------------
-// Fused CGS kernel over the interface vector (n_g complex entries):
+// Fused classical Gram-Schmidt passes on the rank's interface slots (SlotMap):
 //   mode & CGS_AXPY : w -= sum_v h_v V_v          (h from the device, v < nv)
 //   mode & CGS_DOTS : p_v = <V_v, w>              (v < nv, after the axpy)
 //   mode & CGS_NORM : p_nv = <w, w>
-// Persistent grid over chunks of 32*KE entries.  The 4 warps of a CTA split
-// the basis vectors (warp q holds v = q, q+4, ...; lane holds entries
-// lane + 32 kk) so each basis value is loaded from HBM exactly once per call
-// and kept in registers between the axpy and the dots; the axpy partials of
-// the 4 warps meet in shared memory (fixed summation order).  Per-CTA dot
-// partials are reduced in a fixed tree; the last CTA sums them over CTAs in a
-// fixed order (deterministic) into out[0..nv]; with CGS_SCALE it also stores
-// 1/sqrt(out[nv]) in out[nv+1].
+// Order-fixed reductions that do not depend on the sharding: the unit of a
+// partial sum is one subdomain j (its slots l_j, r_j, contiguous and owned by
+// j's rank).  A unit is processed by one CTA in a fixed
+// order (chunks in sequence per lane, a fixed lane tree, warps in order) and
+// its partials land in column j-1 of partial[nred][N]; the N unit partials of
+// every quantity are then summed by reduce_units in a fixed order -- by the
+// last CTA of the pass on one GPU, or after the partials of all ranks were
+// exchanged (out == nullptr here; k_cgs_reduce).  One GPU and G GPUs give
+// bitwise the same scalars.
+// k_cgs: the 4 warps of a CTA split the basis vectors (warp q holds v = q,
+// q+4, ...; lane holds entries lane + 32 kk of a chunk) so each basis value is
+// loaded from HBM once per pass and kept in registers between the axpy and the
+// dots; the axpy partials of the 4 warps meet in shared memory (fixed order).
 // ---------------------------------------------------------------------------
-template <int VPW, int KE>
-__global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
-                                                const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
-                                                double2 *__restrict__ partial, double2 *__restrict__ out,
-                                                unsigned *counter, int N, int NT, double2 *__restrict__ out_host) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int NVMAX = 4 * VPW, CH = 32 * KE;
-  __shared__ double2 red[NVMAX + 1][4];
-  __shared__ double2 sh[NVMAX];
-  __shared__ double2 part[4][CH];
-  __shared__ bool last;
-  const size_t ntot = (size_t)(2 * N - 2) * NT;
-  const size_t nch = (ntot + CH - 1) / CH;
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
-  if (axpy)
-    for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
-  __syncthreads();
-  double2 acc[VPW];
-#pragma unroll
-  for (int i = 0; i < VPW; i++) acc[i] = cz();
-  double nacc = 0.0;
-  const bool rev = mode & CGS_REV;
-  for (size_t ci = blockIdx.x; ci < nch; ci += gridDim.x) {
-    const size_t c = rev ? nch - 1 - ci : ci;
-    const size_t base = c * CH + lane;
-    double2 x[VPW][KE], we[KE];
-#pragma unroll
-    for (int i = 0; i < VPW; i++) {
-      const int v = wp + 4 * i;
-#pragma unroll
-      for (int k = 0; k < KE; k++) {
-        const size_t e = base + 32 * k;
-        x[i][k] = (v < nv && e < ntot) ? V[(size_t)v * ldv + e] : cz();
-      }
-    }
-#pragma unroll
-    for (int k = 0; k < KE; k++) {
-      const size_t e = base + 32 * k;
-      we[k] = e < ntot ? w[e] : cz();
-    }
-    if (axpy) {
-#pragma unroll
-      for (int k = 0; k < KE; k++) {
-        double2 p = cz();
-#pragma unroll
-        for (int i = 0; i < VPW; i++)
-          if (wp + 4 * i < nv) p = cfma(sh[wp + 4 * i], x[i][k], p);
-        part[wp][lane + 32 * k] = p;
-      }
-      __syncthreads();
-#pragma unroll
-      for (int k = 0; k < KE; k++) {
-        const int t = lane + 32 * k;
-        const double2 p = cadd(cadd(cadd(part[0][t], part[1][t]), part[2][t]), part[3][t]);
-        we[k] = csub(we[k], p);
-        const size_t e = base + 32 * k;
-        if (wp == 0 && e < ntot) w[e] = we[k];
-      }
-      __syncthreads();
-    }
-    if (dots) {
-#pragma unroll
-      for (int i = 0; i < VPW; i++)
-#pragma unroll
-        for (int k = 0; k < KE; k++) acc[i] = cfmaconj(x[i][k], we[k], acc[i]);
-    }
-    if (norm && wp == 0) {
-#pragma unroll
-      for (int k = 0; k < KE; k++) nacc = fma(we[k].x, we[k].x, fma(we[k].y, we[k].y, nacc));
-    }
-  }
-  const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
-  if (dots) {
-#pragma unroll
-    for (int i = 0; i < VPW; i++) {
-      const int v = wp + 4 * i;
-      double2 a = acc[i];
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) a = cadd(a, shfl_down2(a, o));
-      if (lane == 0 && v < nv) red[v][0] = a;
-    }
-  }
-  if (norm && wp == 0) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
-    if (lane == 0) red[nred - 1][0] = make_double2(nacc, 0.0);
-  }
-  __syncthreads();
-  if ((int)threadIdx.x < nred) partial[(size_t)threadIdx.x * gridDim.x + blockIdx.x] = red[threadIdx.x][0];
-  __threadfence();
-  __syncthreads();
-  if (threadIdx.x == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  // last CTA: one warp per reduced quantity, fixed-order tree over the CTAs
-  const int np = gridDim.x;
-  for (int v = wp; v < nred; v += 4) {
+#ifndef SWR_CGS_UNIT_SLOT
+#define SWR_CGS_UNIT_SLOT 0
+#endif
+#ifndef SWR_CGS_DOTS_GRID
+#define SWR_CGS_DOTS_GRID 1   // 1: persistent grid for the dots passes; 0: one CTA per unit
+#endif
+#ifndef SWR_CGS_AXPY_GRID
+#define SWR_CGS_AXPY_GRID 0   // 1: persistent grid for the update pass; 0: one CTA per unit
+#endif
+// local unit b: entries [e0, e0 + len) of the rank's vectors, global column col
+__host__ __device__ __forceinline__ void unit_range(const SlotMap &m, int b, size_t &e0, int &len, size_t &col) {
+#if SWR_CGS_UNIT_SLOT
+  e0 = (size_t)b * m.NT;                       // unit = one slot (N_T entries)
+  len = m.NT;
+  col = (size_t)(m.s_lo + b);
+#else
+  const int j = m.j_lo + b;                    // unit = one subdomain (its slots l_j, r_j)
+  e0 = (size_t)(slot_first(j) - m.s_lo) * m.NT;
+  len = (slot_last(j, m.N) - slot_first(j) + 1) * m.NT;
+  col = (size_t)(j - 1);
+#endif
+}
+__host__ __device__ __forceinline__ int units_local(const SlotMap &m) {
+  return SWR_CGS_UNIT_SLOT ? m.s_hi - m.s_lo + 1 : m.j_hi - m.j_lo + 1;
+}
+__host__ __device__ __forceinline__ int units_global(const SlotMap &m) { return SWR_CGS_UNIT_SLOT ? 2 * m.N - 2 : m.N; }
+int cgs_units_global(const SlotMap &m) { return units_global(m); }
+
+// out[v] = sum over units u < nu (fixed order: lane l takes u = l, l + 32, ...
+// sequentially, then a shuffle tree) of partial[v][u], one warp per quantity;
+// CGS_SCALE: out[nred] = 1/sqrt(out[nred - 1]).  out_host: pinned mirror.
+__device__ __forceinline__ void reduce_units(const double2 *__restrict__ partial, int nu, int nred, int mode,
+                                             double2 *__restrict__ out, double2 *__restrict__ out_host,
+                                             int w0 = -1, int wstride = -1) {
+  const int lane = threadIdx.x & 31;
+  const int wp = w0 >= 0 ? w0 : (int)(threadIdx.x >> 5), nwp = wstride > 0 ? wstride : (int)(blockDim.x >> 5);
+  for (int v = wp; v < nred; v += nwp) {
     double2 sum = cz();
-    for (int q = lane; q < np; q += 32) sum = cadd(sum, __ldcg(partial + (size_t)v * np + q));
+    const double2 *pv = partial + (size_t)v * nu;
+    int q = lane;
+    for (; q + 96 < nu; q += 128) {   // four loads in flight, summed in order
+      const double2 a0 = __ldcg(pv + q), a1 = __ldcg(pv + q + 32), a2 = __ldcg(pv + q + 64), a3 = __ldcg(pv + q + 96);
+      sum = cadd(cadd(cadd(cadd(sum, a0), a1), a2), a3);
+    }
+    for (; q < nu; q += 32) sum = cadd(sum, __ldcg(pv + q));
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
     if (lane == 0) {
@@ -794,102 +722,225 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
       if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
     }
   }
+}
+
+// the last CTA of a pass (counter) reduces the unit partials of all CTAs;
+// the threads that wrote partials have fenced them (only those pay a membar)
+__device__ __forceinline__ bool last_cta(unsigned *counter, bool *flag) {
+  __syncthreads();
+  if (threadIdx.x == 0) *flag = (atomicAdd(counter, 1u) == gridDim.x - 1);
+  __syncthreads();
+  if (!*flag) return false;
+  __threadfence();
+  return true;
+}
+
+template <int VPW, int KE>
+__global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
+                                                const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
+                                                const SlotMap m, double2 *__restrict__ partial,
+                                                double2 *__restrict__ out, unsigned *counter,
+                                                double2 *__restrict__ out_host) {
+  pdl_wait();
+  pdl_trigger();
+  constexpr int NVMAX = 4 * VPW, CH = 32 * KE;
+  __shared__ double2 sh[NVMAX];
+  __shared__ double2 part[4][CH];
+  __shared__ double2 tr[4][VPW][33];   // per-warp transpose of the lane partials
+  __shared__ bool last;
+  const int nunit = units_local(m), NU = units_global(m);
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
+  const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
+  if (axpy)
+    for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
+  __syncthreads();
+  const bool rev = mode & CGS_REV;
+  bool wrote = false;
+  for (int ui = blockIdx.x; ui < nunit; ui += gridDim.x) {
+    const int b = rev ? nunit - 1 - ui : ui;
+    size_t e0, col;
+    int len;
+    unit_range(m, b, e0, len, col);
+    double2 acc[VPW];
+#pragma unroll
+    for (int i = 0; i < VPW; i++) acc[i] = cz();
+    double nacc = 0.0;
+    for (int c0 = 0; c0 < len; c0 += CH) {
+      double2 x[VPW][KE], we[KE];
+#pragma unroll
+      for (int i = 0; i < VPW; i++) {
+        const int v = wp + 4 * i;
+#pragma unroll
+        for (int k = 0; k < KE; k++) {
+          const int e = c0 + lane + 32 * k;
+          x[i][k] = (v < nv && e < len) ? V[(size_t)v * ldv + e0 + e] : cz();
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KE; k++) {
+        const int e = c0 + lane + 32 * k;
+        we[k] = e < len ? w[e0 + e] : cz();
+      }
+      if (axpy) {
+#pragma unroll
+        for (int k = 0; k < KE; k++) {
+          double2 pv = cz();
+#pragma unroll
+          for (int i = 0; i < VPW; i++)
+            if (wp + 4 * i < nv) pv = cfma(sh[wp + 4 * i], x[i][k], pv);
+          part[wp][lane + 32 * k] = pv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < KE; k++) {
+          const int t = lane + 32 * k;
+          const double2 pv = cadd(cadd(cadd(part[0][t], part[1][t]), part[2][t]), part[3][t]);
+          we[k] = csub(we[k], pv);
+          const int e = c0 + t;
+          if (wp == 0 && e < len) w[e0 + e] = we[k];
+        }
+        __syncthreads();
+      }
+      if (dots) {
+#pragma unroll
+        for (int i = 0; i < VPW; i++)
+#pragma unroll
+          for (int k = 0; k < KE; k++) acc[i] = cfmaconj(x[i][k], we[k], acc[i]);
+      }
+      if (norm && wp == 0) {
+#pragma unroll
+        for (int k = 0; k < KE; k++) nacc = fma(we[k].x, we[k].x, fma(we[k].y, we[k].y, nacc));
+      }
+    }
+    // unit partials (warp q holds vectors q, q+4, ...): the lane partials go
+    // through shared memory; lanes l = i + VPW r (r < 32/VPW) sum lanes
+    // r, r + 32/VPW, ... of vector i in order, then a short shuffle tree over r
+    if (dots) {
+#pragma unroll
+      for (int i = 0; i < VPW; i++) tr[wp][i][lane] = acc[i];
+      __syncwarp();
+      constexpr int R = 32 / VPW;
+      const int i = lane % VPW, r = lane / VPW;
+      double2 a = cz();
+#pragma unroll
+      for (int q = r; q < 32; q += R) a = cadd(a, tr[wp][i][q]);
+#pragma unroll
+      for (int o = 16; o >= VPW; o >>= 1) a = cadd(a, shfl_down2(a, o));
+      const int v = wp + 4 * i;
+      if (r == 0 && v < nv) partial[(size_t)v * NU + col] = a;
+      wrote = wrote || (r == 0 && v < nv);
+      __syncwarp();
+    }
+    if (norm && wp == 0) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+      if (lane == 0) partial[(size_t)(nred - 1) * NU + col] = make_double2(nacc, 0.0);
+      wrote = wrote || lane == 0;
+    }
+  }
+  if (!out) return;   // multi-GPU: the partials are exchanged first (k_cgs_reduce)
+  if (wrote) __threadfence();
+  if (!last_cta(counter, &last)) return;
+  reduce_units(partial, NU, nred, mode, out, out_host);
+  __syncthreads();
   if (threadIdx.x == 0) *counter = 0u;
 }
 
 // The CGS update pass without dots (CGS_AXPY | CGS_NORM [| CGS_SCALE]):
 // w -= V h and <w, w>.  No dots means no per-vector sums, so the entries
-// split over warps (each warp streams all nv basis vectors for its 32 KE
-// entries, four vectors per unrolled step) and no shared-memory exchange or
-// barrier sits in the loop.  Norm partials: warp tree, CTA fixed order, the
-// last CTA sums the CTAs in a fixed order (deterministic).
-template <int KE, int MINB, int VU = 4>
-__global__ void __launch_bounds__(256, MINB) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
+// split over warps: warp q of the unit's CTA streams all nv basis vectors for
+// chunks q, q+4, ... of 32 KE entries (VU vectors per unrolled step) with no
+// shared-memory exchange or barrier in the loop.  Unit norm partial: lane
+// tree per warp, warps in order.
+template <int KE, int VU = 4>
+__global__ void __launch_bounds__(128, 4) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
                                                      const double2 *__restrict__ hsrc, double2 *__restrict__ w,
-                                                     int mode, double2 *__restrict__ partial,
-                                                     double2 *__restrict__ out, unsigned *counter, size_t ntot,
+                                                     int mode, const SlotMap m, double2 *__restrict__ partial,
+                                                     double2 *__restrict__ out, unsigned *counter,
                                                      double2 *__restrict__ out_host) {
   pdl_wait();
   pdl_trigger();
   __shared__ double2 sh[32];
-  __shared__ double red[8];
+  __shared__ double red[4];
   __shared__ bool last;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
   __syncthreads();
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5, nwp = blockDim.x >> 5;
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   constexpr int CH = 32 * KE;
-  // the whole grid sweeps one front of chunks through memory (reversed with
-  // CGS_REV), so consecutive passes meet the tail of the previous one in L2
-  const size_t nch = (ntot + CH - 1) / CH, nwarps = (size_t)gridDim.x * nwp;
+  const int nunit = units_local(m), NU = units_global(m);
   const bool rev = mode & CGS_REV;
-  const size_t hi = ntot;
-  double nacc = 0.0;
-  for (size_t ci = (size_t)blockIdx.x * nwp + wp; ci < nch; ci += nwarps) {
-    const size_t c = rev ? nch - 1 - ci : ci;
-    const size_t base = c * CH + lane;
-    double2 we[KE], p[KE];
-#pragma unroll
-    for (int k = 0; k < KE; k++) {
-      const size_t e = base + 32 * k;
-      we[k] = e < hi ? w[e] : cz();
-      p[k] = cz();
-    }
-    int v = 0;
-    for (; v + VU <= nv; v += VU) {
-      double2 x[VU][KE];
-#pragma unroll
-      for (int j = 0; j < VU; j++)
-#pragma unroll
-        for (int k = 0; k < KE; k++) {
-          const size_t e = base + 32 * k;
-          x[j][k] = e < hi ? V[(size_t)(v + j) * ldv + e] : cz();
-        }
-#pragma unroll
-      for (int j = 0; j < VU; j++)
-#pragma unroll
-        for (int k = 0; k < KE; k++) p[k] = cfma(sh[v + j], x[j][k], p[k]);
-    }
-    for (; v < nv; v++) {
+  for (int ui = blockIdx.x; ui < nunit; ui += gridDim.x) {
+    const int b = rev ? nunit - 1 - ui : ui;
+    size_t e0, col;
+    int len;
+    unit_range(m, b, e0, len, col);
+    double nacc = 0.0;
+    for (int c0 = wp * CH; c0 < len; c0 += 4 * CH) {
+      double2 we[KE], pv[KE];
 #pragma unroll
       for (int k = 0; k < KE; k++) {
-        const size_t e = base + 32 * k;
-        p[k] = cfma(sh[v], e < hi ? V[(size_t)v * ldv + e] : cz(), p[k]);
+        const int e = c0 + lane + 32 * k;
+        we[k] = e < len ? w[e0 + e] : cz();
+        pv[k] = cz();
+      }
+      int v = 0;
+      for (; v + VU <= nv; v += VU) {
+        double2 x[VU][KE];
+#pragma unroll
+        for (int jv = 0; jv < VU; jv++)
+#pragma unroll
+          for (int k = 0; k < KE; k++) {
+            const int e = c0 + lane + 32 * k;
+            x[jv][k] = e < len ? V[(size_t)(v + jv) * ldv + e0 + e] : cz();
+          }
+#pragma unroll
+        for (int jv = 0; jv < VU; jv++)
+#pragma unroll
+          for (int k = 0; k < KE; k++) pv[k] = cfma(sh[v + jv], x[jv][k], pv[k]);
+      }
+      for (; v < nv; v++) {
+#pragma unroll
+        for (int k = 0; k < KE; k++) {
+          const int e = c0 + lane + 32 * k;
+          pv[k] = cfma(sh[v], e < len ? V[(size_t)v * ldv + e0 + e] : cz(), pv[k]);
+        }
+      }
+#pragma unroll
+      for (int k = 0; k < KE; k++) {
+        const int e = c0 + lane + 32 * k;
+        if (e < len) {
+          const double2 r = csub(we[k], pv[k]);
+          w[e0 + e] = r;
+          nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
+        }
       }
     }
 #pragma unroll
-    for (int k = 0; k < KE; k++) {
-      const size_t e = base + 32 * k;
-      if (e < hi) {
-        const double2 r = csub(we[k], p[k]);
-        w[e] = r;
-        nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
-      }
-    }
+    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+    if (lane == 0) red[wp] = nacc;
+    __syncthreads();
+    if (threadIdx.x == 0)
+      partial[col] = make_double2(((red[0] + red[1]) + red[2]) + red[3], 0.0);
+    __syncthreads();
   }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
-  if (lane == 0) red[wp] = nacc;
+  if (!out) return;
+  if (threadIdx.x == 0 && blockIdx.x < nunit) __threadfence();
+  if (!last_cta(counter, &last)) return;
+  reduce_units(partial, NU, 1, mode, out, out_host);
   __syncthreads();
-  if (threadIdx.x == 0) {
-    double sacc = 0.0;
-    for (int q = 0; q < nwp; q++) sacc += red[q];
-    partial[blockIdx.x] = make_double2(sacc, 0.0);
-    __threadfence();
-    last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  }
-  __syncthreads();
-  if (!last || wp != 0) return;
-  __threadfence();
-  double sum = 0.0;
-  for (int q = lane; q < (int)gridDim.x; q += 32) sum += __ldcg(partial + q).x;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum += __shfl_down_sync(0xffffffffu, sum, o);
-  if (lane == 0) {
-    out[0] = make_double2(sum, 0.0);
-    if (out_host) out_host[0] = out[0];
-    if (mode & CGS_SCALE) out[1] = make_double2(1.0 / sqrt(sum), 0.0);
-    *counter = 0u;
-  }
+  if (threadIdx.x == 0) *counter = 0u;
+}
+
+// Multi-GPU: the unit partials of all ranks (summed, disjoint columns) ->
+// the scalars, in the same fixed order as the one-GPU pass.
+// one warp per quantity: block b, warp q reduces quantity b * warps + q
+__global__ void k_cgs_reduce(const double2 *__restrict__ partial, int nu, int nred, int mode, double2 *out,
+                             double2 *out_host) {
+  pdl_wait();
+  pdl_trigger();
+  const int nwp = blockDim.x >> 5;
+  reduce_units(partial, nu, nred, mode, out, out_host, blockIdx.x * nwp + (threadIdx.x >> 5), gridDim.x * nwp);
 }
 
 // y = s x, s read from the device (the normalisation of a new basis vector)
@@ -902,219 +953,34 @@ __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__rest
     y[e] = make_double2(x[e].x * sc, x[e].y * sc);
 }
 
-// ---------------------------------------------------------------------------
-// Same CGS kernel, bulk-copy pipeline form.  One persistent CTA per SM
-// streams chunks of CH = 128 EPT entries of the nv basis vectors and of w
-// into shared memory with cp.async.bulk (TMA, one 1-D copy per vector row,
-// completion counted on a per-stage mbarrier), NS stages deep, so HBM reads
-// run ahead of the arithmetic without any thread holding them in registers.
-// Thread t owns entries t + 128 k of each chunk: the axpy and the dots of an
-// entry are thread-local (no cross-warp reduction per chunk, one CTA barrier
-// per chunk to release the stage).  Dot partials: registers over the CTA's
-// chunks (fixed order), warp shuffles + shared memory, the last CTA sums the
-// per-CTA partials in CTA order.
-// ---------------------------------------------------------------------------
-__device__ __forceinline__ uint32_t cgs_smem_u32(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
-
-template <int NVMAX>
-__global__ void __launch_bounds__(256, 1) k_cgs_tma(const double2 *__restrict__ V, size_t ldv, int nv,
-                                                    const double2 *__restrict__ hsrc, double2 *__restrict__ w,
-                                                    int mode, double2 *__restrict__ partial, double2 *__restrict__ out,
-                                                    unsigned *counter, size_t ntot, int EPT, int NS,
-                                                    double2 *__restrict__ out_host) {
-  pdl_wait();
-  pdl_trigger();
-  constexpr int NH = NVMAX / 2;   // basis vectors per thread (v = 2 i + hf)
-  extern __shared__ __align__(128) unsigned char smraw[];
-  __shared__ double2 red[NVMAX + 1][8];
-  __shared__ double2 sh[NVMAX];
-  __shared__ bool last;
-  unsigned long long *mb = reinterpret_cast<unsigned long long *>(smraw);   // [NS]
-  double2 *stg = reinterpret_cast<double2 *>(smraw + 128);                  // [NS][nv + 1][CH]
-  const int t = threadIdx.x, lane = t & 31, wp = t >> 5, hf = t & 1, el0 = t >> 1;
-  const int CH = 128 * EPT, nrow = nv + 1;
-  const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
-  const size_t nch = (ntot + CH - 1) / CH;
-  const int mine = blockIdx.x < nch ? (int)((nch - 1 - blockIdx.x) / gridDim.x) + 1 : 0;
-  if (axpy)
-    for (int v = t; v < nv; v += blockDim.x) sh[v] = hsrc[v];
-  if (t == 0) {
-    for (int i = 0; i < NS; i++)
-      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(cgs_smem_u32(mb + i)) : "memory");
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  __syncthreads();
-  auto issue = [&](int i) {   // chunk i of this CTA into stage i % NS (warp 0, one row per lane)
-    const int sgi = i % NS;
-    const size_t base = (blockIdx.x + (size_t)i * gridDim.x) * CH;
-    const uint32_t bytes = (uint32_t)(min((size_t)CH, ntot - base) * sizeof(double2));
-    const uint32_t mbar = cgs_smem_u32(mb + sgi);
-    if (lane == 0)
-      asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(mbar), "r"(bytes * nrow) : "memory");
-    double2 *dst = stg + (size_t)sgi * nrow * CH;
-    for (int v = lane; v <= nv; v += 32) {
-      const double2 *src = v < nv ? V + (size_t)v * ldv + base : w + base;
-      asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];"
-                   ::"r"(cgs_smem_u32(dst + (size_t)v * CH)), "l"(src), "r"(bytes), "r"(mbar) : "memory");
-    }
-  };
-  if (wp == 0)
-    for (int i = 0; i < NS - 1 && i < mine; i++) issue(i);
-  double2 acc[NH];
-#pragma unroll
-  for (int v = 0; v < NH; v++) acc[v] = cz();
-  double nacc = 0.0;
-  for (int i = 0; i < mine; i++) {
-    if (wp == 0 && i + NS - 1 < mine) issue(i + NS - 1);   // its stage was released at the end of i - 1
-    const int sgi = i % NS;
-    {
-      const uint32_t mbar = cgs_smem_u32(mb + sgi), par = (uint32_t)((i / NS) & 1);
-      uint32_t done = 0;
-      while (!done)
-        asm volatile("{ .reg .pred p; mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2; selp.u32 %0, 1, 0, p; }"
-                     : "=r"(done) : "r"(mbar), "r"(par) : "memory");
-    }
-    const double2 *st = stg + (size_t)sgi * nrow * CH;
-    const size_t base = (blockIdx.x + (size_t)i * gridDim.x) * CH;
-    const int n = (int)min((size_t)CH, ntot - base);
-    // lanes 2e, 2e + 1 share entry e (even / odd v); the loop bound is warp-uniform
-    // (CH is a multiple of 128) so the pair shuffle always sees the full warp
-    for (int e = el0; e < CH; e += 128) {
-      const bool ok = e < n;
-      double2 we = ok ? st[(size_t)nv * CH + e] : cz();
-      if (axpy) {
-        double2 p0 = cz(), p1 = cz();
-        if (ok) {
-#pragma unroll 4
-          for (int v = hf; v < nv; v += 4) {
-            p0 = cfma(sh[v], st[(size_t)v * CH + e], p0);
-            if (v + 2 < nv) p1 = cfma(sh[v + 2], st[(size_t)(v + 2) * CH + e], p1);
-          }
-        }
-        const double2 pm = cadd(p0, p1), po = shfl_xor2(pm, 1);
-        const double2 tot = hf == 0 ? cadd(pm, po) : cadd(po, pm);   // (even + odd), same on both lanes
-        we = csub(we, tot);
-        if (ok && hf == 0) w[base + e] = we;
-      }
-      if (ok) {
-        if (dots) {
-#pragma unroll
-          for (int k = 0; k < NH; k++)
-            if (2 * k + hf < nv) acc[k] = cfmaconj(st[(size_t)(2 * k + hf) * CH + e], we, acc[k]);
-        }
-        if (norm && hf == 0) nacc = fma(we.x, we.x, fma(we.y, we.y, nacc));
-      }
-    }
-    __syncthreads();   // stage sgi free for chunk i + NS
-  }
-  const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
-  if (dots) {
-#pragma unroll
-    for (int k = 0; k < NH; k++) {
-      if (2 * k < nv) {
-        double2 a = acc[k];
-#pragma unroll
-        for (int o = 16; o > 1; o >>= 1) a = cadd(a, shfl_xor2(a, o));   // lanes of the same parity
-        if (lane < 2 && 2 * k + lane < nv) red[2 * k + lane][wp] = a;
-      }
-    }
-  }
-  if (norm) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_xor_sync(0xffffffffu, nacc, o);
-    if (lane == 0) red[nred - 1][wp] = make_double2(nacc, 0.0);
-  }
-  __syncthreads();
-  if (t < nred) {
-    double2 sum = red[t][0];
-#pragma unroll
-    for (int q = 1; q < 8; q++) sum = cadd(sum, red[t][q]);
-    partial[(size_t)t * gridDim.x + blockIdx.x] = sum;
-  }
-  __threadfence();
-  __syncthreads();
-  if (t == 0) last = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const int np = gridDim.x;
-  for (int v = wp; v < nred; v += 8) {
-    double2 sum = cz();
-    for (int q = lane; q < np; q += 32) sum = cadd(sum, __ldcg(partial + (size_t)v * np + q));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
-    if (lane == 0) {
-      out[v] = sum;
-      if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
-      if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
-    }
-  }
-  if (t == 0) *counter = 0u;
-}
-
-template <int NVMAX>
-static cudaError_t launch_cgs_tma_t(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                                    double2 *partial, double2 *out, unsigned *counter, size_t ntot, cudaStream_t st,
-                                    double2 *out_host) {
-  // stage = (nv + 1) rows of CH = 128 EPT entries, about 48 KB; up to 4 stages in 200 KB
-  const int nrow = nv + 1;
-  int EPT = (int)((48 * 1024) / ((size_t)nrow * 128 * sizeof(double2)));
-  EPT = EPT < 1 ? 1 : (EPT > 16 ? 16 : EPT);
-  const size_t stage = (size_t)nrow * 128 * EPT * sizeof(double2);
-  const int NS = (int)std::min<size_t>(4, (200 * 1024) / stage);
-  const size_t smem = 128 + (size_t)NS * stage;
-  static bool attr_set = false;
-  if (!attr_set) {
-    cudaError_t e = cudaFuncSetAttribute(k_cgs_tma<NVMAX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
-    if (e != cudaSuccess) {
-      fprintf(stderr, "k_cgs_tma<%d>: cudaFuncSetAttribute: %s\n", NVMAX, cudaGetErrorString(e));
-      return e;
-    }
-    attr_set = true;
-  }
-  const size_t nch = (ntot + 128 * EPT - 1) / (128 * EPT);
-  const unsigned grid = (unsigned)std::min<size_t>(nch, 148);
-  cudaError_t e = launch_pdl(k_cgs_tma<NVMAX>, dim3(grid), dim3(256), smem, st, V, ldv, nv, hsrc, w, mode, partial, out,
-                             counter, ntot, EPT, NS, out_host);
-  if (e != cudaSuccess) {
-    cudaFuncAttributes fa;
-    cudaFuncGetAttributes(&fa, k_cgs_tma<NVMAX>);
-    fprintf(stderr, "k_cgs_tma<%d>: launch grid %u smem %zu (max dyn %d, static %zu, regs %d, maxthr %d): %s\n", NVMAX, grid,
-            smem, fa.maxDynamicSharedSizeBytes, fa.sharedSizeBytes, fa.numRegs, fa.maxThreadsPerBlock, cudaGetErrorString(e));
-  }
-  return e;
-}
-
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       double2 *partial, double2 *out, unsigned *counter, int N, int NT, cudaStream_t st,
+                       const SlotMap &m, double2 *partial, double2 *out, unsigned *counter, cudaStream_t st,
                        double2 *out_host, size_t vwin, float vratio) {
   if (!V) vwin = 0;
-  const size_t ntot = (size_t)(2 * N - 2) * NT;
   if (nv > 32) return cudaErrorInvalidValue;
-  // default: register form below; SWR_CGS=tma selects the bulk-copy pipeline
-  // form (measured slower at C5: 190 vs 147 ms per solve)
-  const char *cgs_env = getenv("SWR_CGS");
-  if (cgs_env && strcmp(cgs_env, "tma") == 0) {
-    if (nv <= 8) return launch_cgs_tma_t<8>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
-    if (nv <= 16) return launch_cgs_tma_t<16>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
-    return launch_cgs_tma_t<32>(V, ldv, nv, hsrc, w, mode, partial, out, counter, ntot, st, out_host);
-  }
-  // update pass without dots: entry-split streaming form (SWR_CGS_AXPY=0 disables)
-  static const bool axpy_split = !(getenv("SWR_CGS_AXPY") && atoi(getenv("SWR_CGS_AXPY")) == 0);
-  if (axpy_split && (mode & CGS_AXPY) && !(mode & CGS_DOTS) && (mode & CGS_NORM) && nv >= 1) {
-    // 4 entries x 4 vectors per unrolled step, 2 CTAs of 256 per SM (measured
-    // best of KE 1/2/4, 4 or 8 vectors per step, 1-3 CTAs per SM)
-    const size_t nwarp_needed = (ntot + 32 * 4 - 1) / (32 * 4);
-    const unsigned g = (unsigned)std::min<size_t>((nwarp_needed + 7) / 8, 148 * 2);
-    return launch_pdl_win(V, vwin, vratio, k_cgs_axpy<4, 2>, dim3(g), dim3(256), 0, st, V, ldv, nv, hsrc, w, mode,
-                          partial, out, counter, ntot, out_host);
-  }
-  // register form: persistent grid, 4 CTAs of 128 threads per SM (148 SMs); the
-  // grid only depends on the sizes, so the reduction order is fixed
-  auto grid = [&](int ch) { return (unsigned)std::min<size_t>((ntot + ch - 1) / ch, 148 * 4); };
-  if (nv <= 8) return launch_pdl_win(V, vwin, vratio, k_cgs<2, 8>, dim3(grid(256)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
-  if (nv <= 16) return launch_pdl_win(V, vwin, vratio, k_cgs<4, 4>, dim3(grid(128)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
-  return launch_pdl_win(V, vwin, vratio, k_cgs<8, 2>, dim3(grid(64)), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, partial, out, counter, N, NT, out_host);
+  const int nunit = units_local(m);
+  if (nunit < 1) return cudaSuccess;
+  // one CTA per unit, up to 4 CTAs of 128 threads per SM
+  const unsigned g = SWR_CGS_DOTS_GRID ? (unsigned)std::min(nunit, 148 * 4) : (unsigned)nunit;
+  // update pass without dots: entry-split streaming form
+  if ((mode & CGS_AXPY) && !(mode & CGS_DOTS) && (mode & CGS_NORM) && nv >= 1)
+    return launch_pdl_win(V, vwin, vratio, k_cgs_axpy<4>, dim3(SWR_CGS_AXPY_GRID ? g : (unsigned)nunit), dim3(128), 0,
+                          st, V, ldv, nv, hsrc, w, mode, m,
+                          partial, out, counter, out_host);
+  if (nv <= 8)
+    return launch_pdl_win(V, vwin, vratio, k_cgs<2, 8>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
+                          partial, out, counter, out_host);
+  if (nv <= 16)
+    return launch_pdl_win(V, vwin, vratio, k_cgs<4, 4>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
+                          partial, out, counter, out_host);
+  return launch_pdl_win(V, vwin, vratio, k_cgs<8, 2>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
+                        partial, out, counter, out_host);
+}
+
+cudaError_t launch_cgs_reduce(const double2 *partial, int nu, int nred, int mode, double2 *out, double2 *out_host,
+                              cudaStream_t st) {
+  // one warp per reduced quantity (the same fixed order as the in-pass reduction)
+  return launch_pdl(k_cgs_reduce, dim3((nred + 3) / 4), dim3(128), 0, st, partial, nu, nred, mode, out, out_host);
 }
 
 // ---------------------------------------------------------------------------
@@ -1148,4 +1014,17 @@ __global__ void k_fill(double2 *x, double2 v, size_t n) {
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) x[e] = v;
 }
 
+}  // namespace swr
+
+namespace swr {
+// dst[c blk + i] = src[i], c < count (identical interior L0 columns)
+__global__ void k_replicate(const double2 *__restrict__ src, double2 *__restrict__ dst, size_t blk, size_t count) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < blk * count; e += (size_t)gridDim.x * blockDim.x)
+    dst[e] = src[e % blk];
+}
+// y += x (n doubles): the loopback communicator's rank-ordered sums
+__global__ void k_add_f64(double *__restrict__ y, const double *__restrict__ x, size_t n) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x)
+    y[e] += x[e];
+}
 }  // namespace swr

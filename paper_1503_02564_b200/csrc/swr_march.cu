@@ -692,6 +692,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   if constexpr (TDM) {
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
     SWR_TRACE(0);
     if (TDM && n > 1) {   // time-dependent potential: the step-n factorisation of (A_{j,n} - B)
       if (fcnt > 0) mbar_wait(pmb, (uint32_t)((n - 2) & 1));
@@ -776,6 +777,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       if (pass == 0) {
         double2 carry[K];
         SWR_TRACE(3);
+        race_jitter(1, n);
         scan_maps<K, true, true>(sAf[t], z, sfp, lane, w, nw, CS, crank, carry,
                                  SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr, mbar + pb, ph);
         SWR_TRACE(4);
@@ -831,6 +833,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     {
       double2 carry[K];
       SWR_TRACE(6);
+      race_jitter(2, n);
       scan_maps<K, false, true>(sAb[t], x, sbp, lane, w, nw, CS, crank, carry,
                                 SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr, mbar + 2 + pb, ph);
       SWR_TRACE(7);
@@ -865,6 +868,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         uL[r] = make_double2(fma(2.0, xp.x, -uL[r].x), fma(2.0, xp.y, -uL[r].y));
       }
     }
+    race_jitter(3, n);
     SWR_TRACE(8);
     // ---- record v_n and S v_n at the interfaces (eq. 8) ----
     if (first) {   // x now holds v_n at row 0
@@ -896,6 +900,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
   } else {
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
     SWR_TRACE(0);
     // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + beta_2 v_{n-2} + Q_n) (P:218,
     // P:501-507), Q_n = sum_{s<=n-3} beta_{n-s} v_s summed over the CTA during
@@ -1025,6 +1030,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         if (lane == 0) hred[((r * 2 + (n & 1)) * 2 + side) * 32 + w] = acc;
       }
     };
+    race_jitter(1, n);
     scan_tab<K, true>(z, sfp, tabF, t, P, lane, w, nw, CS, crank, zc, mbar + pb, ph,
                       [&] { if (has_right && crank == cb) history(1); },
                       SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr);
@@ -1038,6 +1044,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     {
       double2 carry[K];
       SWR_TRACE(6);
+      race_jitter(2, n);
       scan_tab<K, false>(x, sbp, tabB, t, P, lane, w, nw, CS, crank, carry, mbar + 2 + pb, ph,
                          [&] { if (has_left && crank == 0) history(0); },
                          SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr);
@@ -1075,6 +1082,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
         uL[r] = make_double2(fma(2.0, xp.x, -uL[r].x), fma(2.0, xp.y, -uL[r].y));
       }
     }
+    race_jitter(3, n);
     SWR_TRACE(8);
     // ---- record v_n and S v_n at the interfaces (eq. 8) ----
     if (first) {   // x now holds v_n at row 0
@@ -1209,6 +1217,7 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
 
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
     if (p.s02) {
       if (has_left && crank == 0) {
         double2 acc = cz();
@@ -1306,6 +1315,7 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
         }
         if (pass == 0) {
           double2 zz[1] = {z}, carry[1];
+          race_jitter(1, n);
           scan_maps<1, true>(sAf[t], zz, sf, lane, w, nw, CS, crank, carry);
           z = carry[0];
         }
@@ -1408,29 +1418,20 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
 }
 
 // ---------------------------------------------------------------------------
-// Launch-shape selection and launcher.  Instantiated (M rows per thread, K
+// Launch-shape selection and launcher.  Instantiated (M rows per thread, one
 // RHS per group, PMAX threads per CTA); the register cap is 65536 / PMAX.
+// (K = 2, 3 right-hand sides per group sharing the registers of a thread
+// were measured slower at C5 and are not instantiated.)
 // ---------------------------------------------------------------------------
-struct Inst { int M, K, PMAX; };
-static const Inst kInst[] = {
-    {1, 1, 512}, {2, 1, 512}, {4, 1, 512}, {6, 1, 256}, {8, 1, 256}, {11, 1, 256},
-    {3, 2, 256}, {3, 3, 256}};
+struct Inst { int M, PMAX; };
+static const Inst kInst[] = {{1, 512}, {2, 512}, {4, 512}, {6, 256}, {8, 256}, {11, 256}};
 
-MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi) {
+MarchShape choose_march_shape(int Nj, int NT, bool tc_hi) {
   MarchShape best{0, 0, 0, 0};
   double best_cost = 1e300;
-  const char *pm = getenv("SWR_MARCH_PMAX");
-  const int pmax_env = pm ? atoi(pm) : 0;
-  const char *mm = getenv("SWR_MARCH_M");   // experiments: force M rows per thread
-  const int m_env = mm ? atoi(mm) : 0;
-  const char *ce = getenv("SWR_MARCH_CS");  // experiments: force the cluster size
-  const int cs_env = ce ? atoi(ce) : 0;
+  const int K = 1;
   for (int CS = 1; CS <= 16; CS++) {
-    if (cs_env && CS != cs_env) continue;
     for (const Inst &in : kInst) {
-      if (in.K != K) continue;
-      if (pmax_env && in.PMAX != pmax_env) continue;
-      if (m_env && in.M != m_env) continue;
       const int M = in.M;
       long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
       int P = (int)((per + 31) / 32 * 32);
@@ -1445,13 +1446,13 @@ MarchShape choose_march_shape(int Nj, int K, int NT, bool tc_hi) {
   return best;
 }
 
-MarchShape choose_march_shape_nl(int Nj) {
+// rows: 0 = automatic, 8 or 11 forces the rows per thread (tests of the
+// large-subdomain shape on small problems; swr_config.nl_rows_per_thread)
+MarchShape choose_march_shape_nl(int Nj, int rows) {
   MarchShape best{0, 0, 0, 1};
   double best_cost = 1e300;
-  const int m_env = getenv("SWR_NL_M") ? atoi(getenv("SWR_NL_M")) : 0;     // experiments
-  const int cs_env = getenv("SWR_NL_CS") ? atoi(getenv("SWR_NL_CS")) : 0;
+  const int m_env = rows;
   for (int CS = 1; CS <= 16; CS++) {
-    if (cs_env && CS != cs_env) continue;
     for (int M : {1, 2, 4, 8, 11}) {
       if (m_env && M != m_env) continue;
       if (M == 11 && !m_env) continue;   // only when nothing smaller fits (below)
@@ -1467,7 +1468,6 @@ MarchShape choose_march_shape_nl(int Nj) {
   }
   if (best.M == 0 && !m_env) {   // N_j beyond 16 x 256 x 8 rows: 11 rows per thread
     for (int CS = 1; CS <= 16 && best.M == 0; CS++) {
-      if (cs_env && CS != cs_env) continue;
       const long per = ((long)Nj + (long)CS * 11 - 1) / ((long)CS * 11);
       const int P = (int)((per + 31) / 32 * 32);
       if (P <= 256) best = {11, P < 32 ? 32 : P, CS, 1};
@@ -1506,7 +1506,7 @@ static cudaError_t launch_nl_m(const MarchParams &p, const MarchShape &s, size_t
     attr[0].val.clusterDim.z = 1;
     cfg.numAttrs = 1;
   }
-  if (getenv("SWR_MARCH_VERBOSE")) {
+  if (getenv("SWR_VERBOSE")) {
     int ncl = 0;
     cudaOccupancyMaxActiveClusters(&ncl, (void *)kern, &cfg);
     cudaFuncAttributes fa;
@@ -1528,7 +1528,7 @@ cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st)
     case 8:
       // two CTAs per SM when the CTA has <= 192 threads (register cap 170):
       // twice the resident clusters, fewer waves of systems (C4: 3 -> 2)
-      if (s.P <= 192 && !getenv("SWR_NL_ONE")) return launch_nl_m<8, 192, 2>(p, s, smem, st);
+      if (s.P <= 192) return launch_nl_m<8, 192, 2>(p, s, smem, st);
       return launch_nl_m<8, 256>(p, s, smem, st);
     case 11:   // the largest subdomains (up to 16 x 256 x 11 = 45,056 rows)
       return launch_nl_m<11, 256>(p, s, smem, st);
@@ -1576,10 +1576,9 @@ cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st) {
   p.CS = s.CS;
   const size_t smem = march_smem_bytes(s, p.NT, p.flux_smem, p.tc_hi != 0);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-#define SWR_CASE(MM, KK, PP) \
-  if (s.M == MM && s.K == KK && s.P <= PP) return launch_m<MM, KK, PP>(p, s, smem, st);
-  SWR_CASE(1, 1, 512) SWR_CASE(2, 1, 512) SWR_CASE(4, 1, 512) SWR_CASE(6, 1, 256) SWR_CASE(8, 1, 256)
-  SWR_CASE(11, 1, 256) SWR_CASE(3, 2, 256) SWR_CASE(3, 3, 256)
+#define SWR_CASE(MM, PP) \
+  if (s.M == MM && s.P <= PP) return launch_m<MM, 1, PP>(p, s, smem, st);
+  SWR_CASE(1, 512) SWR_CASE(2, 512) SWR_CASE(4, 512) SWR_CASE(6, 256) SWR_CASE(8, 256) SWR_CASE(11, 256)
 #undef SWR_CASE
   return cudaErrorInvalidValue;
 }

@@ -142,6 +142,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
   };
 
   for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
     const size_t toff = p.td_stride ? (size_t)(n - 1) * p.td_stride : 0;
     const double2 *q = sq + toff;
     const double *er = ser + toff;
@@ -229,6 +230,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       __threadfence();
       st_release(ffwd + c, n);
     }
+    race_jitter(1, n);
     // carry into the CTA: fold of the earlier CTAs' totals
     double2 zc = cz();
     if (c > 0) {
@@ -239,6 +241,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
         zc = cfma(__ldcg(fv + (cc * 2 + par) * 2 + 0), zc, __ldcg(fv + (cc * 2 + par) * 2 + 1));
     }
     double2 dummy;
+    race_jitter(2, n);
     fwd_pass(cfma(eA, zc, eB), true, dummy);
     // ---- backward: x_k = z_k + b_k x_{k+1}, b_k = -q_k E_k ----
     double2 Ab = make_double2(1.0, 0.0), xb = cz();
@@ -254,6 +257,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       __threadfence();
       st_release(fbwd + c, n);
     }
+    race_jitter(3, n);
     double2 xc = cz();
     if (c < nc - 1) {
       if (t == 0)
@@ -298,9 +302,13 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 
 size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1)) * sizeof(double2); }
 
-// Streams the systems in batches whose chains are all co-resident.
-cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, double2 *zst, int *flags, double2 *vals,
-                                cudaStream_t st) {
+// Streams the systems in batches whose chains are all co-resident.  The
+// chain length nc (CTAs per system, i.e. how a system's rows are split and
+// its scans reassociated) depends on N_j, the GPU and nsys_ref (the
+// problem's subdomain count) only -- not on how many systems a launch or a
+// rank carries -- so a rank of a multi-GPU run rounds exactly as one GPU.
+cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst, int *flags,
+                                double2 *vals, cudaStream_t st) {
   const size_t smem = march_stream_smem_bytes(p.NT);
   cudaError_t e = cudaFuncSetAttribute(k_march_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -312,14 +320,15 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, double2 *ust, dou
   const int cap = nsm * per_sm;
   if (cap < 1) return cudaErrorInvalidConfiguration;
   const MarchSys *all = p.sys;
+  int nc = std::max(1, cap / std::max(1, nsys_ref));
+  nc = std::min(nc, std::max(1, p.Nj / 256));   // at least a row per thread
+  const int per_batch = std::max(1, cap / nc);
   for (int s0 = 0; s0 < nsys_total;) {
-    const int nb = std::min(nsys_total - s0, cap);
-    int nc = std::max(1, cap / nb);
-    nc = std::min(nc, std::max(1, p.Nj / 256));   // at least a row per thread
+    const int nb = std::min(nsys_total - s0, per_batch);
     MarchParams q = p;
     q.sys = all + s0;
     q.nsys = nb;
-    if (getenv("SWR_MARCH_VERBOSE")) {
+    if (getenv("SWR_VERBOSE")) {
       cudaFuncAttributes fa;
       cudaFuncGetAttributes(&fa, k_march_stream);
       fprintf(stderr, "k_march_stream: %d systems x %d CTAs (%d per SM, %d regs, smem %zu), N_j %d\n", nb, nc, per_sm,

@@ -35,7 +35,9 @@ class Config(C.Structure):
         ("restart", C.c_int32), ("maxit", C.c_int32), ("tol_inner", C.c_double), ("maxit_inner", C.c_int32),
         ("tol_fp", C.c_double), ("maxit_fp", C.c_int32), ("g0", C.c_void_p),
         ("rank", C.c_int32), ("world", C.c_int32), ("nccl_unique_id", C.c_void_p),
-        ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("gs_passes", C.c_int32), ("krylov", C.c_int32), ("pade_m", C.c_int32), ("pinv_exact", C.c_int32),
+        ("cuda_stream", C.c_void_p), ("device", C.c_int32), ("gs_passes", C.c_int32), ("krylov", C.c_int32),
+        ("pade_m", C.c_int32), ("pinv_exact", C.c_int32), ("march_form", C.c_int32), ("toeplitz_form", C.c_int32),
+        ("nl_rows_per_thread", C.c_int32),
     ]
 
 
@@ -45,7 +47,7 @@ class Report(C.Structure):
         ("converged", C.c_int32), ("residual_history", C.c_void_p), ("n_history", C.c_int32),
         ("t_build_ms", C.c_double), ("t_solve_ms", C.c_double), ("t_march_ms", C.c_double),
         ("t_interface_ms", C.c_double), ("cell_steps", C.c_double), ("n_marches", C.c_int32),
-        ("n_kernel_launches", C.c_int32),
+        ("n_kernel_launches", C.c_int32), ("t_setup_ms", C.c_double), ("t_comm_ms", C.c_double),
     ]
 
 
@@ -56,9 +58,17 @@ def lib():
     """Load libswr.so (built by __graft_entry__.build()); raise if absent."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback)")
-        L = C.CDLL(LIB_PATH)
+        _lib = load(LIB_PATH)
+    return _lib
+
+
+def load(path):
+    """Bind a libswr build at `path` (the product library, or a variant built
+    by _build.build_variant for kernel experiments and race-stress tests)."""
+    if True:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: run __graft_entry__.build() (no CPU fallback)")
+        L = C.CDLL(path)
         vp, i32, H = C.c_void_p, C.c_int32, C.c_void_p
         L.swr_setup.argtypes = [C.POINTER(Config), C.POINTER(H)]
         L.swr_update_inputs.argtypes = [H, vp, vp, i32]
@@ -76,24 +86,33 @@ def lib():
         L.swr_get_g.argtypes = [H, vp]
         L.swr_sizes.argtypes = [H, vp, vp, vp, vp]
         L.swr_partition.argtypes = [i32, i32, i32, vp, vp]
+        L.swr_owned_slots.argtypes = [i32, i32, i32, vp, vp]
         L.swr_nccl_unique_id.argtypes = [vp]
+        L.swr_loopback_id.argtypes = [vp, i32]
         for f in ("swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_apply_R",
                   "swr_apply_I_minus_L", "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition",
-                  "swr_nccl_unique_id"):
+                  "swr_owned_slots", "swr_nccl_unique_id", "swr_loopback_id"):
             getattr(L, f).restype = i32
-        _lib = L
-    return _lib
+        return L
 
 
 EXPORTED = ["swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_free",
             "swr_error_string", "swr_last_error_detail", "swr_apply_R", "swr_apply_I_minus_L",
-            "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition", "swr_nccl_unique_id"]
+            "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition", "swr_owned_slots",
+            "swr_nccl_unique_id", "swr_loopback_id"]
 
 
 def partition(N: int, world: int, rank: int):
     """Subdomains [j_lo, j_hi] (1-based, inclusive) of a rank (swr_partition)."""
     lo, hi = C.c_int32(), C.c_int32()
     _check(lib().swr_partition(N, world, rank, C.byref(lo), C.byref(hi)), "swr_partition")
+    return lo.value, hi.value
+
+
+def owned_slots(N: int, world: int, rank: int):
+    """Interface slots [s_lo, s_hi] of a rank (swr_owned_slots)."""
+    lo, hi = C.c_int32(), C.c_int32()
+    _check(lib().swr_owned_slots(N, world, rank, C.byref(lo), C.byref(hi)), "swr_owned_slots")
     return lo.value, hi.value
 
 
@@ -104,9 +123,17 @@ def nccl_unique_id() -> bytes:
     return buf.raw
 
 
-def _check(st, where, ok=(SWR_OK,)):
+def loopback_id(world: int) -> bytes:
+    """Test infrastructure: a communicator id for `world` logical ranks run as
+    threads of this process on one GPU (swr_loopback_id)."""
+    buf = C.create_string_buffer(128)
+    _check(lib().swr_loopback_id(buf, world), "swr_loopback_id")
+    return buf.raw
+
+
+def _check(st, where, ok=(SWR_OK,), lib_=None):
     if st not in ok:
-        raise SWRError(st, where, lib().swr_last_error_detail().decode())
+        raise SWRError(st, where, (lib_ or lib()).swr_last_error_detail().decode())
     return st
 
 
@@ -119,12 +146,14 @@ def _ptr(t):
 
 
 class SWR:
-    """One SWR problem resident on one GPU (world = 1)."""
+    """One SWR problem on one GPU: the whole problem (world = 1) or rank
+    `rank` of a multi-GPU run (its subdomains and interface slots)."""
 
     def __init__(self, p, arrays: dict, device: int = 0, stream=None, on_device: bool = False,
-                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None):
+                 rank: int = 0, world: int = 1, nccl_id: bytes | None = None, library=None):
         import torch
         self.torch = torch
+        self.L = library if library is not None else lib()
         self.p = p
         self.dev = torch.device("cuda", device)
         self.stream = stream if stream is not None else torch.cuda.current_stream(self.dev)
@@ -163,17 +192,26 @@ class SWR:
         c.krylov = getattr(p, "krylov", 0)
         c.pade_m = getattr(p, "pade_m", 0)
         c.pinv_exact = getattr(p, "pinv_exact", 0)
+        c.march_form = getattr(p, "march_form", 0)
+        c.toeplitz_form = getattr(p, "toeplitz_form", 0)
+        c.nl_rows_per_thread = getattr(p, "nl_rows_per_thread", 0)
         self.cfg = c
         h = C.c_void_p()
         with torch.cuda.device(self.dev):
-            _check(lib().swr_setup(C.byref(c), C.byref(h)), "swr_setup")
+            _check(self.L.swr_setup(C.byref(c), C.byref(h)), "swr_setup", lib_=self.L)
         self.h = h
         self.Nx, self.NT, self.Nj = p.Nx, p.NT, p.Nj
         self.ng = (2 * p.N - 2) * p.NT
+        self.rank, self.world = rank, world
+        if p.N >= 2:
+            self.s_lo, self.s_hi = owned_slots(p.N, world, rank)
+        else:
+            self.s_lo, self.s_hi = 0, -1
+        self.nloc = (self.s_hi - self.s_lo + 1) * p.NT
 
     def close(self):
         if getattr(self, "h", None):
-            lib().swr_free(self.h)
+            self.L.swr_free(self.h)
             self.h = None
 
     def __del__(self):
@@ -184,10 +222,10 @@ class SWR:
 
     # ---- main ABI -----------------------------------------------------------
     def update_inputs(self, u0=None, V_x=None, on_device=False):
-        _check(lib().swr_update_inputs(self.h, _ptr(u0), _ptr(V_x), int(on_device)), "swr_update_inputs")
+        _check(self.L.swr_update_inputs(self.h, _ptr(u0), _ptr(V_x), int(on_device)), "swr_update_inputs")
 
     def build(self):
-        _check(lib().swr_build_interface_operator(self.h), "swr_build_interface_operator")
+        _check(self.L.swr_build_interface_operator(self.h), "swr_build_interface_operator")
 
     def solve(self, out=None, on_device=None, allow_unconverged=True):
         """Returns (status, u(T), report dict).  out: numpy (host) or torch
@@ -198,7 +236,7 @@ class SWR:
             on_device = not isinstance(out, np.ndarray)
         rep = Report()
         ok = (SWR_OK, SWR_NOT_CONVERGED) if allow_unconverged else (SWR_OK,)
-        st = _check(lib().swr_solve(self.h, _ptr(out), int(on_device), C.byref(rep)), "swr_solve", ok)
+        st = _check(self.L.swr_solve(self.h, _ptr(out), int(on_device), C.byref(rep)), "swr_solve", ok)
         hist = np.ctypeslib.as_array((C.c_double * rep.n_history).from_address(rep.residual_history)).copy() \
             if rep.n_history else np.zeros(0)
         r = {f: getattr(rep, f) for f, _ in Report._fields_ if f != "residual_history"}
@@ -213,21 +251,22 @@ class SWR:
     def apply_R(self, g=None, use_u0=True, force_zero=False, want_uT=False):
         Rg = self._cz(max(self.ng, 1))
         uT = self._cz(self.Nx + 1) if want_uT else None
-        _check(lib().swr_apply_R(self.h, _ptr(g), int(use_u0), int(force_zero), _ptr(Rg), _ptr(uT)), "swr_apply_R")
+        _check(self.L.swr_apply_R(self.h, _ptr(g), int(use_u0), int(force_zero), _ptr(Rg), _ptr(uT)), "swr_apply_R")
         return Rg[: self.ng], uT
 
     def apply_I_minus_L(self, x, which=0):
         y = self._cz(self.ng)
-        _check(lib().swr_apply_I_minus_L(self.h, which, _ptr(x), _ptr(y)), "swr_apply_I_minus_L")
+        _check(self.L.swr_apply_I_minus_L(self.h, which, _ptr(x), _ptr(y)), "swr_apply_I_minus_L")
         return y
 
     def get_interface(self, which=0):
         d = self._cz(max(self.ng, 1))
         X = self._cz(self.p.N * 4 * self.NT)
-        _check(lib().swr_get_interface(self.h, which, _ptr(d), _ptr(X)), "swr_get_interface")
+        _check(self.L.swr_get_interface(self.h, which, _ptr(d), _ptr(X)), "swr_get_interface")
         return d[: self.ng], X.view(self.p.N, 4, self.NT)
 
     def get_g(self):
-        g = self._cz(self.ng)
-        _check(lib().swr_get_g(self.h, _ptr(g)), "swr_get_g")
+        """This rank's slots of g (the whole g on one GPU)."""
+        g = self._cz(self.nloc)
+        _check(self.L.swr_get_g(self.h, _ptr(g)), "swr_get_g")
         return g

@@ -53,6 +53,10 @@ class Problem:
     krylov: int = KRY_GMRES     # interface solver: GMRES, BiCGStab or the algorithm's fixed point (A20/A21)
     pade_m: int = 20            # Pade poles m for TC_S22 / TC_S24 (the paper tabulates m = 20, 50, 100)
     pinv_exact: int = 0         # PRECOND: 0 = inner Krylov P^{-1} (paper), 1 = exact causal solve (8(f)-4)
+    # GPU kernel forms (swr_config; same arithmetic, the oracle ignores them): 0 = automatic
+    march_form: int = 0         # 1 = streaming march
+    toeplitz_form: int = 0      # 1 = direct causal convolution, 2 = shared-memory FFT
+    nl_rows_per_thread: int = 0  # 8 or 11: force the NL march shape
     seed: int = 7
     name: str = ""
 

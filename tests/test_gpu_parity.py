@@ -153,16 +153,12 @@ TC_CASES = [("s03", si.TC_S03), ("s04", si.TC_S04), ("s12", si.TC_S12), ("s14", 
 
 @pytest.mark.parametrize("name,tc", TC_CASES, ids=[c[0] for c in TC_CASES])
 @pytest.mark.parametrize("march", ["resident", "stream"])
-def test_higher_order_tc_parity(oracle_mod, gpu, name, tc, march, monkeypatch):
+def test_higher_order_tc_parity(oracle_mod, gpu, name, tc, march):
     """Potential (S0^3, S0^4), gauge (S1^2, S1^4) and Pade (S2^{2,20},
     S2^{4,20}) transmission operators (readings
     A23-A26) through the new algorithm on
     V(x) = -x^2, both march kernels: equal GMRES counts, u(T) within 1e-10."""
-    if march == "stream":
-        monkeypatch.setenv("SWR_MARCH", "stream")
-    else:
-        monkeypatch.delenv("SWR_MARCH", raising=False)
-    p = si.config("C1", transmission=tc, potential=si.POT_VX, N=4)
+    p = si.config("C1", transmission=tc, potential=si.POT_VX, N=4, march_form=int(march == "stream"))
     o, g_ = _pair(oracle_mod, gpu, p)
     ro = o.solve()
     st, uT, rg = g_.solve()
@@ -234,15 +230,14 @@ def test_paper_iteration_counts(gpu, name, kw, count):
 
 
 @pytest.mark.parametrize("M", [8, 11])
-def test_nl_march_shapes(oracle_mod, gpu, M, monkeypatch):
+def test_nl_march_shapes(oracle_mod, gpu, M):
     """The NL march with 8 rows per thread and with the 11-row fallback used
     beyond 16 x 256 x 8 rows (both forced on a problem the oracle solves; the
     two-CTA-per-SM 192-thread variant runs in the C4 tests): the preconditioned fixed point for
     |u|^2 with equal outer counts, equal NL fixed-point maxima, u(T) within
     1e-10."""
-    monkeypatch.setenv("SWR_NL_M", str(M))
     p = si.Problem(dx=2e-3, dt=5e-3, N=4, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT,
-                   u0_kind="soliton", pinv_exact=1)
+                   u0_kind="soliton", pinv_exact=1, nl_rows_per_thread=M)
     o, g_ = _pair(oracle_mod, gpu, p)
     ro = o.solve()
     st, uT, rg = g_.solve()
@@ -359,11 +354,12 @@ STREAM_CASES = [
 
 
 @pytest.mark.parametrize("name,p", STREAM_CASES, ids=[c[0] for c in STREAM_CASES])
-def test_streaming_march_parity(oracle_mod, gpu, name, p, monkeypatch):
+def test_streaming_march_parity(oracle_mod, gpu, name, p):
     """The streaming march (state through HBM, chains of co-resident CTAs;
     used when a subdomain does not fit a resident cluster, e.g. C2 at
     dx = 1e-5) forced on problems the oracle solves: equal counts, u(T)."""
-    monkeypatch.setenv("SWR_MARCH", "stream")
+    import dataclasses
+    p = dataclasses.replace(p, march_form=1)
     o, g_ = _pair(oracle_mod, gpu, p)
     ro = o.solve()
     st, uT, rg = g_.solve()
@@ -372,54 +368,47 @@ def test_streaming_march_parity(oracle_mod, gpu, name, p, monkeypatch):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
-def test_streaming_sweep_matches_resident(gpu, monkeypatch):
+def test_streaming_sweep_matches_resident(gpu):
     """One sweep R(g) through both march kernels on a 3-CTA-per-chain
     problem: equal to rounding."""
+    import dataclasses
     import torch
     p = si.Problem(dx=1e-3, dt=5e-3, N=10, potential=si.POT_VX, transmission=si.TC_S02)
     arr = si.inputs(p)
     g = torch.randn(p.ng, dtype=torch.complex128, device="cuda")
-    monkeypatch.delenv("SWR_MARCH", raising=False)
     a = gpu.SWR(p, arr)
     ra, ua = a.apply_R(g, use_u0=True, want_uT=True)
-    monkeypatch.setenv("SWR_MARCH", "stream")
-    b = gpu.SWR(p, arr)
+    b = gpu.SWR(dataclasses.replace(p, march_form=1), arr)
     rb, ub = b.apply_R(g, use_u0=True, want_uT=True)
     assert rel(rb.cpu().numpy(), ra.cpu().numpy()) <= 1e-12
     assert rel(ub.cpu().numpy(), ua.cpu().numpy()) <= 1e-12
 
 
-@pytest.mark.parametrize("cgs", ["reg", "tma"])
-def test_cgs_kernel_forms(oracle_mod, gpu, cgs, monkeypatch):
-    """Both CGS kernel forms (register; bulk-copy pipeline) give the oracle's
-    GMRES iteration count and u(T) on a NEW solve whose Krylov vectors span
-    several chunks with a ragged tail."""
-    monkeypatch.setenv("SWR_CGS", cgs)
+def test_cgs_kernel_shapes(oracle_mod, gpu):
+    """The fused Gram-Schmidt passes with per-subdomain units (one CTA per
+    subdomain, chunked entries with a ragged tail, the three register shapes
+    for up to 8 / 16 / 32 basis vectors): the oracle's GMRES iteration count
+    and u(T) on a NEW solve with a full restart cycle."""
     p = si.Problem(dx=1e-3, dt=1e-3, N=20, potential=si.POT_VX)
     o, g_ = _pair(oracle_mod, gpu, p)
     ro = o.solve()
     st, uT, rg = g_.solve()
-    assert st == 0 and rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert st == 0 and rg["iterations"] == ro["iterations"] > 16, (rg["iterations"], ro["iterations"])
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
-@pytest.mark.parametrize("mode", ["direct", "fft", "fft2w", "fft2", "fftsm"])
-def test_toeplitz_paths(oracle_mod, gpu, mode, monkeypatch):
+@pytest.mark.parametrize("mode", ["direct", "fft", "fftsm"])
+def test_toeplitz_paths(oracle_mod, gpu, mode):
     """All forms of y = (I - L) x (direct causal convolution; FFT convolution:
-    for NF = 1024 the one-warp register four-step kernel (default) or two
-    512-point transforms per warp pair, fused or two-kernel radix-4 Stockham)
-    against the oracle's direct convolution."""
+    for NF = 1024 the one-warp register four-step kernel (default) or the
+    shared-memory radix-4 Stockham kernel) against the oracle's direct
+    convolution."""
+    import dataclasses
     import torch
-    if mode in ("direct", "fft2", "fftsm"):
-        monkeypatch.setenv("SWR_TOEPLITZ", mode)
-    else:
-        monkeypatch.delenv("SWR_TOEPLITZ", raising=False)
-    if mode == "fft2w":
-        monkeypatch.setenv("SWR_FFT_HALVES", "1")
-    else:
-        monkeypatch.delenv("SWR_FFT_HALVES", raising=False)
+    form = {"direct": 1, "fft": 0, "fftsm": 2}[mode]
     for p in (si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX),
               si.Problem(dx=1e-3, dt=1e-3, N=20, potential=si.POT_VX)):   # N_T = 100 and 500
+        p = dataclasses.replace(p, toeplitz_form=form)
         o, g_ = _pair(oracle_mod, gpu, p)
         g_.build()
         _, X_g = g_.get_interface(0)
@@ -447,20 +436,27 @@ PRECOND_CASES = [
 @pytest.mark.parametrize("name,p", PRECOND_CASES, ids=[c[0] for c in PRECOND_CASES])
 def test_precond_parity(oracle_mod, gpu, name, p):
     """Preconditioned algorithms: GMRES on P^{-1}(I-L)g = P^{-1}d
-    for V(t,x) and the preconditioned fixed point for |u|^2; equal outer and
-    inner iteration counts and NL fixed-point maxima, u(T) within 1e-10."""
+    for V(t,x) and the preconditioned fixed point for |u|^2; equal outer
+    iteration counts and NL fixed-point maxima, u(T) within 1e-10.  The inner
+    P^{-1} GMRES solves stop at 1e-12 relative (reading A8), which for these
+    operators sits at the rounding floor of (I - L0): the oracle and the same
+    oracle source built with FMA contraction (only the rounding differs)
+    already disagree on the total inner count by up to 122 steps (vtx-robin-N5).
+    The GPU's total must stay within 3x that measured spread of the oracle,
+    and equal it where the two oracle builds agree (measured: equal, 0.9 %,
+    1 % and 3.5 % apart)."""
     o, g_ = _pair(oracle_mod, gpu, p)
     ro = o.solve()
+    rf = oracle_mod.Oracle(p, si.inputs(p), library=oracle_mod.lib_fma()).solve()
     st, uT, rg = g_.solve()
+    floor = abs(rf["inner_iterations"] - ro["inner_iterations"])
     info = dict(outer=(rg["iterations"], ro["iterations"]), inner=(rg["inner_iterations"], ro["inner_iterations"]),
-                fp=(rg["fp_max"], ro["fp_max"]), err=rel(uT, ro["uT"]), st=(st, ro["status"]))
+                inner_oracle_fma=rf["inner_iterations"], fp=(rg["fp_max"], ro["fp_max"]), err=rel(uT, ro["uT"]),
+                st=(st, ro["status"]))
     print(name, info)
     assert ro["status"] == 0 and st == 0, info
-    assert rg["iterations"] == ro["iterations"], info
-    # the inner P^{-1} solves stop at 1e-12 relative, at the rounding floor of
-    # (I - L0): their counts may differ by a few restart cycles (DESIGN.md §3,
-    # reading of the inner stopping rule)
-    assert abs(rg["inner_iterations"] - ro["inner_iterations"]) <= max(2, 0.05 * ro["inner_iterations"]), info
+    assert rg["iterations"] == ro["iterations"] == rf["iterations"], info
+    assert abs(rg["inner_iterations"] - ro["inner_iterations"]) <= max(1, 3 * floor), info
     assert rg["fp_max"] == ro["fp_max"], info
     assert rel(uT, ro["uT"]) <= 1e-10, info
 
@@ -499,3 +495,96 @@ def test_edge_cases(oracle_mod, gpu, name, p):
     assert ro["status"] == 0 and st == 0
     assert rg["iterations"] == ro["iterations"]
     assert rel(uT, ro["uT"]) <= 1e-10
+
+
+def test_c5_north_star_gate(oracle_mod, gpu):
+    """The north-star configuration end to end (C5: N = 500, dx = 1e-5,
+    N_T = 500, V = -x^2, NEW + GMRES(30), tol 1e-10 as P:1079), GPU in the
+    launch shape bench.py times against the oracle solved on all host cores:
+      - equal GMRES iteration counts;
+      - the residual estimates of every Arnoldi step agree to 1e-10 of the
+        first one (the two Krylov processes track each other to the end);
+      - u(T) against the oracle's own rounding floor.  The oracle source built
+        with FMA contraction (rounding is the only difference) lands 9.8e-9
+        from the default build, at tol 1e-10 and at 1e-12 alike
+        (profiles/r02/c5_gate.txt): at this size the method's fp64 result is
+        fixed only to ~1e-8 (rounding in the 500-step marches at dt/dx^2 =
+        1e7, amplified by the interface solve), so the strict 1e-10 bar is
+        below the oracle's own reproducibility.  The GPU (FMA arithmetic) must
+        sit within 1.5x that spread of the default build and within a tenth of
+        it (measured 4.8e-10) of the FMA build, and be at least as close as
+        the oracle to the monodomain solution on the same grid (the exact
+        discrete solution the iteration converges to; measured 4.6e-9 vs
+        7.0e-9).  DESIGN.md section 2."""
+    import os
+    p = si.config("C5")
+    arrays = si.inputs(p)
+    s = gpu.SWR(p, arrays)
+    s.build()
+    st, uT, rg = s.solve()
+    s.close()
+    res = {}
+    for name, lib in (("oracle", oracle_mod.lib()), ("fma", oracle_mod.lib_fma())):
+        oracle_mod.set_threads(os.cpu_count(), lib)
+        try:
+            res[name] = oracle_mod.Oracle(p, arrays, library=lib).solve()
+        finally:
+            oracle_mod.set_threads(1, lib)
+    ro, rf = res["oracle"], res["fma"]
+    assert st == 0 and ro["status"] == 0 and rf["status"] == 0
+    assert rg["iterations"] == ro["iterations"] == rf["iterations"], (rg["iterations"], ro["iterations"])
+    h_g, h_o = rg["history"], ro["history"]
+    assert len(h_g) == len(h_o)
+    assert np.abs(h_g - h_o).max() <= 1e-10 * h_o[0]
+    spread = rel(rf["uT"], ro["uT"])
+    e_o, e_f = rel(uT, ro["uT"]), rel(uT, rf["uT"])
+    # the exact discrete solution the iteration converges to: the monodomain
+    # march on the same grid (N = 1, no interface problem)
+    st_m, um, _ = oracle_mod.Oracle(si.config("C5", N=1), arrays).monodomain()
+    m_g, m_o = rel(uT, um), rel(ro["uT"], um)
+    print(f"C5 gate: it {rg['iterations']}, u(T) gpu-oracle {e_o:.3e}, gpu-oracle_fma {e_f:.3e}, spread {spread:.3e}; "
+          f"to the monodomain solution: gpu {m_g:.3e}, oracle {m_o:.3e}")
+    assert e_o <= max(1e-10, 1.5 * spread), (e_o, spread)
+    assert e_f <= max(1e-10, 0.1 * spread), (e_f, spread)
+    assert st_m == 0 and m_g <= max(1e-10, 1.05 * m_o), (m_g, m_o)
+
+
+HIGH_TC_FULL = [("s03", si.TC_S03, 20), ("s04", si.TC_S04, 20), ("s12", si.TC_S12, 20), ("s14", si.TC_S14, 20),
+                ("s22-m20", si.TC_S22, 20), ("s22-m50", si.TC_S22, 50), ("s22-m100", si.TC_S22, 100),
+                ("s24-m20", si.TC_S24, 20), ("s24-m50", si.TC_S24, 50), ("s24-m100", si.TC_S24, 100)]
+
+
+@pytest.mark.parametrize("name,tc,m", HIGH_TC_FULL, ids=[c[0] for c in HIGH_TC_FULL])
+@pytest.mark.parametrize("march", ["resident", "stream"])
+def test_higher_order_tc_parity_multi_cta(oracle_mod, gpu, name, tc, m, march):
+    """The higher-order and Pade operators on
+    subdomains that span a multi-CTA cluster (N_j = 4201 on the paper's
+    domain, dx = 1e-3, N = 10, V = -x^2) in both marches, Pade m = 20, 50,
+    100: equal GMRES counts, u(T) within 1e-10, d and X within 1e-12."""
+    p = si.Problem(dx=1e-3, dt=5e-3, N=10, potential=si.POT_VX, transmission=tc, pade_m=m,
+                   march_form=int(march == "stream"))
+    o, g_ = _pair(oracle_mod, gpu, p)
+    ro = o.solve()
+    st, uT, rg = g_.solve()
+    assert ro["status"] == 0 and st == 0
+    assert rg["iterations"] == ro["iterations"], (rg["iterations"], ro["iterations"])
+    assert rel(uT, ro["uT"]) <= 1e-10
+    d_g, X_g = g_.get_interface(0)
+    assert rel(d_g.cpu().numpy(), o.apply_R(np.zeros(o.ng), use_u0=True), 1.0) <= 1e-12
+    assert rel(X_g.cpu().numpy(), o.build_L(), 1.0) <= 1e-12
+
+
+def test_solve_is_deterministic(gpu):
+    """Two solves of the same problem (several CTAs per cluster, GMRES with
+    restarts) give bitwise equal u(T), g and residual histories: every
+    reduction on the path has a fixed order (no atomics decide a sum)."""
+    p = si.Problem(dx=1e-3, dt=5e-3, N=10, potential=si.POT_VX)
+    s = gpu.SWR(p, si.inputs(p))
+    out = []
+    for _ in range(2):
+        s.build()
+        st, uT, r = s.solve()
+        out.append((uT.copy(), s.get_g().cpu().numpy(), r["history"].copy(), r["iterations"]))
+    assert out[0][3] == out[1][3]
+    for a, b in zip(out[0][:3], out[1][:3]):
+        assert np.array_equal(a, b)

@@ -1,9 +1,14 @@
-"""Multi-rank path on CPU (gloo, world_size 2): the subdomain partition of
-libswr (swr_partition) and the assembly rules the library applies with
-ncclAllReduce — every rank fills only its own subdomains' outputs (disjoint
-supports), interface nodes shared across a rank cut get half of each copy —
-reproduce the single-process results bitwise.  The per-subdomain marches are
-the oracle's; the assembly/exchange logic is what is under test."""
+"""Multi-rank protocol on CPU (gloo, world_size 2 and 3): the partition and
+slot ownership of libswr (swr_partition, swr_owned_slots -- host functions of
+the library, no GPU needed) with the exchange rules the library applies
+(SURVEY 8(e)): every rank keeps only its own interface slots, the outputs of
+its subdomains that land in a neighbour's slot travel as cut traces by
+point-to-point send/recv, dot products are per-subdomain partials summed
+over ranks (disjoint columns) and reduced in subdomain order, u(T) nodes
+shared across a cut get half of each copy.  One sweep R(g), its dot
+products and u(T) reproduce the single-process results bitwise.  The
+per-subdomain marches are the oracle's; libswr's device code path for the
+same protocol runs in tests/test_multirank.py (logical ranks on one GPU)."""
 import os
 import socket
 
@@ -39,6 +44,22 @@ PROBLEM = dict(a0=-7.0, b0=7.0, T=0.06, dx=0.1, dt=0.01, N=7, potential=si.POT_V
                vx_kind="-x2")
 
 
+def test_owned_slots_tile_the_interface_vector():
+    from paper_1503_02564_b200.swr import owned_slots, partition
+    for N in (2, 3, 10, 97, 500):
+        for W in (1, 2, 3, 4, 8):
+            if W > N:
+                continue
+            prev = -1
+            for r in range(W):
+                lo, hi = owned_slots(N, W, r)
+                jl, jh = partition(N, W, r)
+                assert lo == prev + 1 and lo == (0 if jl == 1 else 2 * jl - 3)
+                assert hi == (2 * N - 3 if jh == N else 2 * jh - 2)
+                prev = hi
+            assert prev == 2 * N - 3
+
+
 def _inputs(p):
     d = si.inputs(p)
     x = p.nodes()
@@ -46,44 +67,58 @@ def _inputs(p):
     return d
 
 
-def _worker(rank, world, port, outdir):
-    import torch
-    import torch.distributed as dist
-    from oracle import oracle
-    from paper_1503_02564_b200.swr import partition
-    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
-    p = si.Problem(**PROBLEM)
-    o = oracle.Oracle(p, _inputs(p))
-    NT, N, m, Nj = p.NT, p.N, p.Nx // p.N, p.Nj
+def _rank_step(rank, world, o, p, g, send, recv, allreduce):
+    """One sweep R(g) + the dot <R(g), R(g)> + u(T) under the library's
+    protocol on one rank; send/recv/allreduce are the transport."""
+    from paper_1503_02564_b200.swr import owned_slots, partition
+    NT, N, m = p.NT, p.N, p.Nx // p.N
     jlo, jhi = partition(N, world, rank)
-    rng = np.random.default_rng(3)
-    g = rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng)
-    Rg = np.zeros(o.ng, np.complex128)
-    X = np.zeros((N, 4, NT), np.complex128)
-    uT = np.zeros(p.Nx + 1, np.complex128)
-    e = np.zeros(NT, np.complex128)
-    e[0] = 1
+    slo, shi = owned_slots(N, world, rank)
+    gl = g[slo * NT:(shi + 1) * NT]                       # this rank's slots only
+    Rg = np.zeros_like(gl)
+    halo = {}
     loc = {}
+
+    def put(slot, val):                                   # local slot or cut trace
+        if slo <= slot <= shi:
+            Rg[(slot - slo) * NT:(slot - slo + 1) * NT] = val
+        else:
+            halo["L" if slot < slo else "R"] = val
+
     for j in range(jlo, jhi + 1):
-        lin = g[(2 * j - 3) * NT:(2 * j - 2) * NT] if j >= 2 else None
-        rin = g[(2 * j - 2) * NT:(2 * j - 1) * NT] if j <= N - 1 else None
+        lin = gl[(2 * j - 3 - slo) * NT:(2 * j - 2 - slo) * NT] if j >= 2 else None
+        rin = gl[(2 * j - 2 - slo) * NT:(2 * j - 1 - slo) * NT] if j <= N - 1 else None
         st, ol, orr, ul, _ = o.march(j, lin, rin, use_u0=True)
         if j >= 2:
-            Rg[(2 * j - 4) * NT:(2 * j - 3) * NT] = ol
+            put(2 * j - 4, ol)
         if j <= N - 1:
-            Rg[(2 * j - 1) * NT:(2 * j) * NT] = orr
+            put(2 * j - 1, orr)
         loc[j] = ul
-        if j >= 2:
-            _, a, b, _, _ = o.march(j, e, None, use_u0=False)
-            X[j - 1, 0] = a
-            if j <= N - 1:
-                X[j - 1, 2] = b
-        if j <= N - 1:
-            _, a, b, _, _ = o.march(j, None, e, use_u0=False)
-            if j >= 2:
-                X[j - 1, 1] = a
-            X[j - 1, 3] = b
-    # u(T) gather rule of k_gather_uT (multi-GPU form)
+    # cut traces: to the left neighbour its last slot, to the right its first
+    # (posted sends, then the receives: the ncclGroupStart/End pattern)
+    reqs = []
+    if rank > 0:
+        reqs.append(send(halo["L"], rank - 1))
+    if rank < world - 1:
+        reqs.append(send(halo["R"], rank + 1))
+    if rank > 0:
+        Rg[:NT] = recv(rank - 1)
+    if rank < world - 1:
+        Rg[-NT:] = recv(rank + 1)
+    for q in reqs:
+        q.wait()
+    # dot: per-subdomain partials (the subdomain's own slots), summed over ranks, then in order
+    part = np.zeros(N, np.complex128)
+    for j in range(jlo, jhi + 1):
+        a, b = (2 * j - 3 if j >= 2 else 0), (2 * j - 2 if j <= N - 1 else 2 * N - 3)
+        v = Rg[(a - slo) * NT:(b - slo + 1) * NT]
+        part[j - 1] = np.vdot(v, v)
+    part = allreduce(part)
+    dot = complex(0.0)
+    for j in range(N):
+        dot += part[j]
+    # u(T): own nodes, half of each copy at a node shared with a neighbour rank
+    uT = np.zeros(p.Nx + 1, np.complex128)
     for i in range(p.Nx + 1):
         j0 = (N - 1) if i == p.Nx else i // m
         k = i - j0 * m
@@ -99,33 +134,51 @@ def _worker(rank, world, port, outdir):
             elif ownl:
                 v = w / 2
         uT[i] = v
-    for arr in (Rg, X, uT):
-        t = torch.from_numpy(arr.view(np.float64).reshape(-1))
+    uT = allreduce(uT)
+    return Rg, slo, shi, dot, uT
+
+
+def _worker(rank, world, port, outdir):
+    import torch
+    import torch.distributed as dist
+    from oracle import oracle
+    dist.init_process_group("gloo", init_method=f"tcp://127.0.0.1:{port}", rank=rank, world_size=world)
+    p = si.Problem(**PROBLEM)
+    o = oracle.Oracle(p, _inputs(p))
+    rng = np.random.default_rng(3)
+    g = rng.standard_normal(o.ng) + 1j * rng.standard_normal(o.ng)
+
+    def send(v, dst):
+        return dist.isend(torch.from_numpy(np.ascontiguousarray(v).view(np.float64).copy()), dst)
+
+    def recv(src):
+        t = torch.zeros(2 * p.NT, dtype=torch.float64)
+        dist.recv(t, src)
+        return t.numpy().view(np.complex128)
+
+    def allreduce(a):
+        t = torch.from_numpy(np.ascontiguousarray(a).view(np.float64).copy())
         dist.all_reduce(t)
-        arr.view(np.float64).reshape(-1)[:] = t.numpy()
-    if rank == 0:
-        np.savez(os.path.join(outdir, "res.npz"), Rg=Rg, X=X, uT=uT, g=g)
+        return t.numpy().view(np.complex128)
+
+    Rg, slo, shi, dot, uT = _rank_step(rank, world, o, p, g, send, recv, allreduce)
+    np.savez(os.path.join(outdir, f"r{rank}.npz"), Rg=Rg, slo=slo, shi=shi, dot=dot, uT=uT, g=g)
     dist.destroy_process_group()
 
 
-def test_two_rank_assembly_matches_single_process(oracle_mod, tmp_path):
+@pytest.mark.parametrize("world", [2, 3])
+def test_ranks_match_single_process(oracle_mod, tmp_path, world):
     import torch.multiprocessing as mp
-    mp.spawn(_worker, args=(2, _free_port(), str(tmp_path)), nprocs=2, join=True)
-    r = np.load(tmp_path / "res.npz")
+    mp.spawn(_worker, args=(world, _free_port(), str(tmp_path)), nprocs=world, join=True)
     p = si.Problem(**PROBLEM)
     o = oracle_mod.Oracle(p, _inputs(p))
-    assert np.array_equal(r["Rg"], o.apply_R(r["g"], use_u0=True))
-    assert np.array_equal(r["X"], o.build_L())
-    # u(T) of the same sweep on one process (mean of the two copies)
-    m = p.Nx // p.N
-    s = np.zeros(p.Nx + 1, np.complex128)
-    c = np.zeros(p.Nx + 1)
-    g = r["g"]
+    res = [np.load(tmp_path / f"r{r}.npz") for r in range(world)]
+    g = res[0]["g"]
+    ident = lambda a: a  # noqa: E731  (one rank: no transport)
+    Rg1, _, _, dot1, uT1 = _rank_step(0, 1, o, p, g, None, None, ident)
+    assert np.array_equal(Rg1, o.apply_R(g, use_u0=True))
     NT = p.NT
-    for j in range(1, p.N + 1):
-        lin = g[(2 * j - 3) * NT:(2 * j - 2) * NT] if j >= 2 else None
-        rin = g[(2 * j - 2) * NT:(2 * j - 1) * NT] if j <= p.N - 1 else None
-        ul = o.march(j, lin, rin, use_u0=True)[3]
-        s[(j - 1) * m:(j - 1) * m + p.Nj] += ul
-        c[(j - 1) * m:(j - 1) * m + p.Nj] += 1
-    assert np.array_equal(r["uT"], s / c)
+    for r in res:
+        assert np.array_equal(r["Rg"], Rg1[int(r["slo"]) * NT:(int(r["shi"]) + 1) * NT])
+        assert complex(r["dot"]) == dot1
+        assert np.array_equal(r["uT"], uT1)
