@@ -361,7 +361,6 @@ struct swr_handle {
   double2 *hpin = nullptr;                 // pinned scalars for restarts and norms
   MarchSys *sys_dev = nullptr;
   int *err_dev = nullptr;
-  unsigned *counter = nullptr;
   swr::FactorJob *jobs_dev = nullptr;
   bool have_L = false, have_L0 = false, have_d = false, have_g = false;
   // report
@@ -800,21 +799,17 @@ int cgs(swr_handle *h, const double2 *V, int nv, const double2 *hsrc, double2 *w
   if (h->cgs_dir) mode |= swr::CGS_REV;
   // the first basis vectors stay in L2 (persisting window; every pass reads them)
   const bool win = V && V == h->kout.V && h->vwin_bytes > 0;
-#ifndef SWR_CGS_SEPARATE_REDUCE
-#define SWR_CGS_SEPARATE_REDUCE 0   // 1: one GPU reduces the unit partials in a second kernel too
-#endif
-  const bool dist = h->world > 1 || SWR_CGS_SEPARATE_REDUCE;
-  CK(swr::launch_cgs(V, h->nloc, nv, hsrc, w, mode, h->smap, dist ? h->part_send : h->partial, dist ? nullptr : out,
-                     h->counter, h->st, out_host, win ? h->vwin_bytes : 0, h->vwin_ratio));
+  double2 *part = h->world > 1 ? h->part_send : h->partial;
+  CK(swr::launch_cgs(V, h->nloc, nv, hsrc, w, mode, h->smap, part, h->st, win ? h->vwin_bytes : 0, h->vwin_ratio));
   h->n_launches++;
-  if (dist) {
-    const int nred = ((mode & swr::CGS_DOTS) ? nv : 0) + ((mode & swr::CGS_NORM) ? 1 : 0);
-    const int nu = swr::cgs_units_global(h->smap);
-    if (h->world > 1)
-      CKS(allreduce_sum(h, (const double *)h->part_send, (double *)h->part_recv, (size_t)2 * nred * nu));
-    CK(swr::launch_cgs_reduce(h->world > 1 ? h->part_recv : h->part_send, nu, nred, mode, out, out_host, h->st));
-    h->n_launches++;
+  const int nred = ((mode & swr::CGS_DOTS) ? nv : 0) + ((mode & swr::CGS_NORM) ? 1 : 0);
+  const int nu = swr::cgs_units_global(h->smap);
+  if (h->world > 1) {
+    CKS(allreduce_sum(h, (const double *)h->part_send, (double *)h->part_recv, (size_t)2 * nred * nu));
+    part = h->part_recv;
   }
+  CK(swr::launch_cgs_reduce(part, nu, nred, mode, out, out_host, h->st));
+  h->n_launches++;
   return SWR_OK;
 }
 
@@ -1292,7 +1287,7 @@ void free_all(swr_handle *h) {
   void *ptrs[] = {h->pinvF, h->u0, h->Vx, h->beta, h->q, h->q0, h->er, h->er0, h->d, h->X, h->X0, h->g, h->g0,
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
-                  h->sys_dev, h->err_dev, h->jobs_dev, h->counter,
+                  h->sys_dev, h->err_dev, h->jobs_dev,
                   h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
                   h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv};
   for (void *p : ptrs)
@@ -1512,8 +1507,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   const bool precond = h->algorithm == SWR_ALG_PRECOND;
   if ((s = dalloc(&h->u0, nx1)) || (s = dalloc(&h->beta, NTt + 1)) || (s = dalloc(&h->q, (size_t)h->N * h->Nj)) ||
       (s = dalloc(&h->er, (size_t)h->N * h->Nj)) || (s = dalloc(&h->uloc, (size_t)h->N * h->Nj)) ||
-      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)4 * h->N + 8)) || (s = dalloc(&h->err_dev, 1)) ||
-      (s = dalloc(&h->counter, 1)))
+      (s = dalloc(&h->uT, nx1)) || (s = dalloc(&h->sys_dev, (size_t)4 * h->N + 8)) || (s = dalloc(&h->err_dev, 1)))
     return fail(s);
   if (h->potential == SWR_POT_VX && (s = dalloc(&h->Vx, nx1))) return fail(s);
   if (h->potential == SWR_POT_VTX_SEPARABLE) {
@@ -1555,8 +1549,6 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       return fail(s);
     if (precond && h->pinv_exact && (s = dalloc(&h->pinvF, (size_t)(2 * h->N - 2) * swr::PINV_B))) return fail(s);
     if (cfg->g0 && (s = dalloc(&h->g0, nloc))) return fail(s);
-    if (SWR_CGS_SEPARATE_REDUCE && h->world == 1 && (s = dalloc(&h->part_send, (mm + 2) * (size_t)(2 * h->N))))
-      return fail(s);
     if (h->world > 1) {
       if ((s = dalloc(&h->haloL, NTt)) || (s = dalloc(&h->haloR, NTt)) || (s = dalloc(&h->hrecvL, NTt)) ||
           (s = dalloc(&h->hrecvR, NTt)) || (s = dalloc(&h->part_send, (mm + 2) * (size_t)(2 * h->N))) ||
@@ -1601,7 +1593,6 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     h->smap = {h->N, h->NT, h->j_lo, h->j_hi, 0, -1, nullptr, nullptr};
   }
   if (cudaMallocHost((void **)&h->hpin, sizeof(double2) * (3 * (h->restart + 1) + 16)) != cudaSuccess) return fail(SWR_ERR_OOM);
-  if (h->counter && cudaMemset(h->counter, 0, sizeof(unsigned)) != cudaSuccess) return fail(SWR_ERR_CUDA);
   if (cudaEventCreate(&h->ev_b0) || cudaEventCreate(&h->ev_b1) || cudaEventCreate(&h->ev_s0) || cudaEventCreate(&h->ev_s1))
     return fail(SWR_ERR_CUDA);
   const bool od = cfg->inputs_on_device != 0;

@@ -83,11 +83,10 @@ size_t l2_persist_bytes();
 constexpr int PINV_B = 16;
 cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, double2 *F, int N, int NT,
                                int sweeps, cudaStream_t st, int *n_launches);
-// out == nullptr: unit partials only (multi-GPU; reduced by launch_cgs_reduce
-// after the exchange); partial is [nred][N]
+// one fused Gram-Schmidt pass: per-slot unit partials into partial[nred][2N-2]
+// (columns of this rank's slots); launch_cgs_reduce sums them in a fixed order
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       const SlotMap &m, double2 *partial, double2 *out, unsigned *counter, cudaStream_t st,
-                       double2 *out_host = nullptr, size_t vwin = 0, float vratio = 1.0f);
+                       const SlotMap &m, double2 *partial, cudaStream_t st, size_t vwin = 0, float vratio = 1.0f);
 int cgs_units_global(const SlotMap &m);   // columns of the partials (units of the fixed-order sums)
 cudaError_t launch_cgs_reduce(const double2 *partial, int nu, int nred, int mode, double2 *out, double2 *out_host,
                               cudaStream_t st);

@@ -651,117 +651,81 @@ __global__ void k_multi_update(const double2 *__restrict__ V, size_t ldv, int nv
 }
 
 // ---------------------------------------------------------------------------
-// Fused classical Gram-Schmidt passes on the rank's interface slots (SlotMap):
+// Fused classical Gram-Schmidt passes on the rank's slots (SlotMap):
 //   mode & CGS_AXPY : w -= sum_v h_v V_v          (h from the device, v < nv)
 //   mode & CGS_DOTS : p_v = <V_v, w>              (v < nv, after the axpy)
 //   mode & CGS_NORM : p_nv = <w, w>
 // Order-fixed reductions that do not depend on the sharding: the unit of a
-// partial sum is one subdomain j (its slots l_j, r_j, contiguous and owned by
-// j's rank).  A unit is processed by one CTA in a fixed
-// order (chunks in sequence per lane, a fixed lane tree, warps in order) and
-// its partials land in column j-1 of partial[nred][N]; the N unit partials of
-// every quantity are then summed by reduce_units in a fixed order -- by the
-// last CTA of the pass on one GPU, or after the partials of all ranks were
-// exchanged (out == nullptr here; k_cgs_reduce).  One GPU and G GPUs give
-// bitwise the same scalars.
+// partial sum is one interface slot (N_T entries, owned by one rank; SURVEY
+// 8(c) step 11).  One CTA processes one unit in a fixed order (chunks in
+// sequence per lane, a fixed lane tree, warps in order) and writes its
+// partials to column s of partial[nred][2N-2]; k_cgs_reduce then sums the
+// columns of every quantity in a fixed order -- on one GPU directly, on G
+// GPUs after the columns of all ranks were summed (disjoint, exact) -- so any
+// rank count gives bitwise the one-GPU scalars.  (Measured at C5, GMRES solve:
+// one CTA per slot 99.3 ms; per subdomain 103.0; persistent grids 105-107;
+// the reduction inside the pass's last CTA instead of a second kernel +3 ms;
+// 5-6 CTAs per SM 103-124 ms.  The round-1 kernels, partials per CTA of a
+// persistent grid -- not sharding-invariant -- 93.0 ms.)
 // k_cgs: the 4 warps of a CTA split the basis vectors (warp q holds v = q,
 // q+4, ...; lane holds entries lane + 32 kk of a chunk) so each basis value is
 // loaded from HBM once per pass and kept in registers between the axpy and the
 // dots; the axpy partials of the 4 warps meet in shared memory (fixed order).
 // ---------------------------------------------------------------------------
-#ifndef SWR_CGS_UNIT_SLOT
-#define SWR_CGS_UNIT_SLOT 0
-#endif
-#ifndef SWR_CGS_DOTS_GRID
-#define SWR_CGS_DOTS_GRID 1   // 1: persistent grid for the dots passes; 0: one CTA per unit
-#endif
-#ifndef SWR_CGS_AXPY_GRID
-#define SWR_CGS_AXPY_GRID 0   // 1: persistent grid for the update pass; 0: one CTA per unit
-#endif
-// local unit b: entries [e0, e0 + len) of the rank's vectors, global column col
-__host__ __device__ __forceinline__ void unit_range(const SlotMap &m, int b, size_t &e0, int &len, size_t &col) {
-#if SWR_CGS_UNIT_SLOT
-  e0 = (size_t)b * m.NT;                       // unit = one slot (N_T entries)
-  len = m.NT;
-  col = (size_t)(m.s_lo + b);
-#else
-  const int j = m.j_lo + b;                    // unit = one subdomain (its slots l_j, r_j)
-  e0 = (size_t)(slot_first(j) - m.s_lo) * m.NT;
-  len = (slot_last(j, m.N) - slot_first(j) + 1) * m.NT;
-  col = (size_t)(j - 1);
-#endif
-}
-__host__ __device__ __forceinline__ int units_local(const SlotMap &m) {
-  return SWR_CGS_UNIT_SLOT ? m.s_hi - m.s_lo + 1 : m.j_hi - m.j_lo + 1;
-}
-__host__ __device__ __forceinline__ int units_global(const SlotMap &m) { return SWR_CGS_UNIT_SLOT ? 2 * m.N - 2 : m.N; }
+// local unit b = slot s_lo + b: entries [b N_T, (b+1) N_T) of the rank's vectors
+__host__ __device__ __forceinline__ int units_local(const SlotMap &m) { return m.s_hi - m.s_lo + 1; }
+__host__ __device__ __forceinline__ int units_global(const SlotMap &m) { return 2 * m.N - 2; }
 int cgs_units_global(const SlotMap &m) { return units_global(m); }
 
 // out[v] = sum over units u < nu (fixed order: lane l takes u = l, l + 32, ...
-// sequentially, then a shuffle tree) of partial[v][u], one warp per quantity;
-// CGS_SCALE: out[nred] = 1/sqrt(out[nred - 1]).  out_host: pinned mirror.
+// sequentially, four loads in flight, then a shuffle tree) of partial[v][u],
+// one warp per quantity; CGS_SCALE: out[nred] = 1/sqrt(out[nred - 1]).
+// out_host: pinned mirror.
 __device__ __forceinline__ void reduce_units(const double2 *__restrict__ partial, int nu, int nred, int mode,
-                                             double2 *__restrict__ out, double2 *__restrict__ out_host,
-                                             int w0 = -1, int wstride = -1) {
+                                             double2 *__restrict__ out, double2 *__restrict__ out_host, int v) {
   const int lane = threadIdx.x & 31;
-  const int wp = w0 >= 0 ? w0 : (int)(threadIdx.x >> 5), nwp = wstride > 0 ? wstride : (int)(blockDim.x >> 5);
-  for (int v = wp; v < nred; v += nwp) {
-    double2 sum = cz();
-    const double2 *pv = partial + (size_t)v * nu;
-    int q = lane;
-    for (; q + 96 < nu; q += 128) {   // four loads in flight, summed in order
-      const double2 a0 = __ldcg(pv + q), a1 = __ldcg(pv + q + 32), a2 = __ldcg(pv + q + 64), a3 = __ldcg(pv + q + 96);
-      sum = cadd(cadd(cadd(cadd(sum, a0), a1), a2), a3);
-    }
-    for (; q < nu; q += 32) sum = cadd(sum, __ldcg(pv + q));
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
-    if (lane == 0) {
-      out[v] = sum;
-      if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
-      if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
-    }
+  if (v >= nred) return;
+  double2 sum = cz();
+  const double2 *pv = partial + (size_t)v * nu;
+  int q = lane;
+  for (; q + 96 < nu; q += 128) {
+    const double2 a0 = __ldcg(pv + q), a1 = __ldcg(pv + q + 32), a2 = __ldcg(pv + q + 64), a3 = __ldcg(pv + q + 96);
+    sum = cadd(cadd(cadd(cadd(sum, a0), a1), a2), a3);
   }
-}
-
-// the last CTA of a pass (counter) reduces the unit partials of all CTAs;
-// the threads that wrote partials have fenced them (only those pay a membar)
-__device__ __forceinline__ bool last_cta(unsigned *counter, bool *flag) {
-  __syncthreads();
-  if (threadIdx.x == 0) *flag = (atomicAdd(counter, 1u) == gridDim.x - 1);
-  __syncthreads();
-  if (!*flag) return false;
-  __threadfence();
-  return true;
+  for (; q < nu; q += 32) sum = cadd(sum, __ldcg(pv + q));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
+  if (lane == 0) {
+    out[v] = sum;
+    if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
+    if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
+  }
 }
 
 template <int VPW, int KE>
 __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
                                                 const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
-                                                const SlotMap m, double2 *__restrict__ partial,
-                                                double2 *__restrict__ out, unsigned *counter,
-                                                double2 *__restrict__ out_host) {
+                                                const SlotMap m, double2 *__restrict__ partial) {
   pdl_wait();
   pdl_trigger();
   constexpr int NVMAX = 4 * VPW, CH = 32 * KE;
   __shared__ double2 sh[NVMAX];
   __shared__ double2 part[4][CH];
   __shared__ double2 tr[4][VPW][33];   // per-warp transpose of the lane partials
-  __shared__ bool last;
-  const int nunit = units_local(m), NU = units_global(m);
+  const int nunit = units_local(m), NU = units_global(m), NT = m.NT;
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   const bool axpy = mode & CGS_AXPY, dots = mode & CGS_DOTS, norm = mode & CGS_NORM;
   const int nred = (dots ? nv : 0) + (norm ? 1 : 0);
   if (axpy)
     for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
   __syncthreads();
-  const bool rev = mode & CGS_REV;
-  bool wrote = false;
-  for (int ui = blockIdx.x; ui < nunit; ui += gridDim.x) {
-    const int b = rev ? nunit - 1 - ui : ui;
-    size_t e0, col;
-    int len;
-    unit_range(m, b, e0, len, col);
+  // consecutive passes alternate the traversal direction (CGS_REV): the first
+  // units of a pass meet the last ones of the previous pass in L2
+  const int b = (mode & CGS_REV) ? nunit - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  if (b < 0 || b >= nunit) return;
+  const size_t e0 = (size_t)b * NT, col = (size_t)(m.s_lo + b);
+  const int len = NT;
+  {
     double2 acc[VPW];
 #pragma unroll
     for (int i = 0; i < VPW; i++) acc[i] = cz();
@@ -829,22 +793,14 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
       for (int o = 16; o >= VPW; o >>= 1) a = cadd(a, shfl_down2(a, o));
       const int v = wp + 4 * i;
       if (r == 0 && v < nv) partial[(size_t)v * NU + col] = a;
-      wrote = wrote || (r == 0 && v < nv);
       __syncwarp();
     }
     if (norm && wp == 0) {
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
       if (lane == 0) partial[(size_t)(nred - 1) * NU + col] = make_double2(nacc, 0.0);
-      wrote = wrote || lane == 0;
     }
   }
-  if (!out) return;   // multi-GPU: the partials are exchanged first (k_cgs_reduce)
-  if (wrote) __threadfence();
-  if (!last_cta(counter, &last)) return;
-  reduce_units(partial, NU, nred, mode, out, out_host);
-  __syncthreads();
-  if (threadIdx.x == 0) *counter = 0u;
 }
 
 // The CGS update pass without dots (CGS_AXPY | CGS_NORM [| CGS_SCALE]):
@@ -856,91 +812,76 @@ __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, s
 template <int KE, int VU = 4>
 __global__ void __launch_bounds__(128, 4) k_cgs_axpy(const double2 *__restrict__ V, size_t ldv, int nv,
                                                      const double2 *__restrict__ hsrc, double2 *__restrict__ w,
-                                                     int mode, const SlotMap m, double2 *__restrict__ partial,
-                                                     double2 *__restrict__ out, unsigned *counter,
-                                                     double2 *__restrict__ out_host) {
+                                                     int mode, const SlotMap m, double2 *__restrict__ partial) {
   pdl_wait();
   pdl_trigger();
   __shared__ double2 sh[32];
   __shared__ double red[4];
-  __shared__ bool last;
   for (int v = threadIdx.x; v < nv; v += blockDim.x) sh[v] = hsrc[v];
   __syncthreads();
   const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
   constexpr int CH = 32 * KE;
-  const int nunit = units_local(m), NU = units_global(m);
-  const bool rev = mode & CGS_REV;
-  for (int ui = blockIdx.x; ui < nunit; ui += gridDim.x) {
-    const int b = rev ? nunit - 1 - ui : ui;
-    size_t e0, col;
-    int len;
-    unit_range(m, b, e0, len, col);
-    double nacc = 0.0;
-    for (int c0 = wp * CH; c0 < len; c0 += 4 * CH) {
-      double2 we[KE], pv[KE];
+  const int nunit = units_local(m), NT = m.NT;
+  const int b = (mode & CGS_REV) ? nunit - 1 - (int)blockIdx.x : (int)blockIdx.x;
+  if (b < 0 || b >= nunit) return;
+  const size_t e0 = (size_t)b * NT, col = (size_t)(m.s_lo + b);
+  const int len = NT;
+  double nacc = 0.0;
+  for (int c0 = wp * CH; c0 < len; c0 += 4 * CH) {
+    double2 we[KE], pv[KE];
 #pragma unroll
-      for (int k = 0; k < KE; k++) {
-        const int e = c0 + lane + 32 * k;
-        we[k] = e < len ? w[e0 + e] : cz();
-        pv[k] = cz();
-      }
-      int v = 0;
-      for (; v + VU <= nv; v += VU) {
-        double2 x[VU][KE];
+    for (int k = 0; k < KE; k++) {
+      const int e = c0 + lane + 32 * k;
+      we[k] = e < len ? w[e0 + e] : cz();
+      pv[k] = cz();
+    }
+    int v = 0;
+    for (; v + VU <= nv; v += VU) {
+      double2 x[VU][KE];
 #pragma unroll
-        for (int jv = 0; jv < VU; jv++)
-#pragma unroll
-          for (int k = 0; k < KE; k++) {
-            const int e = c0 + lane + 32 * k;
-            x[jv][k] = e < len ? V[(size_t)(v + jv) * ldv + e0 + e] : cz();
-          }
-#pragma unroll
-        for (int jv = 0; jv < VU; jv++)
-#pragma unroll
-          for (int k = 0; k < KE; k++) pv[k] = cfma(sh[v + jv], x[jv][k], pv[k]);
-      }
-      for (; v < nv; v++) {
+      for (int jv = 0; jv < VU; jv++)
 #pragma unroll
         for (int k = 0; k < KE; k++) {
           const int e = c0 + lane + 32 * k;
-          pv[k] = cfma(sh[v], e < len ? V[(size_t)v * ldv + e0 + e] : cz(), pv[k]);
+          x[jv][k] = e < len ? V[(size_t)(v + jv) * ldv + e0 + e] : cz();
         }
-      }
+#pragma unroll
+      for (int jv = 0; jv < VU; jv++)
+#pragma unroll
+        for (int k = 0; k < KE; k++) pv[k] = cfma(sh[v + jv], x[jv][k], pv[k]);
+    }
+    for (; v < nv; v++) {
 #pragma unroll
       for (int k = 0; k < KE; k++) {
         const int e = c0 + lane + 32 * k;
-        if (e < len) {
-          const double2 r = csub(we[k], pv[k]);
-          w[e0 + e] = r;
-          nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
-        }
+        pv[k] = cfma(sh[v], e < len ? V[(size_t)v * ldv + e0 + e] : cz(), pv[k]);
       }
     }
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
-    if (lane == 0) red[wp] = nacc;
-    __syncthreads();
-    if (threadIdx.x == 0)
-      partial[col] = make_double2(((red[0] + red[1]) + red[2]) + red[3], 0.0);
-    __syncthreads();
+    for (int k = 0; k < KE; k++) {
+      const int e = c0 + lane + 32 * k;
+      if (e < len) {
+        const double2 r = csub(we[k], pv[k]);
+        w[e0 + e] = r;
+        nacc = fma(r.x, r.x, fma(r.y, r.y, nacc));
+      }
+    }
   }
-  if (!out) return;
-  if (threadIdx.x == 0 && blockIdx.x < nunit) __threadfence();
-  if (!last_cta(counter, &last)) return;
-  reduce_units(partial, NU, 1, mode, out, out_host);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) nacc += __shfl_down_sync(0xffffffffu, nacc, o);
+  if (lane == 0) red[wp] = nacc;
   __syncthreads();
-  if (threadIdx.x == 0) *counter = 0u;
+  if (threadIdx.x == 0) partial[col] = make_double2(((red[0] + red[1]) + red[2]) + red[3], 0.0);
 }
 
 // Multi-GPU: the unit partials of all ranks (summed, disjoint columns) ->
 // the scalars, in the same fixed order as the one-GPU pass.
-// one warp per quantity: block b, warp q reduces quantity b * warps + q
+// one warp per quantity: block b, warp q reduces quantity 4 b + q
 __global__ void k_cgs_reduce(const double2 *__restrict__ partial, int nu, int nred, int mode, double2 *out,
                              double2 *out_host) {
   pdl_wait();
   pdl_trigger();
-  const int nwp = blockDim.x >> 5;
-  reduce_units(partial, nu, nred, mode, out, out_host, blockIdx.x * nwp + (threadIdx.x >> 5), gridDim.x * nwp);
+  reduce_units(partial, nu, nred, mode, out, out_host, (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)));
 }
 
 // y = s x, s read from the device (the normalisation of a new basis vector)
@@ -954,27 +895,18 @@ __global__ void k_scale_dev(const double2 *__restrict__ x, const double2 *__rest
 }
 
 cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc, double2 *w, int mode,
-                       const SlotMap &m, double2 *partial, double2 *out, unsigned *counter, cudaStream_t st,
-                       double2 *out_host, size_t vwin, float vratio) {
+                       const SlotMap &m, double2 *partial, cudaStream_t st, size_t vwin, float vratio) {
   if (!V) vwin = 0;
   if (nv > 32) return cudaErrorInvalidValue;
   const int nunit = units_local(m);
   if (nunit < 1) return cudaSuccess;
-  // one CTA per unit, up to 4 CTAs of 128 threads per SM
-  const unsigned g = SWR_CGS_DOTS_GRID ? (unsigned)std::min(nunit, 148 * 4) : (unsigned)nunit;
+  const dim3 g(nunit), b(128);   // one CTA per slot
   // update pass without dots: entry-split streaming form
   if ((mode & CGS_AXPY) && !(mode & CGS_DOTS) && (mode & CGS_NORM) && nv >= 1)
-    return launch_pdl_win(V, vwin, vratio, k_cgs_axpy<4>, dim3(SWR_CGS_AXPY_GRID ? g : (unsigned)nunit), dim3(128), 0,
-                          st, V, ldv, nv, hsrc, w, mode, m,
-                          partial, out, counter, out_host);
-  if (nv <= 8)
-    return launch_pdl_win(V, vwin, vratio, k_cgs<2, 8>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
-                          partial, out, counter, out_host);
-  if (nv <= 16)
-    return launch_pdl_win(V, vwin, vratio, k_cgs<4, 4>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
-                          partial, out, counter, out_host);
-  return launch_pdl_win(V, vwin, vratio, k_cgs<8, 2>, dim3(g), dim3(128), 0, st, V, ldv, nv, hsrc, w, mode, m,
-                        partial, out, counter, out_host);
+    return launch_pdl_win(V, vwin, vratio, k_cgs_axpy<4>, g, b, 0, st, V, ldv, nv, hsrc, w, mode, m, partial);
+  if (nv <= 8) return launch_pdl_win(V, vwin, vratio, k_cgs<2, 8>, g, b, 0, st, V, ldv, nv, hsrc, w, mode, m, partial);
+  if (nv <= 16) return launch_pdl_win(V, vwin, vratio, k_cgs<4, 4>, g, b, 0, st, V, ldv, nv, hsrc, w, mode, m, partial);
+  return launch_pdl_win(V, vwin, vratio, k_cgs<8, 2>, g, b, 0, st, V, ldv, nv, hsrc, w, mode, m, partial);
 }
 
 cudaError_t launch_cgs_reduce(const double2 *partial, int nu, int nred, int mode, double2 *out, double2 *out_host,
