@@ -1,6 +1,6 @@
 """Aggregate an ncu --metrics gpu__time_duration.sum --csv launch list by kernel."""
-import collections, csv, sys
-rows = [r for r in csv.reader(open(sys.argv[1])) if len(r) > 5]
+import collections, csv, gzip, sys
+rows = [r for r in csv.reader((gzip.open if sys.argv[1].endswith(".gz") else open)(sys.argv[1], "rt")) if len(r) > 5]
 hdr, data = rows[0], rows[1:]
 iN, iV, iM = hdr.index("Kernel Name"), hdr.index("Metric Value"), hdr.index("Metric Name")
 agg = collections.defaultdict(lambda: [0, 0.0])
