@@ -677,31 +677,6 @@ __host__ __device__ __forceinline__ int units_local(const SlotMap &m) { return m
 __host__ __device__ __forceinline__ int units_global(const SlotMap &m) { return 2 * m.N - 2; }
 int cgs_units_global(const SlotMap &m) { return units_global(m); }
 
-// out[v] = sum over units u < nu (fixed order: lane l takes u = l, l + 32, ...
-// sequentially, four loads in flight, then a shuffle tree) of partial[v][u],
-// one warp per quantity; CGS_SCALE: out[nred] = 1/sqrt(out[nred - 1]).
-// out_host: pinned mirror.
-__device__ __forceinline__ void reduce_units(const double2 *__restrict__ partial, int nu, int nred, int mode,
-                                             double2 *__restrict__ out, double2 *__restrict__ out_host, int v) {
-  const int lane = threadIdx.x & 31;
-  if (v >= nred) return;
-  double2 sum = cz();
-  const double2 *pv = partial + (size_t)v * nu;
-  int q = lane;
-  for (; q + 96 < nu; q += 128) {
-    const double2 a0 = __ldcg(pv + q), a1 = __ldcg(pv + q + 32), a2 = __ldcg(pv + q + 64), a3 = __ldcg(pv + q + 96);
-    sum = cadd(cadd(cadd(cadd(sum, a0), a1), a2), a3);
-  }
-  for (; q < nu; q += 32) sum = cadd(sum, __ldcg(pv + q));
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
-  if (lane == 0) {
-    out[v] = sum;
-    if (out_host) out_host[v] = sum;   // pinned host mirror (read after the step's event)
-    if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
-  }
-}
-
 template <int VPW, int KE>
 __global__ void __launch_bounds__(128, 4) k_cgs(const double2 *__restrict__ V, size_t ldv, int nv,
                                                 const double2 *__restrict__ hsrc, double2 *__restrict__ w, int mode,
@@ -874,14 +849,40 @@ __global__ void __launch_bounds__(128, 4) k_cgs_axpy(const double2 *__restrict__
   if (threadIdx.x == 0) partial[col] = make_double2(((red[0] + red[1]) + red[2]) + red[3], 0.0);
 }
 
-// Multi-GPU: the unit partials of all ranks (summed, disjoint columns) ->
-// the scalars, in the same fixed order as the one-GPU pass.
-// one warp per quantity: block b, warp q reduces quantity 4 b + q
-__global__ void k_cgs_reduce(const double2 *__restrict__ partial, int nu, int nred, int mode, double2 *out,
-                             double2 *out_host) {
+// The unit partials (on G GPUs: of all ranks, summed -- disjoint columns) ->
+// the scalars in a fixed order that depends on the global unit count only:
+// one CTA of 256 threads per quantity; thread t sums units t, t + 256, ...
+// in sequence (all loads issued before the adds), then a fixed shuffle tree
+// per warp and the 8 warp sums in order.  CGS_SCALE: out[nred] =
+// 1/sqrt(out[nred - 1]).  out_host: pinned mirror (read after the step's event).
+constexpr int kRedThreads = 256;
+__global__ void __launch_bounds__(kRedThreads) k_cgs_reduce(const double2 *__restrict__ partial, int nu, int nred,
+                                                            int mode, double2 *out, double2 *out_host) {
   pdl_wait();
   pdl_trigger();
-  reduce_units(partial, nu, nred, mode, out, out_host, (int)(blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5)));
+  __shared__ double2 ws[kRedThreads / 32];
+  const int v = blockIdx.x, t = threadIdx.x, lane = t & 31;
+  const double2 *pv = partial + (size_t)v * nu;
+  double2 sum = cz();
+  int q = t;
+  for (; q + 3 * kRedThreads < nu; q += 4 * kRedThreads) {
+    const double2 a0 = __ldcg(pv + q), a1 = __ldcg(pv + q + kRedThreads), a2 = __ldcg(pv + q + 2 * kRedThreads),
+                  a3 = __ldcg(pv + q + 3 * kRedThreads);
+    sum = cadd(cadd(cadd(cadd(sum, a0), a1), a2), a3);
+  }
+  for (; q < nu; q += kRedThreads) sum = cadd(sum, __ldcg(pv + q));
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) sum = cadd(sum, shfl_down2(sum, o));
+  if (lane == 0) ws[t >> 5] = sum;
+  __syncthreads();
+  if (t == 0) {
+    sum = ws[0];
+#pragma unroll
+    for (int i = 1; i < kRedThreads / 32; i++) sum = cadd(sum, ws[i]);
+    out[v] = sum;
+    if (out_host) out_host[v] = sum;
+    if ((mode & CGS_SCALE) && v == nred - 1) out[v + 1] = make_double2(1.0 / sqrt(sum.x), 0.0);
+  }
 }
 
 // y = s x, s read from the device (the normalisation of a new basis vector)
@@ -911,8 +912,7 @@ cudaError_t launch_cgs(const double2 *V, size_t ldv, int nv, const double2 *hsrc
 
 cudaError_t launch_cgs_reduce(const double2 *partial, int nu, int nred, int mode, double2 *out, double2 *out_host,
                               cudaStream_t st) {
-  // one warp per reduced quantity (the same fixed order as the in-pass reduction)
-  return launch_pdl(k_cgs_reduce, dim3((nred + 3) / 4), dim3(128), 0, st, partial, nu, nred, mode, out, out_host);
+  return launch_pdl(k_cgs_reduce, dim3(nred), dim3(kRedThreads), 0, st, partial, nu, nred, mode, out, out_host);
 }
 
 // ---------------------------------------------------------------------------
