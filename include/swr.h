@@ -59,7 +59,7 @@ enum swr_status {
   SWR_ERR_BREAKDOWN = 4,
   SWR_ERR_INNER_NOT_CONVERGED = 5,/* P^{-1} GMRES or NL fixed point hit its cap */
   SWR_ERR_UNSUPPORTED = 6,        /* e.g. NEW with V(t,x) or f(u); f(u) = |u|^2 with
-                                     N_j > 45,056 rows (the nonlinear march is resident only) */
+                                     N_j > 65,536 rows (the nonlinear march is resident only) */
   SWR_ERR_CUDA = 7,
   SWR_ERR_NCCL = 8,
   SWR_ERR_OOM = 9
@@ -136,8 +136,9 @@ typedef struct {
   int32_t toeplitz_form;      /* (I - L) x: 0: FFT convolution (register four-step kernel for
                                  257 <= N_T <= 512, shared-memory radix-4 for N_T <= 256), the direct
                                  causal convolution for N_T > 512; 1: direct; 2: shared-memory FFT */
-  int32_t nl_rows_per_thread; /* f(u) march: 0: automatic; 8 or 11 forces the rows per thread (the
-                                 11-row shape serves 16 x 256 x 8 < N_j <= 45,056) */
+  int32_t nl_rows_per_thread; /* f(u) march: 0: automatic; 8, 11 or 16 forces the rows per thread
+                                 (the 16-row shape serves subdomains up to 16 x 256 x 16 = 65,536
+                                 rows) */
 } swr_config;
 
 typedef struct {

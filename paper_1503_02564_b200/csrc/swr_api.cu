@@ -350,6 +350,7 @@ struct swr_handle {
   double *ertd = nullptr;
   int *fp_stat = nullptr;
   MarchShape shape_nl;
+  double2 *hv_nl = nullptr;                // NL march: boundary-value histories [owned][2][N_T+1]
   double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr;
   double2 *partial = nullptr;
   // streaming march (subdomains too large for the resident kernel)
@@ -441,6 +442,7 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mo
   p.maxit_fp = h->maxit_fp;
   p.fp_stat = h->fp_stat;
   if (mode == MARCH_NL) {
+    p.hv_glob = h->hv_nl;
     CKS(record_pair(h, EV_MARCH, true));
     CK(swr::launch_march_nl(p, h->shape_nl, h->st));
     CK(cudaGetLastError());
@@ -1289,7 +1291,7 @@ void free_all(swr_handle *h) {
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev,
                   h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
-                  h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv};
+                  h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv, h->hv_nl};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
@@ -1424,8 +1426,9 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     return SWR_ERR_INVALID_ARG;
   }
   if (cfg->march_form < 0 || cfg->march_form > 1 || cfg->toeplitz_form < 0 || cfg->toeplitz_form > 2 ||
-      !(cfg->nl_rows_per_thread == 0 || cfg->nl_rows_per_thread == 8 || cfg->nl_rows_per_thread == 11)) {
-    g_detail = "march_form in {0,1}, toeplitz_form in {0,1,2}, nl_rows_per_thread in {0,8,11}";
+      !(cfg->nl_rows_per_thread == 0 || cfg->nl_rows_per_thread == 8 || cfg->nl_rows_per_thread == 11 ||
+        cfg->nl_rows_per_thread == 16)) {
+    g_detail = "march_form in {0,1}, toeplitz_form in {0,1,2}, nl_rows_per_thread in {0,8,11,16}";
     return SWR_ERR_INVALID_ARG;
   }
 
@@ -1532,11 +1535,13 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   }
   if ((s = dalloc(&h->fp_stat, 2))) return fail(s);
   if (cudaMemset(h->fp_stat, 0, 2 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_CUDA);
-  h->shape_nl = swr::choose_march_shape_nl(h->Nj, h->nl_rows);
-  if (h->potential == SWR_POT_CUBIC &&
-      (h->shape_nl.M == 0 || swr::march_nl_smem_bytes(h->shape_nl, h->NT, true) > 227 * 1024)) {
-    g_detail = "subdomain too large for the resident nonlinear march";
-    return fail(SWR_ERR_UNSUPPORTED);
+  h->shape_nl = swr::choose_march_shape_nl(h->Nj, h->nl_rows, h->j_hi - h->j_lo + 1);
+  if (h->potential == SWR_POT_CUBIC) {
+    if (h->shape_nl.M == 0 || swr::march_nl_smem_bytes(h->shape_nl, h->NT, false) > 227 * 1024) {
+      g_detail = "subdomain too large for the resident nonlinear march";
+      return fail(SWR_ERR_UNSUPPORTED);
+    }
+    if ((s = dalloc(&h->hv_nl, (size_t)(h->j_hi - h->j_lo + 1) * 2 * (NTt + 1)))) return fail(s);
   }
   if (precond && ((s = dalloc(&h->q0, (size_t)3 * h->Nj)) || (s = dalloc(&h->er0, (size_t)3 * h->Nj)))) return fail(s);
   if (ng) {

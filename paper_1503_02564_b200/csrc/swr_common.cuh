@@ -141,6 +141,7 @@ struct MarchParams {
   double tol_fp;
   int32_t maxit_fp;
   int32_t *fp_stat;          // [0] max fixed-point iterations (atomicMax), [1] = 1 if a step hit maxit_fp
+  double2 *hv_glob;          // k_march_nl: boundary-value histories [nsys][2][N_T+1] (scratch)
 };
 
 }  // namespace swr

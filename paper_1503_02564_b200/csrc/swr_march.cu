@@ -29,7 +29,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cooperative_groups.h>
-#include <cstdlib>
+#include <algorithm>
 
 namespace cg = cooperative_groups;
 
@@ -1135,6 +1135,21 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
 // max_k |z^{s+1} - z^s| <= tol_fp max_k |z^{s+1}| (reading A4; the maxima are
 // reduced over the cluster so the decision is uniform).  (A_NL - B) is the
 // V = 0 matrix: constant pivots, Re E_k = 1/h.
+//
+// Per fixed-point iteration: (1) a local forward pass from carry 0 builds the
+// rhs (stencil of u_{n-1} and the load of z^s) once and stores z^loc; (2) the
+// forward scan of the thread maps gives the carry z_{s0-1}; (3) a cheap pass
+// adds the carry's propagation (prefix products of c_k) to z^loc; (4) a local
+// backward pass, (5) the backward scan, (6) the exact backward pass, which
+// also yields the maxima.  The neighbour rows of the next iterate and of u_n
+// come from the scan carries (x_{s0+M} is the backward carry, x_{s0-1} =
+// z_{s0-1} + b_{s0-1} x_{s0}), so no halo exchange is needed; the scan totals
+// and the CTA maxima travel between the CTAs of the cluster by st.async into
+// parity buffers counted by mbarriers.  The thread's rows keep u_{n-1} and z^s
+// in registers; the (scaled) pivots and Re E_k sit in shared memory, so a CTA
+// holds more rows per register budget and more systems are resident at once
+// (C4: the 100 systems in one wave).  The boundary-value histories and the
+// flux series are read from global memory by the threads that own them.
 // ---------------------------------------------------------------------------
 template <int M, int PMAX, int MINB = 1>
 __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
@@ -1142,89 +1157,113 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
   const int P = blockDim.x, t = threadIdx.x, lane = t & 31, w = t >> 5, nw = P >> 5;
   const int CS = p.CS;
   const int crank = blockIdx.x % CS;
-  const MarchSys *G = p.sys + blockIdx.x / CS;
+  const int sysi = blockIdx.x / CS;
+  const MarchSys *G = p.sys + sysi;
   const int Nj = p.Nj, NT = p.NT;
   const int s0 = (crank * P + t) * M;
-  const double eim = p.e_im;
+  const double eim = p.e_im, kappa = p.kappa, ikappa = 1.0 / p.kappa;
+  const double eimk = eim * ikappa, hk = p.h12 * ikappa, lam = p.lambda;
 
-  double2 *ybuf = sm;                                   // [M][P]
-  double2 *hfirst = ybuf + M * P, *hlast = hfirst + P;  // [P] halo of u_{n-1}
-  double2 *zfirst = hlast + P, *zlast = zfirst + P;     // [P] halo of z^s
-  double2 *sAf = zlast + P, *sAb = sAf + P;             // [P]
-  ScanBuf<1> sf, sbk;
-  sf.wA = sAb + P;            sf.wB = sf.wA + 32;       sf.ctot = sf.wB + 32;
-  sbk.wA = sf.ctot + 32;      sbk.wB = sbk.wA + 32;     sbk.ctot = sbk.wB + 32;
-  double2 *hva = sbk.ctot + 32, *hvb = hva + (NT + 1);  // [NT+1]
-  double2 *hred = hvb + (NT + 1);                       // [2][32]
-  double2 *sH = hred + 64;                              // [2]
-  double2 *smax = sH + 2;                               // [32] warp maxima (x: |dz|^2, y: |z|^2); [32+16]: CTA maxima
-  double2 *sflux = smax + 64;                           // [2][NT] if p.flux_smem
-  double *sbeta = reinterpret_cast<double *>(sflux + (p.flux_smem ? 2 * NT : 0));
+  // ---- shared memory ----
+  unsigned long long *mbar = reinterpret_cast<unsigned long long *>(sm);   // [fwd 2][bwd 2][max 2]
+  double2 *ybuf = sm + 4;                               // [max(M,2)][P] z^loc, then z (first: the u_0 halo)
+  double2 *sq = ybuf + (M < 2 ? 2 : M) * P;             // [M][P] scaled pivots i kappa q_k
+  double *ser = reinterpret_cast<double *>(sq + M * P); // [M][P] scaled Re E_k / kappa
+  double2 *sAf = reinterpret_cast<double2 *>(ser + M * P);   // [P]
+  double2 *sAb = sAf + P;                               // [P]
+  ScanBuf<1> sf, sbk;                                   // ctot: [2 parities][16][2]
+  sf.wA = sAb + P;             sf.wB = sf.wA + 32;      sf.ctot = sf.wB + 32;
+  sbk.wA = sf.ctot + 64;       sbk.wB = sbk.wA + 32;    sbk.ctot = sbk.wB + 32;
+  double2 *cmax = sbk.ctot + 64;                        // [2 parities][16] CTA maxima (x: |dz|^2, y: |z|^2)
+  double2 *wmax = cmax + 32;                            // [32] warp maxima
+  double2 *hred = wmax + 32;                            // [2 sides][32] warp partials of the history
+  double2 *sH = hred + 64;                              // [2] H_a, H_b of the step
+  double2 *hva = p.hv_glob + (size_t)sysi * 2 * (NT + 1), *hvb = hva + (NT + 1);   // v_s(a_j), v_s(b_j)
 
   const int flags = G->flags;
   const bool has_left = flags & SYS_HAS_LEFT, has_right = flags & SYS_HAS_RIGHT;
   const int rows_cta = P * M;
   const int cb = (Nj - 1) / rows_cta, tb = ((Nj - 1) % rows_cta) / M;
-  const bool owns_a = has_left && s0 == 0;
-  const bool owns_b = has_right && crank == cb && t == tb;
-
-  for (int i = t; i <= NT; i += P) sbeta[i] = p.beta[i];
-  if (p.flux_smem) {
-    for (int i = t; i < NT; i += P) {
-      sflux[i] = G->lin ? G->lin[i] : cz();
-      sflux[NT + i] = G->rin ? G->rin[i] : cz();
-    }
+  const bool first = s0 == 0;                           // holds row 0
+  const bool last = crank == cb && t == tb;             // holds row N_j - 1
+  const int ib = (Nj - 1) - s0;                         // its index in the thread (if last)
+  const bool owns_a = has_left && first, owns_b = has_right && last;
+  if (t == 0) {
+    for (int i = 0; i < 6; i++) mbar_init(mbar + i, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (t < 2) sH[t] = cz();
 
-  double2 u[M], q[M], ze[M];
-  double er[M];
-  double er_prev;
+  // coefficients (rows beyond N_j: q = 0, which decouples them) and the
+  // per-thread linear parts of the forward / backward maps
+  double2 u[M], ze[M];
+  double2 qprev = cz();
+  double er_prev = 0.0;
   {
-#pragma unroll
-    for (int i = 0; i < M; i++) {
-      const int k = s0 + i;
-      q[i] = k < Nj ? G->q[k] : make_double2(1.0, 0.0);
-      er[i] = k < Nj ? G->er[k] : 0.0;
-      u[i] = (G->u0 && k < Nj) ? G->u0[k] : cz();
-      ze[i] = u[i];                                   // z^0 of step 1 = v_0 = u_0
-    }
-    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? G->er[s0 - 1] : 0.0;
     double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0);
+    er_prev = (s0 >= 1 && s0 - 1 < Nj) ? G->er[s0 - 1] : 0.0;
+    qprev = (s0 >= 1 && s0 - 1 < Nj) ? G->q[s0 - 1] : cz();
+    double erl = er_prev;
 #pragma unroll
     for (int i = 0; i < M; i++) {
       const int k = s0 + i;
-      const double2 c = (k >= 1 && k < Nj) ? negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim) : cz();
-      const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
-      Af = cmul(Af, c);
-      Ab = cmul(Ab, b);
+      const double2 qv = k < Nj ? G->q[k] : cz();
+      const double ev = k < Nj ? G->er[k] : 0.0;
+      Af = cmul(Af, negqe(qv, erl, eim));
+      Ab = cmul(Ab, negqe(qv, ev, eim));
+      sq[i * P + t] = cimul(kappa, qv);
+      ser[i * P + t] = ev * ikappa;
+      erl = ev;
+      u[i] = (G->u0 && k < Nj) ? G->u0[k] : cz();
+      ze[i] = u[i];                                     // z^0 of step 1 = v_0 = u_0
     }
     sAf[t] = Af;
     sAb[t] = Ab;
+    qprev = cimul(kappa, qprev);
+    er_prev *= ikappa;
   }
-  if (s0 == 0) hva[0] = u[0];
+  if (first) hva[0] = u[0];
+  if (last) {
 #pragma unroll
-  for (int i = 0; i < M; i++)
-    if (s0 + i == Nj - 1) hvb[0] = u[i];
-  __syncthreads();
+    for (int i = 0; i < M; i++)
+      if (i == ib) hvb[0] = u[i];
+  }
+  // halo of u_0 and z^0 (later neighbour values come from the scan carries)
+  double2 *hfirst = ybuf, *hlast = ybuf + P;             // ybuf is free before the first pass
+  hfirst[t] = u[0];
+  hlast[t] = u[M - 1];
+  csync(CS, true);
+  double2 uL = cz(), uR = cz();
+  if (t > 0) uL = hlast[t - 1];
+  else if (crank > 0) uL = *remote(hlast + (P - 1), crank - 1);
+  if (t < P - 1) uR = hfirst[t + 1];
+  else if (crank < CS - 1) uR = *remote(hfirst, crank + 1);
+  csync(CS);   // every (remote) halo read is done before ybuf is written
+  double2 zL = uL, zR = uR;
 
   auto flux = [&](int side, int n) -> double2 {
     const int imp = side == 0 ? (flags & SYS_LIN_IMPULSE) : (flags & SYS_RIN_IMPULSE);
     if (imp) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
-    return p.flux_smem ? sflux[side * NT + n - 1] : cz();
+    const double2 *f = side == 0 ? G->lin : G->rin;
+    return f ? f[n - 1] : cz();
   };
+  auto Qc = [&](int i) -> double2 { return sq[i * P + t]; };
+  auto Ec = [&](int i) -> double { return ser[i * P + t]; };
   int fp_max = 0, fp_fail = 0;
+  unsigned sc = 0;   // fixed-point iterations so far: parity buffers and mbarrier phases
 
 #pragma unroll 1
   for (int n = 1; n <= NT; n++) {
     race_jitter(0, n);
+    // ---- S0^2 history H_n = c2 (beta_1 v_{n-1} + sum_{s<=n-2} beta_{n-s} v_s)
     if (p.s02) {
       if (has_left && crank == 0) {
         double2 acc = cz();
         for (int s = t; s < n - 1; s += P) {
-          const double b = sbeta[n - s];
-          acc.x = fma(b, hva[s].x, acc.x);
-          acc.y = fma(b, hva[s].y, acc.y);
+          const double b = __ldg(p.beta + n - s);
+          const double2 hv = hva[s];
+          acc.x = fma(b, hv.x, acc.x);
+          acc.y = fma(b, hv.y, acc.y);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
@@ -1233,177 +1272,197 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
       if (has_right && crank == cb) {
         double2 acc = cz();
         for (int s = t; s < n - 1; s += P) {
-          const double b = sbeta[n - s];
-          acc.x = fma(b, hvb[s].x, acc.x);
-          acc.y = fma(b, hvb[s].y, acc.y);
+          const double b = __ldg(p.beta + n - s);
+          const double2 hv = hvb[s];
+          acc.x = fma(b, hv.x, acc.x);
+          acc.y = fma(b, hv.y, acc.y);
         }
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
         if (lane == 0) hred[32 + w] = acc;
       }
+      __syncthreads();
     }
-    hfirst[t] = u[0];
-    hlast[t] = u[M - 1];
-    csync(CS, t == 0 || t == P - 1);
-    if (p.s02 && (owns_a || owns_b)) {
-      if (owns_a) {
-        double2 hh = cscale(sbeta[1], hva[n - 1]);
-        for (int qq = 0; qq < nw; qq++) hh = cadd(hh, hred[qq]);
-        sH[0] = cmul(p.c2, hh);
+    // ---- end rows: the P1 mass end rows (h/6)(2, 1) and b_n - l_n / b_n - r_n
+    // folded into the stencil neighbours u_{-1} and the row after N_j - 1 ----
+    if (first || last) {
+      if (first) {
+        double2 d = cz();
+        if (owns_a) {
+          double2 h = cz();
+          if (p.s02) {
+            h = cscale(__ldg(p.beta + 1), hva[n - 1]);
+            for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[qq]);
+            h = cmul(p.c2, h);
+          }
+          sH[0] = h;
+          d = csub(h, flux(0, n));
+        }
+        const double2 f = ifold(d, ikappa);
+        uL = make_double2(fma(-2.0, u[0].x, f.x), fma(-2.0, u[0].y, f.y));
       }
-      if (owns_b) {
-        double2 hh = cscale(sbeta[1], hvb[n - 1]);
-        for (int qq = 0; qq < nw; qq++) hh = cadd(hh, hred[32 + qq]);
-        sH[1] = cmul(p.c2, hh);
+      if (last) {
+        double2 d = cz();
+        if (owns_b) {
+          double2 h = cz();
+          if (p.s02) {
+            h = cscale(__ldg(p.beta + 1), hvb[n - 1]);
+            for (int qq = 0; qq < nw; qq++) h = cadd(h, hred[32 + qq]);
+            h = cmul(p.c2, h);
+          }
+          sH[1] = h;
+          d = csub(h, flux(1, n));
+        }
+        const double2 f = ifold(d, ikappa);
+#pragma unroll
+        for (int i = 0; i < M; i++)
+          if (i == ib) {
+            const double2 un = make_double2(fma(-2.0, u[i].x, f.x), fma(-2.0, u[i].y, f.y));
+            if (i == M - 1) uR = un;
+            else u[i == M - 1 ? M - 1 : i + 1] = un;   // the (padding) row after N_j - 1
+          }
       }
     }
-    double2 uL = cz(), uR = cz();
-    if (t > 0) uL = hlast[t - 1];
-    else if (crank > 0) uL = *remote(hlast + (P - 1), crank - 1);
-    if (t < P - 1) uR = hfirst[t + 1];
-    else if (crank < CS - 1) uR = *remote(hfirst, crank + 1);
 
     int it;
     bool conv = false;
+    double2 zc = cz(), xc = cz();
 #pragma unroll 1
-    for (it = 1; it <= p.maxit_fp; it++) {
-      // halo of z^s
-      zfirst[t] = ze[0];
-      zlast[t] = ze[M - 1];
-      csync(CS, t == 0 || t == P - 1);
-      double2 zL = cz(), zR = cz();
-      if (t > 0) zL = zlast[t - 1];
-      else if (crank > 0) zL = *remote(zlast + (P - 1), crank - 1);
-      if (t < P - 1) zR = zfirst[t + 1];
-      else if (crank < CS - 1) zR = *remote(zfirst, crank + 1);
-      // forward sweep with rhs = (2i/dt) M u_{n-1} - M_{f(z)} z + b_n - Q^T(l,r)
+    for (it = 1; it <= p.maxit_fp; it++, sc++) {
+      const int pb = sc & 1;
+      const uint32_t ph = (sc >> 1) & 1;
+      ScanBuf<1> sfp = sf, sbp = sbk;
+      sfp.ctot += pb * 32;
+      sbp.ctot += pb * 32;
+      // (1) local forward pass: rhs = i kappa (u_{k-1} + 4 u_k + u_{k+1}) - (h/12) load_k(z^s),
+      // scaled by 1 / (i kappa) into the stencil (the pivots carry i kappa)
       double2 z = cz();
-#pragma unroll 1
-      for (int pass = 0; pass < 2; pass++) {
-        launder<M>(q, er);
 #pragma unroll
-        for (int i = 0; i < M; i++) {
-          const int k = s0 + i;
-          double2 c = cz(), rr = cz();
-          if (k < Nj) {
-            const double2 um = i == 0 ? uL : u[i == 0 ? 0 : i - 1];
-            const double2 up = i == M - 1 ? uR : u[i == M - 1 ? M - 1 : i + 1];
-            rr = rhs_row<true>(k, Nj, um, u[i], up, p.kappa);
-            // weighted mass load (P1 elements, linear interpolant of W = f(z))
-            const double2 zm = i == 0 ? zL : ze[i == 0 ? 0 : i - 1];
-            const double2 zp = i == M - 1 ? zR : ze[i == M - 1 ? M - 1 : i + 1];
-            const double2 zc = ze[i];
-            const double Wc = p.lambda * fma(zc.x, zc.x, zc.y * zc.y);
-            const double Wm = p.lambda * fma(zm.x, zm.x, zm.y * zm.y);
-            const double Wp = p.lambda * fma(zp.x, zp.x, zp.y * zp.y);
-            double2 ld = cz();
-            if (k > 0) {   // element (k-1, k)
-              ld.x += (Wm + 3.0 * Wc) * zc.x + (Wm + Wc) * zm.x;
-              ld.y += (Wm + 3.0 * Wc) * zc.y + (Wm + Wc) * zm.y;
-            }
-            if (k < Nj - 1) {  // element (k, k+1)
-              ld.x += (3.0 * Wc + Wp) * zc.x + (Wc + Wp) * zp.x;
-              ld.y += (3.0 * Wc + Wp) * zc.y + (Wc + Wp) * zp.y;
-            }
-            rr = make_double2(fma(-p.h12, ld.x, rr.x), fma(-p.h12, ld.y, rr.y));
-            if (k == 0 && owns_a) rr = cadd(rr, csub(sH[0], flux(0, n)));
-            if (k == Nj - 1 && owns_b) rr = cadd(rr, csub(sH[1], flux(1, n)));
-            if (k >= 1) c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
-          }
-          z = cfma(c, z, cmul(q[i], rr));
-          if (pass == 1) ybuf[i * P + t] = z;
+      for (int i = 0; i < M; i++) {
+        const double2 c = ck(Qc(i), i == 0 ? er_prev : Ec(i == 0 ? 0 : i - 1), eimk);
+        const double2 um = i == 0 ? uL : u[i == 0 ? 0 : i - 1];
+        const double2 up = i == M - 1 ? uR : u[i == M - 1 ? M - 1 : i + 1];
+        const double2 sr = srow(um, u[i], up);
+        // weighted mass load (P1 elements, linear interpolant of W = f(z))
+        const double2 zm = i == 0 ? zL : ze[i == 0 ? 0 : i - 1];
+        const double2 zp = i == M - 1 ? zR : ze[i == M - 1 ? M - 1 : i + 1];
+        const double2 zk = ze[i];
+        const double Wc = lam * fma(zk.x, zk.x, zk.y * zk.y);
+        const double Wm = lam * fma(zm.x, zm.x, zm.y * zm.y);
+        const double Wp = lam * fma(zp.x, zp.x, zp.y * zp.y);
+        double2 ld = cz();
+        if (!(first && i == 0)) {             // element (k-1, k)
+          ld.x = fma(Wm + 3.0 * Wc, zk.x, (Wm + Wc) * zm.x);
+          ld.y = fma(Wm + 3.0 * Wc, zk.y, (Wm + Wc) * zm.y);
         }
-        if (pass == 0) {
-          double2 zz[1] = {z}, carry[1];
-          race_jitter(1, n);
-          scan_maps<1, true>(sAf[t], zz, sf, lane, w, nw, CS, crank, carry);
-          z = carry[0];
+        if (!(last && i == ib)) {             // element (k, k+1)
+          ld.x = fma(3.0 * Wc + Wp, zk.x, fma(Wc + Wp, zp.x, ld.x));
+          ld.y = fma(3.0 * Wc + Wp, zk.y, fma(Wc + Wp, zp.y, ld.y));
         }
+        // sr - (h/12) ld / (i kappa) = sr + i (h / (12 kappa)) ld
+        const double2 rr = make_double2(fma(-hk, ld.y, sr.x), fma(hk, ld.x, sr.y));
+        z = cfma(c, z, cmul(Qc(i), rr));
+        ybuf[i * P + t] = z;
       }
-      double2 x = cz();
-      launder<M>(q, er);
+      // (2) forward scan: carry z_{s0-1}
+      {
+        double2 zz[1] = {z}, carry[1];
+        race_jitter(1, n);
+        scan_maps<1, true, true>(sAf[t], zz, sfp, lane, w, nw, CS, crank, carry, nullptr, mbar + pb, ph);
+        zc = carry[0];
+      }
+      // (3) z_i = z^loc_i + (prod_{k<=i} c_k) z_{s0-1}; (4) local backward pass
+      double2 a = zc, x = cz();
 #pragma unroll
-      for (int i = M - 1; i >= 0; i--) {
-        const int k = s0 + i;
-        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
-        x = cfma(b, x, ybuf[i * P + t]);
+      for (int i = 0; i < M; i++) {
+        const double2 c = ck(Qc(i), i == 0 ? er_prev : Ec(i == 0 ? 0 : i - 1), eimk);
+        a = cmul(c, a);
+        ybuf[i * P + t] = cadd(ybuf[i * P + t], a);
       }
+#pragma unroll
+      for (int i = M - 1; i >= 0; i--) x = cfma(ck(Qc(i), Ec(i), eimk), x, ybuf[i * P + t]);
+      // (5) backward scan: carry x_{s0+M}
       {
         double2 xx[1] = {x}, carry[1];
-        scan_maps<1, false>(sAb[t], xx, sbk, lane, w, nw, CS, crank, carry);
-        x = carry[0];
+        race_jitter(2, n);
+        scan_maps<1, false, true>(sAb[t], xx, sbp, lane, w, nw, CS, crank, carry, nullptr, mbar + 2 + pb, ph);
+        xc = carry[0];
       }
-      launder<M>(q, er);
+      // (6) exact backward pass: z^{s+1} and the maxima
+      x = xc;
       double dmax = 0.0, nmax = 0.0;
 #pragma unroll
       for (int i = M - 1; i >= 0; i--) {
-        const int k = s0 + i;
-        const double2 b = (k < Nj - 1) ? negqe(q[i], er[i], eim) : cz();
-        x = cfma(b, x, ybuf[i * P + t]);
-        if (k < Nj) {
-          const double dx = x.x - ze[i].x, dy = x.y - ze[i].y;
-          dmax = fmax(dmax, fma(dx, dx, dy * dy));
-          nmax = fmax(nmax, fma(x.x, x.x, x.y * x.y));
-        }
+        x = cfma(ck(Qc(i), Ec(i), eimk), x, ybuf[i * P + t]);
+        const double dx = x.x - ze[i].x, dy = x.y - ze[i].y;
+        dmax = fmax(dmax, fma(dx, dx, dy * dy));
+        nmax = fmax(nmax, fma(x.x, x.x, x.y * x.y));
         ze[i] = x;
       }
+      // neighbour rows of z^{s+1}: x_{s0+M} (carry), x_{s0-1} = z_{s0-1} + b_{s0-1} x_{s0}
+      zR = xc;
+      zL = s0 > 0 ? cfma(ck(qprev, er_prev, eimk), ze[0], zc) : cz();
       // cluster-wide maxima -> uniform convergence decision
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) {
         dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
         nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
       }
-      if (lane == 0) smax[w] = make_double2(dmax, nmax);
+      if (lane == 0) wmax[w] = make_double2(dmax, nmax);
       __syncthreads();
-      double2 mm = lane < nw ? smax[lane] : cz();
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) {
-        mm.x = fmax(mm.x, __shfl_xor_sync(0xffffffffu, mm.x, o));
-        mm.y = fmax(mm.y, __shfl_xor_sync(0xffffffffu, mm.y, o));
+      double2 mm = make_double2(0.0, 0.0);
+      for (int q = 0; q < nw; q++) {
+        const double2 v = wmax[q];
+        mm.x = fmax(mm.x, v.x);
+        mm.y = fmax(mm.y, v.y);
       }
       if (CS > 1) {
+        double2 *cm = cmax + pb * 16;
         if (t == 0) {
+          const uint32_t src = smem_u32(cm + crank), lmb = smem_u32(mbar + 4 + pb);
 #pragma unroll 1
-          for (int c = 0; c < CS; c++) *remote(smax + 32 + crank, c) = mm;
-          asm volatile("fence.acq_rel.cluster;" ::: "memory");
+          for (int c = 0; c < CS; c++)
+            if (c != crank) st_async(mapa(src, c), mm, mapa(lmb, c));
+          mbar_expect_tx(mbar + 4 + pb, (unsigned)((CS - 1) * 16));
         }
-        asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-        asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-        mm = cz();
+        race_jitter(3, n);
+        mbar_wait(mbar + 4 + pb, ph);
         for (int c = 0; c < CS; c++) {
-          const double2 v = smax[32 + c];
+          if (c == crank) continue;
+          const double2 v = cm[c];
           mm.x = fmax(mm.x, v.x);
           mm.y = fmax(mm.y, v.y);
         }
       }
-      if (sqrt(mm.x) <= p.tol_fp * sqrt(mm.y)) { conv = true; break; }
+      if (sqrt(mm.x) <= p.tol_fp * sqrt(mm.y)) { conv = true; sc++; break; }
     }
     if (!conv) { it = p.maxit_fp; fp_fail = 1; }
     if (it > fp_max) fp_max = it;
     // v_n = z; record S v_n at the interfaces; u_n = 2 v_n - u_{n-1}
-#pragma unroll
-    for (int i = 0; i < M; i++) {
-      const int k = s0 + i;
-      const double2 x = ze[i];
-      if (k == 0 && owns_a) {
-        hva[n] = x;
-        if (G->out_left) {
-          const double2 sv = cfma(p.c0, x, sH[0]);
-          const double2 l = flux(0, n);
-          G->out_left[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
-        }
+    if (first) {
+      hva[n] = ze[0];
+      if (owns_a && G->out_left) {
+        const double2 sv = cfma(p.c0, ze[0], sH[0]);
+        const double2 l = flux(0, n);
+        G->out_left[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
       }
-      if (k == Nj - 1 && owns_b) {
-        hvb[n] = x;
-        if (G->out_right) {
-          const double2 sv = cfma(p.c0, x, sH[1]);
-          const double2 rv = flux(1, n);
-          G->out_right[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
-        }
-      }
-      u[i] = make_double2(fma(2.0, x.x, -u[i].x), fma(2.0, x.y, -u[i].y));
     }
-    __syncthreads();   // smax and the z halo are rewritten next step
+    if (last) {
+#pragma unroll
+      for (int i = 0; i < M; i++)
+        if (i == ib) {
+          hvb[n] = ze[i];
+          if (owns_b && G->out_right) {
+            const double2 sv = cfma(p.c0, ze[i], sH[1]);
+            const double2 rv = flux(1, n);
+            G->out_right[n - 1] = make_double2(fma(2.0, sv.x, -rv.x), fma(2.0, sv.y, -rv.y));
+          }
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < M; i++) u[i] = make_double2(fma(2.0, ze[i].x, -u[i].x), fma(2.0, ze[i].y, -u[i].y));
+    uL = make_double2(fma(2.0, zL.x, -uL.x), fma(2.0, zL.y, -uL.y));
+    uR = make_double2(fma(2.0, zR.x, -uR.x), fma(2.0, zR.y, -uR.y));
   }
   if (G->uT) {
 #pragma unroll
@@ -1414,7 +1473,7 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
     atomicMax(p.fp_stat, fp_max);
     if (fp_fail) atomicOr(p.fp_stat + 1, 1);
   }
-  if (CS > 1) cg::this_cluster().sync();
+  if (CS > 1) cg::this_cluster().sync();  // keep shared memory alive for remote writers
 }
 
 // ---------------------------------------------------------------------------
@@ -1446,40 +1505,52 @@ MarchShape choose_march_shape(int Nj, int NT, bool tc_hi) {
   return best;
 }
 
-// rows: 0 = automatic, 8 or 11 forces the rows per thread (tests of the
-// large-subdomain shape on small problems; swr_config.nl_rows_per_thread)
-MarchShape choose_march_shape_nl(int Nj, int rows) {
+// Nonlinear march instantiations: M rows per thread, PMAX threads, MINB CTAs
+// per SM (register cap 65536 / (PMAX MINB)).  The shape minimises
+// waves x (M + 14) x (1 + 0.1 (CS - 1)): a wave is the systems whose clusters
+// are resident at once (148 SMs x CTAs per SM / CS); the rows per thread set
+// the length of every pass, the scans cost about 14 rows' worth.  rows: 0 = automatic, else forces M
+// (tests of the large-subdomain shapes on small problems;
+// swr_config.nl_rows_per_thread).
+struct InstNL { int M, PMAX, MINB; };
+static const InstNL kInstNL[] = {{1, 512, 1}, {2, 512, 1}, {4, 256, 2}, {8, 192, 2}, {11, 192, 2}, {11, 128, 3},
+                                 {11, 256, 1}, {16, 256, 1}};
+
+size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
+  (void)NT;
+  (void)flux_smem;
+  const size_t MP = (size_t)s.M * s.P;
+  const size_t d2 = 4 + (size_t)(s.M < 2 ? 2 : s.M) * s.P + MP + 2 * (size_t)s.P + 2 * (32 + 32 + 64) + 32 + 32 +
+                    64 + 2;
+  return d2 * sizeof(double2) + MP * sizeof(double);
+}
+
+MarchShape choose_march_shape_nl(int Nj, int rows, int nsys) {
   MarchShape best{0, 0, 0, 1};
   double best_cost = 1e300;
-  const int m_env = rows;
   for (int CS = 1; CS <= 16; CS++) {
-    for (int M : {1, 2, 4, 8, 11}) {
-      if (m_env && M != m_env) continue;
-      if (M == 11 && !m_env) continue;   // only when nothing smaller fits (below)
-      const int PMAX = M <= 2 ? 512 : 256;
+    for (const InstNL &in : kInstNL) {
+      if (rows && in.M != rows) continue;
+      const int M = in.M;
       long per = ((long)Nj + (long)CS * M - 1) / ((long)CS * M);
       int P = (int)((per + 31) / 32 * 32);
       if (P < 32) P = 32;
-      if (P > PMAX) continue;
-      double padded = (double)CS * P * M;
-      double cost = padded * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
-      if (cost < best_cost) { best_cost = cost; best = {M, P, CS, 1}; }
-    }
-  }
-  if (best.M == 0 && !m_env) {   // N_j beyond 16 x 256 x 8 rows: 11 rows per thread
-    for (int CS = 1; CS <= 16 && best.M == 0; CS++) {
-      const long per = ((long)Nj + (long)CS * 11 - 1) / ((long)CS * 11);
-      const int P = (int)((per + 31) / 32 * 32);
-      if (P <= 256) best = {11, P < 32 ? 32 : P, CS, 1};
+      if (P > in.PMAX) continue;
+      const MarchShape sh{M, P, CS, 1};
+      const size_t smem = march_nl_smem_bytes(sh, 0, false);
+      if (smem > 227 * 1024) continue;
+      int per_sm = std::min(in.MINB, (int)((228 * 1024) / (smem + 1024)));
+      per_sm = std::min(per_sm, (int)(65536 / ((size_t)P * (65536 / (in.PMAX * in.MINB)))));
+      if (per_sm < 1) continue;
+      const int clusters = std::max(1, 148 * per_sm / CS);
+      const int waves = (std::max(nsys, 1) + clusters - 1) / clusters;
+      // a step costs ~ (M + 14) row-units: the passes scale with M, the scans and
+      // cluster exchanges (~14 rows' worth at C5) do not
+      const double cost = (double)waves * (M + 14) * (1.0 + 0.10 * (CS - 1)) * (P < 128 ? 1.3 : 1.0);
+      if (cost < best_cost) { best_cost = cost; best = sh; }
     }
   }
   return best;
-}
-
-size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem) {
-  size_t d2 = (size_t)s.M * s.P + 6 * (size_t)s.P + 4 * 32 + 2 * 32 + 2 * (size_t)(NT + 1) + 64 + 2 + 64 +
-              (flux_smem ? 2 * (size_t)NT : 0);
-  return d2 * sizeof(double2) + sizeof(double) * (size_t)(NT + 1);
 }
 
 template <int M, int PMAX, int MINB = 1>
@@ -1511,29 +1582,27 @@ static cudaError_t launch_nl_m(const MarchParams &p, const MarchShape &s, size_t
     cudaOccupancyMaxActiveClusters(&ncl, (void *)kern, &cfg);
     cudaFuncAttributes fa;
     cudaFuncGetAttributes(&fa, kern);
-    fprintf(stderr, "k_march_nl M=%d P=%d CS=%d systems=%d regs=%d smem=%zu: %d clusters resident\n", M, s.P, s.CS,
-            p.nsys, fa.numRegs, smem, ncl);
+    fprintf(stderr, "k_march_nl M=%d P=%d CS=%d systems=%d regs=%d local=%zu smem=%zu: %d clusters resident\n", M,
+            s.P, s.CS, p.nsys, fa.numRegs, fa.localSizeBytes, smem, ncl);
   }
   return cudaLaunchKernelEx(&cfg, kern, p);
 }
 
 cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st) {
   p.CS = s.CS;
-  const size_t smem = march_nl_smem_bytes(s, p.NT, p.flux_smem);
+  if (!p.hv_glob) return cudaErrorInvalidValue;
+  const size_t smem = march_nl_smem_bytes(s, p.NT, false);
   if (smem > 227 * 1024) return cudaErrorInvalidValue;
-  switch (s.M) {
-    case 1: return launch_nl_m<1, 512>(p, s, smem, st);
-    case 2: return launch_nl_m<2, 512>(p, s, smem, st);
-    case 4: return launch_nl_m<4, 256>(p, s, smem, st);
-    case 8:
-      // two CTAs per SM when the CTA has <= 192 threads (register cap 170):
-      // twice the resident clusters, fewer waves of systems (C4: 3 -> 2)
-      if (s.P <= 192) return launch_nl_m<8, 192, 2>(p, s, smem, st);
-      return launch_nl_m<8, 256>(p, s, smem, st);
-    case 11:   // the largest subdomains (up to 16 x 256 x 11 = 45,056 rows)
-      return launch_nl_m<11, 256>(p, s, smem, st);
-    default: return cudaErrorInvalidValue;
-  }
+  // the shape came from kInstNL: the same (M, P range) picks the instantiation
+  if (s.M == 1) return launch_nl_m<1, 512>(p, s, smem, st);
+  if (s.M == 2) return launch_nl_m<2, 512>(p, s, smem, st);
+  if (s.M == 4) return launch_nl_m<4, 256, 2>(p, s, smem, st);
+  if (s.M == 8) return launch_nl_m<8, 192, 2>(p, s, smem, st);
+  if (s.M == 11 && s.P <= 128) return launch_nl_m<11, 128, 3>(p, s, smem, st);
+  if (s.M == 11 && s.P <= 192) return launch_nl_m<11, 192, 2>(p, s, smem, st);
+  if (s.M == 11) return launch_nl_m<11, 256, 1>(p, s, smem, st);
+  if (s.M == 16) return launch_nl_m<16, 256, 1>(p, s, smem, st);
+  return cudaErrorInvalidValue;
 }
 
 size_t march_smem_bytes(const MarchShape &s, int NT, bool flux_smem, bool tc_hi) {

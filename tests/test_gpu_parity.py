@@ -229,11 +229,11 @@ def test_paper_iteration_counts(gpu, name, kw, count):
     assert st == 0 and r["iterations"] == count, (r["iterations"], count)
 
 
-@pytest.mark.parametrize("M", [8, 11])
+@pytest.mark.parametrize("M", [8, 11, 16])
 def test_nl_march_shapes(oracle_mod, gpu, M):
-    """The NL march with 8 rows per thread and with the 11-row fallback used
-    beyond 16 x 256 x 8 rows (both forced on a problem the oracle solves; the
-    two-CTA-per-SM 192-thread variant runs in the C4 tests): the preconditioned fixed point for
+    """The NL march with 8, 11 and 16 rows per thread (the 16-row shape serves
+    the largest resident subdomains; each forced on a problem the oracle
+    solves; the automatic C4 shape runs in the C4 tests): the preconditioned fixed point for
     |u|^2 with equal outer counts, equal NL fixed-point maxima, u(T) within
     1e-10."""
     p = si.Problem(dx=2e-3, dt=5e-3, N=4, potential=si.POT_CUBIC, algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT,
