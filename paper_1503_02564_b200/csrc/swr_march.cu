@@ -123,11 +123,10 @@ struct ScanBuf {
 
 // Exclusive scan of the per-thread affine maps z -> A z + B_k (k < K) in row
 // order (FWD) or reverse row order; returns the carries (the composition of
-// all earlier maps applied to 0).  One bar.sync (+ one cluster barrier).
-// ASYNC: the CTA totals travel by st.async into the parity buffer sb.ctot of
-// every CTA that needs them, counted by that CTA's mbarrier mb (phase parity
-// ph); otherwise by DSMEM stores + fence + cluster barrier.
-template <int K, bool FWD, bool ASYNC = false>
+// all earlier maps applied to 0).  One bar.sync; the CTA totals travel by
+// st.async into the parity buffer sb.ctot of every CTA that needs them,
+// counted by that CTA's mbarrier mb (phase parity ph).
+template <int K, bool FWD>
 __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const ScanBuf<K> &sb, int lane, int w, int nw,
                                           int CS, int crank, double2 (&carry)[K], long long *tr = nullptr,
                                           unsigned long long *mb = nullptr, uint32_t ph = 0) {
@@ -193,67 +192,64 @@ __device__ __forceinline__ void scan_maps(double2 A, double2 (&B)[K], const Scan
     for (int k = 0; k < K; k++) xb[k] = cz();
   }
   if (tr) tr[2] = clock64();
-  if (CS > 1) {
-    // CTA total = inclusive over all warps (lane nw-1 forward, lane 0 backward)
-    const int tl = FWD ? nw - 1 : 0;
-    const bool pusher = (w == 0) && lane == tl;
-    const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
-    if (ASYNC) {
-      if (pusher) {
-        const uint32_t src = smem_u32(sb.ctot + crank * (1 + K)), lmb = smem_u32(mb);
-#pragma unroll 1
-        for (int c = c0; c < c1; c++) {
-          const uint32_t dst = mapa(src, c), rmb = mapa(lmb, c);
-          st_async(dst, a, rmb);
-#pragma unroll
-          for (int k = 0; k < K; k++) st_async(dst + 16 * (1 + k), b[k], rmb);
-        }
-      }
-      if (tr) tr[3] = clock64();
-      const int nin = FWD ? crank : CS - 1 - crank;   // CTAs whose totals this CTA receives
-      if (nin > 0) {
-        if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(nin * 16 * (1 + K)));
-        mbar_wait(mb, ph);
-      }
-    } else {
-      if (pusher) {
-#pragma unroll 1
-        for (int c = c0; c < c1; c++) {
-          double2 *dst = remote(sb.ctot + crank * (1 + K), c);
-          dst[0] = a;
-#pragma unroll
-          for (int k = 0; k < K; k++) dst[1 + k] = b[k];
-        }
-        asm volatile("fence.acq_rel.cluster;" ::: "memory");
-      }
-      if (tr) tr[3] = clock64();
-      asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
-      asm volatile("barrier.cluster.wait.aligned;" ::: "memory");
-    }
-  }
-  if (tr) tr[4] = clock64();
   double2 val[K];
 #pragma unroll
   for (int k = 0; k < K; k++) val[k] = cz();
   if (CS > 1) {
-    if (FWD) {
-#pragma unroll 1
-      for (int c = 0; c < crank; c++) {
-        const double2 *tc = sb.ctot + c * (1 + K);
-        const double2 ca = tc[0];
+    // CTA total = inclusive over all warps (lane nw-1 forward, lane 0 backward),
+    // broadcast over warp 0; lane i of warp 0 pushes it to the i-th CTA that
+    // needs it (st.async, counted by that CTA's mbarrier)
+    const int tl = FWD ? nw - 1 : 0;
+    const int c0 = FWD ? crank + 1 : 0, c1 = FWD ? CS : crank;
+    if (w == 0) {
+      const double2 ta = make_double2(__shfl_sync(0xffffffffu, a.x, tl), __shfl_sync(0xffffffffu, a.y, tl));
+      double2 tb[K];
 #pragma unroll
-        for (int k = 0; k < K; k++) val[k] = cfma(ca, val[k], tc[1 + k]);
-      }
-    } else {
-#pragma unroll 1
-      for (int c = CS - 1; c > crank; c--) {
-        const double2 *tc = sb.ctot + c * (1 + K);
-        const double2 ca = tc[0];
+      for (int k = 0; k < K; k++)
+        tb[k] = make_double2(__shfl_sync(0xffffffffu, b[k].x, tl), __shfl_sync(0xffffffffu, b[k].y, tl));
+      const int c = c0 + lane;
+      if (c < c1) {
+        const uint32_t dst = mapa(smem_u32(sb.ctot + crank * (1 + K)), c), rmb = mapa(smem_u32(mb), c);
+        st_async(dst, ta, rmb);
 #pragma unroll
-        for (int k = 0; k < K; k++) val[k] = cfma(ca, val[k], tc[1 + k]);
+        for (int k = 0; k < K; k++) st_async(dst + 16 * (1 + k), tb[k], rmb);
       }
     }
+    if (tr) tr[3] = clock64();
+    const int nin = FWD ? crank : CS - 1 - crank;   // CTAs whose totals this CTA receives
+    if (nin > 0) {
+      if (threadIdx.x == 0) mbar_expect_tx(mb, (unsigned)(nin * 16 * (1 + K)));
+      mbar_wait(mb, ph);
+      // fold of the received totals in chain order (the earlier CTAs' maps
+      // forward, the later ones' backward) applied to 0: a tree over the
+      // lanes of every warp (lane i holds the i-th map of the chain order)
+      double2 fa = make_double2(1.0, 0.0), fb[K];
+#pragma unroll
+      for (int k = 0; k < K; k++) fb[k] = cz();
+      if (lane < nin) {
+        const int c = FWD ? lane : CS - 1 - lane;
+        const double2 *tc = sb.ctot + c * (1 + K);
+        fa = tc[0];
+#pragma unroll
+        for (int k = 0; k < K; k++) fb[k] = tc[1 + k];
+      }
+#pragma unroll
+      for (int o = 1; o < 16; o <<= 1) {
+        if (o >= nin) break;
+        // lane l (span [l, l+o)) then lane l+o (span [l+o, l+2o)): second o first
+        const double2 na = shfl_down2(fa, o);
+#pragma unroll
+        for (int k = 0; k < K; k++) {
+          const double2 nb = shfl_down2(fb[k], o);
+          if (lane + o < 32) fb[k] = cfma(na, fb[k], nb);
+        }
+        if (lane + o < 32) fa = cmul(na, fa);
+      }
+#pragma unroll
+      for (int k = 0; k < K; k++) val[k] = make_double2(__shfl_sync(0xffffffffu, fb[k].x, 0), __shfl_sync(0xffffffffu, fb[k].y, 0));
+    }
   }
+  if (tr) tr[4] = clock64();
 #pragma unroll
   for (int k = 0; k < K; k++) {
     val[k] = cfma(xa, val[k], xb[k]);
@@ -760,29 +756,44 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     sbp.ctot += pb * 16 * (1 + K);
 #pragma unroll
     for (int r = 0; r < K; r++) z[r] = cz();
-#pragma unroll 1
-    for (int pass = 0; pass < 2; pass++) {
+    // local forward pass from carry 0 (z^loc stored), the scan for the carry
+    // z_{s0-1}, then z_i = z^loc_i + (prod_{k<=i} c_k) z_{s0-1} by a fix-up pass
+    // (the rhs is built once per step)
+    launder<M>(q, er);
+#pragma unroll
+    for (int i = 0; i < M; i++) {
+      const double2 c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
+#pragma unroll
+      for (int r = 0; r < K; r++) {
+        const double2 rr = rhs_row<false>(0, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
+                                          i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], kappa);
+        z[r] = cfma(c, z[r], cmul(q[i], rr));
+        ybuf[(r * M + i) * P + t] = z[r];
+      }
+    }
+    {
+      double2 carry[K];
+      SWR_TRACE(3);
+      race_jitter(1, n);
+      scan_maps<K, true>(sAf[t], z, sfp, lane, w, nw, CS, crank, carry,
+                               SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr, mbar + pb, ph);
+      SWR_TRACE(4);
+#pragma unroll
+      for (int r = 0; r < K; r++) zc[r] = carry[r];
+    }
+    {
+      double2 a[K];
+#pragma unroll
+      for (int r = 0; r < K; r++) a[r] = zc[r];
       launder<M>(q, er);
 #pragma unroll
       for (int i = 0; i < M; i++) {
         const double2 c = negqe(q[i], i == 0 ? er_prev : er[i == 0 ? 0 : i - 1], eim);
 #pragma unroll
         for (int r = 0; r < K; r++) {
-          const double2 rr = rhs_row<false>(0, Nj, i == 0 ? uL[r] : u[r][i == 0 ? 0 : i - 1], u[r][i],
-                                            i == M - 1 ? uR[r] : u[r][i == M - 1 ? M - 1 : i + 1], kappa);
-          z[r] = cfma(c, z[r], cmul(q[i], rr));
-          if (pass == 1) ybuf[(r * M + i) * P + t] = z[r];
+          a[r] = cmul(c, a[r]);
+          ybuf[(r * M + i) * P + t] = cadd(ybuf[(r * M + i) * P + t], a[r]);
         }
-      }
-      if (pass == 0) {
-        double2 carry[K];
-        SWR_TRACE(3);
-        race_jitter(1, n);
-        scan_maps<K, true, true>(sAf[t], z, sfp, lane, w, nw, CS, crank, carry,
-                                 SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr, mbar + pb, ph);
-        SWR_TRACE(4);
-#pragma unroll
-        for (int r = 0; r < K; r++) z[r] = zc[r] = carry[r];
       }
     }
     SWR_TRACE(5);
@@ -834,7 +845,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       double2 carry[K];
       SWR_TRACE(6);
       race_jitter(2, n);
-      scan_maps<K, false, true>(sAb[t], x, sbp, lane, w, nw, CS, crank, carry,
+      scan_maps<K, false>(sAb[t], x, sbp, lane, w, nw, CS, crank, carry,
                                 SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr, mbar + 2 + pb, ph);
       SWR_TRACE(7);
 #pragma unroll
@@ -1368,7 +1379,7 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
       {
         double2 zz[1] = {z}, carry[1];
         race_jitter(1, n);
-        scan_maps<1, true, true>(sAf[t], zz, sfp, lane, w, nw, CS, crank, carry, nullptr, mbar + pb, ph);
+        scan_maps<1, true>(sAf[t], zz, sfp, lane, w, nw, CS, crank, carry, nullptr, mbar + pb, ph);
         zc = carry[0];
       }
       // (3) z_i = z^loc_i + (prod_{k<=i} c_k) z_{s0-1}; (4) local backward pass
@@ -1385,7 +1396,7 @@ __global__ void __launch_bounds__(PMAX, MINB) k_march_nl(const MarchParams p) {
       {
         double2 xx[1] = {x}, carry[1];
         race_jitter(2, n);
-        scan_maps<1, false, true>(sAb[t], xx, sbp, lane, w, nw, CS, crank, carry, nullptr, mbar + 2 + pb, ph);
+        scan_maps<1, false>(sAb[t], xx, sbp, lane, w, nw, CS, crank, carry, nullptr, mbar + 2 + pb, ph);
         xc = carry[0];
       }
       // (6) exact backward pass: z^{s+1} and the maxima
