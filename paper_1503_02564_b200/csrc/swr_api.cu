@@ -351,6 +351,9 @@ struct swr_handle {
   int *fp_stat = nullptr;
   MarchShape shape_nl;
   double2 *hv_nl = nullptr;                // NL march: boundary-value histories [owned][2][N_T+1]
+  bool nl_stream = false;                  // NL subdomains beyond the resident march: k_march_nl_stream
+  double2 *snl_ze = nullptr, *snl_vals = nullptr;
+  int *snl_flags = nullptr;
   double2 *tw = nullptr, *FX = nullptr, *FX0 = nullptr;
   double2 *partial = nullptr;
   // streaming march (subdomains too large for the resident kernel)
@@ -408,6 +411,7 @@ double sum_pairs(swr_handle *h, int kind) {
   return s;
 }
 
+constexpr int kStreamSlots = 148 * 32;   // chain CTAs of one streaming launch, upper bound
 int slot_l(int j) { return 2 * j - 3; }
 int slot_r(int j) { return 2 * j - 2; }
 int zero_matrix_index(swr_handle *h, int j) { return j == 1 ? 0 : (j == h->N ? 2 : 1); }
@@ -444,7 +448,13 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mo
   if (mode == MARCH_NL) {
     p.hv_glob = h->hv_nl;
     CKS(record_pair(h, EV_MARCH, true));
-    CK(swr::launch_march_nl(p, h->shape_nl, h->st));
+    if (h->nl_stream) {
+      if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
+      CK(swr::launch_march_nl_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->snl_ze, h->snl_flags,
+                                     h->snl_vals, kStreamSlots, h->st));
+    } else {
+      CK(swr::launch_march_nl(p, h->shape_nl, h->st));
+    }
     CK(cudaGetLastError());
     CKS(record_pair(h, EV_MARCH, false));
     h->n_marches++;
@@ -1291,7 +1301,7 @@ void free_all(swr_handle *h) {
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev,
                   h->sst_u, h->sst_z, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
-                  h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv, h->hv_nl};
+                  h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv, h->hv_nl, h->snl_ze, h->snl_vals, h->snl_flags};
   for (void *p : ptrs)
     if (p) cudaFree(p);
   for (Krylov *K : {&h->kout, &h->kin}) {
@@ -1527,7 +1537,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   }
   if (h->stream_march) {
     h->sst_cap = 3 * h->N + 2;   // the largest batched march (3 RHS per subdomain in the build)
-    const size_t nslot = 148 * 32;   // chain CTAs of one launch, upper bound
+    const size_t nslot = kStreamSlots;   // chain CTAs of one launch, upper bound
     if ((s = dalloc(&h->sst_u, (size_t)h->sst_cap * h->Nj)) || (s = dalloc(&h->sst_z, (size_t)h->sst_cap * h->Nj)) ||
         (s = dalloc(&h->sst_vals, nslot * 8)))
       return fail(s);
@@ -1537,9 +1547,15 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
   if (cudaMemset(h->fp_stat, 0, 2 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_CUDA);
   h->shape_nl = swr::choose_march_shape_nl(h->Nj, h->nl_rows, h->j_hi - h->j_lo + 1);
   if (h->potential == SWR_POT_CUBIC) {
-    if (h->shape_nl.M == 0 || swr::march_nl_smem_bytes(h->shape_nl, h->NT, false) > 227 * 1024) {
-      g_detail = "subdomain too large for the resident nonlinear march";
-      return fail(SWR_ERR_UNSUPPORTED);
+    if (h->march_form == 1 || h->shape_nl.M == 0 ||
+        swr::march_nl_smem_bytes(h->shape_nl, h->NT, false) > 227 * 1024) {
+      // beyond the resident NL march (or asked for): stream through HBM
+      if (!h->stream_march) { g_detail = "NL streaming march without the streaming scratch"; return fail(SWR_ERR_UNSUPPORTED); }
+      h->nl_stream = true;
+      if ((s = dalloc(&h->snl_ze, (size_t)h->sst_cap * h->Nj)) || (s = dalloc(&h->snl_vals, (size_t)kStreamSlots * 10)))
+        return fail(s);
+      if (cudaMalloc((void **)&h->snl_flags, (size_t)kStreamSlots * 4 * sizeof(int)) != cudaSuccess)
+        return fail(SWR_ERR_OOM);
     }
     if ((s = dalloc(&h->hv_nl, (size_t)(h->j_hi - h->j_lo + 1) * 2 * (NTt + 1)))) return fail(s);
   }

@@ -25,6 +25,7 @@
 #include <cooperative_groups.h>
 #include <cstdio>
 #include <cstdlib>
+#include <algorithm>
 
 namespace swr {
 
@@ -338,6 +339,324 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
     if (e != cudaSuccess) return e;
     void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
     e = cudaLaunchCooperativeKernel((const void *)k_march_stream, dim3(nb * nc), dim3(256), args, smem, st);
+    if (e != cudaSuccess) return e;
+    s0 += nb;
+  }
+  return cudaSuccess;
+}
+
+// ---------------------------------------------------------------------------
+// Nonlinear march for subdomains beyond the resident NL march (N_j > 65,536,
+// e.g. N = 10 at dx = 1e-5): f(u) = lambda |u|^2, the Duran-Sanz-Serna
+// midpoint with the inner fixed point of eq. (12) (readings A3,
+// A4), the arithmetic of k_march_nl with the chain structure of
+// k_march_stream.  Per step n, fixed-point iteration s:
+//   pass 1  forward from carry 0: rhs = i kappa (u_{k-1} + 4u_k + u_{k+1})
+//           - (h/12) load_k(zeta^s) (+ the end-row folds) -> affine map
+//   scan    CTA scan, chain fold of the earlier CTAs' published totals
+//   pass 2  forward from the exact carry, z stored
+//   pass 3  backward from carry 0 over z, scan, chain fold in reverse
+//   pass 4  backward from the exact carry: zeta^{s+1} (in place) and the
+//           maxima max |zeta^{s+1} - zeta^s|^2, max |zeta^{s+1}|^2
+//   maxima  every CTA publishes its maxima (value + iteration flag) and reads
+//           all the chain's: the stop decision is uniform (reading A4)
+// then u_n = 2 zeta - u_{n-1}.  The halo rows of u_{n-1} and zeta^s are read
+// before pass 1 (a neighbour may overwrite them once this CTA has published
+// its forward total).  Flags count global fixed-point iterations (ic), so the
+// value buffers alternate by the parity of ic.
+// ---------------------------------------------------------------------------
+__global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, int nc, double2 *ust, double2 *zst,
+                                                         double2 *zest, int *flags, double2 *vals) {
+  extern __shared__ double2 ssm[];
+  double2 *scanbuf = ssm;                      // [64]
+  double2 *red = scanbuf + 64;                 // [32] block reductions
+  double2 *hvL = red + 32;                     // [NT+1] v_s at row 0
+  double2 *hvR = hvL + (p.NT + 1);             // [NT+1] v_s at row N_j - 1
+  __shared__ double2 sHL, sHR, smx;
+  const int t = threadIdx.x, P = blockDim.x, lane = t & 31, w = t >> 5, nw = P >> 5;
+  const int sidx = blockIdx.x / nc, c = blockIdx.x % nc;
+  const MarchSys &S = p.sys[sidx];
+  const int Nj = p.Nj, NT = p.NT;
+  const double eim = p.e_im, kappa = p.kappa, h12 = p.h12, lam = p.lambda;
+  const int Rc = (Nj + nc - 1) / nc;
+  const int rc0 = min(Nj, c * Rc), rc1 = min(Nj, (c + 1) * Rc);
+  const int Rt = (rc1 - rc0 + P - 1) / P;
+  const int rt0 = min(rc1, rc0 + t * Rt), rt1 = min(rc1, rc0 + (t + 1) * Rt);
+  double2 *__restrict__ u = ust + (size_t)sidx * Nj;
+  double2 *__restrict__ z = zst + (size_t)sidx * Nj;
+  double2 *__restrict__ ze = zest + (size_t)sidx * Nj;
+  int *fdone = flags + (size_t)sidx * nc * 4, *ffwd = fdone + nc, *fbwd = ffwd + nc, *fmx = fbwd + nc;
+  double2 *fv = vals + (size_t)sidx * nc * 10, *bv = fv + nc * 4, *mv = bv + nc * 4;   // [nc][parity](A,B) x2, [nc][parity]
+  const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
+  const bool first_cta = c == 0, last_cta = rc1 == Nj && rc0 < Nj;
+  const bool own0 = first_cta && t == 0 && rt0 == 0 && rt1 > 0;
+  const bool ownL = rt1 == Nj && rt0 < Nj;
+  const bool histL = first_cta && has_left, histR = last_cta && has_right;
+
+  for (int k = rc0 + t; k < rc1; k += P) {
+    const double2 v = S.u0 ? S.u0[k] : cz();
+    u[k] = v;
+    ze[k] = v;                                  // zeta^0 of step 1 = v_0 = u_0
+  }
+  if (histL && t == 0) hvL[0] = S.u0 ? S.u0[0] : cz();
+  if (histR && t == 0) hvR[0] = S.u0 ? S.u0[Nj - 1] : cz();
+  __syncthreads();
+  __threadfence();
+  if (t == 0) st_release(fdone + c, 0);
+
+  const int sflags = S.flags;
+  const double2 *const slin = S.lin, *const srin = S.rin, *const sq = S.q;
+  const double *const ser = S.er;
+  double2 *const sout_l = S.out_left, *const sout_r = S.out_right;
+  auto flux = [&](int sd, int n) -> double2 {
+    if (sflags & (sd == 0 ? SYS_LIN_IMPULSE : SYS_RIN_IMPULSE)) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
+    const double2 *f = sd == 0 ? slin : srin;
+    return f ? f[n - 1] : cz();
+  };
+  int fp_max = 0, fp_fail = 0, ic = 0;
+
+  for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
+    if (t == 0) {
+      if (c > 0) wait_flag(fdone + c - 1, n - 1);
+      if (c < nc - 1) wait_flag(fdone + c + 1, n - 1);
+    }
+    // S0^2 history of the end rows this CTA holds
+    for (int sd = 0; sd < 2; sd++) {
+      if (!(sd == 0 ? histL : histR)) continue;
+      const double2 *hv = sd == 0 ? hvL : hvR;
+      double2 acc = cz();
+      if (p.s02)
+        for (int s = t; s <= n - 1; s += P)
+          acc = make_double2(fma(p.beta[n - s], hv[s].x, acc.x), fma(p.beta[n - s], hv[s].y, acc.y));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+      if (lane == 0) red[w] = acc;
+      __syncthreads();
+      if (t == 0) {
+        double2 hs = cz();
+        for (int q = 0; q < nw; q++) hs = cadd(hs, red[q]);
+        (sd == 0 ? sHL : sHR) = p.s02 ? cmul(p.c2, hs) : cz();
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    const double2 dL = (own0 && has_left) ? csub(sHL, flux(0, n)) : cz();
+    const double2 dR = (ownL && has_right) ? csub(sHR, flux(1, n)) : cz();
+    const double ikappa = 1.0 / kappa;
+    auto sval = [&](int k, double2 um, double2 uk, double2 up) -> double2 {
+      if (k == 0) {
+        const double2 f = make_double2(dL.y * ikappa, -dL.x * ikappa);
+        return make_double2(fma(2.0, uk.x, up.x) + f.x, fma(2.0, uk.y, up.y) + f.y);
+      }
+      if (k == Nj - 1) {
+        const double2 f = make_double2(dR.y * ikappa, -dR.x * ikappa);
+        return make_double2(fma(2.0, uk.x, um.x) + f.x, fma(2.0, uk.y, um.y) + f.y);
+      }
+      return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
+    };
+    // load_k(zeta) of the P1 elements (k-1, k), (k, k+1) (reading A3)
+    auto nload = [&](int k, double2 zm, double2 zk, double2 zp) -> double2 {
+      const double Wc = lam * fma(zk.x, zk.x, zk.y * zk.y);
+      double2 ld = cz();
+      if (k > 0) {
+        const double Wm = lam * fma(zm.x, zm.x, zm.y * zm.y);
+        ld.x = fma(Wm + 3.0 * Wc, zk.x, (Wm + Wc) * zm.x);
+        ld.y = fma(Wm + 3.0 * Wc, zk.y, (Wm + Wc) * zm.y);
+      }
+      if (k < Nj - 1) {
+        const double Wp = lam * fma(zp.x, zp.x, zp.y * zp.y);
+        ld.x = fma(3.0 * Wc + Wp, zk.x, fma(Wc + Wp, zp.x, ld.x));
+        ld.y = fma(3.0 * Wc + Wp, zk.y, fma(Wc + Wp, zp.y, ld.y));
+      }
+      return ld;
+    };
+    auto ldg = [&](const double2 *a, int k) -> double2 { return (k >= rc0 && k < rc1) ? a[k] : __ldcg(a + k); };
+    // u_{n-1} halo rows: final for step n-1, unchanged through the iterations
+    const double2 uh_m = rt0 > 0 && rt0 < rt1 ? ldg(u, rt0 - 1) : cz();
+    const double2 uh_p = rt1 < Nj && rt0 < rt1 ? ldg(u, rt1) : cz();
+    bool conv = false;
+    int it;
+    for (it = 1; it <= p.maxit_fp; it++, ic++) {
+      const int par = ic & 1;
+      // zeta^s halo rows, read before this CTA publishes anything of iteration ic
+      const double2 zh_m = rt0 > 0 && rt0 < rt1 ? ldg(ze, rt0 - 1) : cz();
+      const double2 zh_p = rt1 < Nj && rt0 < rt1 ? ldg(ze, rt1) : cz();
+      auto fwd_pass = [&](double2 zin, bool store, double2 &Aout) -> double2 {
+        double2 zz = zin, A = make_double2(1.0, 0.0);
+        double2 um = uh_m, uk = rt0 < rt1 ? ldg(u, rt0) : cz();
+        double2 zm = zh_m, zk = rt0 < rt1 ? ldg(ze, rt0) : cz();
+        double erp = rt0 > 0 ? ser[rt0 - 1] : 0.0;
+#pragma unroll 2
+        for (int k = rt0; k < rt1; k++) {
+          const bool lastrow = k + 1 == rt1;
+          const double2 up = k + 1 < Nj ? (lastrow ? uh_p : ldg(u, k + 1)) : cz();
+          const double2 zp = k + 1 < Nj ? (lastrow ? zh_p : ldg(ze, k + 1)) : cz();
+          const double2 qk = __ldg(sq + k);
+          const double2 ck = negqe_s(qk, erp, eim);
+          const double2 sv = cimul(kappa, sval(k, um, uk, up));
+          const double2 ld = nload(k, zm, zk, zp);
+          const double2 rr = make_double2(fma(-h12, ld.x, sv.x), fma(-h12, ld.y, sv.y));
+          zz = cfma(ck, zz, cmul(qk, rr));
+          if (store) z[k] = zz;
+          else A = cmul(ck, A);
+          erp = __ldg(ser + k);
+          um = uk;
+          uk = up;
+          zm = zk;
+          zk = zp;
+        }
+        Aout = A;
+        return zz;
+      };
+      double2 A1, F1 = fwd_pass(cz(), false, A1);
+      double2 eA, eB, tA, tB;
+      cta_scan<true>(A1, F1, scanbuf, eA, eB, tA, tB);
+      if (t == 0) {
+        fv[(c * 2 + par) * 2 + 0] = tA;
+        fv[(c * 2 + par) * 2 + 1] = tB;
+        __threadfence();
+        st_release(ffwd + c, ic);
+      }
+      race_jitter(1, n);
+      double2 zc = cz();
+      if (c > 0) {
+        if (t == 0)
+          for (int cc = 0; cc < c; cc++) wait_flag(ffwd + cc, ic);
+        __syncthreads();
+        for (int cc = 0; cc < c; cc++)
+          zc = cfma(__ldcg(fv + (cc * 2 + par) * 2 + 0), zc, __ldcg(fv + (cc * 2 + par) * 2 + 1));
+      }
+      double2 dummy;
+      fwd_pass(cfma(eA, zc, eB), true, dummy);
+      double2 Ab = make_double2(1.0, 0.0), xb = cz();
+      for (int k = rt1 - 1; k >= rt0; k--) {
+        const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
+        xb = cfma(bk, xb, z[k]);
+        Ab = cmul(bk, Ab);
+      }
+      cta_scan<false>(Ab, xb, scanbuf, eA, eB, tA, tB);
+      if (t == 0) {
+        bv[(c * 2 + par) * 2 + 0] = tA;
+        bv[(c * 2 + par) * 2 + 1] = tB;
+        __threadfence();
+        st_release(fbwd + c, ic);
+      }
+      race_jitter(2, n);
+      double2 xc = cz();
+      if (c < nc - 1) {
+        if (t == 0)
+          for (int cc = nc - 1; cc > c; cc--) wait_flag(fbwd + cc, ic);
+        __syncthreads();
+        for (int cc = nc - 1; cc > c; cc--)
+          xc = cfma(__ldcg(bv + (cc * 2 + par) * 2 + 0), xc, __ldcg(bv + (cc * 2 + par) * 2 + 1));
+      }
+      double2 x = cfma(eA, xc, eB);
+      double dmax = 0.0, nmax = 0.0;
+      for (int k = rt1 - 1; k >= rt0; k--) {
+        const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
+        x = cfma(bk, x, z[k]);
+        const double2 zo = ze[k];
+        const double dx = x.x - zo.x, dy = x.y - zo.y;
+        dmax = fmax(dmax, fma(dx, dx, dy * dy));
+        nmax = fmax(nmax, fma(x.x, x.x, x.y * x.y));
+        ze[k] = x;
+      }
+      // chain-wide maxima -> uniform decision
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        dmax = fmax(dmax, __shfl_xor_sync(0xffffffffu, dmax, o));
+        nmax = fmax(nmax, __shfl_xor_sync(0xffffffffu, nmax, o));
+      }
+      if (lane == 0) red[w] = make_double2(dmax, nmax);
+      __syncthreads();
+      if (t == 0) {
+        double2 mm = cz();
+        for (int q = 0; q < nw; q++) mm = make_double2(fmax(mm.x, red[q].x), fmax(mm.y, red[q].y));
+        mv[c * 2 + par] = mm;
+        __threadfence();
+        st_release(fmx + c, ic);
+        race_jitter(3, n);
+        for (int cc = 0; cc < nc; cc++) {
+          if (cc == c) continue;
+          wait_flag(fmx + cc, ic);
+          const double2 v = __ldcg(mv + cc * 2 + par);
+          mm = make_double2(fmax(mm.x, v.x), fmax(mm.y, v.y));
+        }
+        smx = mm;
+      }
+      __syncthreads();
+      const double2 mm = smx;
+      if (sqrt(mm.x) <= p.tol_fp * sqrt(mm.y)) { conv = true; ic++; break; }
+      __syncthreads();   // smx is rewritten next iteration
+    }
+    if (!conv) { it = p.maxit_fp; fp_fail = 1; }
+    if (it > fp_max) fp_max = it;
+    // v_n = zeta; u_n = 2 v_n - u_{n-1}; record S v_n at the interfaces (eq. 8)
+    for (int k = rt0; k < rt1; k++) {
+      const double2 v = ze[k], uo = u[k];
+      u[k] = make_double2(fma(2.0, v.x, -uo.x), fma(2.0, v.y, -uo.y));
+    }
+    if (own0) {
+      const double2 x0v = ze[0];
+      if (histL) hvL[n] = x0v;
+      if (has_left && sout_l) {
+        const double2 sv = cfma(p.c0, x0v, sHL), l = flux(0, n);
+        sout_l[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
+      }
+    }
+    if (ownL) {
+      const double2 xLv = ze[Nj - 1];
+      if (histR) hvR[n] = xLv;
+      if (has_right && sout_r) {
+        const double2 sv = cfma(p.c0, xLv, sHR), r = flux(1, n);
+        sout_r[n - 1] = make_double2(fma(2.0, sv.x, -r.x), fma(2.0, sv.y, -r.y));
+      }
+    }
+    __syncthreads();
+    __threadfence();
+    if (t == 0) st_release(fdone + c, n);
+  }
+  if (S.uT)
+    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
+  if (c == 0 && t == 0 && p.fp_stat) {
+    atomicMax(p.fp_stat, fp_max);
+    if (fp_fail) atomicOr(p.fp_stat + 1, 1);
+  }
+}
+
+// Chains of co-resident CTAs as launch_march_stream (the chain length depends
+// on N_j and the problem's subdomain count only).  scratch (one batch of at
+// most nslot / nc systems): u, z, zeta [batch][N_j]; flags [batch][nc][4];
+// vals [batch][nc][10].
+cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
+                                   double2 *zest, int *flags, double2 *vals, int nslot, cudaStream_t st) {
+  const size_t smem = march_stream_smem_bytes(p.NT);
+  cudaError_t e = cudaFuncSetAttribute(k_march_nl_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_nl_stream, 256, smem);
+  if (e != cudaSuccess) return e;
+  const int cap = std::min(nsm * per_sm, nslot);
+  if (cap < 1) return cudaErrorInvalidConfiguration;
+  const MarchSys *all = p.sys;
+  int nc = std::max(1, cap / std::max(1, nsys_ref));
+  nc = std::min(nc, std::max(1, p.Nj / 256));
+  const int per_batch = std::max(1, cap / nc);
+  for (int s0 = 0; s0 < nsys_total;) {
+    const int nb = std::min(nsys_total - s0, per_batch);
+    MarchParams q = p;
+    q.sys = all + s0;
+    q.nsys = nb;
+    if (getenv("SWR_VERBOSE"))
+      fprintf(stderr, "k_march_nl_stream: %d systems x %d CTAs (%d per SM), N_j %d\n", nb, nc, per_sm, p.Nj);
+    e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 4 * sizeof(int), st);
+    if (e != cudaSuccess) return e;
+    // the scratch holds one batch (batches run in stream order)
+    void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&zest, (void *)&flags, (void *)&vals};
+    e = cudaLaunchCooperativeKernel((const void *)k_march_nl_stream, dim3(nb * nc), dim3(256), args, smem, st);
     if (e != cudaSuccess) return e;
     s0 += nb;
   }

@@ -67,6 +67,9 @@ CASES = [
                                    algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT, u0_kind="soliton",
                                    pinv_exact=1)),
     ("mid-N42-stream", si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX, march_form=1)),
+    ("precond-nl-stream", si.config("C1", transmission=si.TC_S02, potential=si.POT_CUBIC, N=8,
+                                    algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT, u0_kind="soliton",
+                                    pinv_exact=1, march_form=1)),
 ]
 
 

@@ -43,6 +43,9 @@ CASES = [
     # streaming march, chains of co-resident CTAs
     ("march-stream", si.Problem(a0=-0.42, b0=0.42, T=0.02, dx=1e-5, dt=1e-3, N=10, potential=si.POT_VX,
                                 march_form=1)),
+    # streaming NL march: chain-wide fixed-point stops through published maxima
+    ("march-nl-stream", si.Problem(a0=-0.42, b0=0.42, T=0.01, dx=1e-5, dt=1e-3, N=10, potential=si.POT_CUBIC,
+                                   algorithm=si.ALG_PRECOND, march_form=1)),
 ]
 
 
