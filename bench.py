@@ -2,8 +2,8 @@
 """Benchmark of the B200 SWR hot path (driver contract).
 
 One *step* = one pass of the whole hot path on resident inputs:
-swr_build_interface_operator (the batched 3-RHS march building d and the
-Toeplitz interface matrix L) + swr_solve (GMRES on (I-L)g = d and
+swr_build_interface_operator (one batched march of the 3N-2 systems: d and
+the l_j / r_j impulse probes giving L) + swr_solve (GMRES on (I-L)g = d and
 the final sweep, Algorithm 3).  Workload (N=1): BASELINE.json
 configs[4] at N = 500 (C5), the north_star's 500-subdomain configuration:
 V = -x^2, Gaussian u0, (a0,b0) = (-21,21), dx = 1e-5, dt = 1e-3, T = 0.5,
@@ -334,11 +334,12 @@ def main():
                        "d2h_bytes_per_step": out_h.numel() * 16, "ms_per_step": em,
                        "path": "swr_update_inputs(host u0, V_x) + swr_build_interface_operator + swr_solve(host u_T)"}
 
-    # the other BASELINE configs' time-to-solution:
-    # C3 V(t,x) preconditioned GMRES, C4 |u|^2 preconditioned fixed point
+    # the other BASELINE configs' time-to-solution: C2
+    # V(x) NEW + GMRES at N = 10 (the streaming march, N_j = 420,001), C3 V(t,x)
+    # preconditioned GMRES, C4 |u|^2 preconditioned fixed point
     if not args.no_extra and world == 1:
         extra = {}
-        for name in ("C3", "C4"):
+        for name in ("C2", "C3", "C4"):
             q = si.config(name)
             sq = SWR(q, si.inputs(q), device=local, stream=stream)
             with torch.cuda.stream(stream):

@@ -262,8 +262,12 @@ def test_random_g0_and_n1(oracle_mod, gpu):
 def test_c5_full_size_sampled(oracle_mod, gpu):
     """C5 at full size (N = 500, dx = 1e-5, N_T = 500) in the launch shape
     bench.py times: the d = R(0) traces of sampled subdomains (first, last,
-    the Gaussian's support near x = -10, and two random ones) against the
-    oracle's march of those subdomains."""
+    the Gaussian's support near x = -10, and two random ones) and the probe
+    columns X^{j,1}, X^{j,3} of three subdomains against the oracle's marches
+    of those subdomains.  Each comparison is relative to the compared
+    vector's own norm (floor 1e-3 of the unit impulse), with the bar 1e-10
+    raised to 4x the spread between the oracle and its FMA build where the
+    problem amplifies rounding beyond it."""
     p = si.config("C5")
     arrays = si.inputs(p)
     g_ = gpu.SWR(p, arrays)
@@ -272,21 +276,32 @@ def test_c5_full_size_sampled(oracle_mod, gpu):
     d_g = d_g.cpu().numpy()
     X_g = X_g.cpu().numpy()
     o = oracle_mod.Oracle(p, arrays)
+    of = oracle_mod.Oracle(p, arrays, library=oracle_mod.lib_fma())
     NT = p.NT
+    worst = []
+
+    def check(gv, ov, fv, what):
+        spread = rel(fv, ov, 1e-3)
+        tol = max(1e-10, 4.0 * spread)
+        err = rel(gv, ov, 1e-3)
+        worst.append((what, err, spread))
+        assert err <= tol, (what, err, spread)
+
     for j in (1, 131, 132, 260, 500):
         st, ol, orr, _, _ = o.march(j, None, None, use_u0=True)
+        _, olf, orf, _, _ = of.march(j, None, None, use_u0=True)
         if j >= 2:
-            assert rel(d_g[(2 * j - 4) * NT:(2 * j - 3) * NT], ol, 1.0) <= 1e-10
+            check(d_g[(2 * j - 4) * NT:(2 * j - 3) * NT], ol, olf, ("d left", j))
         if j <= p.N - 1:
-            assert rel(d_g[(2 * j - 1) * NT:(2 * j) * NT], orr, 1.0) <= 1e-10
+            check(d_g[(2 * j - 1) * NT:(2 * j) * NT], orr, orf, ("d right", j))
     e = np.zeros(NT, np.complex128)
     e[0] = 1
-    for j in (2, 250):
+    for j in (2, 250, 499):
         st, ol, orr, _, _ = o.march(j, e, None, use_u0=False)
-        # the probe responses are O(1e-7) after cancellation against the unit
-        # impulse (S0^2 is nearly transparent at dx = 1e-5): compare at the
-        # scale of the impulse (parity floor)
-        assert rel(X_g[j - 1, 0], ol, 1.0) <= 1e-10 and rel(X_g[j - 1, 2], orr, 1.0) <= 1e-10
+        _, olf, orf, _, _ = of.march(j, e, None, use_u0=False)
+        check(X_g[j - 1, 0], ol, olf, ("X1", j))
+        check(X_g[j - 1, 2], orr, orf, ("X3", j))
+    print("C5 sampled (what, rel err vs oracle, oracle FMA spread):", worst)
 
 
 def test_c2_full_size_sampled(oracle_mod, gpu):
