@@ -82,6 +82,43 @@ __device__ void cta_scan(double2 A, double2 B, double2 *sm, double2 &eA, double2
   tB = aB;
 }
 
+
+// Fold, applied to 0, of the maps (A, B) the chain CTAs published for step
+// (or iteration) v: those before c in order (fwd) or those after c from the
+// last one down (backward).  Warp 0's lanes wait for the flags in parallel,
+// then every warp composes the maps by a lane tree in chunks of 32 (a serial
+// fold costs one L2 round trip per CTA: chains are ~120 CTAs long at C2).
+__device__ __forceinline__ double2 chain_fold(const int *flg, const double2 *vals, int c, int nc, bool fwd, int par,
+                                              int v) {
+  const int cnt = fwd ? c : nc - 1 - c;
+  if (cnt <= 0) return cz();
+  const int lane = threadIdx.x & 31;
+  if (threadIdx.x < 32)
+    for (int i = lane; i < cnt; i += 32) wait_flag(flg + (fwd ? i : nc - 1 - i), v);
+  __syncthreads();
+  double2 val = cz();
+  for (int b = 0; b < cnt; b += 32) {
+    const int i = b + lane;
+    double2 A = make_double2(1.0, 0.0), B = cz();
+    if (i < cnt) {
+      const int cc = fwd ? i : nc - 1 - i;
+      A = __ldcg(vals + (cc * 2 + par) * 2 + 0);
+      B = __ldcg(vals + (cc * 2 + par) * 2 + 1);
+    }
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {   // lane l's span, then lane l + o's
+      const double2 nA = shfl_down2(A, o), nB = shfl_down2(B, o);
+      if (lane + o < 32) {
+        B = cfma(nA, B, nB);
+        A = cmul(nA, A);
+      }
+    }
+    const double2 cA = make_double2(__shfl_sync(0xffffffffu, A.x, 0), __shfl_sync(0xffffffffu, A.y, 0));
+    const double2 cB = make_double2(__shfl_sync(0xffffffffu, B.x, 0), __shfl_sync(0xffffffffu, B.y, 0));
+    val = cfma(cA, val, cB);
+  }
+  return val;
+}
 }  // namespace
 
 // One CTA per (system, chain index).  scratch: u [nsys][Nj], z [nsys][Nj];
@@ -233,14 +270,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
     }
     race_jitter(1, n);
     // carry into the CTA: fold of the earlier CTAs' totals
-    double2 zc = cz();
-    if (c > 0) {
-      if (t == 0)
-        for (int cc = 0; cc < c; cc++) wait_flag(ffwd + cc, n);
-      __syncthreads();
-      for (int cc = 0; cc < c; cc++)
-        zc = cfma(__ldcg(fv + (cc * 2 + par) * 2 + 0), zc, __ldcg(fv + (cc * 2 + par) * 2 + 1));
-    }
+    double2 zc = chain_fold(ffwd, fv, c, nc, true, par, n);
     double2 dummy;
     race_jitter(2, n);
     fwd_pass(cfma(eA, zc, eB), true, dummy);
@@ -259,14 +289,7 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
       st_release(fbwd + c, n);
     }
     race_jitter(3, n);
-    double2 xc = cz();
-    if (c < nc - 1) {
-      if (t == 0)
-        for (int cc = nc - 1; cc > c; cc--) wait_flag(fbwd + cc, n);
-      __syncthreads();
-      for (int cc = nc - 1; cc > c; cc--)
-        xc = cfma(__ldcg(bv + (cc * 2 + par) * 2 + 0), xc, __ldcg(bv + (cc * 2 + par) * 2 + 1));
-    }
+    double2 xc = chain_fold(fbwd, bv, c, nc, false, par, n);
     double2 x = cfma(eA, xc, eB), x0v = cz(), xLv = cz();
     for (int k = rt1 - 1; k >= rt0; k--) {
       const double2 bk = negqe_s(__ldg(q + k), __ldg(er + k), eim);
@@ -301,6 +324,205 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
     for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
 }
 
+// Constant matrix (V = 0, V(x), and every higher-order operator): two passes
+// per step instead of four.  The linear parts of a thread's forward and
+// backward maps do not change during the window, so they are formed once:
+// Af = prod c_k, Ab = prod b_k, the prefix products Apre_k = prod_{k'<=k} c_k'
+// (one array per system, streamed with z) and G = sum_i (prod_{k<i} b_k)
+// Apre_i.  Per step:
+//   pass A  forward from carry 0: z^loc stored, the forward offset F and the
+//           backward offset B^loc = sum_i (prod_{k<i} b_k) z^loc_i (formed in
+//           forward order: no extra pass over z)
+//   scans   forward (Af, F) -> z_{rt0-1}; backward (Ab, B^loc + G z_{rt0-1})
+//           -> x_{rt1}; each a CTA scan and a chain fold
+//   pass B  backward: x_k = (z^loc_k + Apre_k z_{rt0-1}) + b_k x_{k+1},
+//           u_n = 2 x - u_{n-1}
+// HBM bytes per row and step: pass A reads u, q, Re E (40) and writes z (16);
+// pass B reads z, Apre, q, Re E, u (72) and writes u (16): 144 (the four-pass
+// form: ~224).
+__global__ void __launch_bounds__(256) k_march_stream2(const MarchParams p, int nc, double2 *ust, double2 *zst,
+                                                       double2 *ast, int *flags, double2 *vals) {
+  extern __shared__ double2 ssm[];
+  double2 *scanbuf = ssm;                      // [64]
+  double2 *red = scanbuf + 64;                 // [32] block reduction
+  double2 *hvL = red + 32;                     // [NT+1] v_s at row 0 (CTA 0 of a system with a left interface)
+  double2 *hvR = hvL + (p.NT + 1);             // [NT+1] v_s at row N_j - 1 (last CTA, right interface)
+  __shared__ double2 sHL, sHR;
+  const int t = threadIdx.x, P = blockDim.x;
+  const int sidx = blockIdx.x / nc, c = blockIdx.x % nc;
+  const MarchSys &S = p.sys[sidx];
+  const int Nj = p.Nj, NT = p.NT;
+  const double eim = p.e_im, kappa = p.kappa, ikappa = 1.0 / p.kappa;
+  const int Rc = (Nj + nc - 1) / nc;
+  const int rc0 = min(Nj, c * Rc), rc1 = min(Nj, (c + 1) * Rc);
+  const int Rt = (rc1 - rc0 + P - 1) / P;
+  const int rt0 = min(rc1, rc0 + t * Rt), rt1 = min(rc1, rc0 + (t + 1) * Rt);
+  double2 *__restrict__ u = ust + (size_t)sidx * Nj;
+  double2 *__restrict__ z = zst + (size_t)sidx * Nj;
+  double2 *__restrict__ ap = ast + (size_t)sidx * Nj;
+  int *fdone = flags + (size_t)sidx * nc * 3, *ffwd = fdone + nc, *fbwd = ffwd + nc;
+  double2 *fv = vals + (size_t)sidx * nc * 8, *bv = fv + nc * 4;
+  const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
+  const bool first_cta = c == 0, last_cta = rc1 == Nj && rc0 < Nj;
+  const bool own0 = first_cta && t == 0 && rt0 == 0 && rt1 > 0;
+  const bool ownL = rt1 == Nj && rt0 < Nj;
+  const bool histL = first_cta && has_left, histR = last_cta && has_right;
+  const int sflags = S.flags;
+  const double2 *const slin = S.lin, *const srin = S.rin, *const sq = S.q;
+  const double *const ser = S.er;
+  double2 *const sout_l = S.out_left, *const sout_r = S.out_right;
+
+  // initial state; the constant parts of the thread's maps
+  for (int k = rc0 + t; k < rc1; k += P) u[k] = S.u0 ? S.u0[k] : cz();
+  double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0), Gt = cz();
+  {
+    double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
+    for (int k = rt0; k < rt1; k++) {
+      const double2 qk = __ldg(sq + k);
+      const double ek = __ldg(ser + k);
+      Af = cmul(negqe_s(qk, erp, eim), Af);
+      ap[k] = Af;                                          // Apre_k
+      Gt = cfma(Ab, Af, Gt);                               // (prod_{k'<k} b) Apre_k
+      Ab = cmul(Ab, negqe_s(qk, ek, eim));
+      erp = ek;
+    }
+  }
+  if (histL && t == 0) hvL[0] = p.tc_hi ? cmul(S.f0[0], S.u0 ? S.u0[0] : cz()) : (S.u0 ? S.u0[0] : cz());
+  if (histR && t == 0) hvR[0] = p.tc_hi ? cmul(S.f0[1], S.u0 ? S.u0[Nj - 1] : cz()) : (S.u0 ? S.u0[Nj - 1] : cz());
+  double2 BoL = cz(), BoR = cz();
+  if (p.tc_hi) {
+    if (own0) BoL = cmul(S.rho[0], cmul(S.f0[0], S.u0 ? S.u0[0] : cz()));
+    if (ownL) BoR = cmul(S.rho[1], cmul(S.f0[1], S.u0 ? S.u0[Nj - 1] : cz()));
+  }
+  __syncthreads();
+  __threadfence();
+  if (t == 0) st_release(fdone + c, 0);
+  auto flux = [&](int sd, int n) -> double2 {
+    if (sflags & (sd == 0 ? SYS_LIN_IMPULSE : SYS_RIN_IMPULSE)) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
+    const double2 *f = sd == 0 ? slin : srin;
+    return f ? f[n - 1] : cz();
+  };
+
+  for (int n = 1; n <= NT; n++) {
+    race_jitter(0, n);
+    if (t == 0) {
+      if (c > 0) wait_flag(fdone + c - 1, n - 1);
+      if (c < nc - 1) wait_flag(fdone + c + 1, n - 1);
+    }
+    for (int sd = 0; sd < 2; sd++) {
+      if (!(sd == 0 ? histL : histR)) continue;
+      const double2 *hv = sd == 0 ? hvL : hvR;
+      double2 acc = cz();
+      if (p.tc_hi) {
+        const double2 *kp = S.kap[sd];
+        for (int s = t; s <= n - 1; s += P) acc = cfma(__ldg(kp + n - s), hv[s], acc);
+      } else if (p.s02)
+        for (int s = t; s <= n - 1; s += P)
+          acc = make_double2(fma(p.beta[n - s], hv[s].x, acc.x), fma(p.beta[n - s], hv[s].y, acc.y));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) acc = cadd(acc, shfl_xor2(acc, o));
+      if ((t & 31) == 0) red[t >> 5] = acc;
+      __syncthreads();
+      if (t == 0) {
+        double2 hs = cz();
+        for (int w = 0; w < (P >> 5); w++) hs = cadd(hs, red[w]);
+        (sd == 0 ? sHL : sHR) = p.tc_hi ? hs : (p.s02 ? cmul(p.c2, hs) : cz());
+      }
+      __syncthreads();
+    }
+    __syncthreads();
+    const double2 dL = (own0 && has_left) ? csub(cfma(cscale(2.0, S.dlt[0]), BoL, sHL), flux(0, n)) : cz();
+    const double2 dR = (ownL && has_right) ? csub(cfma(cscale(2.0, S.dlt[1]), BoR, sHR), flux(1, n)) : cz();
+    auto sval = [&](int k, double2 um, double2 uk, double2 up) -> double2 {
+      if (k == 0) {
+        const double2 f = make_double2(dL.y * ikappa, -dL.x * ikappa);
+        return make_double2(fma(2.0, uk.x, up.x) + f.x, fma(2.0, uk.y, up.y) + f.y);
+      }
+      if (k == Nj - 1) {
+        const double2 f = make_double2(dR.y * ikappa, -dR.x * ikappa);
+        return make_double2(fma(2.0, uk.x, um.x) + f.x, fma(2.0, uk.y, um.y) + f.y);
+      }
+      return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
+    };
+    auto ldu = [&](int k) -> double2 { return (k >= rc0 && k < rc1) ? u[k] : __ldcg(u + k); };
+    // halo rows of u_{n-1}: read before this CTA publishes anything of step n
+    const double2 halo_m = rt0 > 0 && rt0 < rt1 ? ldu(rt0 - 1) : cz();
+    const double2 halo_p = rt1 < Nj && rt0 < rt1 ? ldu(rt1) : cz();
+    const int par = n & 1;
+    // ---- pass A ----
+    double2 zl = cz(), Bl = cz(), Pb = make_double2(1.0, 0.0);
+    {
+      double2 um = halo_m, uk = rt0 < rt1 ? ldu(rt0) : cz();
+      double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
+#pragma unroll 4
+      for (int k = rt0; k < rt1; k++) {
+        const double2 up = k + 1 < Nj ? (k + 1 == rt1 ? halo_p : ldu(k + 1)) : cz();
+        const double2 qk = __ldg(sq + k);
+        const double ek = __ldg(ser + k);
+        const double2 rr = cimul(kappa, sval(k, um, uk, up));
+        zl = cfma(negqe_s(qk, erp, eim), zl, cmul(qk, rr));
+        z[k] = zl;
+        Bl = cfma(Pb, zl, Bl);
+        Pb = cmul(Pb, negqe_s(qk, ek, eim));
+        erp = ek;
+        um = uk;
+        uk = up;
+      }
+    }
+    double2 eA, eB, tA, tB;
+    cta_scan<true>(Af, zl, scanbuf, eA, eB, tA, tB);
+    if (t == 0) {
+      fv[(c * 2 + par) * 2 + 0] = tA;
+      fv[(c * 2 + par) * 2 + 1] = tB;
+      __threadfence();
+      st_release(ffwd + c, n);
+    }
+    race_jitter(1, n);
+    double2 zc = chain_fold(ffwd, fv, c, nc, true, par, n);
+    zc = cfma(eA, zc, eB);                                  // z_{rt0-1}
+    cta_scan<false>(Ab, cfma(Gt, zc, Bl), scanbuf, eA, eB, tA, tB);
+    if (t == 0) {
+      bv[(c * 2 + par) * 2 + 0] = tA;
+      bv[(c * 2 + par) * 2 + 1] = tB;
+      __threadfence();
+      st_release(fbwd + c, n);
+    }
+    race_jitter(2, n);
+    double2 xc = chain_fold(fbwd, bv, c, nc, false, par, n);
+    // ---- pass B ----
+    double2 x = cfma(eA, xc, eB), x0v = cz(), xLv = cz();
+    for (int k = rt1 - 1; k >= rt0; k--) {
+      const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
+      x = cfma(bk, x, cfma(ap[k], zc, z[k]));
+      const double2 uo = u[k];
+      u[k] = make_double2(fma(2.0, x.x, -uo.x), fma(2.0, x.y, -uo.y));
+      if (k == Nj - 1) xLv = x;
+      if (k == 0) x0v = x;
+    }
+    if (own0) {
+      if (histL) hvL[n] = x0v;
+      if (p.tc_hi) BoL = cmul(S.rho[0], cadd(BoL, x0v));
+      if (has_left && sout_l) {
+        const double2 sv = cfma(p.tc_hi ? S.c0e[0] : p.c0, x0v, sHL), l = flux(0, n);
+        sout_l[n - 1] = make_double2(fma(2.0, sv.x, -l.x), fma(2.0, sv.y, -l.y));
+      }
+    }
+    if (ownL) {
+      if (histR) hvR[n] = xLv;
+      if (p.tc_hi) BoR = cmul(S.rho[1], cadd(BoR, xLv));
+      if (has_right && sout_r) {
+        const double2 sv = cfma(p.tc_hi ? S.c0e[1] : p.c0, xLv, sHR), r = flux(1, n);
+        sout_r[n - 1] = make_double2(fma(2.0, sv.x, -r.x), fma(2.0, sv.y, -r.y));
+      }
+    }
+    __syncthreads();
+    __threadfence();
+    if (t == 0) st_release(fdone + c, n);
+  }
+  if (S.uT)
+    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
+}
+
 size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1)) * sizeof(double2); }
 
 // Streams the systems in batches whose chains are all co-resident.  The
@@ -308,15 +530,18 @@ size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1))
 // its scans reassociated) depends on N_j, the GPU and nsys_ref (the
 // problem's subdomain count) only -- not on how many systems a launch or a
 // rank carries -- so a rank of a multi-GPU run rounds exactly as one GPU.
-cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst, int *flags,
-                                double2 *vals, cudaStream_t st) {
+cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
+                                double2 *ast, int *flags, double2 *vals, cudaStream_t st) {
+  // constant matrix: the two-pass form (Apre in ast); V(t,x): four passes
+  const bool two = p.td_stride == 0 && ast != nullptr;
+  const void *kfun = two ? (const void *)k_march_stream2 : (const void *)k_march_stream;
   const size_t smem = march_stream_smem_bytes(p.NT);
-  cudaError_t e = cudaFuncSetAttribute(k_march_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  cudaError_t e = cudaFuncSetAttribute(kfun, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   int dev = 0, nsm = 0, per_sm = 0;
   cudaGetDevice(&dev);
   cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_stream, 256, smem);
+  e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kfun, 256, smem);
   if (e != cudaSuccess) return e;
   const int cap = nsm * per_sm;
   if (cap < 1) return cudaErrorInvalidConfiguration;
@@ -337,8 +562,14 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
     }
     e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 3 * sizeof(int), st);   // -1: nothing reported yet
     if (e != cudaSuccess) return e;
-    void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
-    e = cudaLaunchCooperativeKernel((const void *)k_march_stream, dim3(nb * nc), dim3(256), args, smem, st);
+    if (two) {
+      void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&ast, (void *)&flags,
+                      (void *)&vals};
+      e = cudaLaunchCooperativeKernel(kfun, dim3(nb * nc), dim3(256), args, smem, st);
+    } else {
+      void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
+      e = cudaLaunchCooperativeKernel(kfun, dim3(nb * nc), dim3(256), args, smem, st);
+    }
     if (e != cudaSuccess) return e;
     s0 += nb;
   }
@@ -519,14 +750,7 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
         st_release(ffwd + c, ic);
       }
       race_jitter(1, n);
-      double2 zc = cz();
-      if (c > 0) {
-        if (t == 0)
-          for (int cc = 0; cc < c; cc++) wait_flag(ffwd + cc, ic);
-        __syncthreads();
-        for (int cc = 0; cc < c; cc++)
-          zc = cfma(__ldcg(fv + (cc * 2 + par) * 2 + 0), zc, __ldcg(fv + (cc * 2 + par) * 2 + 1));
-      }
+      double2 zc = chain_fold(ffwd, fv, c, nc, true, par, ic);
       double2 dummy;
       fwd_pass(cfma(eA, zc, eB), true, dummy);
       double2 Ab = make_double2(1.0, 0.0), xb = cz();
@@ -543,14 +767,7 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
         st_release(fbwd + c, ic);
       }
       race_jitter(2, n);
-      double2 xc = cz();
-      if (c < nc - 1) {
-        if (t == 0)
-          for (int cc = nc - 1; cc > c; cc--) wait_flag(fbwd + cc, ic);
-        __syncthreads();
-        for (int cc = nc - 1; cc > c; cc--)
-          xc = cfma(__ldcg(bv + (cc * 2 + par) * 2 + 0), xc, __ldcg(bv + (cc * 2 + par) * 2 + 1));
-      }
+      double2 xc = chain_fold(fbwd, bv, c, nc, false, par, ic);
       double2 x = cfma(eA, xc, eB);
       double dmax = 0.0, nmax = 0.0;
       for (int k = rt1 - 1; k >= rt0; k--) {
@@ -570,20 +787,28 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
       }
       if (lane == 0) red[w] = make_double2(dmax, nmax);
       __syncthreads();
-      if (t == 0) {
+      if (w == 0) {
+        // the CTA's maxima, published; then every chain CTA's (lanes in parallel)
         double2 mm = cz();
         for (int q = 0; q < nw; q++) mm = make_double2(fmax(mm.x, red[q].x), fmax(mm.y, red[q].y));
-        mv[c * 2 + par] = mm;
-        __threadfence();
-        st_release(fmx + c, ic);
+        if (lane == 0) {
+          mv[c * 2 + par] = mm;
+          __threadfence();
+          st_release(fmx + c, ic);
+        }
         race_jitter(3, n);
-        for (int cc = 0; cc < nc; cc++) {
+        for (int cc = lane; cc < nc; cc += 32) {
           if (cc == c) continue;
           wait_flag(fmx + cc, ic);
           const double2 v = __ldcg(mv + cc * 2 + par);
           mm = make_double2(fmax(mm.x, v.x), fmax(mm.y, v.y));
         }
-        smx = mm;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+          mm.x = fmax(mm.x, __shfl_xor_sync(0xffffffffu, mm.x, o));
+          mm.y = fmax(mm.y, __shfl_xor_sync(0xffffffffu, mm.y, o));
+        }
+        if (lane == 0) smx = mm;
       }
       __syncthreads();
       const double2 mm = smx;

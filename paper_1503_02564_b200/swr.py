@@ -163,7 +163,8 @@ class SWR:
                 keep[k] = None
             elif on_device:
                 dt = torch.complex128 if k in ("u0", "g0") else torch.float64
-                keep[k] = torch.as_tensor(v, dtype=dt, device=self.dev).contiguous()
+                with torch.cuda.stream(self.stream):   # ordered before the library's reads
+                    keep[k] = torch.as_tensor(v, dtype=dt, device=self.dev).contiguous()
             else:
                 dt = np.complex128 if k in ("u0", "g0") else np.float64
                 keep[k] = np.ascontiguousarray(v, dtype=dt)
@@ -246,7 +247,10 @@ class SWR:
 
     # ---- lower-level entry points (device tensors) ---------------------------
     def _cz(self, n):
-        return self.torch.zeros(n, dtype=self.torch.complex128, device=self.dev)
+        # zero-filled on the handle's stream: the library's copies into it are
+        # ordered after the fill (a fill on another stream could land after them)
+        with self.torch.cuda.stream(self.stream):
+            return self.torch.zeros(n, dtype=self.torch.complex128, device=self.dev)
 
     def apply_R(self, g=None, use_u0=True, force_zero=False, want_uT=False):
         Rg = self._cz(max(self.ng, 1))
