@@ -340,7 +340,9 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 // HBM bytes per row and step: pass A reads u, q, Re E (40) and writes z (16);
 // pass B reads z, Apre, q, Re E, u (72) and writes u (16): 144 (the four-pass
 // form: ~224).
-__global__ void __launch_bounds__(256) k_march_stream2(const MarchParams p, int nc, double2 *ust, double2 *zst,
+// two CTAs per SM (128 registers): measured at C2 against one (208 registers,
+// 441 ms of march), three and four (445, 460 ms): 412 ms
+__global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, int nc, double2 *ust, double2 *zst,
                                                        double2 *ast, int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
   double2 *scanbuf = ssm;                      // [64]
