@@ -1,0 +1,4 @@
+O=gpurun_out/r02aj; mkdir -p $O
+python -c "import __graft_entry__ as g; g.build()" > $O/build.txt 2>&1
+timeout 300 python tools/variant_c5.py build_variants/libswr_fused.so C5 >> $O/variants.txt 2>&1
+timeout 300 python tools/variant_c5.py build_variants/libswr_fused.so C5 >> $O/variants.txt 2>&1
