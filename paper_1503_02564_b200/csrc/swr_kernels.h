@@ -60,7 +60,6 @@ __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, dou
 constexpr int TR = 8;  // outputs per thread of the Toeplitz kernel (N_T = 500: 32 threads per output slot)
 __global__ void k_toeplitz_I_minus_L(const double2 *X, const double2 *x, double2 *y, const SlotMap m);
 __global__ void k_halo_add(const double2 *x, const double2 *h, double2 *y, int NT, const double2 *xs);
-__global__ void k_multi_axpy(const double2 *V, size_t ldv, int nvec, const double2 *h, double2 *w, size_t n);
 __global__ void k_axpby(double2 a, const double2 *x, double2 b, double2 *y, size_t n);
 __global__ void k_lin2(double2 *z, double2 a, const double2 *x, double2 b, const double2 *y, size_t n);
 __global__ void k_bicg_p(double2 *p, const double2 *r, const double2 *v, double2 beta, double2 omega, size_t n);
@@ -69,7 +68,6 @@ __global__ void k_bicg_xr(double2 *x, double2 *r, const double2 *p, const double
 __global__ void k_sub(const double2 *x, const double2 *y, double2 *z, size_t n);
 __global__ void k_multi_update(const double2 *V, size_t ldv, int nvec, const double2 *y, double2 *x, size_t n);
 __global__ void k_gather_uT(const double2 *loc, int N, int m, int Nj, int j_lo, int j_hi, double2 *uT);
-__global__ void k_fill(double2 *x, double2 v, size_t n);
 __global__ void k_replicate(const double2 *src, double2 *dst, size_t blk, size_t count);
 __global__ void k_add_f64(double *y, const double *x, size_t n);
 

@@ -580,19 +580,6 @@ __device__ __forceinline__ double2 block_reduce(double2 v, double2 *red) {
   return v;
 }
 
-// w -= sum_v h_v V_v
-__global__ void k_multi_axpy(const double2 *__restrict__ V, size_t ldv, int nvec, const double2 *__restrict__ h,
-                             double2 *__restrict__ w, size_t n) {
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) {
-    double2 acc = w[e];
-    for (int v = 0; v < nvec; v++) {
-      const double2 hv = h[v], x = V[(size_t)v * ldv + e];
-      acc = make_double2(acc.x - (hv.x * x.x - hv.y * x.y), acc.y - (hv.x * x.y + hv.y * x.x));
-    }
-    w[e] = acc;
-  }
-}
-
 // y = a * x + b * y (complex a, b)
 __global__ void k_axpby(double2 a, const double2 *__restrict__ x, double2 b, double2 *__restrict__ y, size_t n) {
   pdl_wait();
@@ -940,10 +927,6 @@ __global__ void k_gather_uT(const double2 *__restrict__ loc, int N, int m, int N
     }
     uT[i] = v;
   }
-}
-
-__global__ void k_fill(double2 *x, double2 v, size_t n) {
-  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < n; e += (size_t)gridDim.x * blockDim.x) x[e] = v;
 }
 
 }  // namespace swr
