@@ -450,8 +450,8 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mo
     CKS(record_pair(h, EV_MARCH, true));
     if (h->nl_stream) {
       if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
-      CK(swr::launch_march_nl_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->snl_ze, h->snl_flags,
-                                     h->snl_vals, kStreamSlots, h->st));
+      CK(swr::launch_march_nl_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->snl_ze, h->sst_a,
+                                     h->snl_flags, h->snl_vals, kStreamSlots, h->st));
     } else {
       CK(swr::launch_march_nl(p, h->shape_nl, h->st));
     }

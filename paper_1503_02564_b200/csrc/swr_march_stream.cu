@@ -598,8 +598,9 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
 // its forward total).  Flags count global fixed-point iterations (ic), so the
 // value buffers alternate by the parity of ic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, int nc, double2 *ust, double2 *zst,
-                                                         double2 *zest, int *flags, double2 *vals) {
+__global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p, int nc, double2 *ust,
+                                                            double2 *zst, double2 *zest, double2 *ast, int *flags,
+                                                            double2 *vals) {
   extern __shared__ double2 ssm[];
   double2 *scanbuf = ssm;                      // [64]
   double2 *red = scanbuf + 64;                 // [32] block reductions
@@ -618,6 +619,7 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
   double2 *__restrict__ u = ust + (size_t)sidx * Nj;
   double2 *__restrict__ z = zst + (size_t)sidx * Nj;
   double2 *__restrict__ ze = zest + (size_t)sidx * Nj;
+  double2 *__restrict__ ap = ast + (size_t)sidx * Nj;
   int *fdone = flags + (size_t)sidx * nc * 4, *ffwd = fdone + nc, *fbwd = ffwd + nc, *fmx = fbwd + nc;
   double2 *fv = vals + (size_t)sidx * nc * 10, *bv = fv + nc * 4, *mv = bv + nc * 4;   // [nc][parity](A,B) x2, [nc][parity]
   const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
@@ -633,13 +635,28 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
   }
   if (histL && t == 0) hvL[0] = S.u0 ? S.u0[0] : cz();
   if (histR && t == 0) hvR[0] = S.u0 ? S.u0[Nj - 1] : cz();
+  const int sflags = S.flags;
+  const double2 *const slin = S.lin, *const srin = S.rin, *const sq = S.q;
+  const double *const ser = S.er;
+  // the constant parts of the thread's maps (k_march_stream2): Af, Ab, G and
+  // the prefix products Apre_k of the forward map
+  double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0), Gt = cz();
+  {
+    double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
+    for (int k = rt0; k < rt1; k++) {
+      const double2 qk = __ldg(sq + k);
+      const double ek = __ldg(ser + k);
+      Af = cmul(negqe_s(qk, erp, eim), Af);
+      ap[k] = Af;
+      Gt = cfma(Ab, Af, Gt);
+      Ab = cmul(Ab, negqe_s(qk, ek, eim));
+      erp = ek;
+    }
+  }
   __syncthreads();
   __threadfence();
   if (t == 0) st_release(fdone + c, 0);
 
-  const int sflags = S.flags;
-  const double2 *const slin = S.lin, *const srin = S.rin, *const sq = S.q;
-  const double *const ser = S.er;
   double2 *const sout_l = S.out_left, *const sout_r = S.out_right;
   auto flux = [&](int sd, int n) -> double2 {
     if (sflags & (sd == 0 ? SYS_LIN_IMPULSE : SYS_RIN_IMPULSE)) return make_double2(n == 1 ? 1.0 : 0.0, 0.0);
@@ -715,36 +732,36 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
       // zeta^s halo rows, read before this CTA publishes anything of iteration ic
       const double2 zh_m = rt0 > 0 && rt0 < rt1 ? ldg(ze, rt0 - 1) : cz();
       const double2 zh_p = rt1 < Nj && rt0 < rt1 ? ldg(ze, rt1) : cz();
-      auto fwd_pass = [&](double2 zin, bool store, double2 &Aout) -> double2 {
-        double2 zz = zin, A = make_double2(1.0, 0.0);
+      // pass A: forward from carry 0 -- z^loc stored, the forward offset and
+      // the backward offset B^loc = sum_i (prod_{k<i} b_k) z^loc_i
+      double2 zl = cz(), Bl = cz(), Pb = make_double2(1.0, 0.0);
+      {
         double2 um = uh_m, uk = rt0 < rt1 ? ldg(u, rt0) : cz();
         double2 zm = zh_m, zk = rt0 < rt1 ? ldg(ze, rt0) : cz();
-        double erp = rt0 > 0 ? ser[rt0 - 1] : 0.0;
+        double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
 #pragma unroll 2
         for (int k = rt0; k < rt1; k++) {
           const bool lastrow = k + 1 == rt1;
           const double2 up = k + 1 < Nj ? (lastrow ? uh_p : ldg(u, k + 1)) : cz();
           const double2 zp = k + 1 < Nj ? (lastrow ? zh_p : ldg(ze, k + 1)) : cz();
           const double2 qk = __ldg(sq + k);
-          const double2 ck = negqe_s(qk, erp, eim);
+          const double ek = __ldg(ser + k);
           const double2 sv = cimul(kappa, sval(k, um, uk, up));
           const double2 ld = nload(k, zm, zk, zp);
           const double2 rr = make_double2(fma(-h12, ld.x, sv.x), fma(-h12, ld.y, sv.y));
-          zz = cfma(ck, zz, cmul(qk, rr));
-          if (store) z[k] = zz;
-          else A = cmul(ck, A);
-          erp = __ldg(ser + k);
+          zl = cfma(negqe_s(qk, erp, eim), zl, cmul(qk, rr));
+          z[k] = zl;
+          Bl = cfma(Pb, zl, Bl);
+          Pb = cmul(Pb, negqe_s(qk, ek, eim));
+          erp = ek;
           um = uk;
           uk = up;
           zm = zk;
           zk = zp;
         }
-        Aout = A;
-        return zz;
-      };
-      double2 A1, F1 = fwd_pass(cz(), false, A1);
+      }
       double2 eA, eB, tA, tB;
-      cta_scan<true>(A1, F1, scanbuf, eA, eB, tA, tB);
+      cta_scan<true>(Af, zl, scanbuf, eA, eB, tA, tB);
       if (t == 0) {
         fv[(c * 2 + par) * 2 + 0] = tA;
         fv[(c * 2 + par) * 2 + 1] = tB;
@@ -753,15 +770,8 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
       }
       race_jitter(1, n);
       double2 zc = chain_fold(ffwd, fv, c, nc, true, par, ic);
-      double2 dummy;
-      fwd_pass(cfma(eA, zc, eB), true, dummy);
-      double2 Ab = make_double2(1.0, 0.0), xb = cz();
-      for (int k = rt1 - 1; k >= rt0; k--) {
-        const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
-        xb = cfma(bk, xb, z[k]);
-        Ab = cmul(bk, Ab);
-      }
-      cta_scan<false>(Ab, xb, scanbuf, eA, eB, tA, tB);
+      zc = cfma(eA, zc, eB);                              // z_{rt0-1}
+      cta_scan<false>(Ab, cfma(Gt, zc, Bl), scanbuf, eA, eB, tA, tB);
       if (t == 0) {
         bv[(c * 2 + par) * 2 + 0] = tA;
         bv[(c * 2 + par) * 2 + 1] = tB;
@@ -770,11 +780,12 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
       }
       race_jitter(2, n);
       double2 xc = chain_fold(fbwd, bv, c, nc, false, par, ic);
+      // pass B: zeta^{s+1}_k = (z^loc_k + Apre_k z_{rt0-1}) + b_k zeta^{s+1}_{k+1}, in place, and the maxima
       double2 x = cfma(eA, xc, eB);
       double dmax = 0.0, nmax = 0.0;
       for (int k = rt1 - 1; k >= rt0; k--) {
         const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
-        x = cfma(bk, x, z[k]);
+        x = cfma(bk, x, cfma(ap[k], zc, z[k]));
         const double2 zo = ze[k];
         const double dx = x.x - zo.x, dy = x.y - zo.y;
         dmax = fmax(dmax, fma(dx, dx, dy * dy));
@@ -857,7 +868,8 @@ __global__ void __launch_bounds__(256) k_march_nl_stream(const MarchParams p, in
 // most nslot / nc systems): u, z, zeta [batch][N_j]; flags [batch][nc][4];
 // vals [batch][nc][10].
 cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                   double2 *zest, int *flags, double2 *vals, int nslot, cudaStream_t st) {
+                                   double2 *zest, double2 *ast, int *flags, double2 *vals, int nslot,
+                                   cudaStream_t st) {
   const size_t smem = march_stream_smem_bytes(p.NT);
   cudaError_t e = cudaFuncSetAttribute(k_march_nl_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -882,7 +894,8 @@ cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, 
     e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 4 * sizeof(int), st);
     if (e != cudaSuccess) return e;
     // the scratch holds one batch (batches run in stream order)
-    void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&zest, (void *)&flags, (void *)&vals};
+    void *args[] = {(void *)&q,     (void *)&nc,    (void *)&ust, (void *)&zst,
+                    (void *)&zest,  (void *)&ast,   (void *)&flags, (void *)&vals};
     e = cudaLaunchCooperativeKernel((const void *)k_march_nl_stream, dim3(nb * nc), dim3(256), args, smem, st);
     if (e != cudaSuccess) return e;
     s0 += nb;

@@ -211,6 +211,9 @@ PAPER_COUNT_CASES = [
                                    krylov=si.KRY_FIXED_POINT), 71),
     # the NL table: preconditioned fixed point, |u|^2, N = 100 -> N_pc = 22 (C4 grid)
     ("nl-precond-N100", dict(name="C4", maxit=2000), 22),
+    # the NL table's N = 10 row at dx = 1e-5 (N_j = 420,001: the streaming NL march,
+    # the exact causal P^{-1}): preconditioned fixed point -> N_pc = 11
+    ("nl-precond-N10-fine", dict(name="C4", N=10, dx=1e-5, pinv_exact=1, maxit=2000), 11),
     # Table 7: new algorithm, Robin p = 45, fixed point, N = 500, random g0 -> 1690
     ("table7-robin45-N500", dict(name="C5", transmission=si.TC_ROBIN, robin_p=45.0, krylov=si.KRY_FIXED_POINT,
                                  g0_random=True, maxit=2000), 1690),
