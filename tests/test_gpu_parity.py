@@ -214,6 +214,9 @@ PAPER_COUNT_CASES = [
     # the NL table's N = 10 row at dx = 1e-5 (N_j = 420,001: the streaming NL march,
     # the exact causal P^{-1}): preconditioned fixed point -> N_pc = 11
     ("nl-precond-N10-fine", dict(name="C4", N=10, dx=1e-5, pinv_exact=1, maxit=2000), 11),
+    # the same table's N = 500 and 1000 rows at dx = 1e-5 -> N_pc = 25, 26
+    ("nl-precond-N500-fine", dict(name="C4", N=500, dx=1e-5, pinv_exact=1, maxit=2000), 25),
+    ("nl-precond-N1000-fine", dict(name="C4", N=1000, dx=1e-5, pinv_exact=1, maxit=2000), 26),
     # Table 7: new algorithm, Robin p = 45, fixed point, N = 500, random g0 -> 1690
     ("table7-robin45-N500", dict(name="C5", transmission=si.TC_ROBIN, robin_p=45.0, krylov=si.KRY_FIXED_POINT,
                                  g0_random=True, maxit=2000), 1690),
