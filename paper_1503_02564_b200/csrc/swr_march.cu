@@ -1020,7 +1020,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     SWR_TRACE(3);
     // Q_{n+2} = sum_{s<=n-1} beta_{n+2-s} v_s of one side (v_{n-1} is visible
     // after the forward-scan barrier), reduced per warp into hred; run by the
-    // CTA holding that side while it waits for the other CTAs' totals
+    // CTA holding that side inside the backward scan (below)
     auto history = [&](int side) {
       if (!((p.s02 || p.tc_hi) && n + 2 <= NT)) return;
 #pragma unroll
@@ -1043,7 +1043,7 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
     };
     race_jitter(1, n);
     scan_tab<K, true>(z, sfp, tabF, t, P, lane, w, nw, CS, crank, zc, mbar + pb, ph,
-                      [&] { if (has_right && crank == cb) history(1); },
+                      [&] {},
                       SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 10 : nullptr);
     SWR_TRACE(4);
     SWR_TRACE(5);
@@ -1057,7 +1057,14 @@ __global__ void __launch_bounds__(PMAX, PMAX <= 128 ? 2 : 1) k_march(const March
       SWR_TRACE(6);
       race_jitter(2, n);
       scan_tab<K, false>(x, sbp, tabB, t, P, lane, w, nw, CS, crank, carry, mbar + 2 + pb, ph,
-                         [&] { if (has_left && crank == 0) history(0); },
+                         [&] {
+                           // both history sums in the backward scan: the left one where CTA 0
+                           // waits for the later CTAs' totals, the right one after the
+                           // boundary CTA's pushes (its next forward fold has slack; in the
+                           // forward scan it sat on the critical path)
+                           if (has_left && crank == 0) history(0);
+                           if (has_right && crank == cb) history(1);
+                         },
                          SWR_TRACE_ON ? p.trace + blockIdx.x * 32 + 20 : nullptr);
       SWR_TRACE(7);
 #pragma unroll
