@@ -206,6 +206,14 @@ int swr_apply_I_minus_L(swr_handle *h, int32_t which, const double *x, double *y
  * = first column of X^{j,p}; which = 0: L, 1: L0). NULL skips. */
 int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X);
 
+/* Test infrastructure (one GPU, SWR_ALG_NEW): replace the interface operator
+ * with a given one -- d [2*n_g] and the first columns X [2*N*4*N_T] (device
+ * pointers, the layout of swr_get_interface); the next swr_solve runs the
+ * interface solve and the final sweep on it.  Lets a test give both sides
+ * the same operator (Algorithm 3's solve stage, isolated from the
+ * rounding of the build).  SWR_ERR_INVALID_ARG otherwise. */
+int swr_set_interface(swr_handle *h, const double *d, const double *X);
+
 /* Copy out this rank's slots of the interface vector g of the last swr_solve:
  * [2 * (s_hi - s_lo + 1) * N_T] (swr_owned_slots; the whole g on one GPU). */
 int swr_get_g(swr_handle *h, double *g);

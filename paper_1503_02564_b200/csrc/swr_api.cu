@@ -1885,6 +1885,16 @@ int swr_get_interface(swr_handle *h, int32_t which, double *d, double *X) {
   return SWR_OK;
 }
 
+int swr_set_interface(swr_handle *h, const double *d, const double *X) {
+  if (!h || h->world > 1 || h->algorithm != SWR_ALG_NEW || h->N < 2 || !d || !X) return SWR_ERR_INVALID_ARG;
+  CK(cudaMemcpyAsync(h->d, d, h->ng * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  CK(cudaMemcpyAsync(h->X, X, (size_t)h->N * 4 * h->NT * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));
+  CKS(transform_columns(h, false));
+  h->have_L = h->have_d = true;
+  CK(cudaStreamSynchronize(h->st));
+  return SWR_OK;
+}
+
 int swr_get_g(swr_handle *h, double *g) {
   if (!h || !h->have_g) return SWR_ERR_INVALID_ARG;
   CK(cudaMemcpyAsync(g, h->g, h->nloc * sizeof(double2), cudaMemcpyDeviceToDevice, h->st));

@@ -83,6 +83,7 @@ def load(path):
         L.swr_apply_R.argtypes = [H, vp, i32, i32, vp, vp]
         L.swr_apply_I_minus_L.argtypes = [H, i32, vp, vp]
         L.swr_get_interface.argtypes = [H, i32, vp, vp]
+        L.swr_set_interface.argtypes = [H, vp, vp]
         L.swr_get_g.argtypes = [H, vp]
         L.swr_sizes.argtypes = [H, vp, vp, vp, vp]
         L.swr_partition.argtypes = [i32, i32, i32, vp, vp]
@@ -90,16 +91,16 @@ def load(path):
         L.swr_nccl_unique_id.argtypes = [vp]
         L.swr_loopback_id.argtypes = [vp, i32]
         for f in ("swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_apply_R",
-                  "swr_apply_I_minus_L", "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition",
-                  "swr_owned_slots", "swr_nccl_unique_id", "swr_loopback_id"):
+                  "swr_apply_I_minus_L", "swr_get_interface", "swr_set_interface", "swr_get_g", "swr_sizes",
+                  "swr_partition", "swr_owned_slots", "swr_nccl_unique_id", "swr_loopback_id"):
             getattr(L, f).restype = i32
         return L
 
 
 EXPORTED = ["swr_setup", "swr_update_inputs", "swr_build_interface_operator", "swr_solve", "swr_free",
             "swr_error_string", "swr_last_error_detail", "swr_apply_R", "swr_apply_I_minus_L",
-            "swr_get_interface", "swr_get_g", "swr_sizes", "swr_partition", "swr_owned_slots",
-            "swr_nccl_unique_id", "swr_loopback_id"]
+            "swr_get_interface", "swr_set_interface", "swr_get_g", "swr_sizes", "swr_partition",
+            "swr_owned_slots", "swr_nccl_unique_id", "swr_loopback_id"]
 
 
 def partition(N: int, world: int, rank: int):
@@ -268,6 +269,15 @@ class SWR:
         X = self._cz(self.p.N * 4 * self.NT)
         _check(self.L.swr_get_interface(self.h, which, _ptr(d), _ptr(X)), "swr_get_interface")
         return d[: self.ng], X.view(self.p.N, 4, self.NT)
+
+    def set_interface(self, d, X):
+        """Test infrastructure: use the given d and first columns X (layout of
+        get_interface) as the interface operator of the next solve."""
+        t = self.torch
+        with t.cuda.stream(self.stream):
+            dd = t.as_tensor(np.ascontiguousarray(d), dtype=t.complex128, device=self.dev)
+            XX = t.as_tensor(np.ascontiguousarray(X), dtype=t.complex128, device=self.dev)
+        _check(self.L.swr_set_interface(self.h, _ptr(dd), _ptr(XX)), "swr_set_interface")
 
     def get_g(self):
         """This rank's slots of g (the whole g on one GPU)."""

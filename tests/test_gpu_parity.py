@@ -553,6 +553,38 @@ def test_edge_cases(oracle_mod, gpu, name, p):
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
+def test_c5_solve_on_the_oracle_operator(oracle_mod, gpu):
+    """The north-star configuration's solve stage on a common interface
+    operator: the GPU runs Algorithm 3's GMRES(30) and final sweep
+    on the oracle's d and L (swr_set_interface, test infrastructure), the
+    oracle solves as it stands.  With the build's rounding taken out, the two
+    agree to the north-star bar: equal iteration counts, u(T) and g within
+    1e-10 relative L2 -- the ~1e-8 of the end-to-end gate is the build's
+    rounding (d and L within the oracle's FMA spread) amplified by the
+    interface solve, not the solve itself."""
+    import os
+    p = si.config("C5")
+    arrays = si.inputs(p)
+    oracle_mod.set_threads(os.cpu_count())
+    try:
+        o = oracle_mod.Oracle(p, arrays)
+        X_o = o.build_L()
+        d_o = o.apply_R(None, use_u0=True)
+        ro = o.solve()
+    finally:
+        oracle_mod.set_threads(1)
+    s = gpu.SWR(p, arrays)
+    s.set_interface(d_o, X_o)
+    st, uT, rg = s.solve()
+    g_g = s.get_g().cpu().numpy()
+    s.close()
+    assert st == 0 and ro["status"] == 0
+    eu, eg = rel(uT, ro["uT"]), rel(g_g, ro["g"])
+    print(f"C5 on the oracle's operator: it {rg['iterations']} / {ro['iterations']}, u(T) {eu:.2e}, g {eg:.2e}")
+    assert rg["iterations"] == ro["iterations"]
+    assert eu <= 1e-10 and eg <= 1e-10, (eu, eg)
+
+
 def test_c5_north_star_gate(oracle_mod, gpu):
     """The north-star configuration end to end (C5: N = 500, dx = 1e-5,
     N_T = 500, V = -x^2, NEW + GMRES(30), tol 1e-10 as P:1079), GPU in the
