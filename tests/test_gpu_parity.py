@@ -535,13 +535,25 @@ EDGE_CASES = [
     ("two-steps-robin", si.Problem(a0=-2.0, b0=2.0, T=0.02, dx=0.05, dt=0.01, N=5, potential=si.POT_ZERO,
                                    transmission=si.TC_ROBIN, robin_p=3.0)),
     ("N2-fine", si.Problem(a0=-21.0, b0=21.0, T=0.05, dx=1e-2, dt=1e-3, N=2, potential=si.POT_VX)),
+    # |u|^2 (the NL march: first and last row in one thread, N_j = 2 and 5) and V(t,x)
+    ("nl-one-cell", si.Problem(a0=-1.0, b0=1.0, T=0.05, dx=0.25, dt=0.01, N=8, potential=si.POT_CUBIC,
+                               algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT, pinv_exact=1)),
+    ("nl-one-step", si.Problem(a0=-2.0, b0=2.0, T=0.01, dx=0.1, dt=0.01, N=10, potential=si.POT_CUBIC,
+                               algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT)),
+    ("nl-stream-one-cell", si.Problem(a0=-1.0, b0=1.0, T=0.05, dx=0.25, dt=0.01, N=8, potential=si.POT_CUBIC,
+                                      algorithm=si.ALG_PRECOND, krylov=si.KRY_FIXED_POINT, pinv_exact=1,
+                                      march_form=1)),
+    ("vtx-one-cell", si.Problem(a0=-1.0, b0=1.0, T=0.05, dx=0.25, dt=0.01, N=8, potential=si.POT_VTX,
+                                algorithm=si.ALG_PRECOND)),
 ]
 
 
 @pytest.mark.parametrize("name,p", EDGE_CASES, ids=[c[0] for c in EDGE_CASES])
 def test_edge_cases(oracle_mod, gpu, name, p):
     """Degenerate shapes: one-cell subdomains (N_j = 2), a single time step,
-    two steps with Robin, and a long subdomain (N_j = 4201, one CTA) at N = 2."""
+    two steps with Robin, and a long subdomain (N_j = 4201, one CTA) at N = 2;
+    the same for the NL marches (resident and streaming) and the
+    time-dependent march."""
     x = p.nodes()
     arrays = si.inputs(p)
     arrays["u0"] = np.exp(-(x * x) + 2j * x)
@@ -550,6 +562,8 @@ def test_edge_cases(oracle_mod, gpu, name, p):
     st, uT, rg = g_.solve()
     assert ro["status"] == 0 and st == 0
     assert rg["iterations"] == ro["iterations"]
+    if p.potential == si.POT_CUBIC:
+        assert rg["fp_max"] == ro["fp_max"]
     assert rel(uT, ro["uT"]) <= 1e-10
 
 
