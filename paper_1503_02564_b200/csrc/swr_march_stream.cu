@@ -342,8 +342,9 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 // form: ~224).
 // two CTAs per SM (128 registers): measured at C2 against one (208 registers,
 // 441 ms of march), three and four (445, 460 ms): 412 ms
-__global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, int nc, double2 *ust, double2 *zst,
-                                                       double2 *ast, int *flags, double2 *vals) {
+__global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, int nc, size_t stride, double2 *ust,
+                                                       double2 *zst, double2 *ast, double2 *qst, double *est,
+                                                       int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
   double2 *scanbuf = ssm;                      // [64]
   double2 *red = scanbuf + 64;                 // [32] block reduction
@@ -357,11 +358,23 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
   const double eim = p.e_im, kappa = p.kappa, ikappa = 1.0 / p.kappa;
   const int Rc = (Nj + nc - 1) / nc;
   const int rc0 = min(Nj, c * Rc), rc1 = min(Nj, (c + 1) * Rc);
-  const int Rt = (rc1 - rc0 + P - 1) / P;
+  const int Rt = (Rc + P - 1) / P;                     // rows per thread (every CTA)
   const int rt0 = min(rc1, rc0 + t * Rt), rt1 = min(rc1, rc0 + (t + 1) * Rt);
-  double2 *__restrict__ u = ust + (size_t)sidx * Nj;
-  double2 *__restrict__ z = zst + (size_t)sidx * Nj;
-  double2 *__restrict__ ap = ast + (size_t)sidx * Nj;
+  // thread-interleaved layout of the scratch: row rt0 + i of thread t of CTA c
+  // at c P Rt + i P + t, so a warp's access of its threads' i-th rows is one
+  // contiguous 512-byte run (the natural layout made every load touch 32 lines)
+  const size_t cbase = (size_t)c * P * Rt;
+  auto PH = [&](int i) -> size_t { return cbase + (size_t)i * P + t; };
+  auto phys_of = [&](int k) -> size_t {
+    const int cc = k / Rc, r = k - cc * Rc, tt = r / Rt;
+    return (size_t)cc * P * Rt + (size_t)(r - tt * Rt) * P + tt;
+  };
+  double2 *__restrict__ u = ust + (size_t)sidx * stride;
+  double2 *__restrict__ z = zst + (size_t)sidx * stride;
+  double2 *__restrict__ ap = ast + (size_t)sidx * stride;
+  double2 *__restrict__ qp = qst + (size_t)sidx * stride;
+  double *__restrict__ ep = est + (size_t)sidx * stride;
+  const int cnt = rt1 - rt0;
   int *fdone = flags + (size_t)sidx * nc * 3, *ffwd = fdone + nc, *fbwd = ffwd + nc;
   double2 *fv = vals + (size_t)sidx * nc * 8, *bv = fv + nc * 4;
   const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
@@ -374,16 +387,23 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
   const double *const ser = S.er;
   double2 *const sout_l = S.out_left, *const sout_r = S.out_right;
 
-  // initial state; the constant parts of the thread's maps
-  for (int k = rc0 + t; k < rc1; k += P) u[k] = S.u0 ? S.u0[k] : cz();
+  // initial state and the factors, permuted into the interleaved layout
+  for (int k = rc0 + t; k < rc1; k += P) {
+    const size_t ph = phys_of(k);
+    u[ph] = S.u0 ? S.u0[k] : cz();
+    qp[ph] = __ldg(sq + k);
+    ep[ph] = __ldg(ser + k);
+  }
+  __syncthreads();
+  // the constant parts of the thread's maps
   double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0), Gt = cz();
   {
     double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
-    for (int k = rt0; k < rt1; k++) {
-      const double2 qk = __ldg(sq + k);
-      const double ek = __ldg(ser + k);
+    for (int i = 0; i < cnt; i++) {
+      const double2 qk = qp[PH(i)];
+      const double ek = ep[PH(i)];
       Af = cmul(negqe_s(qk, erp, eim), Af);
-      ap[k] = Af;                                          // Apre_k
+      ap[PH(i)] = Af;                                      // Apre_k
       Gt = cfma(Ab, Af, Gt);                               // (prod_{k'<k} b) Apre_k
       Ab = cmul(Ab, negqe_s(qk, ek, eim));
       erp = ek;
@@ -446,7 +466,7 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
       }
       return make_double2(fma(4.0, uk.x, um.x + up.x), fma(4.0, uk.y, um.y + up.y));
     };
-    auto ldu = [&](int k) -> double2 { return (k >= rc0 && k < rc1) ? u[k] : __ldcg(u + k); };
+    auto ldu = [&](int k) -> double2 { return (k >= rc0 && k < rc1) ? u[phys_of(k)] : __ldcg(u + phys_of(k)); };
     // halo rows of u_{n-1}: read before this CTA publishes anything of step n
     const double2 halo_m = rt0 > 0 && rt0 < rt1 ? ldu(rt0 - 1) : cz();
     const double2 halo_p = rt1 < Nj && rt0 < rt1 ? ldu(rt1) : cz();
@@ -454,16 +474,17 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
     // ---- pass A ----
     double2 zl = cz(), Bl = cz(), Pb = make_double2(1.0, 0.0);
     {
-      double2 um = halo_m, uk = rt0 < rt1 ? ldu(rt0) : cz();
+      double2 um = halo_m, uk = cnt > 0 ? u[PH(0)] : cz();
       double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
 #pragma unroll 4
-      for (int k = rt0; k < rt1; k++) {
-        const double2 up = k + 1 < Nj ? (k + 1 == rt1 ? halo_p : ldu(k + 1)) : cz();
-        const double2 qk = __ldg(sq + k);
-        const double ek = __ldg(ser + k);
+      for (int i = 0; i < cnt; i++) {
+        const int k = rt0 + i;
+        const double2 up = k + 1 < Nj ? (i + 1 == cnt ? halo_p : u[PH(i + 1)]) : cz();
+        const double2 qk = qp[PH(i)];
+        const double ek = ep[PH(i)];
         const double2 rr = cimul(kappa, sval(k, um, uk, up));
         zl = cfma(negqe_s(qk, erp, eim), zl, cmul(qk, rr));
-        z[k] = zl;
+        z[PH(i)] = zl;
         Bl = cfma(Pb, zl, Bl);
         Pb = cmul(Pb, negqe_s(qk, ek, eim));
         erp = ek;
@@ -493,11 +514,13 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
     double2 xc = chain_fold(fbwd, bv, c, nc, false, par, n);
     // ---- pass B ----
     double2 x = cfma(eA, xc, eB), x0v = cz(), xLv = cz();
-    for (int k = rt1 - 1; k >= rt0; k--) {
-      const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
-      x = cfma(bk, x, cfma(ap[k], zc, z[k]));
-      const double2 uo = u[k];
-      u[k] = make_double2(fma(2.0, x.x, -uo.x), fma(2.0, x.y, -uo.y));
+    for (int i = cnt - 1; i >= 0; i--) {
+      const int k = rt0 + i;
+      const size_t ph = PH(i);
+      const double2 bk = negqe_s(qp[ph], ep[ph], eim);
+      x = cfma(bk, x, cfma(ap[ph], zc, z[ph]));
+      const double2 uo = u[ph];
+      u[ph] = make_double2(fma(2.0, x.x, -uo.x), fma(2.0, x.y, -uo.y));
       if (k == Nj - 1) xLv = x;
       if (k == 0) x0v = x;
     }
@@ -521,8 +544,10 @@ __global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, i
     __threadfence();
     if (t == 0) st_release(fdone + c, n);
   }
-  if (S.uT)
-    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
+  if (S.uT) {
+    __syncthreads();
+    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[phys_of(k)];
+  }
 }
 
 size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1)) * sizeof(double2); }
@@ -532,8 +557,24 @@ size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1))
 // its scans reassociated) depends on N_j, the GPU and nsys_ref (the
 // problem's subdomain count) only -- not on how many systems a launch or a
 // rank carries -- so a rank of a multi-GPU run rounds exactly as one GPU.
+// chain length and scratch stride of the two-pass streaming march (the
+// interleaved layout pads every CTA's block to P Rt rows)
+size_t stream2_stride(int Nj, int nsys_ref, int NT) {
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_stream2, 256, march_stream_smem_bytes(NT)) !=
+      cudaSuccess || per_sm < 1)
+    per_sm = 1;
+  int nc = std::max(1, nsm * per_sm / std::max(1, nsys_ref));
+  nc = std::min(nc, std::max(1, Nj / 256));
+  const int Rc = (Nj + nc - 1) / nc, Rt = (Rc + 255) / 256;
+  return (size_t)nc * 256 * Rt;
+}
+
 cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                double2 *ast, int *flags, double2 *vals, cudaStream_t st) {
+                                double2 *ast, double2 *qst, double *est, size_t stride, int *flags, double2 *vals,
+                                cudaStream_t st) {
   // constant matrix: the two-pass form (Apre in ast); V(t,x): four passes
   const bool two = p.td_stride == 0 && ast != nullptr;
   const void *kfun = two ? (const void *)k_march_stream2 : (const void *)k_march_stream;
@@ -565,8 +606,9 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
     e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 3 * sizeof(int), st);   // -1: nothing reported yet
     if (e != cudaSuccess) return e;
     if (two) {
-      void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&ast, (void *)&flags,
-                      (void *)&vals};
+      if ((size_t)nc * 256 * (((p.Nj + nc - 1) / nc + 255) / 256) > stride) return cudaErrorInvalidValue;
+      void *args[] = {(void *)&q,   (void *)&nc,  (void *)&stride, (void *)&ust,   (void *)&zst,
+                      (void *)&ast, (void *)&qst, (void *)&est,    (void *)&flags, (void *)&vals};
       e = cudaLaunchCooperativeKernel(kfun, dim3(nb * nc), dim3(256), args, smem, st);
     } else {
       void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
