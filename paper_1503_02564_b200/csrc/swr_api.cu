@@ -452,8 +452,8 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mo
     CKS(record_pair(h, EV_MARCH, true));
     if (h->nl_stream) {
       if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
-      CK(swr::launch_march_nl_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->snl_ze, h->sst_a,
-                                     h->snl_flags, h->snl_vals, kStreamSlots, h->st));
+      CK(swr::launch_march_nl_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->snl_ze, h->sst_a, h->sst_q,
+                                     h->sst_e, h->sst_stride, h->snl_flags, h->snl_vals, kStreamSlots, h->st));
     } else {
       CK(swr::launch_march_nl(p, h->shape_nl, h->st));
     }
@@ -1559,7 +1559,8 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
       // beyond the resident NL march (or asked for): stream through HBM
       if (!h->stream_march) { g_detail = "NL streaming march without the streaming scratch"; return fail(SWR_ERR_UNSUPPORTED); }
       h->nl_stream = true;
-      if ((s = dalloc(&h->snl_ze, (size_t)h->sst_cap * h->Nj)) || (s = dalloc(&h->snl_vals, (size_t)kStreamSlots * 10)))
+      if ((s = dalloc(&h->snl_ze, (size_t)h->sst_cap * h->sst_stride)) ||
+          (s = dalloc(&h->snl_vals, (size_t)kStreamSlots * 10)))
         return fail(s);
       if (cudaMalloc((void **)&h->snl_flags, (size_t)kStreamSlots * 4 * sizeof(int)) != cudaSuccess)
         return fail(SWR_ERR_OOM);

@@ -108,8 +108,8 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
                                 cudaStream_t st);
 MarchShape choose_march_shape_nl(int Nj, int rows = 0, int nsys = 1);
 cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                   double2 *zest, double2 *ast, int *flags, double2 *vals, int nslot,
-                                   cudaStream_t st);
+                                   double2 *zest, double2 *ast, double2 *qst, double *est, size_t stride, int *flags,
+                                   double2 *vals, int nslot, cudaStream_t st);
 size_t march_nl_smem_bytes(const MarchShape &s, int NT, bool flux_smem);
 cudaError_t launch_march_nl(MarchParams p, const MarchShape &s, cudaStream_t st);
 __global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, double h, double dt, double2 c0,

@@ -640,9 +640,9 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
 // its forward total).  Flags count global fixed-point iterations (ic), so the
 // value buffers alternate by the parity of ic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p, int nc, double2 *ust,
-                                                            double2 *zst, double2 *zest, double2 *ast, int *flags,
-                                                            double2 *vals) {
+__global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p, int nc, size_t stride,
+                                                            double2 *ust, double2 *zst, double2 *zest, double2 *ast,
+                                                            double2 *qst, double *est, int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
   double2 *scanbuf = ssm;                      // [64]
   double2 *red = scanbuf + 64;                 // [32] block reductions
@@ -656,12 +656,22 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
   const double eim = p.e_im, kappa = p.kappa, h12 = p.h12, lam = p.lambda;
   const int Rc = (Nj + nc - 1) / nc;
   const int rc0 = min(Nj, c * Rc), rc1 = min(Nj, (c + 1) * Rc);
-  const int Rt = (rc1 - rc0 + P - 1) / P;
+  const int Rt = (Rc + P - 1) / P;                     // rows per thread (every CTA)
   const int rt0 = min(rc1, rc0 + t * Rt), rt1 = min(rc1, rc0 + (t + 1) * Rt);
-  double2 *__restrict__ u = ust + (size_t)sidx * Nj;
-  double2 *__restrict__ z = zst + (size_t)sidx * Nj;
-  double2 *__restrict__ ze = zest + (size_t)sidx * Nj;
-  double2 *__restrict__ ap = ast + (size_t)sidx * Nj;
+  // the thread-interleaved scratch layout of k_march_stream2
+  const size_t cbase = (size_t)c * P * Rt;
+  auto PH = [&](int i) -> size_t { return cbase + (size_t)i * P + t; };
+  auto phys_of = [&](int k) -> size_t {
+    const int cc = k / Rc, r = k - cc * Rc, tt = r / Rt;
+    return (size_t)cc * P * Rt + (size_t)(r - tt * Rt) * P + tt;
+  };
+  const int cnt = rt1 - rt0;
+  double2 *__restrict__ u = ust + (size_t)sidx * stride;
+  double2 *__restrict__ z = zst + (size_t)sidx * stride;
+  double2 *__restrict__ ze = zest + (size_t)sidx * stride;
+  double2 *__restrict__ ap = ast + (size_t)sidx * stride;
+  double2 *__restrict__ qp = qst + (size_t)sidx * stride;
+  double *__restrict__ ep = est + (size_t)sidx * stride;
   int *fdone = flags + (size_t)sidx * nc * 4, *ffwd = fdone + nc, *fbwd = ffwd + nc, *fmx = fbwd + nc;
   double2 *fv = vals + (size_t)sidx * nc * 10, *bv = fv + nc * 4, *mv = bv + nc * 4;   // [nc][parity](A,B) x2, [nc][parity]
   const bool has_left = S.flags & SYS_HAS_LEFT, has_right = S.flags & SYS_HAS_RIGHT;
@@ -672,9 +682,13 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
 
   for (int k = rc0 + t; k < rc1; k += P) {
     const double2 v = S.u0 ? S.u0[k] : cz();
-    u[k] = v;
-    ze[k] = v;                                  // zeta^0 of step 1 = v_0 = u_0
+    const size_t ph = phys_of(k);
+    u[ph] = v;
+    ze[ph] = v;                                 // zeta^0 of step 1 = v_0 = u_0
+    qp[ph] = __ldg(S.q + k);
+    ep[ph] = __ldg(S.er + k);
   }
+  __syncthreads();
   if (histL && t == 0) hvL[0] = S.u0 ? S.u0[0] : cz();
   if (histR && t == 0) hvR[0] = S.u0 ? S.u0[Nj - 1] : cz();
   const int sflags = S.flags;
@@ -685,11 +699,11 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
   double2 Af = make_double2(1.0, 0.0), Ab = make_double2(1.0, 0.0), Gt = cz();
   {
     double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
-    for (int k = rt0; k < rt1; k++) {
-      const double2 qk = __ldg(sq + k);
-      const double ek = __ldg(ser + k);
+    for (int i = 0; i < cnt; i++) {
+      const double2 qk = qp[PH(i)];
+      const double ek = ep[PH(i)];
       Af = cmul(negqe_s(qk, erp, eim), Af);
-      ap[k] = Af;
+      ap[PH(i)] = Af;
       Gt = cfma(Ab, Af, Gt);
       Ab = cmul(Ab, negqe_s(qk, ek, eim));
       erp = ek;
@@ -763,7 +777,9 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
       }
       return ld;
     };
-    auto ldg = [&](const double2 *a, int k) -> double2 { return (k >= rc0 && k < rc1) ? a[k] : __ldcg(a + k); };
+    auto ldg = [&](const double2 *a, int k) -> double2 {
+      return (k >= rc0 && k < rc1) ? a[phys_of(k)] : __ldcg(a + phys_of(k));
+    };
     // u_{n-1} halo rows: final for step n-1, unchanged through the iterations
     const double2 uh_m = rt0 > 0 && rt0 < rt1 ? ldg(u, rt0 - 1) : cz();
     const double2 uh_p = rt1 < Nj && rt0 < rt1 ? ldg(u, rt1) : cz();
@@ -778,21 +794,22 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
       // the backward offset B^loc = sum_i (prod_{k<i} b_k) z^loc_i
       double2 zl = cz(), Bl = cz(), Pb = make_double2(1.0, 0.0);
       {
-        double2 um = uh_m, uk = rt0 < rt1 ? ldg(u, rt0) : cz();
-        double2 zm = zh_m, zk = rt0 < rt1 ? ldg(ze, rt0) : cz();
+        double2 um = uh_m, uk = cnt > 0 ? u[PH(0)] : cz();
+        double2 zm = zh_m, zk = cnt > 0 ? ze[PH(0)] : cz();
         double erp = rt0 > 0 ? __ldg(ser + rt0 - 1) : 0.0;
 #pragma unroll 2
-        for (int k = rt0; k < rt1; k++) {
-          const bool lastrow = k + 1 == rt1;
-          const double2 up = k + 1 < Nj ? (lastrow ? uh_p : ldg(u, k + 1)) : cz();
-          const double2 zp = k + 1 < Nj ? (lastrow ? zh_p : ldg(ze, k + 1)) : cz();
-          const double2 qk = __ldg(sq + k);
-          const double ek = __ldg(ser + k);
+        for (int i = 0; i < cnt; i++) {
+          const int k = rt0 + i;
+          const bool lastrow = i + 1 == cnt;
+          const double2 up = k + 1 < Nj ? (lastrow ? uh_p : u[PH(i + 1)]) : cz();
+          const double2 zp = k + 1 < Nj ? (lastrow ? zh_p : ze[PH(i + 1)]) : cz();
+          const double2 qk = qp[PH(i)];
+          const double ek = ep[PH(i)];
           const double2 sv = cimul(kappa, sval(k, um, uk, up));
           const double2 ld = nload(k, zm, zk, zp);
           const double2 rr = make_double2(fma(-h12, ld.x, sv.x), fma(-h12, ld.y, sv.y));
           zl = cfma(negqe_s(qk, erp, eim), zl, cmul(qk, rr));
-          z[k] = zl;
+          z[PH(i)] = zl;
           Bl = cfma(Pb, zl, Bl);
           Pb = cmul(Pb, negqe_s(qk, ek, eim));
           erp = ek;
@@ -825,14 +842,15 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
       // pass B: zeta^{s+1}_k = (z^loc_k + Apre_k z_{rt0-1}) + b_k zeta^{s+1}_{k+1}, in place, and the maxima
       double2 x = cfma(eA, xc, eB);
       double dmax = 0.0, nmax = 0.0;
-      for (int k = rt1 - 1; k >= rt0; k--) {
-        const double2 bk = negqe_s(__ldg(sq + k), __ldg(ser + k), eim);
-        x = cfma(bk, x, cfma(ap[k], zc, z[k]));
-        const double2 zo = ze[k];
+      for (int i = cnt - 1; i >= 0; i--) {
+        const size_t ph = PH(i);
+        const double2 bk = negqe_s(qp[ph], ep[ph], eim);
+        x = cfma(bk, x, cfma(ap[ph], zc, z[ph]));
+        const double2 zo = ze[ph];
         const double dx = x.x - zo.x, dy = x.y - zo.y;
         dmax = fmax(dmax, fma(dx, dx, dy * dy));
         nmax = fmax(nmax, fma(x.x, x.x, x.y * x.y));
-        ze[k] = x;
+        ze[ph] = x;
       }
       // chain-wide maxima -> uniform decision
 #pragma unroll
@@ -873,12 +891,13 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
     if (!conv) { it = p.maxit_fp; fp_fail = 1; }
     if (it > fp_max) fp_max = it;
     // v_n = zeta; u_n = 2 v_n - u_{n-1}; record S v_n at the interfaces (eq. 8)
-    for (int k = rt0; k < rt1; k++) {
-      const double2 v = ze[k], uo = u[k];
-      u[k] = make_double2(fma(2.0, v.x, -uo.x), fma(2.0, v.y, -uo.y));
+    for (int i = 0; i < cnt; i++) {
+      const size_t ph = PH(i);
+      const double2 v = ze[ph], uo = u[ph];
+      u[ph] = make_double2(fma(2.0, v.x, -uo.x), fma(2.0, v.y, -uo.y));
     }
     if (own0) {
-      const double2 x0v = ze[0];
+      const double2 x0v = ze[phys_of(0)];
       if (histL) hvL[n] = x0v;
       if (has_left && sout_l) {
         const double2 sv = cfma(p.c0, x0v, sHL), l = flux(0, n);
@@ -886,7 +905,7 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
       }
     }
     if (ownL) {
-      const double2 xLv = ze[Nj - 1];
+      const double2 xLv = ze[phys_of(Nj - 1)];
       if (histR) hvR[n] = xLv;
       if (has_right && sout_r) {
         const double2 sv = cfma(p.c0, xLv, sHR), r = flux(1, n);
@@ -897,8 +916,10 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
     __threadfence();
     if (t == 0) st_release(fdone + c, n);
   }
-  if (S.uT)
-    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[k];
+  if (S.uT) {
+    __syncthreads();
+    for (int k = rc0 + t; k < rc1; k += P) S.uT[k] = u[phys_of(k)];
+  }
   if (c == 0 && t == 0 && p.fp_stat) {
     atomicMax(p.fp_stat, fp_max);
     if (fp_fail) atomicOr(p.fp_stat + 1, 1);
@@ -910,8 +931,8 @@ __global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p,
 // most nslot / nc systems): u, z, zeta [batch][N_j]; flags [batch][nc][4];
 // vals [batch][nc][10].
 cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                   double2 *zest, double2 *ast, int *flags, double2 *vals, int nslot,
-                                   cudaStream_t st) {
+                                   double2 *zest, double2 *ast, double2 *qst, double *est, size_t stride, int *flags,
+                                   double2 *vals, int nslot, cudaStream_t st) {
   const size_t smem = march_stream_smem_bytes(p.NT);
   cudaError_t e = cudaFuncSetAttribute(k_march_nl_stream, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
@@ -936,8 +957,9 @@ cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, 
     e = cudaMemsetAsync(flags, 0xff, (size_t)nb * nc * 4 * sizeof(int), st);
     if (e != cudaSuccess) return e;
     // the scratch holds one batch (batches run in stream order)
-    void *args[] = {(void *)&q,     (void *)&nc,    (void *)&ust, (void *)&zst,
-                    (void *)&zest,  (void *)&ast,   (void *)&flags, (void *)&vals};
+    if ((size_t)nc * 256 * (((p.Nj + nc - 1) / nc + 255) / 256) > stride) return cudaErrorInvalidValue;
+    void *args[] = {(void *)&q,   (void *)&nc,  (void *)&stride, (void *)&ust,   (void *)&zst, (void *)&zest,
+                    (void *)&ast, (void *)&qst, (void *)&est,    (void *)&flags, (void *)&vals};
     e = cudaLaunchCooperativeKernel((const void *)k_march_nl_stream, dim3(nb * nc), dim3(256), args, smem, st);
     if (e != cudaSuccess) return e;
     s0 += nb;
