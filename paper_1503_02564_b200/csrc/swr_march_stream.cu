@@ -8,8 +8,12 @@
 // (the march is then HBM-bound, the regime of SURVEY 8(d) "B1 streaming").
 // A system is a chain of nc co-resident CTAs (cooperative launch); CTA c owns
 // the contiguous rows [c Rc, (c+1) Rc) and thread t of it a contiguous block
-// of Rt rows, so each thread streams whole 128-byte lines of its own rows and
-// keeps the Thomas recurrence in registers.  Per step:
+// of Rt rows and keeps the Thomas recurrence in registers.  Three kernels:
+// k_march_stream2 (constant matrix) and k_march_nl_stream (|u|^2) take two
+// passes per step (or fixed-point iteration) over a thread-interleaved
+// scratch layout (row i of thread t at i P + t of the CTA's block: coalesced);
+// k_march_stream (V(t,x): per-step factors in the natural layout) takes the
+// four passes below.  Per step of k_march_stream:
 //   pass 1  forward from carry 0 over the thread's rows -> affine map (A, F)
 //   scan    CTA scan of the maps; the CTA totals are published in global
 //           memory (value + step flag, release/acquire) and folded by the
