@@ -393,7 +393,10 @@ __device__ __forceinline__ void fft1024(double2 (&v)[32], double2 *T, const doub
 // xs (optional, device): the input is s * x with s = xs->x, and xcopy
 // (optional) receives s * x — the GMRES step normalises its new basis vector
 // here instead of in a separate pass.
-__global__ void __launch_bounds__(64, 6) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
+// 4 CTAs per SM at most (255 registers, no spill: the butterflies of a stage
+// stay independent; 6 per SM capped the kernel at 168 registers with spills):
+// C5 applies 20.3 -> 18.4 ms per solve, C4 55 -> 46 ms; 8 per SM: 28.5 ms
+__global__ void __launch_bounds__(64, 4) k_fft_conv_reg(const double2 *__restrict__ Fc, const double2 *__restrict__ x,
                                                      double2 *__restrict__ y, const SlotMap m,
                                                      const double2 *__restrict__ tw, const double2 *__restrict__ xs,
                                                      double2 *__restrict__ xcopy) {
