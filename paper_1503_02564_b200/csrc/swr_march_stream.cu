@@ -344,9 +344,10 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 // HBM bytes per row and step: pass A reads u, q, Re E (40) and writes z (16);
 // pass B reads z, Apre, q, Re E, u (72) and writes u (16): 144 (the four-pass
 // form: ~224).
-// two CTAs per SM (128 registers): measured at C2 against one (208 registers,
-// 441 ms of march), three and four (445, 460 ms): 412 ms
-__global__ void __launch_bounds__(256, 2) k_march_stream2(const MarchParams p, int nc, size_t stride, double2 *ust,
+// four CTAs per SM (64 registers): with the interleaved layout the kernel is
+// bound by memory latency and more warps win (C2 march at 1 / 2 / 3 / 4 per
+// SM: 460 / 277 / 233 / 227 ms)
+__global__ void __launch_bounds__(256, 4) k_march_stream2(const MarchParams p, int nc, size_t stride, double2 *ust,
                                                        double2 *zst, double2 *ast, double2 *qst, double *est,
                                                        int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
@@ -561,21 +562,6 @@ size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1))
 // its scans reassociated) depends on N_j, the GPU and nsys_ref (the
 // problem's subdomain count) only -- not on how many systems a launch or a
 // rank carries -- so a rank of a multi-GPU run rounds exactly as one GPU.
-// chain length and scratch stride of the two-pass streaming march (the
-// interleaved layout pads every CTA's block to P Rt rows)
-size_t stream2_stride(int Nj, int nsys_ref, int NT) {
-  int dev = 0, nsm = 0, per_sm = 0;
-  cudaGetDevice(&dev);
-  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_march_stream2, 256, march_stream_smem_bytes(NT)) !=
-      cudaSuccess || per_sm < 1)
-    per_sm = 1;
-  int nc = std::max(1, nsm * per_sm / std::max(1, nsys_ref));
-  nc = std::min(nc, std::max(1, Nj / 256));
-  const int Rc = (Nj + nc - 1) / nc, Rt = (Rc + 255) / 256;
-  return (size_t)nc * 256 * Rt;
-}
-
 cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
                                 double2 *ast, double2 *qst, double *est, size_t stride, int *flags, double2 *vals,
                                 cudaStream_t st) {
@@ -644,7 +630,9 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
 // its forward total).  Flags count global fixed-point iterations (ic), so the
 // value buffers alternate by the parity of ic.
 // ---------------------------------------------------------------------------
-__global__ void __launch_bounds__(256, 2) k_march_nl_stream(const MarchParams p, int nc, size_t stride,
+// four CTAs per SM as k_march_stream2 (one R_nl sweep at N_j = 420,001:
+// 615 ms at two per SM, 320 ms at four)
+__global__ void __launch_bounds__(256, 4) k_march_nl_stream(const MarchParams p, int nc, size_t stride,
                                                             double2 *ust, double2 *zst, double2 *zest, double2 *ast,
                                                             double2 *qst, double *est, int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
@@ -969,6 +957,27 @@ cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, 
     s0 += nb;
   }
   return cudaSuccess;
+}
+
+// chain length and scratch stride of the two-pass streaming march (the
+// interleaved layout pads every CTA's block to P Rt rows)
+size_t stream2_stride(int Nj, int nsys_ref, int NT) {
+  int dev = 0, nsm = 0, per_sm = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+  // the largest block layout of the two interleaved kernels (their chain
+  // lengths follow their own occupancy)
+  size_t best = 0;
+  for (const void *kf : {(const void *)k_march_stream2, (const void *)k_march_nl_stream}) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kf, 256, march_stream_smem_bytes(NT)) != cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    int nc = std::max(1, nsm * per_sm / std::max(1, nsys_ref));
+    nc = std::min(nc, std::max(1, Nj / 256));
+    const int Rc = (Nj + nc - 1) / nc, Rt = (Rc + 255) / 256;
+    best = std::max(best, (size_t)nc * 256 * Rt);
+  }
+  return best;
 }
 
 }  // namespace swr
