@@ -68,29 +68,62 @@ __global__ void __launch_bounds__(256) k_pinv_far(const double2 *__restrict__ X0
   if (lane == 0) F[(size_t)s * B + (n - n0)] = acc;
 }
 
-// Steps n0 .. n0+B-1 in one CTA.  smem: h[2][ni], xa/xb ping-pong [2][2][ni].
+// Steps n0 .. n0+B-1 in one CTA.  The block's own history is a sum of at
+// most B - 1 lag products per slot: the lags 1..B-1 of the slot's two source
+// columns and the block's x values are staged in shared memory (the block
+// writes x and reads it back at every later step of the block), so the
+// per-step history runs out of shared memory.  smem: h[2 ni], x ping-pong
+// [2][2 ni], lags [2 ni][2][B], block x [2 ni][B].
+// staged = 0 (the staging does not fit shared memory, large N): lags and
+// block x read from global memory.
 __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ X0, const double2 *__restrict__ y,
                                                     const double2 *__restrict__ F, double2 *x, int N, int NT,
-                                                    int n0, int B, int sweeps, int has_far) {
+                                                    int n0, int B, int sweeps, int has_far, int staged) {
   pdl_wait();
   pdl_trigger();
   extern __shared__ double2 sm[];
-  const int ni = N - 1;
-  double2 *hs = sm, *xs = sm + 2 * ni;   // hs[2*i0 + w]; xs[buf][2*i0 + w]
+  const int ni = N - 1, ns = 2 * ni;
+  double2 *hs = sm, *xs = sm + ns;          // hs[2*i0 + w]; xs[buf][2*i0 + w]
+  double2 *lag = xs + 2 * ns;               // [ns][2][B]: c1[l], c2[l] (l < B)
+  double2 *xb = lag + (size_t)ns * 2 * B;   // [ns][B]: x of this block
   const int n_end = min(n0 + B, NT);
+  for (int e = threadIdx.x; staged && e < ns * B; e += blockDim.x) {
+    const int s = e / B, l = e % B;
+    const double2 *c1, *x1, *c2, *x2;
+    pinv_sources(s, N, NT, X0, x, c1, x1, c2, x2);
+    lag[((size_t)s * 2 + 0) * B + l] = l < NT ? __ldg(c1 + l) : cz();
+    lag[((size_t)s * 2 + 1) * B + l] = (c2 && l < NT) ? __ldg(c2 + l) : cz();
+  }
+  __syncthreads();
+  // the sources of slot s are slots s +- 1 and s +- 2 (pinv_sources)
+  auto src = [&](int s, int &a1, int &a2) {
+    const int i = s / 2 + 1;
+    if ((s & 1) == 0) { a1 = s + 1; a2 = (i + 1 <= N - 1) ? s + 2 : -1; }
+    else { a1 = s - 1; a2 = (i >= 2) ? s - 2 : -1; }
+  };
   for (int n = n0; n < n_end; n++) {
     for (int i0 = threadIdx.x; i0 < ni; i0 += blockDim.x) {
       double2 hv[2];
 #pragma unroll
       for (int w = 0; w < 2; w++) {
         const int s = 2 * i0 + w;
-        const double2 *c1, *x1, *c2, *x2;
-        pinv_sources(s, N, NT, X0, x, c1, x1, c2, x2);
+        int a1, a2;
+        src(s, a1, a2);
         double2 acc = y[(size_t)s * NT + n];
         if (has_far) acc = cadd(acc, F[(size_t)s * B + (n - n0)]);
-        for (int t = n0; t < n; t++) {   // x of this block: written by this CTA (plain loads)
-          acc = cfma(__ldg(c1 + n - t), x1[t], acc);
-          if (c2) acc = cfma(__ldg(c2 + n - t), x2[t], acc);
+        if (staged) {
+          const double2 *l1 = lag + ((size_t)s * 2 + 0) * B, *l2 = lag + ((size_t)s * 2 + 1) * B;
+          for (int t = n0; t < n; t++) {   // x of this block (shared memory), lags n - t in 1 .. B-1
+            acc = cfma(l1[n - t], xb[(size_t)a1 * B + (t - n0)], acc);
+            if (a2 >= 0) acc = cfma(l2[n - t], xb[(size_t)a2 * B + (t - n0)], acc);
+          }
+        } else {
+          const double2 *c1, *x1, *c2, *x2;
+          pinv_sources(s, N, NT, X0, x, c1, x1, c2, x2);
+          for (int t = n0; t < n; t++) {   // x of this block: written by this CTA (plain loads)
+            acc = cfma(__ldg(c1 + n - t), x1[t], acc);
+            if (c2) acc = cfma(__ldg(c2 + n - t), x2[t], acc);
+          }
         }
         hv[w] = acc;
         hs[s] = acc;
@@ -104,8 +137,8 @@ __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ 
     __syncthreads();
     int cur = 0;
     for (int sw = 0; sw < sweeps; sw++) {
-      const double2 *xo = xs + cur * 2 * ni;
-      double2 *xn = xs + (cur ^ 1) * 2 * ni;
+      const double2 *xo = xs + cur * ns;
+      double2 *xn = xs + (cur ^ 1) * ns;
       for (int i0 = threadIdx.x; i0 < ni; i0 += blockDim.x) {
         double2 ha = hs[2 * i0], hb = hs[2 * i0 + 1];
         if (i0 + 1 < ni) ha = cfma(__ldg(X0 + ((size_t)(i0 + 1) * 4 + 1) * NT), xo[2 * (i0 + 1)], ha);  // X^{i+1,2}_0 a_{i+1}
@@ -118,8 +151,11 @@ __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ 
       __syncthreads();
       cur ^= 1;
     }
-    const double2 *xf = xs + cur * 2 * ni;
-    for (int s = threadIdx.x; s < 2 * ni; s += blockDim.x) x[(size_t)s * NT + n] = xf[s];
+    const double2 *xf = xs + cur * ns;
+    for (int s = threadIdx.x; s < ns; s += blockDim.x) {
+      x[(size_t)s * NT + n] = xf[s];
+      if (staged) xb[(size_t)s * B + (n - n0)] = xf[s];
+    }
     __syncthreads();
   }
 }
@@ -128,7 +164,9 @@ cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, 
                                int sweeps, cudaStream_t st, int *n_launches) {
   const int ni = N - 1, ns = 2 * N - 2;
   if (ni < 1) return cudaSuccess;
-  const size_t smem = (size_t)6 * ni * sizeof(double2);
+  const size_t smem_st = ((size_t)6 * ni + (size_t)ns * 3 * PINV_B) * sizeof(double2);
+  const int staged = smem_st <= 200 * 1024;
+  const size_t smem = staged ? smem_st : (size_t)6 * ni * sizeof(double2);
   if (smem > 48 * 1024) {
     cudaError_t e = cudaFuncSetAttribute(k_pinv_near, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -143,7 +181,7 @@ cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, 
       ++*n_launches;
     }
     cudaError_t e = launch_pdl(k_pinv_near, dim3(1), dim3(thr), smem, st, X0, y, (const double2 *)F, x, N, NT, n0,
-                               (int)PINV_B, sweeps, n0 > 0 ? 1 : 0);
+                               (int)PINV_B, sweeps, n0 > 0 ? 1 : 0, staged);
     if (e != cudaSuccess) return e;
     ++*n_launches;
   }
