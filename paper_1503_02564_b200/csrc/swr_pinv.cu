@@ -86,7 +86,16 @@ __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ 
   double2 *hs = sm, *xs = sm + ns;          // hs[2*i0 + w]; xs[buf][2*i0 + w]
   double2 *lag = xs + 2 * ns;               // [ns][2][B]: c1[l], c2[l] (l < B)
   double2 *xb = lag + (size_t)ns * 2 * B;   // [ns][B]: x of this block
+  double2 *cst = xb + (size_t)ns * B;       // staged: [ni][5] p, q, 1/(1 - pq), X^{i+1,2}_0, X^{i,3}_0
   const int n_end = min(n0 + B, NT);
+  for (int i0 = threadIdx.x; staged && i0 < ni; i0 += blockDim.x) {
+    const double2 p = __ldg(X0 + (size_t)(i0 + 1) * 4 * NT), q = __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
+    cst[5 * i0 + 0] = p;
+    cst[5 * i0 + 1] = q;
+    cst[5 * i0 + 2] = crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
+    cst[5 * i0 + 3] = i0 + 1 < ni ? __ldg(X0 + ((size_t)(i0 + 1) * 4 + 1) * NT) : cz();
+    cst[5 * i0 + 4] = i0 >= 1 ? __ldg(X0 + ((size_t)i0 * 4 + 2) * NT) : cz();
+  }
   for (int e = threadIdx.x; staged && e < ns * B; e += blockDim.x) {
     const int s = e / B, l = e % B;
     const double2 *c1, *x1, *c2, *x2;
@@ -129,8 +138,9 @@ __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ 
         hs[s] = acc;
       }
       // x^(0) = D_i^{-1} h, D_i = [[1, -p], [-q, 1]], p = X^{i+1,1}_0, q = X^{i,4}_0
-      const double2 p = __ldg(X0 + (size_t)(i0 + 1) * 4 * NT), q = __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
-      const double2 rd = crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
+      const double2 p = staged ? cst[5 * i0] : __ldg(X0 + (size_t)(i0 + 1) * 4 * NT);
+      const double2 q = staged ? cst[5 * i0 + 1] : __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
+      const double2 rd = staged ? cst[5 * i0 + 2] : crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
       xs[2 * i0] = cmul(cfma(p, hv[1], hv[0]), rd);
       xs[2 * i0 + 1] = cmul(cfma(q, hv[0], hv[1]), rd);
     }
@@ -141,10 +151,16 @@ __global__ void __launch_bounds__(1024) k_pinv_near(const double2 *__restrict__ 
       double2 *xn = xs + (cur ^ 1) * ns;
       for (int i0 = threadIdx.x; i0 < ni; i0 += blockDim.x) {
         double2 ha = hs[2 * i0], hb = hs[2 * i0 + 1];
-        if (i0 + 1 < ni) ha = cfma(__ldg(X0 + ((size_t)(i0 + 1) * 4 + 1) * NT), xo[2 * (i0 + 1)], ha);  // X^{i+1,2}_0 a_{i+1}
-        if (i0 >= 1) hb = cfma(__ldg(X0 + ((size_t)i0 * 4 + 2) * NT), xo[2 * (i0 - 1) + 1], hb);        // X^{i,3}_0 b_{i-1}
-        const double2 p = __ldg(X0 + (size_t)(i0 + 1) * 4 * NT), q = __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
-        const double2 rd = crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
+        if (staged) {
+          if (i0 + 1 < ni) ha = cfma(cst[5 * i0 + 3], xo[2 * (i0 + 1)], ha);
+          if (i0 >= 1) hb = cfma(cst[5 * i0 + 4], xo[2 * (i0 - 1) + 1], hb);
+        } else {
+          if (i0 + 1 < ni) ha = cfma(__ldg(X0 + ((size_t)(i0 + 1) * 4 + 1) * NT), xo[2 * (i0 + 1)], ha);  // X^{i+1,2}_0 a_{i+1}
+          if (i0 >= 1) hb = cfma(__ldg(X0 + ((size_t)i0 * 4 + 2) * NT), xo[2 * (i0 - 1) + 1], hb);        // X^{i,3}_0 b_{i-1}
+        }
+        const double2 p = staged ? cst[5 * i0] : __ldg(X0 + (size_t)(i0 + 1) * 4 * NT);
+        const double2 q = staged ? cst[5 * i0 + 1] : __ldg(X0 + ((size_t)i0 * 4 + 3) * NT);
+        const double2 rd = staged ? cst[5 * i0 + 2] : crcp(csub(make_double2(1.0, 0.0), cmul(p, q)));
         xn[2 * i0] = cmul(cfma(p, hb, ha), rd);
         xn[2 * i0 + 1] = cmul(cfma(q, ha, hb), rd);
       }
@@ -164,7 +180,7 @@ cudaError_t launch_pinv_causal(const double2 *X0, const double2 *y, double2 *x, 
                                int sweeps, cudaStream_t st, int *n_launches) {
   const int ni = N - 1, ns = 2 * N - 2;
   if (ni < 1) return cudaSuccess;
-  const size_t smem_st = ((size_t)6 * ni + (size_t)ns * 3 * PINV_B) * sizeof(double2);
+  const size_t smem_st = ((size_t)6 * ni + (size_t)ns * 3 * PINV_B + (size_t)5 * ni) * sizeof(double2);
   const int staged = smem_st <= 200 * 1024;
   const size_t smem = staged ? smem_st : (size_t)6 * ni * sizeof(double2);
   if (smem > 48 * 1024) {
