@@ -338,6 +338,10 @@ def main():
     # V(x) NEW + GMRES at N = 10 (the streaming march, N_j = 420,001), C3 V(t,x)
     # preconditioned GMRES, C4 |u|^2 preconditioned fixed point
     if not args.no_extra and world == 1:
+        # free the C5 handle first: its persisting-L2 set-aside (device-wide,
+        # released with the last handle) would otherwise shrink the L2 the
+        # other configs see (C2's streaming march: 228 vs 248 ms)
+        s.close()
         extra = {}
         # C3 / C4 also with the exact causal P^{-1} (reading A27)
         # in place of the paper's inner Krylov P^{-1}
