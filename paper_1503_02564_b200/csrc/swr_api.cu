@@ -358,7 +358,8 @@ struct swr_handle {
   double2 *partial = nullptr;
   // streaming march (subdomains too large for the resident kernel)
   bool stream_march = false;
-  double2 *sst_u = nullptr, *sst_z = nullptr, *sst_a = nullptr, *sst_q = nullptr, *sst_vals = nullptr;
+  double2 *sst_u = nullptr, *sst_z = nullptr, *sst_a = nullptr, *sst_q = nullptr, *sst_b = nullptr,
+          *sst_vals = nullptr;
   double *sst_e = nullptr;
   size_t sst_stride = 0;
   int *sst_flags = nullptr;
@@ -493,7 +494,7 @@ int run_march(swr_handle *h, const std::vector<MarchSys> &sys, int nreal, int mo
     // in batches of co-resident chains
     if ((int)sys.size() > h->sst_cap) { g_detail = "streaming scratch too small"; return SWR_ERR_UNSUPPORTED; }
     CK(swr::launch_march_stream(p, (int)sys.size(), h->N, h->sst_u, h->sst_z, h->sst_a, h->sst_q, h->sst_e,
-                                h->sst_stride, h->sst_flags, h->sst_vals, h->st));
+                                h->sst_b, h->sst_stride, h->sst_flags, h->sst_vals, h->st));
   } else {
     CK(swr::launch_march(p, h->shape, h->st));
   }
@@ -1303,7 +1304,7 @@ void free_all(swr_handle *h) {
                   h->uloc, h->uT, h->tmp, h->tmp2, h->rhs, h->partial, h->tw, h->FX, h->FX0,
                   h->tau, h->xi, h->qtd, h->ertd, h->fp_stat,
                   h->sys_dev, h->err_dev, h->jobs_dev,
-                  h->sst_u, h->sst_z, h->sst_a, h->sst_q, h->sst_e, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
+                  h->sst_u, h->sst_z, h->sst_a, h->sst_q, h->sst_e, h->sst_b, h->sst_vals, h->sst_flags, h->kap, h->pinv_y, h->pinv_x,
                   h->haloL, h->haloR, h->hrecvL, h->hrecvR, h->part_send, h->part_recv, h->hv_nl, h->snl_ze, h->snl_vals, h->snl_flags};
   for (void *p : ptrs)
     if (p) cudaFree(p);
@@ -1545,7 +1546,7 @@ int swr_setup(const swr_config *cfg, swr_handle **out) {
     h->sst_stride = std::max((size_t)h->Nj, swr::stream2_stride(h->Nj, h->N, h->NT));
     const size_t sn = (size_t)h->sst_cap * h->sst_stride;
     if ((s = dalloc(&h->sst_u, sn)) || (s = dalloc(&h->sst_z, sn)) || (s = dalloc(&h->sst_a, sn)) ||
-        (s = dalloc(&h->sst_q, sn)) || (s = dalloc(&h->sst_e, sn)) ||
+        (s = dalloc(&h->sst_q, sn)) || (s = dalloc(&h->sst_e, sn)) || (s = dalloc(&h->sst_b, sn)) ||
         (s = dalloc(&h->sst_vals, nslot * 8)))
       return fail(s);
     if (cudaMalloc((void **)&h->sst_flags, nslot * 3 * sizeof(int)) != cudaSuccess) return fail(SWR_ERR_OOM);

@@ -104,8 +104,8 @@ cudaError_t launch_march(MarchParams p, const MarchShape &s, cudaStream_t st);
 size_t march_stream_smem_bytes(int NT);
 size_t stream2_stride(int Nj, int nsys_ref, int NT);
 cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                double2 *ast, double2 *qst, double *est, size_t stride, int *flags, double2 *vals,
-                                cudaStream_t st);
+                                double2 *ast, double2 *qst, double *est, double2 *bst, size_t stride, int *flags,
+                                double2 *vals, cudaStream_t st);
 MarchShape choose_march_shape_nl(int Nj, int rows = 0, int nsys = 1);
 cudaError_t launch_march_nl_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
                                    double2 *zest, double2 *ast, double2 *qst, double *est, size_t stride, int *flags,

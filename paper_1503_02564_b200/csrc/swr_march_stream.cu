@@ -342,14 +342,15 @@ __global__ void __launch_bounds__(256) k_march_stream(const MarchParams p, int n
 //   pass B  backward: x_k = (z^loc_k + Apre_k z_{rt0-1}) + b_k x_{k+1},
 //           u_n = 2 x - u_{n-1}
 // HBM bytes per row and step: pass A reads u, q, Re E (40) and writes z (16);
-// pass B reads z, Apre, q, Re E, u (72) and writes u (16): 144 (the four-pass
+// pass B reads z, Apre, b, u (64) and writes u (16): 136 (b_k formed once per
+// launch instead of from q and Re E every step: 144 -> 136; the four-pass
 // form: ~224).
 // four CTAs per SM (64 registers): with the interleaved layout the kernel is
 // bound by memory latency and more warps win (C2 march at 1 / 2 / 3 / 4 per
 // SM: 460 / 277 / 233 / 227 ms)
 __global__ void __launch_bounds__(256, 4) k_march_stream2(const MarchParams p, int nc, size_t stride, double2 *ust,
                                                        double2 *zst, double2 *ast, double2 *qst, double *est,
-                                                       int *flags, double2 *vals) {
+                                                       double2 *bst, int *flags, double2 *vals) {
   extern __shared__ double2 ssm[];
   double2 *scanbuf = ssm;                      // [64]
   double2 *red = scanbuf + 64;                 // [32] block reduction
@@ -379,6 +380,7 @@ __global__ void __launch_bounds__(256, 4) k_march_stream2(const MarchParams p, i
   double2 *__restrict__ ap = ast + (size_t)sidx * stride;
   double2 *__restrict__ qp = qst + (size_t)sidx * stride;
   double *__restrict__ ep = est + (size_t)sidx * stride;
+  double2 *__restrict__ bp = bst + (size_t)sidx * stride;
   const int cnt = rt1 - rt0;
   int *fdone = flags + (size_t)sidx * nc * 3, *ffwd = fdone + nc, *fbwd = ffwd + nc;
   double2 *fv = vals + (size_t)sidx * nc * 8, *bv = fv + nc * 4;
@@ -410,7 +412,9 @@ __global__ void __launch_bounds__(256, 4) k_march_stream2(const MarchParams p, i
       Af = cmul(negqe_s(qk, erp, eim), Af);
       ap[PH(i)] = Af;                                      // Apre_k
       Gt = cfma(Ab, Af, Gt);                               // (prod_{k'<k} b) Apre_k
-      Ab = cmul(Ab, negqe_s(qk, ek, eim));
+      const double2 bk = negqe_s(qk, ek, eim);
+      bp[PH(i)] = bk;                                      // b_k for pass B
+      Ab = cmul(Ab, bk);
       erp = ek;
     }
   }
@@ -522,8 +526,7 @@ __global__ void __launch_bounds__(256, 4) k_march_stream2(const MarchParams p, i
     for (int i = cnt - 1; i >= 0; i--) {
       const int k = rt0 + i;
       const size_t ph = PH(i);
-      const double2 bk = negqe_s(qp[ph], ep[ph], eim);
-      x = cfma(bk, x, cfma(ap[ph], zc, z[ph]));
+      x = cfma(bp[ph], x, cfma(ap[ph], zc, z[ph]));
       const double2 uo = u[ph];
       u[ph] = make_double2(fma(2.0, x.x, -uo.x), fma(2.0, x.y, -uo.y));
       if (k == Nj - 1) xLv = x;
@@ -563,8 +566,8 @@ size_t march_stream_smem_bytes(int NT) { return (size_t)(64 + 32 + 2 * (NT + 1))
 // problem's subdomain count) only -- not on how many systems a launch or a
 // rank carries -- so a rank of a multi-GPU run rounds exactly as one GPU.
 cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, double2 *ust, double2 *zst,
-                                double2 *ast, double2 *qst, double *est, size_t stride, int *flags, double2 *vals,
-                                cudaStream_t st) {
+                                double2 *ast, double2 *qst, double *est, double2 *bst, size_t stride, int *flags,
+                                double2 *vals, cudaStream_t st) {
   // constant matrix: the two-pass form (Apre in ast); V(t,x): four passes
   const bool two = p.td_stride == 0 && ast != nullptr;
   const void *kfun = two ? (const void *)k_march_stream2 : (const void *)k_march_stream;
@@ -598,7 +601,7 @@ cudaError_t launch_march_stream(MarchParams p, int nsys_total, int nsys_ref, dou
     if (two) {
       if ((size_t)nc * 256 * (((p.Nj + nc - 1) / nc + 255) / 256) > stride) return cudaErrorInvalidValue;
       void *args[] = {(void *)&q,   (void *)&nc,  (void *)&stride, (void *)&ust,   (void *)&zst,
-                      (void *)&ast, (void *)&qst, (void *)&est,    (void *)&flags, (void *)&vals};
+                      (void *)&ast, (void *)&qst, (void *)&est,    (void *)&bst,   (void *)&flags, (void *)&vals};
       e = cudaLaunchCooperativeKernel(kfun, dim3(nb * nc), dim3(256), args, smem, st);
     } else {
       void *args[] = {(void *)&q, (void *)&nc, (void *)&ust, (void *)&zst, (void *)&flags, (void *)&vals};
@@ -836,7 +839,7 @@ __global__ void __launch_bounds__(256, 4) k_march_nl_stream(const MarchParams p,
       double dmax = 0.0, nmax = 0.0;
       for (int i = cnt - 1; i >= 0; i--) {
         const size_t ph = PH(i);
-        const double2 bk = negqe_s(qp[ph], ep[ph], eim);
+        const double2 bk = negqe_s(qp[ph], ep[ph], eim);   // (a stored b_k measured slower here: 324 -> 350 ms)
         x = cfma(bk, x, cfma(ap[ph], zc, z[ph]));
         const double2 zo = ze[ph];
         const double dx = x.x - zo.x, dy = x.y - zo.y;
