@@ -1,4 +1,4 @@
-# experiment: 17 rows per thread (2-CTA clusters, all 148 SMs; ~500 B of spill) vs the product's 11 (3-CTA clusters)
+# experiment: 17 rows per thread (2-CTA clusters) -- the chooser rejected it (258 KB of shared memory), so both libraries ran the 11-row shape; see DESIGN.md section 6
 O=gpurun_out/r02ch; mkdir -p $O
 for i in 1 2; do
   for v in base m17; do
