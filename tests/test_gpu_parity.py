@@ -690,3 +690,48 @@ def test_solve_is_deterministic(gpu):
     assert out[0][3] == out[1][3]
     for a, b in zip(out[0][:3], out[1][:3]):
         assert np.array_equal(a, b)
+
+
+@pytest.mark.gpu
+def test_update_inputs_equals_fresh_setup(gpu):
+    """swr_update_inputs (d depends on u0, L on V through the
+    factorisation) gives bitwise the solve of a fresh handle set up with the
+    new inputs: host u0 + V_x together (u0's copy on the side stream,
+    overlapping V_x's copy and the factorisation), from pinned and pageable
+    buffers, and u0 alone."""
+    import torch
+    p = si.Problem(dx=1e-3, dt=5e-3, N=42, potential=si.POT_VX, transmission=si.TC_S02)
+    base = si.inputs(p)
+    x = p.nodes()
+    u0_b = (2.0 / np.cosh(np.sqrt(2.0) * (x + 5.0)) * np.exp(3j * x)).astype(np.complex128)
+    vx_b = (-0.5 * x * x + 0.25 * x).astype(np.float64)
+    u0_c = np.exp(-(x - 3.0) ** 2 - 7j * x).astype(np.complex128)
+
+    def fresh(u0, vx):
+        arr = dict(base, u0=u0, V_x=vx)
+        s = gpu.SWR(p, arr)
+        s.build()
+        st, uT, r = s.solve()
+        s.close()
+        return uT.copy(), r["iterations"]
+
+    s = gpu.SWR(p, base)
+    s.build()
+    s.solve()
+    for pinned in (True, False):
+        u0h = torch.from_numpy(u0_b).pin_memory().numpy() if pinned else u0_b.copy()
+        vxh = torch.from_numpy(vx_b).pin_memory().numpy() if pinned else vx_b.copy()
+        s.update_inputs(u0=u0h, V_x=vxh)
+        s.build()
+        st, uT, r = s.solve()
+        ref, it = fresh(u0_b, vx_b)
+        assert r["iterations"] == it
+        assert np.array_equal(uT, ref)
+        # back to the base inputs so the next round changes both again
+        s.update_inputs(u0=base["u0"], V_x=base["V_x"])
+    s.update_inputs(u0=u0_c)
+    s.build()
+    st, uT, r = s.solve()
+    ref, it = fresh(u0_c, base["V_x"])
+    assert r["iterations"] == it and np.array_equal(uT, ref)
+    s.close()
