@@ -171,8 +171,8 @@ int swr_setup(const swr_config *cfg, swr_handle **out);
  * of the same sizes; on_device as cfg->inputs_on_device.  Stream-ordered on
  * the handle's stream (a host u0 given with V_x is copied on an internal
  * stream that the handle's stream waits for, overlapping the factorisation);
- * host buffers may be reused once the call returns (it waits for the
- * factorisation's pivot check).  Returns SWR_ERR_ZERO_PIVOT if A - B cannot
+ * host buffers may be reused once the call returns (it waits for its
+ * copies and the factorisation's pivot check).  Returns SWR_ERR_ZERO_PIVOT if A - B cannot
  * be factored.  Collective. */
 int swr_update_inputs(swr_handle *h, const double *u0, const double *V_x, int32_t on_device);
 

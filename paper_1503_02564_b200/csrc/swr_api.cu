@@ -1682,6 +1682,8 @@ int swr_update_inputs(swr_handle *h, const double *u0, const double *V_x, int32_
     h->have_L = false;
   }
   if (overlap) CK(cudaStreamWaitEvent(h->st, h->ev_in1, 0));
+  // host buffers are free for reuse on return (the copies are done)
+  if (!on_device && (u0 || (V_x && h->Vx))) CK(cudaStreamSynchronize(h->st));
   h->have_d = false;
   return SWR_OK;
 }
