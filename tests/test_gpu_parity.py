@@ -734,4 +734,14 @@ def test_update_inputs_equals_fresh_setup(gpu):
     st, uT, r = s.solve()
     ref, it = fresh(u0_c, base["V_x"])
     assert r["iterations"] == it and np.array_equal(uT, ref)
+    # device inputs (stream-ordered copies on the handle's stream)
+    with torch.cuda.stream(s.stream):
+        du0 = torch.from_numpy(u0_b).to("cuda", non_blocking=False)
+        dvx = torch.from_numpy(vx_b).to("cuda", non_blocking=False)
+    torch.cuda.synchronize()
+    s.update_inputs(u0=du0, V_x=dvx, on_device=True)
+    s.build()
+    st, uT, r = s.solve()
+    ref, it = fresh(u0_b, vx_b)
+    assert r["iterations"] == it and np.array_equal(uT, ref)
     s.close()
