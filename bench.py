@@ -38,6 +38,8 @@ UNIT = "cell-steps/s"
 PAPER_T_NEW_GMRES_N500_S = 6.86      # 500 Sandy Bridge cores
 FLOP_PER_CELL_STEP = 36.0            # algorithmic flops of one CN cell-step
 BYTES_PER_CELL_STEP = 32.0           # u_{n-1} read + u_n write, complex fp64
+STREAM2_BYTES_PER_CELL_STEP = 136.0  # k_march_stream2: u, q, Re E, z, Apre, b traffic per row-step
+RESIDENT_MAX_ROWS = 16 * 256 * 11    # N_j above this: the streaming marches
 FP64_DERIVED_TFLOPS = 148 * 64 * 2 * 1.965e9 / 1e12   # 37.2: 148 SMs x 64 DFMA/clk at 1965 MHz
 FP64_PROBE = os.path.join(ROOT, "profiles", "r02", "probe_fp64_b200.txt")
 
@@ -372,6 +374,13 @@ def main():
                                               / 1e12 / fp64,
                            "march_streaming_equiv_bw_frac": BYTES_PER_CELL_STEP * rq["cell_steps"]
                                                             / (rq["t_march_ms"] / 1e3) / 1e9 / hbm}
+            if q.Nj > RESIDENT_MAX_ROWS and q.potential == si.POT_VX:
+                # the two-pass streaming march's own HBM bytes (DESIGN.md section 6:
+                # 136 B per row-step) against the measured copy peak: a real roofline
+                extra[name]["march_kernel"] = "k_march_stream2 (streaming, state through HBM)"
+                extra[name]["march_bytes_per_cell_step"] = STREAM2_BYTES_PER_CELL_STEP
+                extra[name]["march_hbm_frac"] = (STREAM2_BYTES_PER_CELL_STEP * rq["cell_steps"]
+                                                 / (rq["t_march_ms"] / 1e3) / 1e9 / hbm)
             sq.close()
         line["other_configs"] = extra
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
