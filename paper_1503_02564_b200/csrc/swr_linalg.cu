@@ -55,7 +55,7 @@ __global__ void k_factor(const FactorJob *jobs, int njobs, int Nj, double h, dou
           const double2 E = make_double2(er_prev, eim);
           p = csub(p, cmul(E, cmul(E, qprev)));
         }
-        if (!(hypot(p.x, p.y) >= 1e-300)) bad = true;   // zero pivot
+        if (tiny_pivot(p)) bad = true;   // zero pivot
         qprev = crcp(p);
         sQ[wl][i] = qprev;
         er_prev = sE[wl][i];
@@ -108,7 +108,7 @@ __global__ void k_factor_td(const FactorJob *jobs, int njobs, int Nj, int NT, do
       const double2 E = make_double2(er_prev, eim);
       p = csub(D, cmul(E, cmul(E, qprev)));
     }
-    if (!(hypot(p.x, p.y) >= 1e-300)) atomicExch(err, 3);
+    if (tiny_pivot(p)) atomicExch(err, 3);
     const double2 qk = crcp(p);
     const double erk = (k < Nj - 1) ? 1.0 / h + h * (Wk + Wr) / 12.0 : 0.0;
     qo[k] = qk;

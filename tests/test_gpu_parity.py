@@ -745,3 +745,27 @@ def test_update_inputs_equals_fresh_setup(gpu):
     ref, it = fresh(u0_b, vx_b)
     assert r["iterations"] == it and np.array_equal(uT, ref)
     s.close()
+
+
+@pytest.mark.gpu
+def test_factor_flags_nan_pivot(gpu):
+    """The factorisation's pivot check (a zero or non-finite pivot of
+    A - B) surfaces as SWR_ERR_ZERO_PIVOT at setup and at swr_update_inputs
+    (a NaN in V_x poisons the pivots from its row on)."""
+    from paper_1503_02564_b200.swr import SWRError
+    p = si.Problem(dx=1e-3, dt=5e-3, N=10, potential=si.POT_VX)
+    arr = si.inputs(p)
+    bad = arr["V_x"].copy()
+    bad[len(bad) // 3] = np.nan
+    with pytest.raises(SWRError) as e:
+        gpu.SWR(p, dict(arr, V_x=bad))
+    assert e.value.status == 3
+    s = gpu.SWR(p, arr)
+    with pytest.raises(SWRError) as e:
+        s.update_inputs(V_x=bad)
+    assert e.value.status == 3
+    s.update_inputs(V_x=arr["V_x"])   # recovers with valid data
+    s.build()
+    st, uT, r = s.solve()
+    assert st == 0 and np.all(np.isfinite(uT))
+    s.close()
