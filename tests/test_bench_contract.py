@@ -1,11 +1,13 @@
 """The bench.py reference arm (the CPU oracle, rank 0 only) keeps the driver's
 JSON-line contract: one line with the contract's keys, its cpu_baseline and
 a zero-copy e2e; the other ranks of a multi-rank launch print nothing and
-exit 0.  (The product arm needs a GPU; its line is checked on the box.)"""
+exit 0.  The product arm's line is checked on the GPU (`-m gpu`)."""
 import json
 import os
 import subprocess
 import sys
+
+import pytest
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 KEYS = {"impl", "metric", "value", "unit", "n_gpus", "steps", "warmup", "ms_per_step", "higher_is_better",
@@ -39,3 +41,28 @@ def test_reference_arm_other_ranks_silent(oracle_mod):
     r = _run({"RANK": "1", "WORLD_SIZE": "2", "LOCAL_RANK": "1"})
     assert r.returncode == 0, r.stderr
     assert r.stdout.strip() == ""
+
+
+PRODUCT_KEYS = KEYS - {"impl"} | {"roofline", "gpu_launches", "clocks"}
+
+
+@pytest.mark.gpu
+def test_product_arm_line():
+    """The product arm on a small config: one JSON line with the contract's
+    keys, a device-timed value, an e2e through host buffers with its copy
+    sizes, the roofline block of the dominant kernel, the clocks sampled in
+    the timed region and a nonzero count of the library's kernel launches."""
+    r = subprocess.run([sys.executable, os.path.join(ROOT, "bench.py"), "--config", "C1", "--steps", "3",
+                        "--warmup", "3", "--no-extra"], cwd=ROOT, capture_output=True, text=True, timeout=600)
+    assert r.returncode == 0, r.stderr
+    lines = [l for l in r.stdout.splitlines() if l.strip()]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    assert PRODUCT_KEYS <= set(d)
+    assert d["steps"] == 3 and d["warmup"] == 3 and d["n_gpus"] == 1 and d["value"] > 0
+    assert d["gpu_launches"] > 0
+    e = d["e2e"]
+    assert e["value"] > 0 and e["h2d_bytes_per_step"] > 0 and e["d2h_bytes_per_step"] > 0
+    rf = d["roofline"]
+    assert {"bound", "achieved", "peak", "unit", "frac"} <= set(rf) and rf["peak"] > 0
+    assert d["cpu_baseline"]["kind"] == "oracle" and d["cpu_baseline"]["value"] > 0
